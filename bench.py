@@ -1,0 +1,312 @@
+#!/usr/bin/env python3
+"""Benchmark of the placement-cost / partition-search hot path.
+
+Default workload (N=1 and scaling runs): BASELINE.json configs[1] — the
+Llama-2-7B training workflow (34 layer cells) over a 32-device heterogeneous
+fleet, EXHAUSTIVE split sweep: all 8,589,934,558 contiguous splits with run q
+on worker q, each scored with the reference cost model (fits + compute +
+crossing read, makespan) and reduced to the first strict minimum by
+(makespan, rank).  One step = one full sweep over the whole population,
+sharded across the ranks (strong scaling), plus one NCCL all-gather of the
+per-rank winner records.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+       (multi-GPU: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "candidate placements evaluated/sec (+ partition DPs solved/sec)"
+UNIT = "candidates/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2"])
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary measurements")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload
+def c2_instance():
+    from paper_2309_01172_b200 import configs as CF
+    stages = CF.model_stages("llama2-7b-layers")
+    fleet = CF.load(CF.c2_fleet_doc(0))
+    return stages, fleet
+
+
+def workload_config(total):
+    return {"workload": "C2 llama2-7b (34 layer cells) x 32 heterogeneous workers, exhaustive split sweep",
+            "candidates_per_step": total, "stages": 34, "workers": 32,
+            "candidate_source": "in-kernel enumeration (rank -> splits), ~0 HBM bytes per candidate",
+            "l2_policy": "inputs are generated on chip; no HBM-resident candidate stream to flush",
+            "parallelism": "rank-range sharding + 1 all-gather of winners"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        except OSError:
+            return None
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- b200 arm
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_01172_b200 import dist as D
+    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200.tensorize import build_host
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream()
+    stages, fleet = c2_instance()
+    n, p = len(stages), len(fleet.worker_ids())
+    total = engine.splits_total(n, p)
+    k0, k1 = D.shard(total, rank, world)
+    host = build_host(stages, fleet, True)
+    batch = engine.device_batch([host], device=dev)
+    bufs = engine.WinnerBuffers(dev)
+
+    def step():
+        engine.enum(batch, "splits", k0, k1, bufs)
+        if world > 1:
+            return D.all_gather_winner(bufs.out)
+        return bufs.out
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    clocks = ClockSampler(local_rank)
+    if rank == 0:
+        clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev0.record(stream)
+    for s in range(args.steps):
+        kev[s][0].record(stream)
+        engine.enum(batch, "splits", k0, k1, bufs)
+        kev[s][1].record(stream)
+        if world > 1:
+            D.all_gather_winner(bufs.out)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop() if rank == 0 else None
+    ms = ev0.elapsed_time(ev1)
+    kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, kernel_ms = float(t[0]), float(t[1])
+    res = D.merge_records(step().cpu().numpy()) if world > 1 else bufs.read()
+
+    # ---- e2e: public API with host buffers, copies inside the timed region
+    import numpy as np
+    host_rec = batch.host_buf
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pinned_out = torch.empty(bufs.out.numel() * world, dtype=torch.uint8, pin_memory=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        batch.dev_buf.copy_(host_rec, non_blocking=True)
+        batch.structs_dev.copy_(batch.records_host, non_blocking=True)
+        engine.enum(batch, "splits", k0, k1, bufs)
+        out = D.all_gather_winner(bufs.out).view(-1) if world > 1 else bufs.out
+        pinned_out.narrow(0, 0, out.numel()).copy_(out, non_blocking=True)
+        stream.synchronize()
+        D.merge_records(pinned_out.numpy()[: out.numel()])
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te[0])
+
+    extras = {}
+    if rank == 0 and not args.no_extras and world == 1:
+        extras = secondary_measurements(dev)
+    if rank != 0:
+        return None
+    value = total * args.steps / (ms / 1e3)
+    e2e_val = total * args.steps / (e2e_ms / 1e3)
+    mean_runs = mean_runs_splits(n, p)
+    fp64_ops = 6 * mean_runs - 3
+    peak = extras.get("fp64_peak_ops_per_s")
+    achieved = total / (kernel_ms / 1e3) * fp64_ops / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(total),
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(batch.h2d_bytes),
+                "d2h_bytes_per_step": int(D.WINNER_BYTES * world)},
+        "gpu_launches": 2 * args.steps,
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": (peak / 1e12) if peak else None,
+                     "unit": "TFLOP/s", "frac": (achieved / (peak / 1e12)) if peak else None, "traffic": None,
+                     "algorithmic_ops_per_candidate": fp64_ops, "kernel_ms": kernel_ms,
+                     "note": "algorithmic fp64 add/mul/div per candidate (SURVEY 8d Mode B: 6r-3, r = mean runs "
+                             "of the population) / kernel time, vs the microbenchmarked fp64 op rate"},
+        "winner": {"makespan": res["makespan"], "rank": res["rank"], "n_feasible": res["n_feasible"],
+                   "checksum": res["checksum"]},
+    }
+    if clk:
+        line["clocks"] = clk
+    line.update(extras)
+    return line
+
+
+def mean_runs_splits(n, p):
+    import math
+    tot = sum(math.comb(n - 1, r - 1) for r in range(1, min(n, p) + 1))
+    return sum(r * math.comb(n - 1, r - 1) for r in range(1, min(n, p) + 1)) / tot
+
+
+def secondary_measurements(dev):
+    """FP64 peak microbenchmark (roofline denominator) and the CPU baseline."""
+    out = {}
+    try:
+        from paper_2309_01172_b200 import engine
+        out["fp64_peak_ops_per_s"] = engine.fp64_peak()
+    except Exception as exc:  # the microbenchmark is optional
+        out["fp64_peak_error"] = str(exc)
+    out["cpu_baseline"] = cpu_baseline(threads=1, seconds=10.0)
+    return out
+
+
+# ------------------------------------------------------------- CPU oracle
+def cpu_baseline(threads=1, seconds=10.0):
+    """Time the oracle (C restatement of brute_force_schedule's inner body,
+    scheduling.py:264-272, in the identity-split order) on a bounded sample of
+    the same population."""
+    from oracle import oracle
+    from paper_2309_01172_b200 import engine
+    oracle.build()
+    stages, fleet = c2_instance()
+    inst = oracle.Instance(stages, fleet)
+    total = engine.splits_total(inst.n, inst.p)
+    # calibrate on a small sample from the middle of the population
+    mid = total // 2
+    t0 = time.perf_counter()
+    inst.enum("splits", mid, mid + 20000)
+    rate1 = 20000 / (time.perf_counter() - t0)
+    per_thread = max(int(rate1 * seconds), 1000)
+    from concurrent.futures import ThreadPoolExecutor
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda i: inst.enum("splits", mid + i * per_thread, mid + (i + 1) * per_thread), range(threads)))
+    el = time.perf_counter() - t0
+    return {"value": threads * per_thread / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{threads * per_thread} consecutive ranks from the middle of the C2 split population "
+                      f"({el:.1f}s), oracle/dm_oracle.c or_enum mode 1"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    base = cpu_baseline(threads=threads, seconds=max(2.0, 20.0 / max(args.steps, 1)))
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(8589934558),
+            "cpu_baseline": {"value": base["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": base["sample"]},
+            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+def main():
+    args = _args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        line = run_b200(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

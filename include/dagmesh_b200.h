@@ -1,0 +1,263 @@
+/*
+ * dagmesh_b200.h — C ABI of the B200 placement-cost / partition-search engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference planner
+ * `dagmesh` (FusionAI, arXiv 2309.01172).  The reference has no FFI of its
+ * own: its boundary is the Python API of `dagmesh.scheduling` and
+ * `dagmesh.pipeline`.  Every entry point below replaces one reference
+ * function (cited as pkg/src/dagmesh/<file>:<line>, relative to the
+ * reference tree) and is bound from Python with ctypes by
+ * `paper_2309_01172_b200/_lib.py` (see INTEGRATION.md for the binding a
+ * maintainer adds to the reference package itself).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch types.  Pointers inside the
+ *     structs passed to dm_* calls are DEVICE pointers (caller-owned).
+ *   - every call is stream-ordered (`stream` is a cudaStream_t, NULL = legacy
+ *     default stream), reentrant, and keeps no global mutable state except a
+ *     thread-local last-error string (dm_last_error()).
+ *   - functions return DM_OK (0) or a negative DM_E_* status; they never
+ *     throw across the ABI.
+ *   - all arithmetic is IEEE-754 binary64 with the reference's rounding
+ *     sequence (no FMA contraction: the library is built with -fmad=false,
+ *     division is correctly rounded), so results are bit-identical to the
+ *     CPython reference.
+ *
+ * The same struct layout is consumed by the CPU oracle under oracle/ (host
+ * pointers there); the oracle is test infrastructure only.
+ */
+#ifndef DAGMESH_B200_H
+#define DAGMESH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DM_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DM_API __attribute__((visibility("default")))
+#else
+#define DM_API
+#endif
+
+/* ---------------------------------------------------------------- status */
+#define DM_OK              0
+#define DM_E_ARG          -1   /* bad argument (sizes, null pointers)            */
+#define DM_E_CUDA         -2   /* CUDA runtime error; see dm_last_error()        */
+#define DM_E_UNKNOWN_PEER -3   /* FleetError("unknown peer")  hardware.py:122-126 */
+#define DM_E_UNASSIGNED   -4   /* KeyError: crossing edge from an unowned stage
+                                  (peer_of[src] in scheduling.py:167)            */
+#define DM_E_TOO_LARGE    -5   /* instance exceeds a device-side size limit      */
+
+/* ------------------------------------------------------ violation codes
+ * First violation found by verify_assignment (scheduling.py:179-207), in the
+ * reference's check order.  The Python layer rebuilds the reason string. */
+#define DM_V_OK             0
+#define DM_V_TWO_RUNS       1  /* "peer X holds two runs"          :186-187 */
+#define DM_V_UNKNOWN_PEER   2  /* "unknown peer X"                 :189-190 */
+#define DM_V_NOT_CONTIGUOUS 3  /* "peer X run [...] is not contiguous" :191-193 */
+#define DM_V_ASSIGNED_TWICE 4  /* "stage i assigned twice"         :194-196 */
+#define DM_V_GPU            5  /* "peer X exceeds gpu capacity"    :199-203 */
+#define DM_V_CPU            6  /*                  cpu                      */
+#define DM_V_DISK           7  /*                  disk                     */
+#define DM_V_UNASSIGNED     8  /* "stages [...] unassigned"        :204-206 */
+
+/* ------------------------------------------------------------ table flags */
+#define DM_F_FLOPS_EXACT  1u   /* flops integral, every prefix < 2^53: pre_flops valid */
+#define DM_F_BYTES_EXACT  2u   /* gpu/cpu/disk integral, prefixes < 2^53: pre_* valid  */
+#define DM_F_PAIR_LINKS   4u   /* link_alpha/link_beta (P x P) hold link_between()    */
+#define DM_F_CHAIN        8u   /* every in-edge of stage i has src == i-1             */
+#define DM_F_BACKWARD    16u   /* some in-edge has src >= its own stage               */
+#define DM_F_INCLUDE_COMM 32u  /* include_comm=True (scheduling.py:162)               */
+
+/*
+ * One scheduling instance: the stage table (scheduling.Stage, :32-42) and the
+ * fleet (hardware.Fleet, hardware.py:103-144) in structure-of-arrays form.
+ *
+ * Peer indexing: 0..p-1 are fleet.worker_ids() in order (hardware.py:131-134,
+ * ir.peer_sort_key ordering); p..P-1 are the remaining peers (backups) in
+ * peer_ids() order.  Worker order defines brute-force permutation order,
+ * subset-DP masks and pinned-run mapping.
+ */
+typedef struct dm_tables {
+    int32_t n;          /* stages                                     */
+    int32_t p;          /* schedulable workers                        */
+    int32_t P;          /* all addressable peers (workers + backups)  */
+    int32_t n_edges;    /* CSR length                                  */
+    uint32_t flags;     /* DM_F_*                                      */
+    int32_t pad_;
+    double def_alpha;   /* fleet.default_link.alpha  (s)               */
+    double def_beta;    /* fleet.default_link.beta   (s/B)             */
+    /* stage columns, length n */
+    const double* flops;
+    const double* gpu;
+    const double* cpu;
+    const double* disk;
+    /* exact prefix sums, length n+1 (valid per DM_F_*_EXACT) */
+    const int64_t* pre_flops;
+    const int64_t* pre_gpu;
+    const int64_t* pre_cpu;
+    const int64_t* pre_disk;
+    /* in-edges in stored order: stage i owns edge_ptr[i] .. edge_ptr[i+1]-1 */
+    const int32_t* edge_ptr;   /* [n+1] */
+    const int32_t* edge_src;   /* [n_edges] source stage                     */
+    const double* edge_m;      /* [n_edges] nbytes * fleet.msg_ratio (>= 0)   */
+    /* peer columns, length P */
+    const double* speed;       /* effective_speed = peak_flops * lam (hardware.py:153-154) */
+    const double* cap_gpu;
+    const double* cap_cpu;
+    const double* cap_disk;
+    /* resolved link_between(a, b) (hardware.py:136-140), row a = source owner,
+       column b = reading peer, diagonal = ZERO_LINK; only with DM_F_PAIR_LINKS */
+    const double* link_alpha;  /* [P*P] */
+    const double* link_beta;   /* [P*P] */
+} dm_tables;
+
+/* Arg-min record shared by every enumeration: first strict minimum in rank
+ * order (brute_force_schedule, scheduling.py:269-272). */
+typedef struct dm_winner {
+    double   makespan;     /* +inf if no candidate was feasible           */
+    int64_t  rank;         /* global rank of the winner, -1 if none       */
+    int64_t  n_evaluated;  /* candidates scored                           */
+    int64_t  n_feasible;   /* candidates that passed _fits                */
+    uint64_t checksum;     /* sum (mod 2^64) of makespan bit patterns of
+                              all feasible candidates — order independent  */
+} dm_winner;
+
+/* --------------------------------------------------------------- general */
+DM_API int         dm_abi_version(void);
+DM_API const char* dm_last_error(void);
+/* bytes of device scratch the enumeration calls need (per-CTA partials) */
+DM_API int64_t     dm_enum_scratch_bytes(void);
+
+/*
+ * dm_eval_runs — replaces scheduling._evaluate / evaluate_runs
+ * (scheduling.py:210-239) including verify_assignment (:179-207) and
+ * _run_cost (:156-169), for arbitrary Runs in CSR form:
+ *   candidate c owns runs cand_ptr[c] .. cand_ptr[c+1]-1 (runs order as given);
+ *   run r is (run_peer[r], stage indices run_idx[run_ptr[r] .. run_ptr[r+1]-1]).
+ * run_peer[r] < 0 or >= P encodes a peer unknown to the fleet.
+ * Outputs: per run compute_s / read_s (only for non-empty runs; the order is the
+ * given order, the Python layer sorts by first stage as :217-218 does),
+ * per candidate makespan (max(0.0, loads)), violation code and the index of the
+ * run that triggered it.  Status DM_E_UNKNOWN_PEER / DM_E_UNASSIGNED mirror the
+ * FleetError / KeyError the reference raises while costing; out_status[c] holds
+ * the per-candidate status.
+ */
+DM_API int dm_eval_runs(const dm_tables* t, int32_t n_cand,
+                 const int32_t* cand_ptr, const int32_t* run_peer,
+                 const int32_t* run_ptr, const int32_t* run_idx,
+                 double* out_compute, double* out_read,
+                 double* out_makespan, int32_t* out_code,
+                 int32_t* out_code_run, int32_t* out_status, void* stream);
+
+/*
+ * dm_eval_owner — Mode A scoring stream (the scoring-service form of
+ * evaluate_runs).  Candidate c is the owner vector owner[c*n .. c*n+n-1]
+ * (uint8 when owner_bytes == 1, uint16 when 2) whose Runs are the stages of
+ * each peer grouped in first-appearance order.  Writes makespan (f64) and
+ * violation code (u8, DM_V_*; 0xFF = owner index >= P, i.e. FleetError).
+ */
+DM_API int dm_eval_owner(const dm_tables* t, int64_t n_cand, const void* owner,
+                  int32_t owner_bytes, double* out_makespan,
+                  uint8_t* out_code, void* stream);
+
+/*
+ * dm_argmin_scores — block/warp arg-min over (makespan, rank) of a scored
+ * stream (codes != 0 are skipped), ranks = rank_base + index.
+ * out is a device dm_winner.
+ */
+DM_API int dm_argmin_scores(const double* makespan, const uint8_t* code, int64_t n,
+                     int64_t rank_base, dm_winner* out, void* scratch,
+                     void* stream);
+
+/*
+ * dm_enum_bruteforce — brute_force_schedule's exhaustive order
+ * (scheduling.py:245-278): global rank k in [k0, k1) over
+ * r = 1..min(n,p); cut sets = combinations(range(1,n), r-1) (lexicographic);
+ * peer tuples = permutations(workers, r) (lexicographic by worker index).
+ * Candidates failing _fits (:172-176) are skipped; winner = first strict min.
+ */
+DM_API int dm_enum_bruteforce(const dm_tables* t, int64_t k0, int64_t k1,
+                       dm_winner* out, void* scratch, void* stream);
+
+/*
+ * dm_enum_splits — the identity-order subset of the brute-force order: run q
+ * goes to worker q.  Rank order: r ascending, then cut sets lexicographic.
+ * Total Σ_{r=1..min(n,p)} C(n-1, r-1).
+ */
+DM_API int dm_enum_splits(const dm_tables* t, int64_t k0, int64_t k1,
+                   dm_winner* out, void* scratch, void* stream);
+
+/*
+ * dm_enum_random — counter-RNG random contiguous placements (config C5):
+ * candidate k (k0 <= k < k1) is generated from SplitMix64 keyed (seed, k):
+ * each cut position 1..n-1 is present with probability 1/2, and the r runs go
+ * to r distinct peers online[(a*q + b) mod n_online], q = 0..r-1, with
+ * a = mults[h % n_mults] (every mult coprime to n_online) and b drawn from
+ * the same stream.  Requires chain-structured stages (DM_F_CHAIN) when
+ * include_comm is set, and n <= n_online.
+ * See paper_2309_01172_b200/rng.py for the exact recipe (shared with the oracle).
+ */
+DM_API int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,
+                   const int32_t* mults, int32_t n_mults, uint64_t seed,
+                   int64_t k0, int64_t k1, dm_winner* out,
+                   void* scratch, void* stream);
+
+/* dm_finalize_winners — reduce per-CTA partials left in scratch by the
+ * enumeration calls into out (called internally; exposed for multi-stream use) */
+DM_API int dm_finalize_winners(void* scratch, int32_t n_parts, dm_winner* out,
+                        void* stream);
+
+/*
+ * dm_subset_dp — batched _subset_dp (scheduling.py:288-325): one CTA per
+ * scenario, tables[s] is a device array of dm_tables (device pointers).
+ * Output per scenario: out_owner[s*n_max + i] = worker index of stage i
+ * (-1 beyond n), out_makespan[s] = DP value of the chosen final state
+ * (+inf and out_found[s] = 0 when no final state exists → schedule() marks
+ * the instance infeasible, :408-411).
+ * scratch: device bytes for DP tables that do not fit shared memory; query
+ * dm_subset_dp_scratch_bytes(n_max, p_max, n_scen).
+ */
+DM_API int64_t dm_subset_dp_scratch_bytes(int32_t n_max, int32_t p_max, int32_t n_scen);
+DM_API int dm_subset_dp(const dm_tables* tables, int32_t n_scen, int32_t n_max,
+                 int32_t p_max, int16_t* out_owner, double* out_makespan,
+                 int32_t* out_found, void* scratch, void* stream);
+
+/*
+ * dm_prop_hill — batched _proportional_runs (:328-351) followed by
+ * _hill_climb (:354-388) when do_hill[s] != 0 (one warp per scenario).
+ * When init_owner != NULL the hill climb starts from those runs instead of
+ * the proportional split (schedule()'s DP + pairwise-links polish, :412-413).
+ * Output: final owner vectors and the hill-climb score (inf when infeasible).
+ */
+DM_API int dm_prop_hill(const dm_tables* tables, int32_t n_scen, int32_t n_max,
+                 const int16_t* init_owner, const uint8_t* do_hill,
+                 int16_t* out_owner, double* out_score, int32_t* out_moves,
+                 void* stream);
+
+/*
+ * dm_pipeline_epilogue — per scenario, from an owner vector with contiguous
+ * runs: _evaluate's makespan and feasibility (:210-232), then
+ * fp_latency (Neumaier sum, pipeline.py:41-43), bottleneck (:46-50),
+ * pipeline_time (:53-56) and throughput (:59-62).
+ * out[s*6 + {0..5}] = makespan, latency, bottleneck, pipe_time, throughput,
+ * violation code (as double).
+ */
+DM_API int dm_pipeline_epilogue(const dm_tables* tables, int32_t n_scen, int32_t n_max,
+                         const int16_t* owner, int64_t n_batches,
+                         int64_t samples_per_batch, double* out, void* stream);
+
+/* dm_microbench_fp64 — FP64 DMUL+DADD issue-rate microbenchmark (the
+ * roofline denominator of the generated-candidate kernels).  *ops receives
+ * the number of fp64 operations the launch performs; time it with events. */
+DM_API int dm_microbench_fp64(int64_t iters, double* sink, int64_t* ops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DAGMESH_B200_H */

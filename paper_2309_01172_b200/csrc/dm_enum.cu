@@ -1,0 +1,363 @@
+// dm_enum.cu — Mode B candidate streams generated in-kernel from a rank or a
+// counter, scored with the reference cost model and reduced to the first
+// strict minimum (brute_force_schedule, scheduling.py:245-278).
+//
+// Work decomposition: a persistent grid (a multiple of the SM count), each
+// thread owns a contiguous rank range, unranks its first candidate once and
+// then walks the reference's itertools order with O(1)-amortised successor
+// steps.  The winner is reduced warp -> block -> one partial per CTA; a final
+// single-CTA pass merges the partials (deterministic: the key is
+// (makespan, global rank), independent of grid shape and GPU count).
+#include "dm_common.cuh"
+
+namespace dm {
+
+// ----------------------------------------------------------- combinatorics
+// Saturating binomial C(a, b) (int64 max on overflow) — only used when a
+// thread unranks its first candidate.
+__device__ inline int64_t binom_sat(int a, int b) {
+    if (b < 0 || b > a) return 0;
+    if (b > a - b) b = a - b;
+    unsigned __int128 r = 1;
+    for (int i = 1; i <= b; ++i) {
+        r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
+        if (r > (unsigned __int128)INT64_MAX) return INT64_MAX;
+    }
+    return (int64_t)r;
+}
+
+__device__ inline int64_t perm_sat(int p, int r) {
+    unsigned __int128 v = 1;
+    for (int i = 0; i < r; ++i) {
+        v *= (unsigned __int128)(p - i);
+        if (v > (unsigned __int128)INT64_MAX) return INT64_MAX;
+    }
+    return (int64_t)v;
+}
+
+// Lexicographic unrank of combination c of m cut positions from {1..n-1}
+// (itertools.combinations(range(1, n), m) order).
+__device__ inline void unrank_comb(int n, int m, int64_t c, int32_t* cuts) {
+    int lo = 1;
+    for (int q = 0; q < m; ++q) {
+        for (int v = lo; v <= n - 1; ++v) {
+            int64_t cnt = binom_sat((n - 1) - v, m - q - 1);
+            if (c < cnt) { cuts[q] = v; lo = v + 1; break; }
+            c -= cnt;
+        }
+    }
+}
+
+// successor in lexicographic order; false when c was the last combination
+__device__ inline bool next_comb(int n, int m, int32_t* cuts) {
+    for (int q = m - 1; q >= 0; --q) {
+        if (cuts[q] < n - m + q) {
+            int v = cuts[q] + 1;
+            for (int z = q; z < m; ++z) cuts[z] = v + (z - q);
+            return true;
+        }
+    }
+    return false;
+}
+
+// Partial permutations of r workers out of p, itertools.permutations order.
+struct PermSet {  // used-worker bitmap for p <= 1024
+    uint32_t w[32];
+    __device__ void clear(int p) { for (int i = 0; i < ((p + 31) >> 5); ++i) w[i] = 0; }
+    __device__ bool get(int v) const { return (w[v >> 5] >> (v & 31)) & 1u; }
+    __device__ void set(int v) { w[v >> 5] |= 1u << (v & 31); }
+    __device__ void unset(int v) { w[v >> 5] &= ~(1u << (v & 31)); }
+    // smallest free value > v (v = -1 for the smallest), -1 if none
+    __device__ int next_free(int v, int p) const {
+        for (int x = v + 1; x < p; ) {
+            int wi = x >> 5;
+            uint32_t free_bits = ~w[wi] & (0xffffffffu << (x & 31));
+            if (free_bits) {
+                int c = (wi << 5) + __ffs(free_bits) - 1;
+                return c < p ? c : -1;
+            }
+            x = (wi + 1) << 5;
+        }
+        return -1;
+    }
+};
+
+__device__ inline void unrank_perm(int p, int r, int64_t pi, int32_t* out, PermSet& used) {
+    used.clear(p);
+    for (int q = 0; q < r; ++q) {
+        int64_t blk = perm_sat(p - q - 1, r - q - 1);
+        int64_t d = pi / blk;
+        pi -= d * blk;
+        int v = used.next_free(-1, p);
+        while (d-- > 0) v = used.next_free(v, p);
+        out[q] = v;
+        used.set(v);
+    }
+}
+
+__device__ inline bool next_perm(int p, int r, int32_t* a, PermSet& used) {
+    for (int i = r - 1; i >= 0; --i) {
+        used.unset(a[i]);
+        int c = used.next_free(a[i], p);
+        if (c >= 0) {
+            a[i] = c; used.set(c);
+            for (int j = i + 1; j < r; ++j) { int f = used.next_free(-1, p); a[j] = f; used.set(f); }
+            return true;
+        }
+    }
+    return false;
+}
+
+// --------------------------------------------------- contiguous candidate
+// Inner body of brute_force_schedule (scheduling.py:266-270): skip when a run
+// fails _fits; else max over runs of compute + read.
+template <int RMAX>
+__device__ __forceinline__ bool score_contig(const dm_tables& t, int r, const int32_t* bounds,
+                                             const int32_t* peers, double& mk) {
+    for (int q = 0; q < r; ++q)
+        if (!fits_range(t, peers[q], bounds[q], bounds[q + 1])) return false;
+    double best = 0.0;
+    for (int q = 0; q < r; ++q) {
+        double c, rd;
+        int a = bounds[q];
+        if (chain(t)) {
+            int prev = q > 0 ? peers[q - 1] : -1;
+            run_cost_contig(t, a, bounds[q + 1], peers[q], [&](int) { return prev; }, c, rd);
+        } else {
+            BoundsOwner own{bounds, peers, r};
+            run_cost_contig(t, a, bounds[q + 1], peers[q], own, c, rd);
+        }
+        double load = c + rd;
+        if (q == 0 || load > best) best = load;
+    }
+    mk = best;
+    return true;
+}
+
+__device__ __forceinline__ void win_add(Win& w, double mk, int64_t rank) {
+    w.n_feas++;
+    w.csum += (uint64_t)__double_as_longlong(mk);
+    if (w.rank < 0 || mk < w.mk) { w.mk = mk; w.rank = rank; }
+}
+
+// MODE 0: full brute-force order; MODE 1: identity-order splits.
+template <int MODE, int RMAX>
+__global__ void __launch_bounds__(256) enum_kernel(dm_tables t, int64_t k0, int64_t k1,
+                                                   int64_t per_thread, dm_winner* partial) {
+    Win w; win_init(w);
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t kb = k0 + tid * per_thread;
+    int64_t ke = kb + per_thread < k1 ? kb + per_thread : k1;
+    if (kb < ke) {
+        const int n = t.n, p = t.p, rmax = n < p ? n : p;
+        int32_t cuts[RMAX + 1], bounds[RMAX + 2], peers[RMAX + 1];
+        PermSet used;
+        // locate r and the in-block offset of kb
+        int r = 1;
+        int64_t off = kb;
+        for (; r <= rmax; ++r) {
+            int64_t nc = binom_sat(n - 1, r - 1);
+            int64_t np = MODE == 0 ? perm_sat(p, r) : 1;
+            unsigned __int128 blk = (unsigned __int128)nc * (unsigned __int128)np;
+            if ((unsigned __int128)off < blk) break;
+            off -= (int64_t)blk;
+        }
+        int64_t np = MODE == 0 ? perm_sat(p, r) : 1;
+        unrank_comb(n, r - 1, off / np, cuts);
+        if (MODE == 0) unrank_perm(p, r, off % np, peers, used);
+        else for (int q = 0; q < r; ++q) peers[q] = q;
+        for (int64_t k = kb; k < ke; ++k) {
+            bounds[0] = 0;
+            for (int q = 0; q < r - 1; ++q) bounds[q + 1] = cuts[q];
+            bounds[r] = n;
+            double mk;
+            w.n_eval++;
+            if (score_contig<RMAX>(t, r, bounds, peers, mk)) win_add(w, mk, k);
+            // successor in the reference's itertools order
+            if (MODE == 0 && next_perm(p, r, peers, used)) continue;
+            if (next_comb(n, r - 1, cuts)) {
+                if (MODE == 0) { used.clear(p); for (int q = 0; q < r; ++q) { peers[q] = q; used.set(q); } }
+                continue;
+            }
+            ++r;
+            if (r > rmax) break;
+            for (int q = 0; q < r - 1; ++q) cuts[q] = q + 1;
+            used.clear(p);
+            for (int q = 0; q < r; ++q) { peers[q] = q; if (MODE == 0) used.set(q); }
+        }
+    }
+    block_reduce_win_store(w, partial);
+}
+
+// --------------------------------------------------------- random stream
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t rng_word(uint64_t key, int64_t k, int j) {
+    return fmix64(key + fmix64((uint64_t)k * 8ULL + (uint64_t)j + 1ULL));
+}
+
+// Config C5: candidate k is a random contiguous placement (see
+// paper_2309_01172_b200/rng.py).  Runs are walked on the fly from the cut
+// bits, so no per-candidate arrays are needed for chain-structured stages.
+__global__ void __launch_bounds__(256) enum_random_kernel(dm_tables t, const int32_t* __restrict__ online,
+                                                          int32_t n_online, const int32_t* __restrict__ mults,
+                                                          int32_t n_mults, uint64_t key, int64_t k0, int64_t k1,
+                                                          dm_winner* partial) {
+    Win w; win_init(w);
+    const int n = t.n;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1; k += stride) {
+        uint64_t h4 = rng_word(key, k, 6), h5 = rng_word(key, k, 7);
+        int64_t am = mults[h4 % (uint64_t)n_mults];
+        int64_t b0 = (int64_t)(h5 % (uint64_t)n_online);
+        // pass 1: _fits for every run (skip candidate on the first failure)
+        bool ok = true;
+        {
+            int a = 0, q = 0;
+            uint64_t wd = rng_word(key, k, 0);
+            for (int pos = 1; pos <= n && ok; ++pos) {
+                bool cut = pos == n;
+                if (!cut) {
+                    int j = (pos - 1) >> 6, bb = (pos - 1) & 63;
+                    if (bb == 0 && j > 0) wd = rng_word(key, k, j);
+                    cut = (wd >> bb) & 1ULL;
+                }
+                if (cut) {
+                    int pe = online[(b0 + am * q) % n_online];
+                    ok = fits_range(t, pe, a, pos);
+                    a = pos; ++q;
+                }
+            }
+        }
+        w.n_eval++;
+        if (!ok) continue;
+        // pass 2: cost (chain stages: the crossing read of run q comes from run q-1)
+        double best = 0.0;
+        {
+            int a = 0, q = 0, prev = -1;
+            uint64_t wd = rng_word(key, k, 0);
+            for (int pos = 1; pos <= n; ++pos) {
+                bool cut = pos == n;
+                if (!cut) {
+                    int j = (pos - 1) >> 6, bb = (pos - 1) & 63;
+                    if (bb == 0 && j > 0) wd = rng_word(key, k, j);
+                    cut = (wd >> bb) & 1ULL;
+                }
+                if (cut) {
+                    int pe = online[(b0 + am * q) % n_online];
+                    double c, rd;
+                    run_cost_contig(t, a, pos, pe, [&](int) { return prev; }, c, rd);
+                    double load = c + rd;
+                    if (q == 0 || load > best) best = load;
+                    prev = pe; a = pos; ++q;
+                }
+            }
+        }
+        win_add(w, best, k);
+    }
+    block_reduce_win_store(w, partial);
+}
+
+// ------------------------------------------------------------ final merge
+__global__ void finalize_kernel(const dm_winner* partial, int n_parts, dm_winner* out) {
+    Win w; win_init(w);
+    for (int i = threadIdx.x; i < n_parts; i += blockDim.x) {
+        Win o;
+        o.mk = partial[i].makespan; o.rank = partial[i].rank; o.n_eval = partial[i].n_evaluated;
+        o.n_feas = partial[i].n_feasible; o.csum = partial[i].checksum;
+        win_merge(w, o);
+    }
+    __shared__ dm_winner tmp[1];
+    block_reduce_win_store(w, tmp);  // writes tmp[blockIdx.x == 0]
+    __syncthreads();
+    if (threadIdx.x == 0) *out = tmp[0];
+}
+
+}  // namespace dm
+
+// ================================================================== C ABI
+#include "dm_abi_util.cuh"
+
+namespace {
+constexpr int kThreads = 256;
+
+int enum_grid() {
+    static thread_local int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms * 8;  // 8 CTAs x 256 threads per SM resident
+}
+
+template <int MODE>
+int launch_enum(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* out, void* scratch,
+                cudaStream_t s) {
+    int grid = enum_grid();
+    dm_winner* partial = (dm_winner*)scratch;
+    int64_t total_threads = (int64_t)grid * kThreads;
+    int64_t span = k1 > k0 ? k1 - k0 : 0;
+    int64_t per = (span + total_threads - 1) / total_threads;
+    if (per < 1) per = 1;
+    int rmax = t->n < t->p ? t->n : t->p;
+    if (rmax <= 16) dm::enum_kernel<MODE, 16><<<grid, kThreads, 0, s>>>(*t, k0, k1, per, partial);
+    else if (rmax <= 64) dm::enum_kernel<MODE, 64><<<grid, kThreads, 0, s>>>(*t, k0, k1, per, partial);
+    else if (rmax <= 256) dm::enum_kernel<MODE, 256><<<grid, kThreads, 0, s>>>(*t, k0, k1, per, partial);
+    else return dmabi::fail(DM_E_TOO_LARGE, "enumeration supports at most 256 runs");
+    DM_CHECK_LAUNCH();
+    dm::finalize_kernel<<<1, 1024, 0, s>>>(partial, grid, out);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t dm_enum_scratch_bytes(void) { return (int64_t)sizeof(dm_winner) * enum_grid(); }
+
+int dm_enum_bruteforce(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* out,
+                       void* scratch, void* stream) {
+    if (!t || !out || !scratch || t->n <= 0 || t->p <= 0) return dmabi::fail(DM_E_ARG, "bad arguments");
+    if (t->p > 1024) return dmabi::fail(DM_E_TOO_LARGE, "brute force supports at most 1024 workers");
+    return launch_enum<0>(t, k0, k1, out, scratch, (cudaStream_t)stream);
+}
+
+int dm_enum_splits(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* out,
+                   void* scratch, void* stream) {
+    if (!t || !out || !scratch || t->n <= 0 || t->p <= 0) return dmabi::fail(DM_E_ARG, "bad arguments");
+    return launch_enum<1>(t, k0, k1, out, scratch, (cudaStream_t)stream);
+}
+
+int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,
+                   const int32_t* mults, int32_t n_mults, uint64_t seed, int64_t k0, int64_t k1,
+                   dm_winner* out, void* scratch, void* stream) {
+    if (!t || !online || !mults || n_online <= 0 || n_mults <= 0 || !out || !scratch)
+        return dmabi::fail(DM_E_ARG, "bad arguments");
+    if (t->n > n_online) return dmabi::fail(DM_E_ARG, "random placements need n <= online peers");
+    if (t->n > 385) return dmabi::fail(DM_E_TOO_LARGE, "random placements support n <= 385");
+    if (!(t->flags & DM_F_CHAIN) && (t->flags & DM_F_INCLUDE_COMM))
+        return dmabi::fail(DM_E_ARG, "random placements need chain-structured stages");
+    cudaStream_t s = (cudaStream_t)stream;
+    int grid = enum_grid();
+    uint64_t key = dm::fmix64(seed + 0x9E3779B97F4A7C15ULL);
+    dm::enum_random_kernel<<<grid, kThreads, 0, s>>>(*t, online, n_online, mults, n_mults, key, k0, k1,
+                                                     (dm_winner*)scratch);
+    DM_CHECK_LAUNCH();
+    dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, grid, out);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+int dm_finalize_winners(void* scratch, int32_t n_parts, dm_winner* out, void* stream) {
+    if (!scratch || !out || n_parts <= 0) return dmabi::fail(DM_E_ARG, "bad arguments");
+    dm::finalize_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>((dm_winner*)scratch, n_parts, out);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+}  // extern "C"

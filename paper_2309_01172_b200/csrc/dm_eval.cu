@@ -1,0 +1,388 @@
+// dm_eval.cu — candidate scoring.
+//
+//  * eval_runs_kernel: the general evaluate_runs (scheduling.py:210-239) for
+//    arbitrary Runs (overlaps, gaps, repeated or unknown peers), one thread per
+//    candidate, restating verify_assignment (:179-207) and _run_cost (:156-169)
+//    step by step.  Used by the API calls that score a handful of assignments
+//    (evaluate_runs, pinned runs, final reports, backup ranking).
+//  * eval_owner_kernel: Mode A scoring stream.  A CTA stages a tile of owner
+//    vectors through shared memory with 16-byte coalesced loads, then each
+//    thread walks its vector run by run (contiguous fast path); a candidate
+//    whose peer reappears falls back to the grouped general evaluation.
+//  * argmin kernels: block/warp arg-min over (makespan, rank).
+#include "dm_common.cuh"
+#include "dm_abi_util.cuh"
+
+namespace dm {
+
+// ------------------------------------------------------- general evaluate
+// Indices inside each run arrive sorted ascending (the reference only ever
+// uses sorted(indices): verify :191, _evaluate :217); duplicates may remain.
+__device__ inline bool in_run(const int32_t* idx, int k, int s) {
+    int lo = 0, hi = k - 1;
+    while (lo <= hi) {
+        int mid = (lo + hi) >> 1;
+        int v = idx[mid];
+        if (v == s) return true;
+        if (v < s) lo = mid + 1; else hi = mid - 1;
+    }
+    return false;
+}
+
+__device__ inline double col_items(const double* col, const int64_t* pre, bool exact,
+                                   const int32_t* idx, int k) {
+    if (exact) {
+        int64_t s = 0;
+        for (int q = 0; q < k; ++q) s += pre[idx[q] + 1] - pre[idx[q]];
+        return (double)s;
+    }
+    PySum acc;
+    for (int q = 0; q < k; ++q) acc.add(col[idx[q]]);
+    return acc.value();
+}
+
+__global__ void eval_runs_kernel(dm_tables t, int32_t n_cand, const int32_t* __restrict__ cand_ptr,
+                                 const int32_t* __restrict__ run_peer, const int32_t* __restrict__ run_ptr,
+                                 const int32_t* __restrict__ run_idx, double* out_compute, double* out_read,
+                                 double* out_makespan, int32_t* out_code, int32_t* out_code_run,
+                                 int32_t* out_status, int32_t* ws_owner, uint8_t* ws_seen, int32_t* ws_order) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_cand) return;
+    const int n = t.n;
+    int32_t* peer_of = ws_owner + (int64_t)c * n;
+    uint8_t* seen = ws_seen + (int64_t)c * n;
+    int r0 = cand_ptr[c], r1 = cand_ptr[c + 1];
+    bool ex = bytes_exact(t);
+
+    // ---- verify_assignment (:179-207), runs in the given order
+    for (int i = 0; i < n; ++i) { seen[i] = 0; peer_of[i] = -1; }
+    int code = DM_V_OK, bad = -1, n_seen = 0;
+    for (int r = r0; r < r1 && code == DM_V_OK; ++r) {
+        const int32_t* idx = run_idx + run_ptr[r];
+        int k = run_ptr[r + 1] - run_ptr[r];
+        if (!k) continue;
+        int pe = run_peer[r];
+        for (int u = r0; u < r; ++u)
+            if (run_ptr[u + 1] > run_ptr[u] && run_peer[u] == pe) { code = DM_V_TWO_RUNS; break; }
+        if (code) { bad = r - r0; break; }
+        if (pe < 0 || pe >= t.P) { code = DM_V_UNKNOWN_PEER; bad = r - r0; break; }
+        for (int q = 1; q < k; ++q)
+            if (idx[q] != idx[0] + q) { code = DM_V_NOT_CONTIGUOUS; break; }
+        if (code) { bad = r - r0; break; }
+        for (int q = 0; q < k; ++q) {
+            if (seen[idx[q]]) { code = DM_V_ASSIGNED_TWICE; break; }
+            seen[idx[q]] = 1; ++n_seen;
+        }
+        if (code) { bad = r - r0; break; }
+        if (col_items(t.gpu, t.pre_gpu, ex, idx, k) > t.cap_gpu[pe]) code = DM_V_GPU;
+        else if (col_items(t.cpu, t.pre_cpu, ex, idx, k) > t.cap_cpu[pe]) code = DM_V_CPU;
+        else if (col_items(t.disk, t.pre_disk, ex, idx, k) > t.cap_disk[pe]) code = DM_V_DISK;
+        if (code) bad = r - r0;
+    }
+    if (code == DM_V_OK && n_seen != n) code = DM_V_UNASSIGNED;
+    out_code[c] = code;
+    out_code_run[c] = bad;
+
+    // ---- peer_of: last writer in runs order (:213)
+    for (int r = r0; r < r1; ++r)
+        for (int q = run_ptr[r]; q < run_ptr[r + 1]; ++q) peer_of[run_idx[q]] = run_peer[r];
+
+    // ---- ordered_runs: non-empty runs stably sorted by first index (:217-218)
+    int32_t* order = ws_order + r0;
+    int no = 0;
+    for (int r = r0; r < r1; ++r) {
+        out_compute[r] = 0.0; out_read[r] = 0.0;
+        if (run_ptr[r + 1] == run_ptr[r]) continue;
+        int fr = run_idx[run_ptr[r]];
+        int pos = no++;
+        while (pos > 0 && run_idx[run_ptr[order[pos - 1]]] > fr) { order[pos] = order[pos - 1]; --pos; }
+        order[pos] = r;
+    }
+
+    // ---- cost every run in that order (:219-222)
+    double makespan = 0.0;
+    int status = DM_OK;
+    for (int o = 0; o < no; ++o) {
+        int r = order[o];
+        const int32_t* idx = run_idx + run_ptr[r];
+        int k = run_ptr[r + 1] - run_ptr[r];
+        int pe = run_peer[r];
+        if (pe < 0 || pe >= t.P) { status = DM_E_UNKNOWN_PEER; break; }  // fleet.peer :158
+        double fl = col_items(t.flops, t.pre_flops, flops_exact(t), idx, k);
+        double compute = fl / t.speed[pe];
+        double rd = 0.0;
+        if (include_comm(t)) {
+            for (int q = 0; q < k && status == DM_OK; ++q) {
+                int i = idx[q];
+                for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e) {
+                    int src = t.edge_src[e];
+                    if (in_run(idx, k, src)) continue;
+                    int own = peer_of[src];
+                    if (own == -1) { status = DM_E_UNASSIGNED; break; }
+                    double al, be;
+                    link_of(t, own, pe, al, be);
+                    rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
+                }
+            }
+            if (status != DM_OK) break;
+        }
+        out_compute[r] = compute;
+        out_read[r] = rd;
+        double load = compute + rd;
+        if (load > makespan) makespan = load;
+    }
+    out_makespan[c] = makespan;
+    out_status[c] = status;
+}
+
+// ------------------------------------------------------------ Mode A stream
+constexpr int kTile = 128;          // candidates per CTA tile (= threads)
+
+template <typename OT>
+__device__ __forceinline__ int owner_at(const OT* row, int i) { return (int)row[i]; }
+
+// Grouped general evaluation of one owner vector (non-contiguous case):
+// Runs = stages of each peer in first-appearance order (verify order), each
+// costed over its sorted indices with peer_of = the owner vector.
+template <typename OT>
+__device__ void eval_owner_grouped(const dm_tables& t, const OT* row, double& mk_out, int& code_out) {
+    const int n = t.n;
+    bool ex = bytes_exact(t), fex = flops_exact(t);
+    int code = DM_V_OK;
+    double mk = 0.0;
+    for (int i0 = 0; i0 < n; ++i0) {
+        int pe = owner_at(row, i0);
+        bool first = true;
+        for (int z = 0; z < i0; ++z) if (owner_at(row, z) == pe) { first = false; break; }
+        if (!first) continue;
+        // stages of pe, ascending; contiguity, capacities (verify :191-203)
+        int last = -1, k = 0;
+        bool contig = true;
+        int64_t sg = 0, sc = 0, sd = 0, sf = 0;
+        PySum pg, pc, pd, pf;
+        for (int i = i0; i < n; ++i) {
+            if (owner_at(row, i) != pe) continue;
+            if (last >= 0 && i != last + 1) contig = false;
+            last = i; ++k;
+            if (ex) { sg += t.pre_gpu[i + 1] - t.pre_gpu[i]; sc += t.pre_cpu[i + 1] - t.pre_cpu[i];
+                      sd += t.pre_disk[i + 1] - t.pre_disk[i]; }
+            else { pg.add(t.gpu[i]); pc.add(t.cpu[i]); pd.add(t.disk[i]); }
+            if (fex) sf += t.pre_flops[i + 1] - t.pre_flops[i]; else pf.add(t.flops[i]);
+        }
+        if (code == DM_V_OK) {
+            if (!contig) code = DM_V_NOT_CONTIGUOUS;
+            else if ((ex ? (double)sg : pg.value()) > t.cap_gpu[pe]) code = DM_V_GPU;
+            else if ((ex ? (double)sc : pc.value()) > t.cap_cpu[pe]) code = DM_V_CPU;
+            else if ((ex ? (double)sd : pd.value()) > t.cap_disk[pe]) code = DM_V_DISK;
+        }
+        double compute = (fex ? (double)sf : pf.value()) / t.speed[pe];
+        double rd = 0.0;
+        if (include_comm(t)) {
+            for (int i = i0; i < n; ++i) {
+                if (owner_at(row, i) != pe) continue;
+                for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e) {
+                    int src = t.edge_src[e];
+                    int own = owner_at(row, src);
+                    if (own == pe) continue;  // src inside this peer's run
+                    double al, be;
+                    link_of(t, own, pe, al, be);
+                    rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
+                }
+            }
+        }
+        double load = compute + rd;
+        if (load > mk) mk = load;
+    }
+    mk_out = mk;
+    code_out = code;
+}
+
+template <typename OT>
+__global__ void __launch_bounds__(kTile) eval_owner_kernel(dm_tables t, int64_t n_cand,
+                                                           const OT* __restrict__ owner,
+                                                           double* __restrict__ out_mk,
+                                                           uint8_t* __restrict__ out_code) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = t.n;
+    OT* tile = reinterpret_cast<OT*>(smem);
+    uint32_t* seen = reinterpret_cast<uint32_t*>(smem + (((size_t)kTile * n * sizeof(OT) + 15) & ~(size_t)15));
+    const int seen_words = (t.P + 31) >> 5;
+    const int64_t n_tiles = (n_cand + kTile - 1) / kTile;
+    for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x) {
+        int64_t c0 = tl * kTile;
+        int cnt = (int)((n_cand - c0) < kTile ? (n_cand - c0) : kTile);
+        // ---- stage the tile: 16-byte loads when the tile is 16-byte aligned
+        size_t bytes = (size_t)cnt * n * sizeof(OT);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(owner + c0 * n);
+        __syncthreads();
+        if ((((uintptr_t)src) & 15) == 0) {
+            size_t nv = bytes >> 4;
+            for (size_t v = threadIdx.x; v < nv; v += blockDim.x)
+                reinterpret_cast<uint4*>(smem)[v] = __ldcs(reinterpret_cast<const uint4*>(src) + v);
+            for (size_t b = (nv << 4) + threadIdx.x; b < bytes; b += blockDim.x) smem[b] = src[b];
+        } else {
+            for (size_t b = threadIdx.x; b < bytes; b += blockDim.x) smem[b] = src[b];
+        }
+        __syncthreads();
+        if (threadIdx.x >= cnt) continue;
+        const OT* row = tile + (size_t)threadIdx.x * n;
+        // ---- contiguous fast path
+        for (int w = 0; w < seen_words; ++w) seen[w * kTile + threadIdx.x] = 0u;
+        bool unknown = false, grouped = false;
+        int code = DM_V_OK;
+        double mk = 0.0;
+        int a = 0, pe = owner_at(row, 0), prev = -1;
+        for (int i = 1; i <= n; ++i) {
+            int o = i < n ? owner_at(row, i) : -2;
+            if (o == pe) continue;
+            // run [a, i) on pe
+            if (pe >= t.P) { unknown = true; break; }
+            uint32_t& sw = seen[(pe >> 5) * kTile + threadIdx.x];
+            uint32_t bit = 1u << (pe & 31);
+            if (sw & bit) { grouped = true; break; }
+            sw |= bit;
+            if (code == DM_V_OK) code = cap_violation(t, pe, a, i);
+            double c, rd;
+            if (chain(t)) {
+                run_cost_contig(t, a, i, pe, [&](int) { return prev; }, c, rd);
+            } else {
+                run_cost_contig(t, a, i, pe, [&](int s) { return owner_at(row, s); }, c, rd);
+            }
+            double load = c + rd;
+            if (load > mk) mk = load;
+            prev = pe; pe = o; a = i;
+        }
+        if (!unknown && grouped) {
+            for (int i = 0; i < n; ++i) if (owner_at(row, i) >= t.P) { unknown = true; break; }
+            if (!unknown) eval_owner_grouped(t, row, mk, code);
+        }
+        int64_t c = c0 + threadIdx.x;
+        out_mk[c] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
+        out_code[c] = unknown ? (uint8_t)0xFF : (uint8_t)code;
+    }
+}
+
+// ---------------------------------------------------------------- arg-min
+__global__ void __launch_bounds__(256) argmin_kernel(const double* __restrict__ mk, const uint8_t* __restrict__ code,
+                                                     int64_t n, int64_t rank_base, dm_winner* partial) {
+    Win w; win_init(w);
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        w.n_eval++;
+        if (code[i] != 0) continue;
+        double v = mk[i];
+        w.n_feas++;
+        w.csum += (uint64_t)__double_as_longlong(v);
+        if (win_better(v, rank_base + i, w.mk, w.rank)) { w.mk = v; w.rank = rank_base + i; }
+    }
+    block_reduce_win_store(w, partial);
+}
+
+__global__ void finalize_argmin_kernel(const dm_winner* partial, int n_parts, dm_winner* out) {
+    Win w; win_init(w);
+    for (int i = threadIdx.x; i < n_parts; i += blockDim.x) {
+        Win o;
+        o.mk = partial[i].makespan; o.rank = partial[i].rank; o.n_eval = partial[i].n_evaluated;
+        o.n_feas = partial[i].n_feasible; o.csum = partial[i].checksum;
+        win_merge(w, o);
+    }
+    __shared__ dm_winner tmp[1];
+    block_reduce_win_store(w, tmp);
+    __syncthreads();
+    if (threadIdx.x == 0) *out = tmp[0];
+}
+
+}  // namespace dm
+
+namespace {
+int sm_count() {
+    static thread_local int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+}  // namespace
+
+extern "C" {
+
+int dm_abi_version(void) { return DM_ABI_VERSION; }
+const char* dm_last_error(void) { return dmabi::last_error_buf(); }
+
+int dm_eval_runs(const dm_tables* t, int32_t n_cand, const int32_t* cand_ptr, const int32_t* run_peer,
+                 const int32_t* run_ptr, const int32_t* run_idx, double* out_compute, double* out_read,
+                 double* out_makespan, int32_t* out_code, int32_t* out_code_run, int32_t* out_status,
+                 void* stream) {
+    if (!t || n_cand < 0 || !cand_ptr || !run_peer || !run_ptr || t->n <= 0)
+        return dmabi::fail(DM_E_ARG, "dm_eval_runs: bad arguments");
+    if (n_cand == 0) return DM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    // per-candidate workspace: peer_of (int32 x n), seen (u8 x n), run order
+    int32_t n_runs_total = 0;
+    DM_CUDA(cudaMemcpyAsync(&n_runs_total, cand_ptr + n_cand, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    DM_CUDA(cudaStreamSynchronize(s));
+    size_t b_owner = (size_t)n_cand * t->n * sizeof(int32_t);
+    size_t b_seen = ((size_t)n_cand * t->n + 15) & ~(size_t)15;
+    size_t b_order = (size_t)(n_runs_total + 1) * sizeof(int32_t);
+    void* ws = nullptr;
+    DM_CUDA(cudaMallocAsync(&ws, b_owner + b_seen + b_order, s));
+    int32_t* ws_owner = (int32_t*)ws;
+    uint8_t* ws_seen = (uint8_t*)ws + b_owner;
+    int32_t* ws_order = (int32_t*)((uint8_t*)ws + b_owner + b_seen);
+    int threads = 128, blocks = (n_cand + threads - 1) / threads;
+    dm::eval_runs_kernel<<<blocks, threads, 0, s>>>(*t, n_cand, cand_ptr, run_peer, run_ptr, run_idx, out_compute,
+                                                    out_read, out_makespan, out_code, out_code_run, out_status,
+                                                    ws_owner, ws_seen, ws_order);
+    cudaError_t le = cudaGetLastError();
+    cudaFreeAsync(ws, s);
+    if (le != cudaSuccess) return dmabi::cuda_fail(le, "eval_runs_kernel");
+    return DM_OK;
+}
+
+int dm_eval_owner(const dm_tables* t, int64_t n_cand, const void* owner, int32_t owner_bytes,
+                  double* out_makespan, uint8_t* out_code, void* stream) {
+    if (!t || n_cand < 0 || !owner || !out_makespan || !out_code || t->n <= 0 ||
+        (owner_bytes != 1 && owner_bytes != 2))
+        return dmabi::fail(DM_E_ARG, "dm_eval_owner: bad arguments");
+    if (owner_bytes == 1 && t->P > 256) return dmabi::fail(DM_E_ARG, "uint8 owners need P <= 256");
+    if (n_cand == 0) return DM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t tile_bytes = (((size_t)dm::kTile * t->n * owner_bytes) + 15) & ~(size_t)15;
+    size_t seen_bytes = (size_t)((t->P + 31) / 32) * dm::kTile * sizeof(uint32_t);
+    size_t smem = tile_bytes + seen_bytes;
+    if (smem > 200 * 1024) return dmabi::fail(DM_E_TOO_LARGE, "dm_eval_owner: tile exceeds shared memory");
+    int64_t n_tiles = (n_cand + dm::kTile - 1) / dm::kTile;
+    int per_sm = (int)((220 * 1024) / (smem + 1024));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 16) per_sm = 16;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > n_tiles) grid = n_tiles;
+    if (owner_bytes == 1) {
+        cudaFuncSetAttribute(dm::eval_owner_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        dm::eval_owner_kernel<uint8_t><<<(int)grid, dm::kTile, smem, s>>>(*t, n_cand, (const uint8_t*)owner,
+                                                                           out_makespan, out_code);
+    } else {
+        cudaFuncSetAttribute(dm::eval_owner_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        dm::eval_owner_kernel<uint16_t><<<(int)grid, dm::kTile, smem, s>>>(*t, n_cand, (const uint16_t*)owner,
+                                                                            out_makespan, out_code);
+    }
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+int dm_argmin_scores(const double* makespan, const uint8_t* code, int64_t n, int64_t rank_base, dm_winner* out,
+                     void* scratch, void* stream) {
+    if (!makespan || !code || !out || !scratch || n < 0) return dmabi::fail(DM_E_ARG, "dm_argmin_scores: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    int grid = sm_count() * 8;
+    dm::argmin_kernel<<<grid, 256, 0, s>>>(makespan, code, n, rank_base, (dm_winner*)scratch);
+    DM_CHECK_LAUNCH();
+    dm::finalize_argmin_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, grid, out);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+}  // extern "C"

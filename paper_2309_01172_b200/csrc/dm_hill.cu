@@ -1,0 +1,252 @@
+// dm_hill.cu — batched proportional split + boundary hill climb, and the
+// pipeline epilogue.  One warp per scenario:
+//   * _proportional_runs (scheduling.py:328-351) runs on lane 0 (O(n + p),
+//     order-sensitive sums restated exactly);
+//   * _hill_climb (:354-388) keeps the reference's sequential first-improvement
+//     walk (uniform control flow across the warp) and parallelises each
+//     score() (:357-362) over runs: lanes cost runs, a warp max-reduce
+//     combines them;
+//   * the epilogue scores the final runs (_evaluate :210-232) and applies
+//     Eq. 3 / Eq. 4 (pipeline.py:41-62).
+#include "dm_common.cuh"
+#include "dm_abi_util.cuh"
+
+namespace dm {
+
+constexpr int kWarpsPerCta = 4;
+
+__device__ __forceinline__ double warp_max(double v) {
+    for (int off = 16; off > 0; off >>= 1) {
+        double o = __shfl_xor_sync(0xffffffffu, v, off);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+
+// score() of _hill_climb over contiguous runs bounds[0..r] / peers[0..r)
+// held in shared memory: inf if verify_assignment fails (only capacities can
+// fail for these runs), else max over runs of compute + read.
+__device__ double hill_score(const dm_tables& t, int r, const int32_t* bounds, const int32_t* peers, int lane) {
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    bool bad = false;
+    double best = 0.0;
+    for (int q = lane; q < r; q += 32) {
+        int a = bounds[q], b = bounds[q + 1], w = peers[q];
+        if (cap_violation(t, w, a, b)) { bad = true; continue; }
+        double c, rd;
+        if (chain(t)) {
+            int prev = q > 0 ? peers[q - 1] : -1;
+            run_cost_contig(t, a, b, w, [&](int) { return prev; }, c, rd);
+        } else {
+            BoundsOwner own{bounds, peers, r};
+            run_cost_contig(t, a, b, w, own, c, rd);
+        }
+        double load = c + rd;
+        best = load > best ? load : best;
+    }
+    if (__any_sync(0xffffffffu, bad)) return inf;
+    return warp_max(best);
+}
+
+// _proportional_runs on lane 0; returns r and fills bounds/peers.
+__device__ int proportional(const dm_tables& t, int32_t* bounds, int32_t* peers) {
+    const int n = t.n, p = t.p;
+    PySum ts;
+    for (int w = 0; w < p; ++w) ts.add(t.speed[w]);
+    double total_speed = ts.value();                                     // :332
+    double total_flops = col_range(t.flops, t.pre_flops, flops_exact(t), 0, n);  // :333
+    if (total_flops == 0.0) total_flops = 1.0;
+    int start = 0, nr = 0;
+    double acc = 0.0, pf = t.flops[0];   // pf = prefix[end-1] (itertools.accumulate :334)
+    int pf_at = 0;
+    bounds[0] = 0;
+    for (int wi = 0; wi < p; ++wi) {                                     // :337
+        if (start >= n) break;
+        int end;
+        if (wi == p - 1) end = n;
+        else {
+            acc = acc + (total_flops * t.speed[wi]) / total_speed;        // :343
+            end = start + 1;
+            while (true) {                                               // :345-346
+                if (end >= n) break;
+                while (pf_at < end - 1) { ++pf_at; pf = pf + t.flops[pf_at]; }
+                if (!(pf < acc)) break;
+                ++end;
+            }
+            int remaining = p - wi - 1;
+            int lim = n - remaining;
+            end = end < lim ? end : lim;
+            end = end > start + 1 ? end : start + 1;                     // :348
+        }
+        peers[nr] = wi;
+        bounds[++nr] = end;
+        start = end;
+    }
+    return nr;
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
+        const dm_tables* __restrict__ tables, int32_t n_scen, int32_t n_max, const int16_t* __restrict__ init_owner,
+        const uint8_t* __restrict__ do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves) {
+    extern __shared__ int32_t sh[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    int32_t* bounds = sh + (size_t)wl * 2 * (n_max + 2);
+    int32_t* peers = bounds + (n_max + 2);
+    const int gw = blockIdx.x * kWarpsPerCta + wl, nw = gridDim.x * kWarpsPerCta;
+    for (int sc = gw; sc < n_scen; sc += nw) {
+        const dm_tables t = tables[sc];
+        const int n = t.n;
+        __syncwarp();
+        int r = 0;
+        if (lane == 0) {
+            if (init_owner) {
+                const int16_t* o = init_owner + (size_t)sc * n_max;
+                bounds[0] = 0; peers[0] = o[0];
+                for (int i = 1; i < n; ++i) if (o[i] != o[i - 1]) { bounds[++r] = i; peers[r] = o[i]; }
+                bounds[++r] = n;
+            } else {
+                r = proportional(t, bounds, peers);
+            }
+        }
+        r = __shfl_sync(0xffffffffu, r, 0);
+        __syncwarp();
+        double cur = hill_score(t, r, bounds, peers, lane);               // :365
+        int moves = 0;
+        if (!do_hill || do_hill[sc]) {
+            for (int round = 0; round < 200; ++round) {                   // :366
+                bool improved = false;
+                for (int a = 0; a + 1 < r; ++a) {                         // :368-369
+                    for (int dir = 0; dir < 2; ++dir) {                   // :370
+                        int la = bounds[a + 1] - bounds[a], lb = bounds[a + 2] - bounds[a + 1];
+                        int nb;
+                        if (dir == 0 && la > 1) nb = bounds[a + 1] - 1;   // :373-374
+                        else if (dir == 1 && lb > 1) nb = bounds[a + 1] + 1;  // :375-376
+                        else continue;
+                        int old = bounds[a + 1];
+                        __syncwarp();
+                        if (lane == 0) bounds[a + 1] = nb;
+                        __syncwarp();
+                        double cs = hill_score(t, r, bounds, peers, lane);
+                        if (cs < cur - 1e-15) { cur = cs; improved = true; ++moves; }  // :383-385
+                        else {
+                            __syncwarp();
+                            if (lane == 0) bounds[a + 1] = old;
+                            __syncwarp();
+                        }
+                    }
+                }
+                if (!improved) break;                                     // :386-387
+            }
+        }
+        __syncwarp();
+        int16_t* o = out_owner + (size_t)sc * n_max;
+        for (int q = 0; q < r; ++q)
+            for (int i = bounds[q] + lane; i < bounds[q + 1]; i += 32) o[i] = (int16_t)peers[q];
+        for (int i = n + lane; i < n_max; i += 32) o[i] = -1;
+        if (lane == 0) { out_score[sc] = cur; if (out_moves) out_moves[sc] = moves; }
+    }
+}
+
+// ------------------------------------------------------------- epilogue
+__global__ void __launch_bounds__(32 * kWarpsPerCta) epilogue_kernel(
+        const dm_tables* __restrict__ tables, int32_t n_scen, int32_t n_max, const int16_t* __restrict__ owner,
+        int64_t n_batches, int64_t spb, double* out) {
+    extern __shared__ int32_t sh[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    int32_t* bounds = sh + (size_t)wl * 2 * (n_max + 2);
+    int32_t* peers = bounds + (n_max + 2);
+    double* loads = reinterpret_cast<double*>(sh + (size_t)kWarpsPerCta * 2 * (n_max + 2)) + (size_t)wl * (n_max + 1);
+    const int gw = blockIdx.x * kWarpsPerCta + wl, nw = gridDim.x * kWarpsPerCta;
+    for (int sc = gw; sc < n_scen; sc += nw) {
+        const dm_tables t = tables[sc];
+        const int n = t.n;
+        const int16_t* o = owner + (size_t)sc * n_max;
+        __syncwarp();
+        int r = 0;
+        if (lane == 0) {
+            bounds[0] = 0; peers[0] = o[0];
+            for (int i = 1; i < n; ++i) if (o[i] != o[i - 1]) { bounds[++r] = i; peers[r] = o[i]; }
+            bounds[++r] = n;
+        }
+        r = __shfl_sync(0xffffffffu, r, 0);
+        __syncwarp();
+        int first_bad = 0x7fffffff, bad_code = 0;
+        double mk = 0.0, bn = 0.0;
+        for (int q = lane; q < r; q += 32) {
+            int a = bounds[q], b = bounds[q + 1], w = peers[q];
+            int v = cap_violation(t, w, a, b);
+            if (v && q < first_bad) { first_bad = q; bad_code = v; }
+            double c, rd;
+            int prev = q > 0 ? peers[q - 1] : -1;
+            if (chain(t)) run_cost_contig(t, a, b, w, [&](int) { return prev; }, c, rd);
+            else { BoundsOwner own{bounds, peers, r}; run_cost_contig(t, a, b, w, own, c, rd); }
+            double load = c + rd;
+            loads[q] = load;
+            mk = load > mk ? load : mk;
+            double m = c >= rd ? c : rd;          // max(p.compute_s, p.read_s) pipeline.py:50
+            bn = m > bn ? m : bn;
+        }
+        mk = warp_max(mk);
+        bn = warp_max(bn);
+        for (int off = 16; off > 0; off >>= 1) {
+            int of = __shfl_xor_sync(0xffffffffu, first_bad, off);
+            int oc = __shfl_xor_sync(0xffffffffu, bad_code, off);
+            if (of < first_bad) { first_bad = of; bad_code = oc; }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            PySum lat;                                 // fp_latency, builtin sum :43
+            for (int q = 0; q < r; ++q) lat.add(loads[q]);
+            double latency = lat.value();
+            double fill = (double)(n_batches - 1) * bn;   // (n_b - 1) * bottleneck :56
+            double pipe = latency + fill;
+            double thr = (double)(n_batches * spb) / pipe; // :62
+            double* ob = out + (size_t)sc * 6;
+            ob[0] = mk; ob[1] = latency; ob[2] = bn; ob[3] = pipe; ob[4] = thr; ob[5] = (double)bad_code;
+        }
+    }
+}
+
+}  // namespace dm
+
+namespace {
+int hill_grid(int32_t n_scen) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t g = (int64_t)sms * 16;
+    int64_t need = (n_scen + dm::kWarpsPerCta - 1) / dm::kWarpsPerCta;
+    return (int)(g < need ? g : need);
+}
+}  // namespace
+
+extern "C" {
+
+int dm_prop_hill(const dm_tables* tables, int32_t n_scen, int32_t n_max, const int16_t* init_owner,
+                 const uint8_t* do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves, void* stream) {
+    if (!tables || n_scen < 0 || n_max <= 0 || !out_owner || !out_score) return dmabi::fail(DM_E_ARG, "dm_prop_hill: bad arguments");
+    if (n_scen == 0) return DM_OK;
+    size_t smem = (size_t)dm::kWarpsPerCta * 2 * (n_max + 2) * sizeof(int32_t);
+    if (smem > 200 * 1024) return dmabi::fail(DM_E_TOO_LARGE, "dm_prop_hill: too many stages");
+    cudaFuncSetAttribute(dm::prop_hill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dm::prop_hill_kernel<<<hill_grid(n_scen), 32 * dm::kWarpsPerCta, smem, (cudaStream_t)stream>>>(
+        tables, n_scen, n_max, init_owner, do_hill, out_owner, out_score, out_moves);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+int dm_pipeline_epilogue(const dm_tables* tables, int32_t n_scen, int32_t n_max, const int16_t* owner,
+                         int64_t n_batches, int64_t samples_per_batch, double* out, void* stream) {
+    if (!tables || n_scen < 0 || n_max <= 0 || !owner || !out) return dmabi::fail(DM_E_ARG, "dm_pipeline_epilogue: bad arguments");
+    if (n_scen == 0) return DM_OK;
+    size_t smem = (size_t)dm::kWarpsPerCta * 2 * (n_max + 2) * sizeof(int32_t) +
+                  (size_t)dm::kWarpsPerCta * (n_max + 1) * sizeof(double) + 16;
+    if (smem > 200 * 1024) return dmabi::fail(DM_E_TOO_LARGE, "dm_pipeline_epilogue: too many stages");
+    cudaFuncSetAttribute(dm::epilogue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dm::epilogue_kernel<<<hill_grid(n_scen), 32 * dm::kWarpsPerCta, smem, (cudaStream_t)stream>>>(
+        tables, n_scen, n_max, owner, n_batches, samples_per_batch, out);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+"""Thin Python front of the C ABI: device buffers, stream handling, result
+read-back.  Every function here launches CUDA work through
+``libdagmesh_b200.so``; nothing computes cost-model values on the host."""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib
+from .tensorize import DeviceBatch, HostTables, build_host
+
+_WINNER_BYTES = C.sizeof(_lib.DmWinner)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def device_batch(hosts, device=None) -> DeviceBatch:
+    _lib.load()
+    torch = _torch()
+    return DeviceBatch(hosts, device=device or torch.device("cuda", torch.cuda.current_device()))
+
+
+# ------------------------------------------------------------ evaluate_runs
+def eval_runs(hosts_or_batch, runs_per_cand, *, index: int = 0):
+    """Score candidate Runs of ONE instance with dm_eval_runs.
+
+    runs_per_cand: list (one per candidate) of lists of (peer_index, sorted
+    tuple of stage indices).  Returns dict of numpy arrays."""
+    lib = _lib.load()
+    torch = _torch()
+    batch = hosts_or_batch if isinstance(hosts_or_batch, DeviceBatch) else device_batch([hosts_or_batch])
+    n_cand = len(runs_per_cand)
+    cand_ptr = [0]
+    run_peer, run_ptr, run_idx = [], [0], []
+    for runs in runs_per_cand:
+        for pe, idxs in runs:
+            run_peer.append(pe)
+            run_idx.extend(idxs)
+            run_ptr.append(len(run_idx))
+        cand_ptr.append(len(run_peer))
+    R = len(run_peer)
+    ints = np.concatenate([np.array(cand_ptr, np.int32), np.array(run_peer or [0], np.int32),
+                           np.array(run_ptr, np.int32), np.array(run_idx or [0], np.int32)])
+    dev = batch.dev_buf.device
+    ints_d = torch.from_numpy(ints).pin_memory().to(dev, non_blocking=True)
+    o1 = len(cand_ptr)
+    o2 = o1 + max(R, 1)
+    o3 = o2 + len(run_ptr)
+    out_f = torch.empty(2 * max(R, 1) + n_cand, dtype=torch.float64, device=dev)
+    out_i = torch.empty(3 * n_cand, dtype=torch.int32, device=dev)
+    base = ints_d.data_ptr()
+    st = batch.struct(index)
+    s = _lib.stream_ptr()
+    _lib.check(lib.dm_eval_runs(C.byref(st), n_cand, base, base + 4 * o1, base + 4 * o2, base + 4 * o3,
+                                out_f.data_ptr(), out_f.data_ptr() + 8 * max(R, 1),
+                                out_f.data_ptr() + 16 * max(R, 1), out_i.data_ptr(),
+                                out_i.data_ptr() + 4 * n_cand, out_i.data_ptr() + 8 * n_cand, s))
+    f = out_f.cpu().numpy()
+    i = out_i.cpu().numpy()
+    return dict(compute=f[:R], read=f[max(R, 1): max(R, 1) + R], makespan=f[2 * max(R, 1):],
+                code=i[:n_cand], code_run=i[n_cand: 2 * n_cand], status=i[2 * n_cand:],
+                cand_ptr=np.array(cand_ptr))
+
+
+# ---------------------------------------------------------------- scoring
+def eval_owner(batch: DeviceBatch, owner, index: int = 0):
+    """Mode A: score a device tensor of owner vectors [n_cand, n] (uint8/int16)."""
+    lib = _lib.load()
+    torch = _torch()
+    n_cand = owner.shape[0]
+    ob = owner.element_size()
+    mk = torch.empty(n_cand, dtype=torch.float64, device=owner.device)
+    code = torch.empty(n_cand, dtype=torch.uint8, device=owner.device)
+    st = batch.struct(index)
+    _lib.check(lib.dm_eval_owner(C.byref(st), n_cand, owner.data_ptr(), ob, mk.data_ptr(), code.data_ptr(),
+                                 _lib.stream_ptr()))
+    return mk, code
+
+
+class WinnerBuffers:
+    """Device scratch + one device dm_winner record for enumeration calls."""
+
+    def __init__(self, device):
+        lib = _lib.load()
+        torch = _torch()
+        self.scratch = torch.empty(int(lib.dm_enum_scratch_bytes()) + 256, dtype=torch.uint8, device=device)
+        self.out = torch.empty(_WINNER_BYTES, dtype=torch.uint8, device=device)
+
+    def read(self) -> dict:
+        raw = self.out.cpu().numpy().tobytes()
+        w = _lib.DmWinner.from_buffer_copy(raw)
+        return dict(makespan=w.makespan, rank=w.rank, n_evaluated=w.n_evaluated,
+                    n_feasible=w.n_feasible, checksum=w.checksum)
+
+
+def argmin_scores(mk, code, rank_base: int = 0, bufs: WinnerBuffers | None = None):
+    lib = _lib.load()
+    bufs = bufs or WinnerBuffers(mk.device)
+    _lib.check(lib.dm_argmin_scores(mk.data_ptr(), code.data_ptr(), mk.numel(), rank_base,
+                                    bufs.out.data_ptr(), bufs.scratch.data_ptr(), _lib.stream_ptr()))
+    return bufs
+
+
+def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | None = None,
+         index: int = 0, online=None, mults=None, seed: int = 0):
+    """Mode B enumeration: 'bruteforce' | 'splits' | 'random'. Returns bufs
+    (call bufs.read() to synchronise and fetch the winner)."""
+    lib = _lib.load()
+    bufs = bufs or WinnerBuffers(batch.dev_buf.device)
+    st = batch.struct(index)
+    s = _lib.stream_ptr()
+    if mode == "bruteforce":
+        _lib.check(lib.dm_enum_bruteforce(C.byref(st), k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
+    elif mode == "splits":
+        _lib.check(lib.dm_enum_splits(C.byref(st), k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
+    elif mode == "random":
+        _lib.check(lib.dm_enum_random(C.byref(st), online.data_ptr(), online.numel(), mults.data_ptr(),
+                                      mults.numel(), seed & 0xFFFFFFFFFFFFFFFF, k0, k1, bufs.out.data_ptr(),
+                                      bufs.scratch.data_ptr(), s))
+    else:
+        raise ValueError(mode)
+    return bufs
+
+
+# ------------------------------------------------------------ partitioners
+def subset_dp(batch: DeviceBatch, n_max: int, p_max: int):
+    """Batched _subset_dp over every instance of the batch."""
+    lib = _lib.load()
+    torch = _torch()
+    dev = batch.dev_buf.device
+    ns = len(batch.hosts)
+    owner = torch.empty((ns, n_max), dtype=torch.int16, device=dev)
+    mk = torch.empty(ns, dtype=torch.float64, device=dev)
+    found = torch.empty(ns, dtype=torch.int32, device=dev)
+    sb = int(lib.dm_subset_dp_scratch_bytes(n_max, p_max, ns))
+    if sb < 0:
+        raise _lib.EngineError(_lib.DM_E_TOO_LARGE, "subset DP instance too large")
+    scratch = torch.empty(max(sb, 256), dtype=torch.uint8, device=dev)
+    _lib.check(lib.dm_subset_dp(batch.struct_ptr(), ns, n_max, p_max, owner.data_ptr(), mk.data_ptr(),
+                                found.data_ptr(), scratch.data_ptr(), _lib.stream_ptr()))
+    return owner, mk, found, scratch
+
+
+def prop_hill(batch: DeviceBatch, n_max: int, init_owner=None, do_hill=None):
+    lib = _lib.load()
+    torch = _torch()
+    dev = batch.dev_buf.device
+    ns = len(batch.hosts)
+    owner = torch.empty((ns, n_max), dtype=torch.int16, device=dev)
+    score = torch.empty(ns, dtype=torch.float64, device=dev)
+    moves = torch.empty(ns, dtype=torch.int32, device=dev)
+    _lib.check(lib.dm_prop_hill(batch.struct_ptr(), ns, n_max, _lib.ptr(init_owner), _lib.ptr(do_hill),
+                                owner.data_ptr(), score.data_ptr(), moves.data_ptr(), _lib.stream_ptr()))
+    return owner, score, moves
+
+
+def epilogue(batch: DeviceBatch, n_max: int, owner, n_batches: int, samples_per_batch: int):
+    lib = _lib.load()
+    torch = _torch()
+    ns = len(batch.hosts)
+    out = torch.empty((ns, 6), dtype=torch.float64, device=batch.dev_buf.device)
+    _lib.check(lib.dm_pipeline_epilogue(batch.struct_ptr(), ns, n_max, owner.data_ptr(), int(n_batches),
+                                        int(samples_per_batch), out.data_ptr(), _lib.stream_ptr()))
+    return out
+
+
+# ------------------------------------------------------------- rank codecs
+def bruteforce_total(n: int, p: int) -> int:
+    return sum(math.comb(n - 1, r - 1) * math.perm(p, r) for r in range(1, min(n, p) + 1))
+
+
+def splits_total(n: int, p: int) -> int:
+    return sum(math.comb(n - 1, r - 1) for r in range(1, min(n, p) + 1))
+
+
+def unrank(n: int, p: int, k: int, mode: str):
+    """Global rank -> (bounds, worker indices) in the reference's itertools
+    order (scheduling.py:260-264); mode 'bruteforce' or 'splits'."""
+    for r in range(1, min(n, p) + 1):
+        npm = math.perm(p, r) if mode == "bruteforce" else 1
+        blk = math.comb(n - 1, r - 1) * npm
+        if k >= blk:
+            k -= blk
+            continue
+        c, pi = divmod(k, npm)
+        cuts, lo, m = [], 1, r - 1
+        for q in range(m):
+            for v in range(lo, n):
+                cnt = math.comb(n - 1 - v, m - q - 1)
+                if c < cnt:
+                    cuts.append(v)
+                    lo = v + 1
+                    break
+                c -= cnt
+        if mode == "bruteforce":
+            free = list(range(p))
+            peers = []
+            for q in range(r):
+                blkp = math.perm(p - q - 1, r - q - 1)
+                d, pi = divmod(pi, blkp)
+                peers.append(free.pop(d))
+        else:
+            peers = list(range(r))
+        return [0] + cuts + [n], peers
+    raise IndexError(k)
+
+
+def fp64_peak(iters: int = 20000, repeats: int = 3) -> float:
+    """Measured fp64 (DMUL/DADD) operations per second on the current device."""
+    lib = _lib.load()
+    torch = _torch()
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ops = C.c_int64(0)
+    s = _lib.stream_ptr()
+    _lib.check(lib.dm_microbench_fp64(200, sink.data_ptr(), C.byref(ops), s))
+    best = 0.0
+    for _ in range(repeats):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.check(lib.dm_microbench_fp64(iters, sink.data_ptr(), C.byref(ops), s))
+        b.record()
+        b.synchronize()
+        best = max(best, ops.value / (a.elapsed_time(b) / 1e3))
+    return best

@@ -1,0 +1,289 @@
+"""Drop-in replacement of the reference's ``dagmesh.scheduling`` hot path.
+
+Same names, signatures, return types and error behaviour as
+pkg/src/dagmesh/scheduling.py:179-474; every cost-model evaluation, search
+and arg-min runs as CUDA on the B200 through the C ABI
+(include/dagmesh_b200.h).  Host Python only tensorises inputs, launches, and
+assembles the ``ScheduleReport`` (formatting the reason string, summing the
+byte columns of the chosen runs for the report rows with the reference's
+own expressions, so CSV/summary output is byte-identical).
+
+There is no CPU fallback: without the built library or a CUDA device every
+call raises ``EngineUnavailable``.
+"""
+
+from __future__ import annotations
+
+import math
+from types import SimpleNamespace
+
+from . import _lib, engine
+from . import model as _model
+from .model import peer_sort_key
+from .tensorize import build_host
+
+# Result/error classes; install() points these at the reference's own
+# classes so reports built here are instances of dagmesh.scheduling types.
+T = SimpleNamespace(ScheduleReport=_model.ScheduleReport, PeerLoad=_model.PeerLoad,
+                    SchedulingError=_model.SchedulingError, FleetError=_model.FleetError)
+
+_DIM = {_lib.DM_V_GPU: "gpu", _lib.DM_V_CPU: "cpu", _lib.DM_V_DISK: "disk"}
+_INF = math.inf
+
+
+def _check_inputs(stages, workers):
+    """scheduling.py:281-285."""
+    if not stages:
+        raise T.SchedulingError("empty stage list")
+    if not workers:
+        raise T.SchedulingError("empty fleet: no schedulable peers")
+
+
+def _encode_runs(host, runs):
+    """Runs -> [(peer index, sorted indices)]; unknown peers get indices >= P
+    (distinct per distinct id, so 'holds two runs' and link_between's
+    same-peer test keep working)."""
+    unknown: dict = {}
+    out = []
+    n = host.n
+    for peer, idxs in runs:
+        key = peer
+        if key in host.index_of:
+            pi = host.index_of[key]
+        else:
+            pi = unknown.setdefault(key, host.P + len(unknown))
+        sidx = tuple(sorted(idxs))
+        for i in sidx:
+            if not 0 <= i < n:
+                raise IndexError("list index out of range")
+        out.append((pi, sidx))
+    return out
+
+
+def _raise_cost_error(stages, fleet, runs, include_comm):
+    """Re-derive which exception the reference raises first while costing
+    (ordered runs, scheduling.py:217-221): FleetError for an unknown run peer,
+    KeyError for a crossing edge from an unassigned stage."""
+    peer_of = {i: peer for peer, idxs in runs for i in idxs}
+    ordered = sorted(((p, tuple(sorted(i))) for p, i in runs if i), key=lambda r: r[1][0])
+    for peer, idxs in ordered:
+        if str(peer) not in fleet.peers:
+            raise T.FleetError(f"unknown peer {peer!r}")
+        if include_comm:
+            inside = set(idxs)
+            for i in idxs:
+                for src, _ in stages[i].in_edges:
+                    if src not in inside and src not in peer_of:
+                        raise KeyError(src)
+    raise RuntimeError("engine reported a costing error the host cannot reproduce")
+
+
+def _reason(stages, fleet, runs, code, bad):
+    """verify_assignment's message for violation `code` at run `bad`
+    (scheduling.py:179-207)."""
+    if code == _lib.DM_V_OK:
+        return ""
+    if code == _lib.DM_V_UNASSIGNED:
+        seen = {i for _, idxs in runs for i in idxs}
+        missing = sorted(set(range(len(stages))) - seen)
+        return f"stages {[m + 1 for m in missing]} unassigned"
+    peer, indices = runs[bad]
+    ordered = sorted(indices)
+    if code == _lib.DM_V_TWO_RUNS:
+        return f"peer {peer} holds two runs"
+    if code == _lib.DM_V_UNKNOWN_PEER:
+        return f"unknown peer {peer}"
+    if code == _lib.DM_V_NOT_CONTIGUOUS:
+        return f"peer {peer} run {ordered} is not contiguous"
+    if code == _lib.DM_V_ASSIGNED_TWICE:
+        before = {i for _, idxs in runs[:bad] for i in idxs}
+        for i in ordered:
+            if i in before:
+                return f"stage {i + 1} assigned twice"
+        return "stage assigned twice"
+    dim = _DIM[code]
+    p = fleet.peer(peer)
+    cap = getattr(p, f"{dim}_bytes")
+    used = sum(getattr(stages[i], f"{dim}_bytes") for i in ordered)
+    return f"peer {peer} exceeds {dim} capacity: {used:.0f} > {cap:.0f} bytes"
+
+
+def _report(stages, fleet, runs, include_comm, trace, res, c=0):
+    """Assemble the ScheduleReport of candidate c from device results
+    (scheduling.py:210-232)."""
+    lo = int(res["cand_ptr"][c])
+    code = int(res["code"][c])
+    reason = _reason(stages, fleet, runs, code, int(res["code_run"][c]))
+    comp = {}
+    for r, (peer, idxs) in enumerate(runs):
+        if idxs:
+            comp[r] = (float(res["compute"][lo + r]), float(res["read"][lo + r]))
+    order = sorted((r for r, (_, i) in enumerate(runs) if i), key=lambda r: min(runs[r][1]))
+    rows, ordered_runs = [], []
+    for r in order:
+        peer, idxs = runs[r]
+        indices = tuple(sorted(idxs))
+        compute, read = comp[r]
+        ordered_runs.append((peer, indices))
+        rows.append(T.PeerLoad(peer, indices, compute, read, compute + read,
+                               sum(stages[i].gpu_bytes for i in indices),
+                               sum(stages[i].cpu_bytes for i in indices),
+                               sum(stages[i].disk_bytes for i in indices)))
+    assigned = {peer for peer, idxs in runs if idxs}
+    for peer in fleet.worker_ids():
+        if peer not in assigned:
+            rows.append(T.PeerLoad(peer, (), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0))
+    return T.ScheduleReport(tuple(stages), tuple(ordered_runs), tuple(rows), float(res["makespan"][c]),
+                            feasible=(code == _lib.DM_V_OK), reason=reason,
+                            include_comm=include_comm, trace=trace)
+
+
+def _evaluate_many(stages, fleet, runs_list, include_comm, traces, host=None):
+    """Score several candidate Runs of one instance in one dm_eval_runs launch."""
+    host = host or build_host(stages, fleet, include_comm)
+    enc = [_encode_runs(host, runs) for runs in runs_list]
+    res = engine.eval_runs(host, enc)
+    out = []
+    for c, runs in enumerate(runs_list):
+        if int(res["status"][c]) != _lib.DM_OK:
+            out.append(None)
+            continue
+        out.append(_report(stages, fleet, tuple(runs), include_comm, traces[c], res, c))
+    return out, res
+
+
+def _evaluate(stages, fleet, runs, include_comm, trace=(), host=None):
+    runs = tuple(runs)
+    reps, res = _evaluate_many(stages, fleet, [runs], include_comm, [trace], host)
+    if reps[0] is None:
+        _raise_cost_error(stages, fleet, runs, include_comm)
+    return reps[0]
+
+
+def _mark_infeasible(report, reason):
+    """scheduling.py:426-428."""
+    return T.ScheduleReport(report.stages, report.runs, report.per_peer, _INF, False, reason,
+                            report.include_comm, report.trace)
+
+
+# ============================================================== public API
+def evaluate_runs(stages, fleet, runs, *, include_comm: bool = True, trace: tuple = ()):
+    """Score a concrete assignment without optimizing it (scheduling.py:235-239)."""
+    return _evaluate(list(stages), fleet, runs, include_comm, trace)
+
+
+def verify_assignment(stages, fleet, runs) -> str:
+    """Feasibility check, '' or the violated constraint (scheduling.py:179-207)."""
+    stages = list(stages)
+    runs = tuple(runs)
+    host = build_host(stages, fleet, include_comm=False)
+    res = engine.eval_runs(host, [_encode_runs(host, runs)])
+    return _reason(stages, fleet, runs, int(res["code"][0]), int(res["code_run"][0]))
+
+
+def brute_force_schedule(stages, fleet, *, include_comm: bool = True, limit: int = 1_000_000):
+    """Exhaustive optimum over contiguous assignments (scheduling.py:245-278),
+    enumerated on the GPU in the reference's itertools order."""
+    stages = list(stages)
+    workers = fleet.worker_ids()
+    _check_inputs(stages, workers)
+    n, p = len(stages), len(workers)
+    total = engine.bruteforce_total(n, p)
+    if total > limit:
+        raise T.SchedulingError(f"instance too large for enumeration: "
+                                f"{total} contiguous assignments > {limit}")
+    host = build_host(stages, fleet, include_comm)
+    batch = engine.device_batch([host])
+    win = engine.enum(batch, "bruteforce", 0, total).read()
+    if win["rank"] < 0:
+        report = _evaluate(stages, fleet, ((workers[0], tuple(range(n))),), include_comm,
+                           ("enumeration: no feasible assignment",), host)
+        return _mark_infeasible(report, "no feasible assignment under memory constraints")
+    bounds, peers = engine.unrank(n, p, int(win["rank"]), "bruteforce")
+    runs = tuple((workers[peers[q]], tuple(range(bounds[q], bounds[q + 1]))) for q in range(len(peers)))
+    return _evaluate(stages, fleet, runs, include_comm, (f"enumeration over {total} assignments",), host)
+
+
+def _owner_to_runs(workers, owner_row, n):
+    runs = []
+    a = 0
+    for i in range(1, n + 1):
+        if i == n or owner_row[i] != owner_row[a]:
+            runs.append((workers[int(owner_row[a])], tuple(range(a, i))))
+            a = i
+    return tuple(runs)
+
+
+def schedule(stages, fleet, *, include_comm: bool = True):
+    """Assign stages to the fleet's workers minimising the makespan
+    (scheduling.py:391-423): pinned runs, exact subset DP (+ exact-link hill
+    climb when overrides exist), or proportional split + hill climb."""
+    stages = list(stages)
+    workers = fleet.worker_ids()
+    _check_inputs(stages, workers)
+    n, p = len(stages), len(workers)
+
+    if fleet.pinned_runs is not None:
+        if len(fleet.pinned_runs) > p:
+            raise T.SchedulingError(f"{len(fleet.pinned_runs)} pinned runs but only {p} workers")
+        runs = tuple((workers[k], tuple(run)) for k, run in enumerate(fleet.pinned_runs))
+        return _evaluate(stages, fleet, runs, include_comm, ("pinned runs",))
+
+    host = build_host(stages, fleet, include_comm)
+    batch = engine.device_batch([host])
+    if n * n * p * (2 ** p) <= 3_000_000:
+        owner, _, found, _ = engine.subset_dp(batch, n, p)
+        if not int(found.cpu()[0]):
+            report = _evaluate(stages, fleet, ((workers[0], tuple(range(n))),), include_comm,
+                               ("exact search: no feasible assignment",), host)
+            return _mark_infeasible(report, "no feasible assignment under memory constraints")
+        if fleet.links:
+            owner, _, _ = engine.prop_hill(batch, n, init_owner=owner)
+        runs = _owner_to_runs(workers, owner.cpu().numpy()[0], n)
+        return _evaluate(stages, fleet, runs, include_comm, ("exact subset search",), host)
+
+    owner, _, _ = engine.prop_hill(batch, n)
+    runs = _owner_to_runs(workers, owner.cpu().numpy()[0], n)
+    report = _evaluate(stages, fleet, runs, include_comm, ("proportional split with boundary search",), host)
+    if not report.feasible:
+        return _mark_infeasible(report, report.reason or "no feasible assignment under memory constraints")
+    return report
+
+
+def reschedule_on_failure(report, failed_peer, fleet):
+    """Replace a failed peer's run with the best backup, or re-solve without
+    it (scheduling.py:431-474).  All backups are scored in one launch."""
+    failed_peer = str(failed_peer)
+    stages = report.stages
+    lost = tuple(idxs for peer, idxs in report.runs if peer == failed_peer)
+    if not lost:
+        return report
+    survivors = {pid: p for pid, p in fleet.peers.items() if pid != failed_peer}
+    assigned = {peer for peer, idxs in report.runs if idxs and peer != failed_peer}
+    candidates = sorted((b for b in fleet.backup_pool
+                         if b != failed_peer and b in survivors and b not in assigned), key=peer_sort_key)
+    if candidates:
+        runs_list = [tuple((b if peer == failed_peer else peer, idxs) for peer, idxs in report.runs)
+                     for b in candidates]
+        traces = [report.trace + (f"replaced {failed_peer} with {b}",) for b in candidates]
+        reps, res = _evaluate_many(list(stages), fleet, runs_list, report.include_comm, traces)
+        scored = []
+        for b, rep, runs in zip(candidates, reps, runs_list):
+            if rep is None:
+                _raise_cost_error(list(stages), fleet, runs, report.include_comm)
+            if rep.feasible:
+                scored.append((rep.makespan, peer_sort_key(b), rep))
+        if scored:
+            scored.sort(key=lambda t: (t[0], t[1]))
+            return scored[0][2]
+
+    reduced = type(fleet)(peers=survivors, default_link=fleet.default_link,
+                          links={k: v for k, v in fleet.links.items() if failed_peer not in k},
+                          backup_pool=(), msg_ratio=fleet.msg_ratio, pinned_runs=None, name=fleet.name)
+    if not reduced.peers:
+        raise T.SchedulingError("no surviving peers to reschedule onto")
+    solved = schedule(stages, reduced, include_comm=report.include_comm)
+    if not solved.feasible:
+        raise T.SchedulingError(f"no feasible recovery after losing {failed_peer}: {solved.reason}")
+    return T.ScheduleReport(solved.stages, solved.runs, solved.per_peer, solved.makespan, True, "",
+                            solved.include_comm, report.trace + (f"re-solved without {failed_peer}",))

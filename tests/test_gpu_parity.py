@@ -1,0 +1,280 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the CPU oracle on
+identical seeded inputs.  Bar: bit-identical float64 values, identical
+violation codes, identical chosen runs (the reference's tie-breaks)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from gen import big_instance, criterion6_instances, random_stages, uniform_fleet
+from paper_2309_01172_b200 import engine, model as M, rng as R, scheduling as S
+from paper_2309_01172_b200.tensorize import build_host
+
+pytestmark = pytest.mark.gpu
+
+
+def same(a, b):
+    return (math.isnan(a) and math.isnan(b)) or a == b
+
+
+def _oracle_runs(inst, own):
+    return inst.owner_to_runs(own)
+
+
+# ------------------------------------------------------------ evaluate_runs
+def _random_runs(rng, stages, fleet, kind):
+    n = len(stages)
+    workers = list(fleet.worker_ids())
+    if kind == "contig":
+        r = int(rng.integers(1, min(n, len(workers)) + 1))
+        cuts = sorted(rng.choice(np.arange(1, n), r - 1, replace=False).tolist()) if r > 1 else []
+        b = [0] + cuts + [n]
+        peers = rng.choice(workers, r, replace=False).tolist()
+        return tuple((peers[q], tuple(range(b[q], b[q + 1]))) for q in range(r))
+    if kind == "owner":
+        own = rng.integers(0, len(workers), n)
+        d = {}
+        for i, o in enumerate(own):
+            d.setdefault(workers[o], []).append(i)
+        return tuple((k, tuple(v)) for k, v in d.items())
+    if kind == "twice":
+        runs = list(_random_runs(rng, stages, fleet, "contig"))
+        if len(runs) > 1:
+            pe, idx = runs[1]
+            runs[1] = (pe, idx + (runs[0][1][-1],))
+        return tuple(runs)
+    if kind == "gap":
+        runs = list(_random_runs(rng, stages, fleet, "contig"))
+        pe, idx = runs[-1]
+        runs[-1] = (pe, idx[:-1])
+        return tuple(runs)
+    raise ValueError(kind)
+
+
+def test_evaluate_runs_matches_oracle(oracle_mod, engine_ready):
+    rng = np.random.default_rng(5)
+    insts = criterion6_instances(count=60)
+    for k in range(12):
+        insts.append(big_instance(rng, int(rng.integers(10, 60)), int(rng.integers(3, 20)), dag=k % 2 == 0,
+                                  frac=k % 3 == 0, links=k % 4 == 0))
+    checked = 0
+    for stages, fleet in insts:
+        inst = oracle_mod.Instance(stages, fleet)
+        for kind in ("contig", "owner", "twice", "gap"):
+            for _ in range(4):
+                runs = _random_runs(rng, stages, fleet, kind)
+                mk, code, bad, status, comp, read = inst.eval_runs(runs)
+                if status != 0:
+                    with pytest.raises((KeyError, M.FleetError)):
+                        S.evaluate_runs(stages, fleet, runs)
+                    continue
+                rep = S.evaluate_runs(stages, fleet, runs)
+                assert same(rep.makespan, mk), (kind, runs, rep.makespan.hex(), mk.hex())
+                assert rep.feasible == (code == 0), (kind, runs, rep.reason, code)
+                by_run = {(pe, tuple(sorted(ix))): (c, r) for (pe, ix), c, r in zip(runs, comp, read) if ix}
+                for row in rep.per_peer:
+                    if row.stage_indices and (row.peer, row.stage_indices) in by_run:
+                        c, r = by_run[(row.peer, row.stage_indices)]
+                        assert row.compute_s == c and row.read_s == r
+                checked += 1
+    assert checked > 500
+
+
+def test_unknown_peer_raises(engine_ready):
+    stages = random_stages(np.random.default_rng(1), 4)
+    fleet = uniform_fleet([1e9, 2e9])
+    with pytest.raises(M.FleetError, match="unknown peer"):
+        S.evaluate_runs(stages, fleet, (("9", (0, 1, 2, 3)),))
+    assert "unknown peer" in S.verify_assignment(stages, fleet, (("9", (0, 1, 2, 3)),))
+
+
+# ---------------------------------------------------------------- solvers
+def test_schedule_matches_oracle_dp_path(oracle_mod, engine_ready):
+    for stages, fleet in criterion6_instances():
+        inst = oracle_mod.Instance(stages, fleet)
+        path, own = inst.schedule()
+        rep = S.schedule(stages, fleet)
+        if path < 0:
+            assert not rep.feasible and rep.makespan == math.inf
+            continue
+        assert rep.runs == inst.owner_to_runs(own)
+        assert rep.trace == ("exact subset search",)
+
+
+def test_schedule_matches_oracle_hill_path(oracle_mod, engine_ready):
+    rng = np.random.default_rng(7)
+    for k in range(40):
+        stages, fleet = big_instance(rng, int(rng.integers(15, 70)), int(rng.integers(6, 24)), dag=k % 2 == 0,
+                                     frac=k % 4 == 1, links=k % 3 == 0)
+        inst = oracle_mod.Instance(stages, fleet)
+        path, own = inst.schedule()
+        rep = S.schedule(stages, fleet)
+        assert rep.runs == inst.owner_to_runs(own), k
+        assert rep.feasible == (path > 0), k
+
+
+def test_schedule_dp_with_pair_links(oracle_mod, engine_ready):
+    rng = np.random.default_rng(99)
+    for k in range(30):
+        stages = random_stages(rng, int(rng.integers(3, 10)))
+        fleet = uniform_fleet(list(rng.uniform(1e8, 1e9, int(rng.integers(2, 5)))),
+                              link=M.Link(float(rng.uniform(0, 1e-3)), float(rng.uniform(0, 1e-7))))
+        ids = fleet.worker_ids()
+        fleet.links[(ids[0], ids[-1])] = M.Link(float(rng.uniform(0, 1e-3)), float(rng.uniform(0, 1e-7)))
+        inst = oracle_mod.Instance(stages, fleet)
+        path, own = inst.schedule()
+        rep = S.schedule(stages, fleet)
+        assert rep.runs == inst.owner_to_runs(own)
+
+
+def test_brute_force_matches_oracle(oracle_mod, engine_ready):
+    for stages, fleet in criterion6_instances(count=120):
+        inst = oracle_mod.Instance(stages, fleet)
+        total = oracle_mod.bruteforce_total(inst.n, inst.p)
+        w = inst.enum("bruteforce", 0, total)
+        rep = S.brute_force_schedule(stages, fleet)
+        if w["rank"] < 0:
+            assert not rep.feasible
+            continue
+        b, pe = inst.unrank("bruteforce", w["rank"])
+        runs = tuple((inst.workers[pe[q]], tuple(range(b[q], b[q + 1]))) for q in range(len(pe)))
+        assert rep.runs == tuple(sorted(runs, key=lambda r: r[1][0]))
+        assert rep.makespan == w["makespan"]
+
+
+def test_enumeration_winner_checksum_and_sharding(oracle_mod, engine_ready):
+    rng = np.random.default_rng(11)
+    stages = random_stages(rng, 9)
+    fleet = uniform_fleet(list(rng.uniform(1e8, 1e9, 5)), link=M.Link(2e-4, 3e-8), gpu_gb=0.02)
+    inst = oracle_mod.Instance(stages, fleet)
+    host = build_host(stages, fleet)
+    batch = engine.device_batch([host])
+    total = engine.bruteforce_total(9, 5)
+    for k0, k1 in [(0, total), (0, 1), (17, 4000), (total // 3, total)]:
+        want = inst.enum("bruteforce", k0, k1)
+        got = engine.enum(batch, "bruteforce", k0, k1).read()
+        assert got == want, (k0, k1)
+    total_s = engine.splits_total(9, 5)
+    assert engine.enum(batch, "splits", 0, total_s).read() == inst.enum("splits", 0, total_s)
+
+
+def test_splits_enumeration_larger(oracle_mod, engine_ready):
+    rng = np.random.default_rng(12)
+    st, fleet = big_instance(rng, 20, 12, dag=False, pressure=(0.2, 0.9))
+    inst = oracle_mod.Instance(st, fleet)
+    batch = engine.device_batch([build_host(st, fleet)])
+    total = engine.splits_total(20, 12)
+    assert engine.enum(batch, "splits", 0, total).read() == inst.enum("splits", 0, total)
+    st2, fleet2 = big_instance(rng, 14, 6, dag=True, links=True, pressure=(0.3, 0.9))
+    inst2 = oracle_mod.Instance(st2, fleet2)
+    batch2 = engine.device_batch([build_host(st2, fleet2)])
+    total2 = engine.splits_total(14, 6)
+    assert engine.enum(batch2, "splits", 0, total2).read() == inst2.enum("splits", 0, total2)
+
+
+def test_random_placements(oracle_mod, engine_ready):
+    import torch
+    rng = np.random.default_rng(13)
+    st, fleet = big_instance(rng, 60, 256, dag=False, links=True, pressure=(0.05, 0.4))
+    inst = oracle_mod.Instance(st, fleet)
+    host = build_host(st, fleet)
+    batch = engine.device_batch([host])
+    online = np.sort(rng.choice(256, 200, replace=False)).astype(np.int32)
+    mults = np.array(R.coprime_multipliers(200, 5), np.int32)
+    dev = batch.dev_buf.device
+    on_d, mu_d = torch.from_numpy(online).to(dev), torch.from_numpy(mults).to(dev)
+    for seed, k0, k1 in [(1, 0, 30000), (2, 1000, 21000)]:
+        got = engine.enum(batch, "random", k0, k1, online=on_d, mults=mu_d, seed=seed).read()
+        want = inst.enum_random(online, mults, seed, k0, k1)
+        assert got == want
+        if got["rank"] >= 0:
+            b, pe = R.candidate(60, online, mults, seed, got["rank"])
+            runs = tuple((host.peer_ids[pe[q]], tuple(range(b[q], b[q + 1]))) for q in range(len(pe)))
+            assert S.evaluate_runs(st, fleet, runs).makespan == got["makespan"]
+
+
+# --------------------------------------------------------------- Mode A
+@pytest.mark.parametrize("dag,links,wide", [(False, False, False), (True, True, False), (False, True, True)])
+def test_eval_owner_stream(oracle_mod, engine_ready, dag, links, wide):
+    import torch
+    rng = np.random.default_rng(21)
+    n, p = 34, (300 if wide else 32)
+    st, fleet = big_instance(rng, n, p, dag=dag, links=links, pressure=(0.05, 0.5))
+    inst = oracle_mod.Instance(st, fleet)
+    host = build_host(st, fleet)
+    batch = engine.device_batch([host])
+    N = 3000
+    own = np.zeros((N, n), np.int64)
+    for c in range(N):
+        kind = c % 3
+        if kind == 0:
+            own[c] = rng.integers(0, p, n)
+        else:
+            r = int(rng.integers(1, 20))
+            cuts = sorted(rng.choice(np.arange(1, n), r - 1, replace=False).tolist())
+            b = [0] + cuts + [n]
+            pe = rng.choice(p, r, replace=False)
+            for q in range(r):
+                own[c, b[q]:b[q + 1]] = pe[q]
+    own[7, 3] = host.P + 2  # unknown peer
+    dt = torch.int16 if wide else torch.uint8
+    o_d = torch.from_numpy(own.astype(np.int16 if wide else np.uint8)).to(batch.dev_buf.device).to(dt)
+    mk, code = engine.eval_owner(batch, o_d)
+    mk, code = mk.cpu().numpy(), code.cpu().numpy()
+    for c in range(N):
+        m_o, c_o = inst.eval_owner(own[c])
+        assert int(code[c]) == c_o, c
+        assert same(float(mk[c]), m_o), (c, float(mk[c]).hex(), m_o.hex())
+
+
+def test_argmin_scores(engine_ready):
+    import torch
+    rng = np.random.default_rng(3)
+    mk = rng.integers(0, 50, 100000).astype(np.float64) / 7.0
+    code = (rng.random(100000) < 0.3).astype(np.uint8)
+    bufs = engine.argmin_scores(torch.from_numpy(mk).cuda(), torch.from_numpy(code).cuda(), rank_base=1000)
+    got = bufs.read()
+    ok = np.where(code == 0)[0]
+    best = ok[np.argmin(mk[ok])]
+    assert got["rank"] == 1000 + best and got["makespan"] == mk[best]
+    assert got["n_feasible"] == ok.size and got["n_evaluated"] == 100000
+
+
+# ------------------------------------------------------------ batched solvers
+def test_subset_dp_batch(oracle_mod, engine_ready):
+    insts = [i for i in criterion6_instances(count=80)]
+    hosts = [build_host(s, f) for s, f in insts]
+    batch = engine.device_batch(hosts)
+    n_max = max(h.n for h in hosts)
+    p_max = max(h.p for h in hosts)
+    owner, mk, found, _ = engine.subset_dp(batch, n_max, p_max)
+    owner, mk, found = owner.cpu().numpy(), mk.cpu().numpy(), found.cpu().numpy()
+    for s, (st, fl) in enumerate(insts):
+        own, m = oracle_mod.Instance(st, fl).subset_dp()
+        if own is None:
+            assert found[s] == 0
+            continue
+        assert found[s] == 1 and mk[s] == m
+        assert owner[s, :len(st)].tolist() == own.tolist()
+
+
+def test_prop_hill_batch_and_epilogue(oracle_mod, engine_ready):
+    rng = np.random.default_rng(31)
+    insts = [big_instance(rng, int(rng.integers(20, 80)), int(rng.integers(12, 40)), dag=k % 2 == 1, links=k % 5 == 0)
+             for k in range(64)]
+    hosts = [build_host(s, f) for s, f in insts]
+    batch = engine.device_batch(hosts)
+    n_max = max(h.n for h in hosts)
+    owner, score, moves = engine.prop_hill(batch, n_max)
+    epi = engine.epilogue(batch, n_max, owner, 512, 8).cpu().numpy()
+    owner = owner.cpu().numpy()
+    for s, (st, fl) in enumerate(insts):
+        inst = oracle_mod.Instance(st, fl)
+        path, own = inst.schedule()
+        assert owner[s, :len(st)].tolist() == own.tolist(), s
+        runs = inst.owner_to_runs(own)
+        mk, code, _, _, comp, read = inst.eval_runs(runs)
+        assert epi[s, 0] == mk and int(epi[s, 5]) == code
+        lat, bn, pipe, thr = oracle_mod.epilogue(comp, read, 512, 8)
+        assert (epi[s, 1], epi[s, 2], epi[s, 3], epi[s, 4]) == (lat, bn, pipe, thr)
