@@ -207,6 +207,12 @@ DM_API int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_o
                    int64_t k0, int64_t k1, dm_winner* out,
                    void* scratch, void* stream);
 
+/* dm_materialize — write candidates [k0, k0+count) of the brute-force
+ * (mode 0) or identity-split (mode 1) order as owner vectors (uint8/uint16
+ * worker indices, count x n): the input stream of dm_eval_owner. */
+DM_API int dm_materialize(int32_t n, int32_t p, int32_t mode, int64_t k0, int64_t count,
+                          void* owner, int32_t owner_bytes, void* stream);
+
 /* dm_finalize_winners — reduce per-CTA partials left in scratch by the
  * enumeration calls into out (called internally; exposed for multi-stream use) */
 DM_API int dm_finalize_winners(void* scratch, int32_t n_parts, dm_winner* out,

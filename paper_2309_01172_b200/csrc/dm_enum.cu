@@ -189,6 +189,222 @@ __global__ void __launch_bounds__(256) enum_kernel(dm_tables t, int64_t k0, int6
     block_reduce_win_store(w, partial);
 }
 
+// ------------------------------------------------ memoised identity splits
+// For the identity-order split population (run q on worker q) the load of a
+// run depends only on (q, a, b) whenever the crossing read does not depend on
+// which run owns a source stage: include_comm off, a uniform link (no pair
+// overrides: every crossing source sits on another worker), or
+// chain-structured stages (the source of run q's crossing edges is stage a-1,
+// owned by worker q-1).  Each CTA then tabulates
+//     T[q][a][b] = _fits(q, a..b) ? compute + read : +inf
+// once in shared memory (n(n+1)(n+2)/6 doubles at most, 57 KB for n = 34)
+// with exactly the reference's arithmetic, and every candidate is scored
+// from scratch as the max over its r runs of T.
+//
+// Each thread keeps its current combination as cut bytes in shared memory
+// (column-major per thread, 4 cuts per 32-bit word, the final boundary n
+// stored as a sentinel), so the run loop costs one LDS.32 per four runs, a
+// row-offset LDS, the table LDS.64 and the max.  The lexicographic successor
+// (itertools.combinations order) rewrites only the changed suffix.  Lanes of
+// a warp own ADJACENT rank chunks, so they share long run prefixes and most
+// table reads are shared-memory broadcasts.
+constexpr int kMemoThreads = 512;
+constexpr int kMemoChunk = 64;
+
+// Shared-memory layout of the memo kernel.  rowoff[q * S + a] is the byte
+// offset of T[q][a][0] (so &T[q][a][b] = sm + rowoff + 8b); row a = n of
+// every q points at a row of -inf so that runs past the final boundary
+// (groups of 4 are scored unconditionally) never change the max.
+struct MemoLayout {
+    int n, rmax, W, S;
+    int t_elems;
+    size_t off_dummy, off_rowoff, off_binom, off_cum, off_cuts, bytes;
+};
+
+__host__ __device__ inline MemoLayout memo_layout(int n, int p) {
+    MemoLayout L;
+    L.n = n; L.rmax = n < p ? n : p; L.W = n - 1; L.S = n < 64 ? 64 : 256;
+    int tot = 0;
+    for (int q = 0; q < L.rmax; ++q) { int Lq = n - q; tot += Lq * (Lq + 1) / 2; }
+    L.t_elems = tot;
+    size_t off = (size_t)tot * 8;
+    L.off_dummy = off; off += (size_t)(n + 1) * 8;
+    off = (off + 15) & ~(size_t)15;
+    L.off_rowoff = off; off += (size_t)(L.rmax + 4) * L.S * 4;
+    L.off_binom = off; off += (size_t)n * (L.rmax + 1) * 8;
+    L.off_cum = off; off += (size_t)(L.rmax + 2) * 8;
+    off = (off + 15) & ~(size_t)15;
+    L.off_cuts = off; off += (size_t)((L.rmax + 4) / 4 + 2) * kMemoThreads * 4;
+    L.bytes = off;
+    return L;
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+
+template <int S>
+__global__ void __launch_bounds__(kMemoThreads, 2) splits_memo_kernel(dm_tables t, int64_t k0, int64_t k1,
+                                                                      dm_winner* partial) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int n = t.n;
+    const MemoLayout L = memo_layout(n, t.p);
+    const int rmax = L.rmax, W = L.W, R1 = rmax + 1;
+    int32_t* rowoff = reinterpret_cast<int32_t*>(sm + L.off_rowoff);
+    int64_t* binom = reinterpret_cast<int64_t*>(sm + L.off_binom);   // C(a, b), a < n, b <= rmax
+    int64_t* cum = reinterpret_cast<int64_t*>(sm + L.off_cum);       // cum[m] = first rank with m cuts
+    unsigned char* cutb = sm + L.off_cuts;                            // byte z of thread t: ((z>>2)*BS+t)*4+(z&3)
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+
+    const uint32_t sm_base = (uint32_t)__cvta_generic_to_shared(sm);
+    for (int i = threadIdx.x; i < (rmax + 4) * S; i += blockDim.x) {
+        int q = i / S, a = i % S;
+        int32_t v = (int32_t)L.off_dummy;
+        if (q < rmax && a >= q && a < n) {
+            int base = 0;
+            for (int qq = 0; qq < q; ++qq) { int Lq = n - qq; base += Lq * (Lq + 1) / 2; }
+            int within = (a - q) * n - ((a - q) * (a + q - 1)) / 2;
+            v = (base + within - (a + 1)) * 8;
+        }
+        rowoff[i] = (int32_t)(sm_base + (uint32_t)v);   // absolute shared address of T[q][a][0]
+    }
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) reinterpret_cast<double*>(sm + L.off_dummy)[i] = -inf;
+    for (int i = threadIdx.x; i < n * R1; i += blockDim.x) binom[i] = binom_sat(i / R1, i % R1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cum[0] = 0;
+        for (int m = 1; m <= rmax; ++m) cum[m] = cum[m - 1] + binom[(n - 1) * R1 + (m - 1)];
+    }
+    for (int row = threadIdx.x; row < rmax * n; row += blockDim.x) {
+        int q = row / n, a = row % n;
+        if (a < q) continue;
+        double* Trow = reinterpret_cast<double*>(sm + ((uint32_t)rowoff[q * S + a] - sm_base));
+        for (int b = a + 1; b <= n; ++b) {
+            double v = inf;
+            if ((q > 0 || a == 0) && fits_range(t, q, a, b)) {
+                double c, rd;
+                if (chain(t)) run_cost_contig(t, a, b, q, [&](int) { return q - 1; }, c, rd);
+                else run_cost_contig(t, a, b, q, [&](int s) { return s < a ? -1 : q + 1; }, c, rd);
+                v = c + rd;
+            }
+            Trow[b] = v;
+        }
+    }
+    __syncthreads();
+
+    const int BS = blockDim.x, tid = threadIdx.x;
+    uint32_t* cutw = reinterpret_cast<uint32_t*>(cutb) + tid;   // word j at cutw[j * BS]
+    const int n_words = (rmax + 4) / 4;
+    Win w; win_init(w);
+    const int lane = tid & 31;
+    const int64_t warps_total = (int64_t)gridDim.x * (BS >> 5);
+    const int64_t gw = (int64_t)blockIdx.x * (BS >> 5) + (tid >> 5);
+    const int64_t span = k1 - k0, task_ranks = 32LL * kMemoChunk;
+    const int64_t n_tasks = (span + task_ranks - 1) / task_ranks;
+    const uint32_t npad = (uint32_t)n * 0x01010101u;
+    const unsigned long long FULL = (W >= 64) ? ~0ull : ((1ull << W) - 1ull);
+    // write the cut bytes of mask x (m cuts, bit v-1 <-> position v) + sentinel n
+    auto write_all = [&](unsigned long long x, int m) {
+        for (int j = 0; j < n_words + 2; ++j) cutw[j * BS] = npad;
+        unsigned long long y = x;
+        for (int z = 0; z < m; ++z) {
+            int hb = __ffsll((long long)y) - 1;
+            y &= y - 1;
+            uint32_t& wd = cutw[(z >> 2) * BS];
+            int sh = 8 * (z & 3);
+            wd = (wd & ~(0xffu << sh)) | ((uint32_t)(hb + 1) << sh);
+        }
+    };
+    for (int64_t task = gw; task < n_tasks; task += warps_total) {
+        int64_t kb = k0 + task * task_ranks + (int64_t)lane * kMemoChunk;
+        int64_t ke = kb + kMemoChunk < k1 ? kb + kMemoChunk : k1;
+        if (kb >= ke) continue;
+        w.n_eval += ke - kb;
+        // ---- unrank kb: m cuts, lexicographic combination of positions 1..W
+        int m = 0;
+        while (m + 1 < rmax && cum[m + 1] <= kb) ++m;
+        int64_t c = kb - cum[m];
+        unsigned long long x = 0;
+        int lo = 1;
+        for (int z = 0; z < m; ++z) {
+            for (int v = lo; v <= W; ++v) {
+                int64_t cnt = binom[(W - v) * R1 + (m - z - 1)];
+                if (c < cnt) { x |= 1ull << (v - 1); lo = v + 1; break; }
+                c -= cnt;
+            }
+        }
+        write_all(x, m);
+        for (int64_t k = kb; k < ke; ++k) {
+            // ---- score: max over the m + 1 runs of T (from scratch), in
+            //      unconditional groups of four (padding runs read -inf)
+            double mk = -inf;
+            uint32_t a8 = 0;  // 4 * a
+            const unsigned char* rq = reinterpret_cast<const unsigned char*>(rowoff);
+            for (int z4 = 0; z4 <= m; z4 += 4, rq += 4 * 4 * S) {
+                uint32_t wd = cutw[(z4 >> 2) * BS];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t b = __byte_perm(wd, 0u, 0x4440u + u);
+                    uint32_t ro = *reinterpret_cast<const uint32_t*>(rq + u * 4 * S + a8);
+                    double v = lds_f64(ro + 8 * b);
+                    mk = v > mk ? v : mk;
+                    a8 = 4 * b;
+                }
+            }
+            if (mk < inf) {
+                w.n_feas++;
+                w.csum += (uint64_t)__double_as_longlong(mk);
+                if (w.rank < 0 || mk < w.mk) { w.mk = mk; w.rank = k; }
+            }
+            // ---- lexicographic successor in O(1) on the mask: the top L cuts
+            //      sit at positions W-L+1..W; the pivot cut (index z = m-1-L,
+            //      position hb+1) moves up by one and the L cuts after it
+            //      follow consecutively.
+            unsigned long long t0 = ~x & FULL;
+            int hz = 63 - __clzll((long long)t0);          // highest non-cut position - 1 (-1: none)
+            int L = W - 1 - hz;                             // saturated cuts at the top
+            int z = m - 1 - L;                              // pivot index
+            if (z < 0) {                                    // block exhausted: one more cut
+                ++m;
+                if (m >= rmax) break;
+                x = (1ull << m) - 1ull;
+                write_all(x, m);
+                continue;
+            }
+            unsigned long long below = x & ((1ull << hz) - 1ull);
+            int hb = 63 - __clzll((long long)below);       // pivot bit
+            x = (x & ((1ull << hb) - 1ull)) | ((((1ull << (L + 1)) - 1ull)) << (hb + 1));
+            // bytes z..m-1 <- hb+2, hb+3, ...: predicated rewrite of three words
+            const int base = hb + 2 - z;                    // value of byte index i is base + i
+            const int jz = z >> 2;
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj) {
+                int j = jz + dj;
+                int lo_b = z - 4 * j, hi_b = m - 1 - 4 * j;
+                lo_b = lo_b < 0 ? 0 : lo_b;
+                if (hi_b > 3) hi_b = 3;
+                if (hi_b >= lo_b) {
+                    uint32_t msk = (0xffffffffu << (8 * lo_b)) & (0xffffffffu >> (8 * (3 - hi_b)));
+                    uint32_t pat = (uint32_t)((base + 4 * j) & 0xff) * 0x01010101u + 0x03020100u;
+                    uint32_t& wd = cutw[j * BS];
+                    wd = (wd & ~msk) | (pat & msk);
+                }
+            }
+            for (int j = jz + 3; 4 * j <= m - 1; ++j) {      // L >= 9: rare
+                int hi_b = m - 1 - 4 * j;
+                if (hi_b > 3) hi_b = 3;
+                uint32_t msk = 0xffffffffu >> (8 * (3 - hi_b));
+                uint32_t pat = (uint32_t)((base + 4 * j) & 0xff) * 0x01010101u + 0x03020100u;
+                uint32_t& wd = cutw[j * BS];
+                wd = (wd & ~msk) | (pat & msk);
+            }
+        }
+    }
+    block_reduce_win_store(w, partial);
+}
+
 // --------------------------------------------------------- random stream
 __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -261,6 +477,54 @@ __global__ void __launch_bounds__(256) enum_random_kernel(dm_tables t, const int
     block_reduce_win_store(w, partial);
 }
 
+// -------------------------------------------------- candidate materialiser
+// Writes candidates [k0, k0 + count) of the brute-force (MODE 0) or
+// identity-split (MODE 1) order as owner vectors (worker index per stage):
+// the Mode A scoring stream's input, and a cross-check of the Mode B walk.
+template <typename OT, int MODE, int RMAX>
+__global__ void __launch_bounds__(256) materialize_kernel(int n, int p, int64_t k0, int64_t count,
+                                                          int64_t per_thread, OT* __restrict__ out) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t kb = tid * per_thread;
+    int64_t ke = kb + per_thread < count ? kb + per_thread : count;
+    if (kb >= ke) return;
+    const int rmax = n < p ? n : p;
+    int32_t cuts[RMAX + 1], peers[RMAX + 1];
+    PermSet used;
+    int r = 1;
+    int64_t off = k0 + kb;
+    for (; r <= rmax; ++r) {
+        int64_t nc = binom_sat(n - 1, r - 1);
+        int64_t np = MODE == 0 ? perm_sat(p, r) : 1;
+        unsigned __int128 blk = (unsigned __int128)nc * (unsigned __int128)np;
+        if ((unsigned __int128)off < blk) break;
+        off -= (int64_t)blk;
+    }
+    int64_t np = MODE == 0 ? perm_sat(p, r) : 1;
+    unrank_comb(n, r - 1, off / np, cuts);
+    if (MODE == 0) unrank_perm(p, r, off % np, peers, used);
+    else for (int q = 0; q < r; ++q) peers[q] = q;
+    for (int64_t k = kb; k < ke; ++k) {
+        OT* row = out + k * n;
+        int a = 0;
+        for (int q = 0; q < r; ++q) {
+            int b = q + 1 < r ? cuts[q] : n;
+            for (int i = a; i < b; ++i) row[i] = (OT)peers[q];
+            a = b;
+        }
+        if (MODE == 0 && next_perm(p, r, peers, used)) continue;
+        if (next_comb(n, r - 1, cuts)) {
+            if (MODE == 0) { used.clear(p); for (int q = 0; q < r; ++q) { peers[q] = q; used.set(q); } }
+            continue;
+        }
+        ++r;
+        if (r > rmax) break;
+        for (int q = 0; q < r - 1; ++q) cuts[q] = q + 1;
+        used.clear(p);
+        for (int q = 0; q < r; ++q) { peers[q] = q; if (MODE == 0) used.set(q); }
+    }
+}
+
 // ------------------------------------------------------------ final merge
 __global__ void finalize_kernel(const dm_winner* partial, int n_parts, dm_winner* out) {
     Win w; win_init(w);
@@ -280,9 +544,15 @@ __global__ void finalize_kernel(const dm_winner* partial, int n_parts, dm_winner
 
 // ================================================================== C ABI
 #include "dm_abi_util.cuh"
+#include <cstdlib>
 
 namespace {
 constexpr int kThreads = 256;
+
+bool getenv_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] && v[0] != '0';
+}
 
 int enum_grid() {
     static thread_local int sms = 0;
@@ -330,7 +600,25 @@ int dm_enum_bruteforce(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* ou
 int dm_enum_splits(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* out,
                    void* scratch, void* stream) {
     if (!t || !out || !scratch || t->n <= 0 || t->p <= 0) return dmabi::fail(DM_E_ARG, "bad arguments");
-    return launch_enum<1>(t, k0, k1, out, scratch, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t f = t->flags;
+    bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
+    dm::MemoLayout L = dm::memo_layout(t->n, t->p);
+    if (memo_ok && t->n <= 64 && L.bytes <= 110 * 1024 && !getenv_flag("DM_DISABLE_MEMO")) {
+        int grid = enum_grid() / 8 * 2;  // 2 CTAs x 512 threads per SM
+        if (L.S == 64) {
+            cudaFuncSetAttribute(dm::splits_memo_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+            dm::splits_memo_kernel<64><<<grid, dm::kMemoThreads, L.bytes, s>>>(*t, k0, k1, (dm_winner*)scratch);
+        } else {
+            cudaFuncSetAttribute(dm::splits_memo_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+            dm::splits_memo_kernel<256><<<grid, dm::kMemoThreads, L.bytes, s>>>(*t, k0, k1, (dm_winner*)scratch);
+        }
+        DM_CHECK_LAUNCH();
+        dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, grid, out);
+        DM_CHECK_LAUNCH();
+        return DM_OK;
+    }
+    return launch_enum<1>(t, k0, k1, out, scratch, s);
 }
 
 int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,
@@ -349,6 +637,25 @@ int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,
                                                      (dm_winner*)scratch);
     DM_CHECK_LAUNCH();
     dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, grid, out);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+int dm_materialize(int32_t n, int32_t p, int32_t mode, int64_t k0, int64_t count, void* owner, int32_t owner_bytes,
+                   void* stream) {
+    if (n <= 0 || p <= 0 || count < 0 || !owner || (owner_bytes != 1 && owner_bytes != 2) || (mode != 0 && mode != 1))
+        return dmabi::fail(DM_E_ARG, "dm_materialize: bad arguments");
+    int rmax = n < p ? n : p;
+    if (rmax > 64) return dmabi::fail(DM_E_TOO_LARGE, "dm_materialize: at most 64 runs");
+    if (count == 0) return DM_OK;
+    const int64_t per = 64;
+    int64_t threads = (count + per - 1) / per;
+    int blocks = (int)((threads + 255) / 256);
+    cudaStream_t s = (cudaStream_t)stream;
+#define DM_MAT(OT, M) dm::materialize_kernel<OT, M, 64><<<blocks, 256, 0, s>>>(n, p, k0, count, per, (OT*)owner)
+    if (owner_bytes == 1) { if (mode == 0) DM_MAT(uint8_t, 0); else DM_MAT(uint8_t, 1); }
+    else { if (mode == 0) DM_MAT(uint16_t, 0); else DM_MAT(uint16_t, 1); }
+#undef DM_MAT
     DM_CHECK_LAUNCH();
     return DM_OK;
 }

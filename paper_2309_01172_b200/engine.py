@@ -228,3 +228,13 @@ def fp64_peak(iters: int = 20000, repeats: int = 3) -> float:
         b.synchronize()
         best = max(best, ops.value / (a.elapsed_time(b) / 1e3))
     return best
+
+
+def materialize(n: int, p: int, mode: str, k0: int, count: int, device="cuda", owner_bytes: int = 1):
+    """Owner vectors of candidates [k0, k0+count) (mode 'bruteforce' | 'splits')."""
+    lib = _lib.load()
+    torch = _torch()
+    out = torch.empty((count, n), dtype=torch.uint8 if owner_bytes == 1 else torch.int16, device=device)
+    _lib.check(lib.dm_materialize(n, p, {"bruteforce": 0, "splits": 1}[mode], k0, count, out.data_ptr(),
+                                  owner_bytes, _lib.stream_ptr()))
+    return out

@@ -278,3 +278,43 @@ def test_prop_hill_batch_and_epilogue(oracle_mod, engine_ready):
         assert epi[s, 0] == mk and int(epi[s, 5]) == code
         lat, bn, pipe, thr = oracle_mod.epilogue(comp, read, 512, 8)
         assert (epi[s, 1], epi[s, 2], epi[s, 3], epi[s, 4]) == (lat, bn, pipe, thr)
+
+
+def test_splits_memo_matches_generic(engine_ready, monkeypatch):
+    """The shared-memory memo kernel and the generic per-run kernel agree
+    (winner, counts, checksum) on chain, DAG and no-comm instances."""
+    rng = np.random.default_rng(44)
+    for dag, links, inc in [(False, False, True), (False, True, True), (True, False, True), (True, True, False)]:
+        st, fleet = big_instance(rng, 22, 14, dag=dag, links=links, pressure=(0.1, 0.8))
+        batch = engine.device_batch([build_host(st, fleet, inc)])
+        total = engine.splits_total(22, 14)
+        a = engine.enum(batch, "splits", 0, total).read()
+        b = engine.enum(batch, "splits", 12345, total - 999).read()
+        monkeypatch.setenv("DM_DISABLE_MEMO", "1")
+        a2 = engine.enum(batch, "splits", 0, total).read()
+        b2 = engine.enum(batch, "splits", 12345, total - 999).read()
+        monkeypatch.delenv("DM_DISABLE_MEMO")
+        assert a == a2 and b == b2
+
+
+def test_materialized_stream_matches_enumeration(engine_ready):
+    """Mode A (materialised owner vectors scored from HBM + arg-min) and Mode B
+    (in-kernel enumeration) agree on the same rank range: winner, counts and
+    the checksum of every feasible candidate's makespan."""
+    rng = np.random.default_rng(8)
+    for dag, links in [(False, False), (False, True), (True, False)]:
+        st, fleet = big_instance(rng, 30, 24, dag=dag, links=links, pressure=(0.1, 0.6))
+        batch = engine.device_batch([build_host(st, fleet)])
+        total = engine.splits_total(30, 24)
+        k0, cnt = total // 3, 2_000_000
+        own = engine.materialize(30, 24, "splits", k0, cnt)
+        mk, code = engine.eval_owner(batch, own)
+        a = engine.argmin_scores(mk, code, rank_base=k0).read()
+        b = engine.enum(batch, "splits", k0, k0 + cnt).read()
+        assert a == b
+    bf_total = engine.bruteforce_total(9, 5)
+    st, fleet = big_instance(rng, 9, 5, dag=False, links=True, pressure=(0.2, 0.9))
+    batch = engine.device_batch([build_host(st, fleet)])
+    own = engine.materialize(9, 5, "bruteforce", 0, bf_total)
+    mk, code = engine.eval_owner(batch, own)
+    assert engine.argmin_scores(mk, code).read() == engine.enum(batch, "bruteforce", 0, bf_total).read()

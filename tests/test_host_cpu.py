@@ -1,0 +1,114 @@
+"""Host-side logic that runs without a GPU: the mirror types and fleet
+parser, the rank codecs against itertools, the counter RNG (Python vs C
+oracle), sharding/merging, closed-form stage tables against the reference's
+build_stages digests, and the tensoriser's flags."""
+
+import hashlib
+import itertools
+import json
+import math
+import pathlib
+
+import numpy as np
+import pytest
+
+from paper_2309_01172_b200 import configs as CF
+from paper_2309_01172_b200 import dist as D
+from paper_2309_01172_b200 import engine, model as M, rng as R
+from paper_2309_01172_b200.tensorize import build_host
+
+GOLD = pathlib.Path(__file__).resolve().parent / "golden"
+
+
+def test_unrank_matches_itertools_order():
+    for n in range(1, 8):
+        for p in range(1, 5):
+            k = 0
+            for r in range(1, min(n, p) + 1):
+                for cuts in itertools.combinations(range(1, n), r - 1):
+                    for chosen in itertools.permutations(range(p), r):
+                        b, pe = engine.unrank(n, p, k, "bruteforce")
+                        assert b == [0, *cuts, n] and pe == list(chosen)
+                        k += 1
+            assert k == engine.bruteforce_total(n, p)
+
+
+def test_oracle_unrank_matches_python(oracle_mod):
+    rng = np.random.default_rng(0)
+    st = [M.Stage(i, "s", 1.0, 1, 1, 1) for i in range(12)]
+    fl = M.Fleet(peers={str(i): M.Peer(str(i)) for i in range(1, 6)})
+    inst = oracle_mod.Instance(st, fl)
+    for mode, tot in (("bruteforce", engine.bruteforce_total(12, 5)), ("splits", engine.splits_total(12, 5))):
+        for k in rng.integers(0, tot, 200):
+            assert inst.unrank(mode, int(k)) == engine.unrank(12, 5, int(k), mode)
+
+
+def test_rng_python_matches_c(oracle_mod):
+    online = np.arange(0, 900, 3, dtype=np.int32)
+    mults = np.array(R.coprime_multipliers(len(online), 9), np.int32)
+    assert all(math.gcd(int(a), len(online)) == 1 for a in mults)
+    import ctypes as C
+    L = oracle_mod.lib()
+    b = np.zeros(300, np.int32)
+    pe = np.zeros(300, np.int32)
+    for k in [0, 1, 2, 17, 10**9, 2**40 + 3]:
+        r = L.or_random_candidate(194, len(online), online.ctypes.data, mults.ctypes.data, len(mults), 12345, k,
+                                  b.ctypes.data, pe.ctypes.data)
+        bb, pp = R.candidate(194, online, mults, 12345, k)
+        assert b[: r + 1].tolist() == bb and pe[:r].tolist() == pp
+        assert len(set(pp)) == len(pp)
+
+
+def test_shard_covers_range():
+    for total in (0, 1, 7, 1000, 8589934558):
+        for world in (1, 2, 3, 8):
+            parts = [D.shard(total, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == total
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+
+
+def test_merge_records_first_strict_min():
+    import struct
+    recs = [(2.0, 10, 5, 4, 7), (1.0, 30, 5, 5, 9), (1.0, 20, 5, 5, 1), (math.inf, -1, 3, 0, 0)]
+    raw = np.frombuffer(b"".join(struct.pack(D.WINNER_FMT, *r) for r in recs), np.uint8)
+    m = D.merge_records(raw)
+    assert (m["makespan"], m["rank"], m["n_evaluated"], m["n_feasible"], m["checksum"]) == (1.0, 20, 18, 14, 17)
+
+
+def test_closed_form_stages_match_reference_digests():
+    digests = json.loads((GOLD / "stage_digests.json").read_text())
+    for name, d in digests.items():
+        st = CF.model_stages(name) if name in CF.MODELS else CF.encoder_stages(**d["kw"])
+        blob = repr([(s.index, s.label, s.flops, s.gpu_bytes, s.cpu_bytes, s.disk_bytes, s.in_edges) for s in st])
+        assert len(st) == d["n"] and hashlib.sha256(blob.encode()).hexdigest() == d["sha256"], name
+
+
+def test_fleet_parser_and_tensoriser_flags():
+    doc = {"name": "t", "peers": [{"id": "10", "gpu": "h100"}, {"id": "2", "gpu": "rtx3080", "lambda": 0.5},
+                                  {"id": "b", "tflops_tensor": 1.0, "gpu_gb": 2}],
+           "links": {"default_alpha_s": 0.001, "bandwidth_gbps": 2.0,
+                     "overrides": [{"src": "2", "dst": "10", "alpha_s": 0.5, "bandwidth_gbps": 1.0}]},
+           "backup_pool": ["2"], "pinned_runs": [[1, 2], [3]]}
+    fl = M.parse_fleet(json.dumps(doc))
+    assert fl.worker_ids() == ("10", "b") and fl.peer_ids() == ("2", "10", "b")
+    assert fl.pinned_runs == ((0, 1), (2,))
+    assert fl.link_between("10", "2").alpha == 0.5 and fl.link_between("b", "2").alpha == 0.001
+    st = [M.Stage(0, "a", 3.0, 10, 10, 10), M.Stage(1, "b", 4.0, 10, 10, 10, ((0, 100),))]
+    h = build_host(st, fl)
+    assert h.peer_ids == ("10", "b", "2") and h.p == 2 and h.P == 3
+    from paper_2309_01172_b200 import _lib
+    assert h.flags & _lib.DM_F_CHAIN and h.flags & _lib.DM_F_PAIR_LINKS and h.flags & _lib.DM_F_FLOPS_EXACT
+    la = h.arrays["link_alpha"].reshape(3, 3)
+    assert la[2, 0] == 0.5 and la[0, 2] == 0.5 and la[1, 2] == 0.001 and la[0, 0] == 0.0
+    with pytest.raises(M.FleetError):
+        M.parse_fleet({"peers": [{"id": "1", "gpu": "nope"}]})
+    frac = [M.Stage(0, "a", 0.5, 1, 1, 1)]
+    assert not build_host(frac, fl).flags & _lib.DM_F_FLOPS_EXACT
+
+
+def test_reference_fleet_files_parse_identically(dagmesh_ref):
+    from golden_io import dump_fleet
+    for f in pathlib.Path("/root/reference/pkg/fleets").glob("*.json"):
+        a = dump_fleet(dagmesh_ref.hardware.load_fleet(f))
+        b = dump_fleet(M.load_fleet(f))
+        assert a == b, f
