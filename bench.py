@@ -233,15 +233,202 @@ def mean_runs_splits(n, p):
     return sum(r * math.comb(n - 1, r - 1) for r in range(1, min(n, p) + 1)) / tot
 
 
-def secondary_measurements(dev):
-    """FP64 peak microbenchmark (roofline denominator) and the CPU baseline."""
-    out = {}
+def _hbm_peak():
     try:
-        from paper_2309_01172_b200 import engine
-        out["fp64_peak_ops_per_s"] = engine.fp64_peak()
-    except Exception as exc:  # the microbenchmark is optional
-        out["fp64_peak_error"] = str(exc)
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _time_ms(fn, steps=5, warmup=3):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def mode_a_measure(dev, which):
+    """Mode A scoring stream (owner vectors resident in HBM, > L2) with the
+    fused arg-min; roofline = HBM bytes n*w + 9 per candidate."""
+    import math
+    import time as _t
+    import torch
+    from oracle import oracle
+    from paper_2309_01172_b200 import configs as CF
+    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200.tensorize import build_host
+    if which == "c2":
+        stages, fleet = c2_instance()
+        n, p = 34, 32
+        N = 1 << 28
+        total = engine.splits_total(n, p)
+        k0 = total // 2 - N // 2
+        own = engine.materialize(n, p, "splits", k0, N, device=dev)
+        desc = f"C2 split ranks [{k0}, {k0 + N}) materialised as uint8 owner vectors ({N * n / 1e9:.1f} GB)"
+    else:
+        stages = CF.model_stages("gpt2-small")
+        fleet = CF.load(CF.c1_fleet_doc(10.0, 1e-3))
+        n, p = 26, 4
+        total = engine.bruteforce_total(n, p)
+        base = engine.materialize(n, p, "bruteforce", 0, total, device=dev)
+        N = 1 << 27
+        own = base.repeat(math.ceil(N / total), 1)[:N].contiguous()
+        del base
+        k0 = 0
+        desc = (f"C1 (gpt2-small x 4 mixed GPUs, 10 Gbit/s, 1 ms) brute-force-order candidates, the 62,704 "
+                f"population tiled to {N} uint8 owner vectors ({N * n / 1e9:.1f} GB)")
+    host = build_host(stages, fleet, True)
+    batch = engine.device_batch([host], device=dev)
+    out = (torch.empty(N, dtype=torch.float64, device=dev), torch.empty(N, dtype=torch.uint8, device=dev))
+    bufs = engine.WinnerBuffers(dev)
+    ms = _time_ms(lambda: engine.eval_owner_argmin(batch, own, k0, bufs, out))
+    win = bufs.read()
+    res = {"config": desc, "candidates": N, "ms": ms, "value": N / (ms / 1e3), "unit": UNIT,
+           "winner": {"makespan": win["makespan"], "rank": win["rank"], "n_feasible": win["n_feasible"],
+                      "checksum": win["checksum"]}}
+    if which == "c2":   # Mode A == Mode B on the same ranks (full-size property)
+        res["matches_mode_b"] = engine.enum(batch, "splits", k0, k0 + N).read() == win
+    peak, src = _hbm_peak()
+    algo = N * (n * 1 + 9)
+    achieved = algo / (ms / 1e3) / 1e9
+    res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                       "traffic": None, "bytes_per_candidate": n + 9, "peak_source": src}
+    inst = oracle.Instance(stages, fleet)
+    sample = own[:20000].cpu().numpy().astype("int64")
+    t0 = _t.perf_counter()
+    for row in sample:
+        inst.eval_owner(row)
+    res["cpu_baseline_1core"] = 20000 / (_t.perf_counter() - t0)
+    del own, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def dp_measure(dev):
+    """Partition DPs solved/s: config C1's 32 x 32 link grid, one _subset_dp per fleet."""
+    import time as _t
+    from oracle import oracle
+    from paper_2309_01172_b200 import configs as CF
+    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200.tensorize import build_host
+    stages = CF.model_stages("gpt2-small")
+    bws, alphas = CF.c1_link_grid()
+    fleets = [CF.load(CF.c1_fleet_doc(bw, al)) for bw in bws for al in alphas]
+    hosts = [build_host(stages, f, True) for f in fleets]
+    batch = engine.device_batch(hosts, device=dev)
+    ms = _time_ms(lambda: engine.subset_dp(batch, 26, 4))
+    own, mk, found, _ = engine.subset_dp(batch, 26, 4)
+    own = own.cpu().numpy()
+    ok = True
+    t0 = _t.perf_counter()
+    for i in range(0, len(fleets), 64):
+        o, _ = oracle.Instance(stages, fleets[i]).subset_dp()
+        ok &= o is not None and own[i, :26].tolist() == o.tolist()
+    cpu = 16 / (_t.perf_counter() - t0)
+    return {"config": "C1 gpt2-small (26 stages) x 4 workers, 1024 link-grid fleets (bw logspace(-1,2,32) x "
+                      "alpha linspace(0,10ms,32)), one _subset_dp each", "dps": len(fleets), "ms": ms,
+            "value": len(fleets) / (ms / 1e3), "unit": "DPs/s", "oracle_spot_check": bool(ok),
+            "cpu_baseline_1core": cpu}
+
+
+def c4_measure(dev, n_scen=1 << 18):
+    """schedule() solves/s over config C4 scenarios (proportional split + hill climb + epilogue)."""
+    import time as _t
+    from oracle import oracle
+    from paper_2309_01172_b200 import batch as B
+    from paper_2309_01172_b200 import engine
+    sb = B.c4_batch(n_scen, seed=0, device=dev)
+
+    def run():
+        owner, _, _ = engine.prop_hill(sb, sb.n_max)
+        return engine.epilogue(sb, sb.n_max, owner, 512, 4)
+    ms = _time_ms(run, steps=3, warmup=3)
+    owner, _, moves = engine.prop_hill(sb, sb.n_max)
+    epi = engine.epilogue(sb, sb.n_max, owner, 512, 4).cpu().numpy()
+    owner = owner.cpu().numpy()
+    ok = True
+    t0 = _t.perf_counter()
+    for s in range(0, n_scen, n_scen // 16):
+        st, fl = B.scenario_instance(sb, s)
+        _, o = oracle.Instance(st, fl).schedule()
+        ok &= owner[s, :len(st)].tolist() == o.tolist()
+    cpu = 16 / (_t.perf_counter() - t0)
+    feas = float((epi[:, 5] == 0).mean())
+    return {"config": f"C4: {n_scen} scenarios, L~U{{32..80}}, h in {{2048,4096,5120,8192}}, p~U{{8..64}}, "
+                      "GPU_TABLE mix, lambda~U[.3,1], alpha~U[0,10ms], bw~LogU[.1,10] Gbit/s",
+            "schedules": n_scen, "ms": ms, "value": n_scen / (ms / 1e3), "unit": "schedules/s",
+            "feasible_frac": feas, "mean_hill_moves": float(moves.float().mean()),
+            "oracle_spot_check": bool(ok), "cpu_baseline_1core": cpu}
+
+
+def random_measure(dev, which):
+    """Random contiguous placements scored in-kernel (counter RNG):
+    C5 = OPT-175B x 1024 workers with 10% churn (922 online), 10^9 candidates;
+    C3 = Llama-2-70B x 256 workers with 32,640 randomised pairwise links."""
+    import time as _t
+    import numpy as np
+    import torch
+    from oracle import oracle
+    from paper_2309_01172_b200 import configs as CF
+    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200 import rng as R
+    from paper_2309_01172_b200.tensorize import build_host
+    if which == "c5":
+        stages = CF.model_stages("opt-175b")
+        fleet = CF.load(CF.c5_fleet_doc(0))
+        _, online_ids = CF.c5_churn(1024, 0.1, 0)
+        N = 10 ** 9
+        desc = "C5 OPT-175B (194 stages) x 1024 workers, 922 online after 10% churn, default 5 ms / 10 Gbit/s"
+    else:
+        stages = CF.model_stages("llama2-70b")
+        fleet = CF.load(CF.c3_fleet_doc(0))
+        online_ids = list(fleet.worker_ids())
+        N = 1 << 28
+        desc = "C3 Llama-2-70B (162 stages) x 256 workers, 32,640 randomised pairwise links (alpha U[0,20ms], bw LogU[.1,100])"
+    host = build_host(stages, fleet, True)
+    batch = engine.device_batch([host], device=dev)
+    online = np.array([host.index_of[i] for i in online_ids], np.int32)
+    mults = np.array(R.coprime_multipliers(len(online), 1234), np.int32)
+    on_d, mu_d = torch.from_numpy(online).to(dev), torch.from_numpy(mults).to(dev)
+    bufs = engine.WinnerBuffers(dev)
+    seed = 20260
+    ms = _time_ms(lambda: engine.enum(batch, "random", 0, N, bufs, online=on_d, mults=mu_d, seed=seed), steps=3)
+    win = bufs.read()
+    inst = oracle.Instance(stages, fleet)
+    t0 = _t.perf_counter()
+    ref = inst.enum_random(online, mults, seed, 0, 2000)
+    cpu = 2000 / (_t.perf_counter() - t0)
+    got = engine.enum(batch, "random", 0, 2000, online=on_d, mults=mu_d, seed=seed).read()
+    return {"config": desc, "candidates": N, "ms": ms, "value": N / (ms / 1e3), "unit": UNIT,
+            "winner": {"makespan": win["makespan"], "rank": win["rank"], "n_feasible": win["n_feasible"],
+                       "checksum": win["checksum"]},
+            "oracle_prefix_check": got == ref, "cpu_baseline_1core": cpu}
+
+
+def secondary_measurements(dev):
+    """FP64 peak microbenchmark (roofline denominator), CPU baseline, and the
+    secondary paths of the metric: Mode A streams (HBM roofline), DPs/s, schedules/s."""
+    out = {}
+    from paper_2309_01172_b200 import engine
+    out["fp64_peak_ops_per_s"] = engine.fp64_peak()
     out["cpu_baseline"] = cpu_baseline(threads=1, seconds=10.0)
+    sec = {}
+    for name, fn in (("mode_a_c1", lambda: mode_a_measure(dev, "c1")), ("mode_a_c2", lambda: mode_a_measure(dev, "c2")),
+                     ("dp_c1_grid", lambda: dp_measure(dev)), ("schedule_c4", lambda: c4_measure(dev)),
+                     ("random_c5", lambda: random_measure(dev, "c5")), ("random_c3", lambda: random_measure(dev, "c3"))):
+        try:
+            sec[name] = fn()
+        except Exception as exc:
+            sec[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    out["secondary"] = sec
     return out
 
 

@@ -165,6 +165,12 @@ DM_API int dm_eval_owner(const dm_tables* t, int64_t n_cand, const void* owner,
                   int32_t owner_bytes, double* out_makespan,
                   uint8_t* out_code, void* stream);
 
+/* dm_eval_owner_argmin — dm_eval_owner with the arg-min fused into the
+ * scoring kernel (ranks = rank_base + index; scratch as dm_enum_scratch_bytes). */
+DM_API int dm_eval_owner_argmin(const dm_tables* t, int64_t n_cand, const void* owner,
+                                int32_t owner_bytes, double* out_makespan, uint8_t* out_code,
+                                int64_t rank_base, dm_winner* out, void* scratch, void* stream);
+
 /*
  * dm_argmin_scores — block/warp arg-min over (makespan, rank) of a scored
  * stream (codes != 0 are skipped), ranks = rank_base + index.

@@ -62,6 +62,7 @@ _SIGS = {
     "dm_enum_scratch_bytes": (C.c_int64, []),
     "dm_eval_runs": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "dm_eval_owner": (C.c_int, [_P, C.c_int64, _P, C.c_int32, _P, _P, _P]),
+    "dm_eval_owner_argmin": (C.c_int, [_P, C.c_int64, _P, C.c_int32, _P, _P, C.c_int64, _P, _P, _P]),
     "dm_argmin_scores": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P, _P]),
     "dm_enum_bruteforce": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P]),
     "dm_enum_splits": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P]),

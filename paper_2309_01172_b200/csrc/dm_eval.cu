@@ -12,6 +12,7 @@
 //  * argmin kernels: block/warp arg-min over (makespan, rank).
 #include "dm_common.cuh"
 #include "dm_abi_util.cuh"
+#include <cstdlib>
 
 namespace dm {
 
@@ -262,6 +263,206 @@ __global__ void __launch_bounds__(kTile) eval_owner_kernel(dm_tables t, int64_t 
     }
 }
 
+// ----------------------------------------------- Mode A, memoised stream
+// Owner-vector stream for uint8 owners, n <= 64, P <= 64 when the load of a
+// contiguous run [a, b) on peer w depends only on (a, b, w) (uniform link or
+// include_comm off), or additionally on the previous run's peer for
+// chain-structured stages with pairwise links (then the table holds the
+// compute term and the crossing read alpha + beta*M is added per run).
+// Per-(a, b, w) loads and violation codes are tabulated once per CTA in
+// shared memory with the reference's arithmetic; candidate tiles stream in
+// through a ring of 1-D TMA bulk copies (cp.async.bulk + mbarrier), one
+// elected thread issuing, while every thread scores one candidate:
+// SIMD byte compares build the run-boundary mask, then each run costs a
+// table lookup.  A candidate whose peer reappears (non-contiguous) or whose
+// owner index is out of range takes the general grouped path.
+constexpr int kStreamThreads = 256;
+constexpr int kStreamStages = 4;
+
+// shared-memory layout; every segment 16-byte aligned (TMA destinations)
+struct StreamLayout {
+    int n, P, npairs;
+    size_t off_T, off_fit, off_rowidx, off_tiles, off_bar, bytes, tile_bytes;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline StreamLayout stream_layout(int n, int P) {
+    StreamLayout L;
+    L.n = n; L.P = P; L.npairs = n * (n + 1) / 2;
+    size_t off = 0;
+    L.off_T = off; off = al16(off + (size_t)L.npairs * P * 8);          // load (or compute) per (a,b,w)
+    L.off_fit = off;
+    L.off_rowidx = off; off = al16(off + (size_t)(n + 1) * 4);
+    L.tile_bytes = al16((size_t)kStreamThreads * n);
+    L.off_tiles = off; off = al16(off + L.tile_bytes * kStreamStages + 16);
+    L.off_bar = off; off += 8 * kStreamStages;
+    L.bytes = al16(off);
+    return L;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+template <bool PAIR>
+__global__ void __launch_bounds__(kStreamThreads) eval_owner_stream_kernel(dm_tables t, int64_t n_cand,
+                                                                           const uint8_t* __restrict__ owner,
+                                                                           double* __restrict__ out_mk,
+                                                                           uint8_t* __restrict__ out_code,
+                                                                           int64_t rank_base, dm_winner* partial) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int n = t.n, P = t.P;
+    const StreamLayout L = stream_layout(n, P);
+    // T[pr * P + w]: load of run (a, b) on w (compute only when PAIR), sign bit
+    // set when the run fails _fits (|T| is the value, -0.0 keeps the flag)
+    double* T = reinterpret_cast<double*>(sm + L.off_T);
+    int32_t* rowidx = reinterpret_cast<int32_t*>(sm + L.off_rowidx);  // pair index of (a, b) = rowidx[a] + b
+    unsigned char* tiles = sm + L.off_tiles;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.off_bar);
+    const int64_t n_tiles = (n_cand + kStreamThreads - 1) / kStreamThreads;
+    const int64_t full_tiles = n_cand / kStreamThreads;
+
+    // ---- kick off the first tile loads before building the tables
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kStreamStages; ++st) mbar_init(&bars[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int st = 0; st < kStreamStages; ++st) {
+            int64_t tl = blockIdx.x + (int64_t)st * gridDim.x;
+            if (tl < full_tiles) {
+                mbar_expect_tx(&bars[st], (uint32_t)(kStreamThreads * n));
+                tma_load_1d(tiles + st * L.tile_bytes, owner + tl * kStreamThreads * n,
+                            (uint32_t)(kStreamThreads * n), &bars[st]);
+            }
+        }
+    }
+    for (int a = threadIdx.x; a <= n; a += blockDim.x) rowidx[a] = a * n - a * (a - 1) / 2 - a - 1;
+    __syncthreads();
+    for (int it = threadIdx.x; it < L.npairs * P; it += blockDim.x) {
+        int pr = it / P, w = it % P;
+        int a = 0;
+        while (a + 1 < n && rowidx[a + 1] + (a + 2) <= pr) ++a;
+        int b = pr - rowidx[a];
+        double v, c, rd;
+        if (PAIR) {
+            v = col_range(t.flops, t.pre_flops, flops_exact(t), a, b) / t.speed[w];
+        } else {
+            run_cost_contig(t, a, b, w, [&](int) { return -1; }, c, rd);  // uniform link: every source is remote
+            v = c + rd;
+        }
+        if (!fits_range(t, w, a, b)) v = -v;
+        T[it] = v;
+    }
+    __syncthreads();
+
+    const int tid = threadIdx.x;
+    const int nw = (n + 3) >> 2;
+    const int last_valid = n - 4 * (nw - 1);                            // bytes of the last word in the row
+    const uint32_t last_mask = last_valid >= 4 ? 0xffffffffu : (0xffffffffu >> (8 * (4 - last_valid)));
+    Win win; win_init(win);
+    int64_t it_local = 0;
+    for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x, ++it_local) {
+        const int st = (int)(it_local % kStreamStages);
+        const uint32_t parity = (uint32_t)((it_local / kStreamStages) & 1);
+        const int64_t c0 = tl * kStreamThreads;
+        const int cnt = (int)((n_cand - c0) < kStreamThreads ? (n_cand - c0) : kStreamThreads);
+        unsigned char* tile = tiles + st * L.tile_bytes;
+        if (tl < full_tiles) {
+            mbar_wait(&bars[st], parity);
+        } else {  // ragged last tile: plain loads
+            for (int b = tid; b < cnt * n; b += blockDim.x) tile[b] = owner[c0 * n + b];
+            __syncthreads();
+        }
+        if (tid < cnt) {
+            const uint32_t row0 = (uint32_t)tid * n;
+            const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile) + (row0 >> 2);
+            const int sh = (row0 & 3) * 8;
+            // ---- run-boundary mask: bit i-1 <=> owner[i] != owner[i-1] (i >= 1)
+            uint32_t mlo = 0, mhi = 0, prevw = 0, cur = tw[0];
+            for (int j = 0; j < nw; ++j) {
+                uint32_t nxt = tw[j + 1];
+                uint32_t wd = __funnelshift_r(cur, nxt, sh);
+                cur = nxt;
+                uint32_t x = wd ^ __byte_perm(prevw, wd, 0x6543);    // byte k vs byte k-1
+                if (j == nw - 1) x &= last_mask;
+                uint32_t nz = (x | ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu)) & 0x80808080u;
+                uint32_t nib = (nz * 0x00204081u) >> 28;             // bit k <=> byte k differs
+                int pos = 4 * j - 1;                                   // bit of byte 0 (stage 4j)
+                if (j == 0) nib >>= 1, pos = 0;
+                if (pos < 32) { mlo |= nib << pos; if (pos > 28) mhi |= nib >> (32 - pos); }
+                else mhi |= nib << (pos - 32);
+                prevw = wd;
+            }
+            // ---- runs: b = each boundary in ascending order, then n
+            const uint8_t* row = tile + row0;
+            double mk = 0.0;
+            int code = DM_V_OK, flag = 0, a = 0, prev = -1;
+            unsigned long long seen = 0;
+            auto run = [&](int b) {
+                int w = row[a];
+                flag |= (w >= P);
+                w = w < P ? w : P - 1;
+                unsigned long long bit = 1ull << w;
+                flag |= ((seen & bit) != 0) << 1;
+                seen |= bit;
+                const int pr = rowidx[a] + b;
+                const double tv = T[pr * P + w];
+                double v = fabs(tv);
+                if (PAIR && a > 0) {
+                    double al, be;
+                    link_of(t, prev, w, al, be);
+                    double rd = 0.0;
+                    for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
+                        rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
+                    v = v + rd;
+                }
+                mk = v > mk ? v : mk;
+                if (signbit(tv) && code == DM_V_OK) code = cap_violation(t, w, a, b);
+                prev = w; a = b;
+            };
+            for (uint32_t y = mlo; y; y &= y - 1) run(__ffs(y));
+            for (uint32_t y = mhi; y; y &= y - 1) run(32 + __ffs(y));
+            run(n);
+            bool unknown = flag & 1;
+            if (flag == 2) eval_owner_grouped(t, row, mk, code);   // a peer holds two runs
+            out_mk[c0 + tid] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
+            out_code[c0 + tid] = unknown ? (uint8_t)0xFF : (uint8_t)code;
+            if (partial) {                       // fused arg-min (first strict minimum by rank)
+                win.n_eval++;
+                if (!unknown && code == DM_V_OK) {
+                    win.n_feas++;
+                    win.csum += (uint64_t)__double_as_longlong(mk);
+                    if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank_base + c0 + tid; }
+                }
+            }
+        }
+        __syncthreads();  // every thread is done with this slot
+        if (tid == 0) {
+            int64_t nt = tl + (int64_t)kStreamStages * gridDim.x;
+            if (nt < full_tiles) {
+                mbar_expect_tx(&bars[st], (uint32_t)(kStreamThreads * n));
+                tma_load_1d(tile, owner + nt * kStreamThreads * n, (uint32_t)(kStreamThreads * n), &bars[st]);
+            }
+        }
+    }
+    if (partial) block_reduce_win_store(win, partial);
+}
+
 // ---------------------------------------------------------------- arg-min
 __global__ void __launch_bounds__(256) argmin_kernel(const double* __restrict__ mk, const uint8_t* __restrict__ code,
                                                      int64_t n, int64_t rank_base, dm_winner* partial) {
@@ -342,14 +543,60 @@ int dm_eval_runs(const dm_tables* t, int32_t n_cand, const int32_t* cand_ptr, co
     return DM_OK;
 }
 
+static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner, int32_t owner_bytes,
+                           double* out_makespan, uint8_t* out_code, int64_t rank_base, dm_winner* out,
+                           void* scratch, void* stream);
+
 int dm_eval_owner(const dm_tables* t, int64_t n_cand, const void* owner, int32_t owner_bytes,
                   double* out_makespan, uint8_t* out_code, void* stream) {
+    return eval_owner_impl(t, n_cand, owner, owner_bytes, out_makespan, out_code, 0, nullptr, nullptr, stream);
+}
+
+int dm_eval_owner_argmin(const dm_tables* t, int64_t n_cand, const void* owner, int32_t owner_bytes,
+                         double* out_makespan, uint8_t* out_code, int64_t rank_base, dm_winner* out,
+                         void* scratch, void* stream) {
+    if (!out || !scratch) return dmabi::fail(DM_E_ARG, "dm_eval_owner_argmin: bad arguments");
+    return eval_owner_impl(t, n_cand, owner, owner_bytes, out_makespan, out_code, rank_base, out, scratch, stream);
+}
+
+static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner, int32_t owner_bytes,
+                           double* out_makespan, uint8_t* out_code, int64_t rank_base, dm_winner* out,
+                           void* scratch, void* stream) {
     if (!t || n_cand < 0 || !owner || !out_makespan || !out_code || t->n <= 0 ||
         (owner_bytes != 1 && owner_bytes != 2))
         return dmabi::fail(DM_E_ARG, "dm_eval_owner: bad arguments");
     if (owner_bytes == 1 && t->P > 256) return dmabi::fail(DM_E_ARG, "uint8 owners need P <= 256");
     if (n_cand == 0) return DM_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    {
+        const uint32_t f = t->flags;
+        bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
+        dm::StreamLayout L = dm::stream_layout(t->n, t->P);
+        const char* dis = std::getenv("DM_DISABLE_MEMO");
+        bool aligned = (((uintptr_t)owner) & 15) == 0;
+        if (owner_bytes == 1 && memo_ok && aligned && t->n <= 64 && t->P <= 64 && L.bytes <= 220 * 1024 &&
+            !(dis && dis[0] && dis[0] != '0')) {
+            int per_sm = (int)((225 * 1024) / (L.bytes + 1024));
+            if (per_sm < 1) per_sm = 1;
+            if (per_sm > 12) per_sm = 12;
+            int64_t n_tiles = (n_cand + dm::kStreamThreads - 1) / dm::kStreamThreads;
+            int64_t grid = (int64_t)sm_count() * per_sm;
+            if (grid > n_tiles) grid = n_tiles;
+            if (out && grid > 8 * sm_count()) grid = 8 * sm_count();   // partial slots in scratch
+            const bool pair = (t->flags & DM_F_INCLUDE_COMM) && (t->flags & DM_F_PAIR_LINKS);
+            auto kern = pair ? dm::eval_owner_stream_kernel<true> : dm::eval_owner_stream_kernel<false>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+            kern<<<(int)grid, dm::kStreamThreads, L.bytes, s>>>(*t, n_cand, (const uint8_t*)owner, out_makespan,
+                                                               out_code, rank_base,
+                                                               out ? (dm_winner*)scratch : nullptr);
+            DM_CHECK_LAUNCH();
+            if (out) {
+                dm::finalize_argmin_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, (int)grid, out);
+                DM_CHECK_LAUNCH();
+            }
+            return DM_OK;
+        }
+    }
     size_t tile_bytes = (((size_t)dm::kTile * t->n * owner_bytes) + 15) & ~(size_t)15;
     size_t seen_bytes = (size_t)((t->P + 31) / 32) * dm::kTile * sizeof(uint32_t);
     size_t smem = tile_bytes + seen_bytes;
@@ -370,6 +617,7 @@ int dm_eval_owner(const dm_tables* t, int64_t n_cand, const void* owner, int32_t
                                                                             out_makespan, out_code);
     }
     DM_CHECK_LAUNCH();
+    if (out) return dm_argmin_scores(out_makespan, out_code, n_cand, rank_base, out, scratch, stream);
     return DM_OK;
 }
 

@@ -83,6 +83,22 @@ def eval_owner(batch: DeviceBatch, owner, index: int = 0):
     return mk, code
 
 
+def eval_owner_argmin(batch: DeviceBatch, owner, rank_base: int = 0, bufs=None, out=None, index: int = 0):
+    """Mode A with the arg-min fused into the scoring kernel."""
+    lib = _lib.load()
+    torch = _torch()
+    n_cand = owner.shape[0]
+    if out is None:
+        out = (torch.empty(n_cand, dtype=torch.float64, device=owner.device),
+               torch.empty(n_cand, dtype=torch.uint8, device=owner.device))
+    bufs = bufs or WinnerBuffers(owner.device)
+    st = batch.struct(index)
+    _lib.check(lib.dm_eval_owner_argmin(C.byref(st), n_cand, owner.data_ptr(), owner.element_size(),
+                                        out[0].data_ptr(), out[1].data_ptr(), rank_base, bufs.out.data_ptr(),
+                                        bufs.scratch.data_ptr(), _lib.stream_ptr()))
+    return out, bufs
+
+
 class WinnerBuffers:
     """Device scratch + one device dm_winner record for enumeration calls."""
 

@@ -176,7 +176,13 @@ def test_splits_enumeration_larger(oracle_mod, engine_ready):
 def test_random_placements(oracle_mod, engine_ready):
     import torch
     rng = np.random.default_rng(13)
-    st, fleet = big_instance(rng, 60, 256, dag=False, links=True, pressure=(0.05, 0.4))
+    for links in (True, False):
+        _random_case(oracle_mod, rng, links)
+
+
+def _random_case(oracle_mod, rng, links):
+    import torch
+    st, fleet = big_instance(rng, 60, 256, dag=False, links=links, pressure=(0.05, 0.4))
     inst = oracle_mod.Instance(st, fleet)
     host = build_host(st, fleet)
     batch = engine.device_batch([host])
@@ -195,7 +201,8 @@ def test_random_placements(oracle_mod, engine_ready):
 
 
 # --------------------------------------------------------------- Mode A
-@pytest.mark.parametrize("dag,links,wide", [(False, False, False), (True, True, False), (False, True, True)])
+@pytest.mark.parametrize("dag,links,wide", [(False, False, False), (True, True, False), (False, True, True),
+                                            (False, True, False), (True, False, False)])
 def test_eval_owner_stream(oracle_mod, engine_ready, dag, links, wide):
     import torch
     rng = np.random.default_rng(21)
@@ -312,6 +319,9 @@ def test_materialized_stream_matches_enumeration(engine_ready):
         a = engine.argmin_scores(mk, code, rank_base=k0).read()
         b = engine.enum(batch, "splits", k0, k0 + cnt).read()
         assert a == b
+        (mk2, code2), bufs = engine.eval_owner_argmin(batch, own, rank_base=k0)
+        assert bufs.read() == b
+        assert bool((mk2 == mk).all()) and bool((code2 == code).all())
     bf_total = engine.bruteforce_total(9, 5)
     st, fleet = big_instance(rng, 9, 5, dag=False, links=True, pressure=(0.2, 0.9))
     batch = engine.device_batch([build_host(st, fleet)])
