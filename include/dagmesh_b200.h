@@ -199,6 +199,14 @@ DM_API int dm_enum_splits(const dm_tables* t, int64_t k0, int64_t k1,
                    dm_winner* out, void* scratch, void* stream);
 
 /*
+ * dm_enum_splits_part — the share of dm_enum_splits owned by part `part` of
+ * `nparts` (multi-GPU): rank tasks are interleaved across parts so every GPU
+ * gets the same mix of run counts; the union over parts is [k0, k1) exactly.
+ */
+DM_API int dm_enum_splits_part(const dm_tables* t, int64_t k0, int64_t k1, int32_t part,
+                               int32_t nparts, dm_winner* out, void* scratch, void* stream);
+
+/*
  * dm_enum_random — counter-RNG random contiguous placements (config C5):
  * candidate k (k0 <= k < k1) is generated from SplitMix64 keyed (seed, k):
  * each cut position 1..n-1 is present with probability 1/2, and the r runs go

@@ -142,11 +142,11 @@ __device__ __forceinline__ void win_add(Win& w, double mk, int64_t rank) {
 
 // MODE 0: full brute-force order; MODE 1: identity-order splits.
 template <int MODE, int RMAX>
-__global__ void __launch_bounds__(256) enum_kernel(dm_tables t, int64_t k0, int64_t k1,
+__global__ void __launch_bounds__(256) enum_kernel(dm_tables t, int64_t k0, int64_t k1, int part, int nparts,
                                                    int64_t per_thread, dm_winner* partial) {
     Win w; win_init(w);
     int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t kb = k0 + tid * per_thread;
+    int64_t kb = k0 + (tid * nparts + part) * per_thread;
     int64_t ke = kb + per_thread < k1 ? kb + per_thread : k1;
     if (kb < ke) {
         const int n = t.n, p = t.p, rmax = n < p ? n : p;
@@ -247,7 +247,7 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
 
 template <int S>
 __global__ void __launch_bounds__(kMemoThreads, 2) splits_memo_kernel(dm_tables t, int64_t k0, int64_t k1,
-                                                                      dm_winner* partial) {
+                                                                      int part, int nparts, dm_winner* partial) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int n = t.n;
     const MemoLayout L = memo_layout(n, t.p);
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kMemoThreads, 2) splits_memo_kernel(dm_tables 
             wd = (wd & ~(0xffu << sh)) | ((uint32_t)(hb + 1) << sh);
         }
     };
-    for (int64_t task = gw; task < n_tasks; task += warps_total) {
+    for (int64_t task = gw * nparts + part; task < n_tasks; task += warps_total * nparts) {
         int64_t kb = k0 + task * task_ranks + (int64_t)lane * kMemoChunk;
         int64_t ke = kb + kMemoChunk < k1 ? kb + kMemoChunk : k1;
         if (kb >= ke) continue;
@@ -537,16 +537,21 @@ __global__ void __launch_bounds__(256) materialize_kernel(int n, int p, int64_t 
 // correctly rounded quotient (validated bitwise against div.rn in
 // tests/test_gpu_parity.py and on 2e8 CPU samples).
 struct RandLayout {
-    size_t off_pre, off_R, off_peer, off_online, off_mults, bytes;
+    size_t off_stage, off_peer, off_online, off_mults, bytes;
 };
+
+// Stage record (boundary i): exact prefix sums of flops / gpu / cpu / disk as
+// doubles (integers < 2^53, so differences are exact) and R[i], the uniform
+// read of a run starting at stage i.  Peer record: speed, RN(1/speed), caps.
+struct __align__(16) StageRec { double pf, pg, pc, pd, R, pad; };
+struct __align__(16) PeerRec { double speed, rcp, cg, cc, cd; int32_t pe, pad; };
 
 __host__ __device__ inline RandLayout rand_layout(int n, int P, int n_online, int n_mults) {
     RandLayout L;
     size_t off = 0;
-    L.off_pre = off; off += (size_t)(n + 1) * 4 * 8;            // flops, gpu, cpu, disk prefixes
-    L.off_R = off; off += (size_t)(n + 1) * 8;
-    L.off_peer = off; off += (size_t)P * 5 * 8;                 // speed, rcp, cap gpu, cpu, disk
-    L.off_online = off; off += ((size_t)n_online * 4 + 15) & ~(size_t)15;
+    L.off_stage = off; off += (size_t)(n + 1) * sizeof(StageRec);
+    L.off_peer = off; off += (size_t)n_online * sizeof(PeerRec);   // in online order
+    L.off_online = off;
     L.off_mults = off; off += ((size_t)n_mults * 4 + 15) & ~(size_t)15;
     L.bytes = off;
     return L;
@@ -565,27 +570,28 @@ __global__ void __launch_bounds__(256) enum_random_fast_kernel(dm_tables t, cons
     extern __shared__ __align__(16) unsigned char sm[];
     const int n = t.n, P = t.P;
     const RandLayout L = rand_layout(n, P, n_online, n_mults);
-    int64_t* pre = reinterpret_cast<int64_t*>(sm + L.off_pre);  // [4][n+1]
-    double* R = reinterpret_cast<double*>(sm + L.off_R);
-    double* pc = reinterpret_cast<double*>(sm + L.off_peer);    // [5][P]
-    int32_t* onl = reinterpret_cast<int32_t*>(sm + L.off_online);
+    StageRec* SR = reinterpret_cast<StageRec*>(sm + L.off_stage);
+    PeerRec* PR = reinterpret_cast<PeerRec*>(sm + L.off_peer);
     int32_t* mul = reinterpret_cast<int32_t*>(sm + L.off_mults);
     const bool comm = include_comm(t), pair = pair_links(t);
     for (int i = threadIdx.x; i <= n; i += blockDim.x) {
-        pre[i] = t.pre_flops[i]; pre[(n + 1) + i] = t.pre_gpu[i];
-        pre[2 * (n + 1) + i] = t.pre_cpu[i]; pre[3 * (n + 1) + i] = t.pre_disk[i];
+        StageRec r;
+        r.pf = (double)t.pre_flops[i]; r.pg = (double)t.pre_gpu[i];
+        r.pc = (double)t.pre_cpu[i]; r.pd = (double)t.pre_disk[i];
         double rd = 0.0;
         if (comm && i < n)
             for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e)
                 rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
-        R[i] = rd;
+        r.R = rd; r.pad = 0.0;
+        SR[i] = r;
     }
-    for (int w = threadIdx.x; w < P; w += blockDim.x) {
-        double sp = t.speed[w];
-        pc[w] = sp; pc[P + w] = 1.0 / sp;
-        pc[2 * P + w] = t.cap_gpu[w]; pc[3 * P + w] = t.cap_cpu[w]; pc[4 * P + w] = t.cap_disk[w];
+    for (int i = threadIdx.x; i < n_online; i += blockDim.x) {
+        const int w = online[i];
+        PeerRec r;
+        r.speed = t.speed[w]; r.rcp = 1.0 / r.speed;
+        r.cg = t.cap_gpu[w]; r.cc = t.cap_cpu[w]; r.cd = t.cap_disk[w]; r.pe = w; r.pad = 0;
+        PR[i] = r;
     }
-    for (int i = threadIdx.x; i < n_online; i += blockDim.x) onl[i] = online[i];
     for (int i = threadIdx.x; i < n_mults; i += blockDim.x) mul[i] = mults[i];
     __syncthreads();
 
@@ -599,6 +605,7 @@ __global__ void __launch_bounds__(256) enum_random_fast_kernel(dm_tables t, cons
         bool ok = true;
         double mk = 0.0;
         int a = 0, prev = -1;
+        StageRec ra = SR[0];
         for (int j = 0; j <= nwords; ++j) {
             uint64_t bits = 0;
             if (j < nwords) {
@@ -611,17 +618,15 @@ __global__ void __launch_bounds__(256) enum_random_fast_kernel(dm_tables t, cons
                 if (bits) { b = 64 * j + __ffsll((long long)bits); bits &= bits - 1; }
                 else if (j == nwords) b = n;
                 else break;
-                const int pe = onl[pos_peer];
+                const StageRec rb = SR[b];
+                const PeerRec pr = PR[pos_peer];
+                const int pe = pr.pe;
                 pos_peer += am;
                 if (pos_peer >= n_online) pos_peer -= n_online;
-                // _fits (scheduling.py:172-176) with exact prefix sums
-                const double g = (double)(pre[(n + 1) + b] - pre[(n + 1) + a]);
-                const double c = (double)(pre[2 * (n + 1) + b] - pre[2 * (n + 1) + a]);
-                const double d = (double)(pre[3 * (n + 1) + b] - pre[3 * (n + 1) + a]);
-                ok &= (g <= pc[2 * P + pe]) & (c <= pc[3 * P + pe]) & (d <= pc[4 * P + pe]);
+                // _fits (scheduling.py:172-176): exact prefix differences vs capacities
+                ok &= (rb.pg - ra.pg <= pr.cg) & (rb.pc - ra.pc <= pr.cc) & (rb.pd - ra.pd <= pr.cd);
                 // _run_cost: compute + crossing read from the previous run's peer
-                const double fl = (double)(pre[b] - pre[a]);
-                const double compute = div_markstein(fl, pc[pe], pc[P + pe]);
+                const double compute = div_markstein(rb.pf - ra.pf, pr.speed, pr.rcp);
                 double rd = 0.0;
                 if (comm && a > 0) {
                     if (pair) {
@@ -630,12 +635,12 @@ __global__ void __launch_bounds__(256) enum_random_fast_kernel(dm_tables t, cons
                         for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
                             rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
                     } else {
-                        rd = R[a];
+                        rd = ra.R;
                     }
                 }
                 const double load = compute + rd;
                 mk = load > mk ? load : mk;
-                prev = pe; a = b;
+                prev = pe; a = b; ra = rb;
                 if (b == n) break;
             }
         }
@@ -686,23 +691,50 @@ int enum_grid() {
 }
 
 template <int MODE>
-int launch_enum(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* out, void* scratch,
+int launch_enum(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts, dm_winner* out, void* scratch,
                 cudaStream_t s) {
     int grid = enum_grid();
     dm_winner* partial = (dm_winner*)scratch;
-    int64_t total_threads = (int64_t)grid * kThreads;
+    int64_t total_threads = (int64_t)grid * kThreads * nparts;
     int64_t span = k1 > k0 ? k1 - k0 : 0;
     int64_t per = (span + total_threads - 1) / total_threads;
     if (per < 1) per = 1;
     int rmax = t->n < t->p ? t->n : t->p;
-    if (rmax <= 16) dm::enum_kernel<MODE, 16><<<grid, kThreads, 0, s>>>(*t, k0, k1, per, partial);
-    else if (rmax <= 64) dm::enum_kernel<MODE, 64><<<grid, kThreads, 0, s>>>(*t, k0, k1, per, partial);
-    else if (rmax <= 256) dm::enum_kernel<MODE, 256><<<grid, kThreads, 0, s>>>(*t, k0, k1, per, partial);
+    if (rmax <= 16) dm::enum_kernel<MODE, 16><<<grid, kThreads, 0, s>>>(*t, k0, k1, part, nparts, per, partial);
+    else if (rmax <= 64) dm::enum_kernel<MODE, 64><<<grid, kThreads, 0, s>>>(*t, k0, k1, part, nparts, per, partial);
+    else if (rmax <= 256) dm::enum_kernel<MODE, 256><<<grid, kThreads, 0, s>>>(*t, k0, k1, part, nparts, per, partial);
     else return dmabi::fail(DM_E_TOO_LARGE, "enumeration supports at most 256 runs");
     DM_CHECK_LAUNCH();
     dm::finalize_kernel<<<1, 1024, 0, s>>>(partial, grid, out);
     DM_CHECK_LAUNCH();
     return DM_OK;
+}
+
+int enum_splits_impl(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts, dm_winner* out,
+                     void* scratch, void* stream) {
+    if (!t || !out || !scratch || t->n <= 0 || t->p <= 0 || nparts < 1 || part < 0 || part >= nparts)
+        return dmabi::fail(DM_E_ARG, "bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t f = t->flags;
+    bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
+    dm::MemoLayout L = dm::memo_layout(t->n, t->p);
+    if (memo_ok && t->n <= 64 && L.bytes <= 110 * 1024 && !getenv_flag("DM_DISABLE_MEMO")) {
+        int grid = enum_grid() / 8 * 2;  // 2 CTAs x 512 threads per SM
+        if (L.S == 64) {
+            cudaFuncSetAttribute(dm::splits_memo_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+            dm::splits_memo_kernel<64><<<grid, dm::kMemoThreads, L.bytes, s>>>(*t, k0, k1, part, nparts,
+                                                                              (dm_winner*)scratch);
+        } else {
+            cudaFuncSetAttribute(dm::splits_memo_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+            dm::splits_memo_kernel<256><<<grid, dm::kMemoThreads, L.bytes, s>>>(*t, k0, k1, part, nparts,
+                                                                               (dm_winner*)scratch);
+        }
+        DM_CHECK_LAUNCH();
+        dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, grid, out);
+        DM_CHECK_LAUNCH();
+        return DM_OK;
+    }
+    return launch_enum<1>(t, k0, k1, part, nparts, out, scratch, s);
 }
 }  // namespace
 
@@ -714,31 +746,17 @@ int dm_enum_bruteforce(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* ou
                        void* scratch, void* stream) {
     if (!t || !out || !scratch || t->n <= 0 || t->p <= 0) return dmabi::fail(DM_E_ARG, "bad arguments");
     if (t->p > 1024) return dmabi::fail(DM_E_TOO_LARGE, "brute force supports at most 1024 workers");
-    return launch_enum<0>(t, k0, k1, out, scratch, (cudaStream_t)stream);
+    return launch_enum<0>(t, k0, k1, 0, 1, out, scratch, (cudaStream_t)stream);
 }
 
 int dm_enum_splits(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* out,
                    void* scratch, void* stream) {
-    if (!t || !out || !scratch || t->n <= 0 || t->p <= 0) return dmabi::fail(DM_E_ARG, "bad arguments");
-    cudaStream_t s = (cudaStream_t)stream;
-    const uint32_t f = t->flags;
-    bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
-    dm::MemoLayout L = dm::memo_layout(t->n, t->p);
-    if (memo_ok && t->n <= 64 && L.bytes <= 110 * 1024 && !getenv_flag("DM_DISABLE_MEMO")) {
-        int grid = enum_grid() / 8 * 2;  // 2 CTAs x 512 threads per SM
-        if (L.S == 64) {
-            cudaFuncSetAttribute(dm::splits_memo_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-            dm::splits_memo_kernel<64><<<grid, dm::kMemoThreads, L.bytes, s>>>(*t, k0, k1, (dm_winner*)scratch);
-        } else {
-            cudaFuncSetAttribute(dm::splits_memo_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-            dm::splits_memo_kernel<256><<<grid, dm::kMemoThreads, L.bytes, s>>>(*t, k0, k1, (dm_winner*)scratch);
-        }
-        DM_CHECK_LAUNCH();
-        dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, grid, out);
-        DM_CHECK_LAUNCH();
-        return DM_OK;
-    }
-    return launch_enum<1>(t, k0, k1, out, scratch, s);
+    return enum_splits_impl(t, k0, k1, 0, 1, out, scratch, stream);
+}
+
+int dm_enum_splits_part(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts,
+                        dm_winner* out, void* scratch, void* stream) {
+    return enum_splits_impl(t, k0, k1, part, nparts, out, scratch, stream);
 }
 
 int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,

@@ -277,26 +277,28 @@ __global__ void __launch_bounds__(kTile) eval_owner_kernel(dm_tables t, int64_t 
 // table lookup.  A candidate whose peer reappears (non-contiguous) or whose
 // owner index is out of range takes the general grouped path.
 constexpr int kStreamThreads = 256;
-constexpr int kStreamStages = 4;
 
-// shared-memory layout; every segment 16-byte aligned (TMA destinations)
+// shared-memory layout; every segment 16-byte aligned (TMA destinations).
+// The load table is square T[(a*(n+1) + b)*P + w] when it fits (no row-offset
+// lookup per run), else triangular T[(rowidx[a] + b)*P + w].
 struct StreamLayout {
-    int n, P, npairs;
-    size_t off_T, off_fit, off_rowidx, off_tiles, off_bar, bytes, tile_bytes;
+    int n, P, stages, cpt;
+    bool square;
+    size_t t_elems, off_T, off_rowidx, off_tiles, off_bar, bytes, tile_bytes;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-__host__ __device__ inline StreamLayout stream_layout(int n, int P) {
+__host__ __device__ inline StreamLayout stream_layout(int n, int P, int stages, int cpt, bool square) {
     StreamLayout L;
-    L.n = n; L.P = P; L.npairs = n * (n + 1) / 2;
+    L.n = n; L.P = P; L.stages = stages; L.cpt = cpt; L.square = square;
+    L.t_elems = square ? (size_t)n * (n + 1) * P : (size_t)n * (n + 1) / 2 * P;
     size_t off = 0;
-    L.off_T = off; off = al16(off + (size_t)L.npairs * P * 8);          // load (or compute) per (a,b,w)
-    L.off_fit = off;
+    L.off_T = off; off = al16(off + L.t_elems * 8);
     L.off_rowidx = off; off = al16(off + (size_t)(n + 1) * 4);
-    L.tile_bytes = al16((size_t)kStreamThreads * n);
-    L.off_tiles = off; off = al16(off + L.tile_bytes * kStreamStages + 16);
-    L.off_bar = off; off += 8 * kStreamStages;
+    L.tile_bytes = al16((size_t)kStreamThreads * cpt * n);
+    L.off_tiles = off; off = al16(off + L.tile_bytes * stages + 16);
+    L.off_bar = off; off += 8 * stages;
     L.bytes = al16(off);
     return L;
 }
@@ -320,40 +322,92 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                  "@!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
-template <bool PAIR>
-__global__ void __launch_bounds__(kStreamThreads) eval_owner_stream_kernel(dm_tables t, int64_t n_cand,
-                                                                           const uint8_t* __restrict__ owner,
-                                                                           double* __restrict__ out_mk,
-                                                                           uint8_t* __restrict__ out_code,
-                                                                           int64_t rank_base, dm_winner* partial) {
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64s(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
+// Run-boundary mask of one owner row (NW 32-bit words, row starting `sh`
+// bits into the first aligned word): bit i-1 <=> owner[i] != owner[i-1].
+// Fully unrolled per word count so every shift is a compile-time constant.
+template <int NW>
+__device__ __forceinline__ unsigned long long boundary_mask(uint32_t waddr, int sh) {
+    uint32_t m0 = 0, m1 = 0, prevw = 0, cur = lds_u32(waddr);
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        uint32_t nxt = lds_u32(waddr + 4 * (j + 1));
+        uint32_t wd = __funnelshift_r(cur, nxt, sh);
+        cur = nxt;
+        uint32_t x = wd ^ __byte_perm(prevw, wd, 0x6543);    // byte k vs byte k-1
+        uint32_t nz = (x | ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu)) & 0x80808080u;
+        uint32_t nib = (nz * 0x00204081u) >> 28;             // bit k <=> byte k differs
+        if (j < 8) m0 |= nib << (4 * j); else m1 |= nib << (4 * j - 32);
+        prevw = wd;
+    }
+    return (((unsigned long long)m1 << 32) | m0) >> 1;
+}
+
+__device__ __forceinline__ unsigned long long boundary_mask_n(int nw, uint32_t waddr, int sh) {
+    switch (nw) {
+        case 1: return boundary_mask<1>(waddr, sh);   case 2: return boundary_mask<2>(waddr, sh);
+        case 3: return boundary_mask<3>(waddr, sh);   case 4: return boundary_mask<4>(waddr, sh);
+        case 5: return boundary_mask<5>(waddr, sh);   case 6: return boundary_mask<6>(waddr, sh);
+        case 7: return boundary_mask<7>(waddr, sh);   case 8: return boundary_mask<8>(waddr, sh);
+        case 9: return boundary_mask<9>(waddr, sh);   case 10: return boundary_mask<10>(waddr, sh);
+        case 11: return boundary_mask<11>(waddr, sh); case 12: return boundary_mask<12>(waddr, sh);
+        case 13: return boundary_mask<13>(waddr, sh); case 14: return boundary_mask<14>(waddr, sh);
+        case 15: return boundary_mask<15>(waddr, sh); default: return boundary_mask<16>(waddr, sh);
+    }
+}
+
+template <bool PAIR, bool SQUARE>
+__global__ void __launch_bounds__(kStreamThreads, 2) eval_owner_stream_kernel(dm_tables t, int64_t n_cand,
+                                                                              const uint8_t* __restrict__ owner,
+                                                                              double* __restrict__ out_mk,
+                                                                              uint8_t* __restrict__ out_code,
+                                                                              int64_t rank_base, dm_winner* partial,
+                                                                              int stages, int cpt) {
     extern __shared__ __align__(128) unsigned char sm[];
     const int n = t.n, P = t.P;
-    const StreamLayout L = stream_layout(n, P);
-    // T[pr * P + w]: load of run (a, b) on w (compute only when PAIR), sign bit
-    // set when the run fails _fits (|T| is the value, -0.0 keeps the flag)
+    const StreamLayout L = stream_layout(n, P, stages, cpt, SQUARE);
+    // T: load of run (a, b) on w (compute only when PAIR); sign bit set when
+    // the run fails _fits (|T| is the value; -0.0 keeps the flag)
     double* T = reinterpret_cast<double*>(sm + L.off_T);
-    int32_t* rowidx = reinterpret_cast<int32_t*>(sm + L.off_rowidx);  // pair index of (a, b) = rowidx[a] + b
+    int32_t* rowidx = reinterpret_cast<int32_t*>(sm + L.off_rowidx);
     unsigned char* tiles = sm + L.off_tiles;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.off_bar);
-    const int64_t n_tiles = (n_cand + kStreamThreads - 1) / kStreamThreads;
-    const int64_t full_tiles = n_cand / kStreamThreads;
+    const int tile_cand = kStreamThreads * cpt;
+    const int64_t n_tiles = (n_cand + tile_cand - 1) / tile_cand;
+    const int64_t full_tiles = n_cand / tile_cand;
+    const uint32_t tile_load = (uint32_t)(tile_cand * n);
 
-    // ---- kick off the first tile loads before building the tables
     if (threadIdx.x == 0) {
-        for (int st = 0; st < kStreamStages; ++st) mbar_init(&bars[st], 1);
+        for (int st = 0; st < stages; ++st) mbar_init(&bars[st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int st = 0; st < kStreamStages; ++st) {
+        for (int st = 0; st < stages; ++st) {
             int64_t tl = blockIdx.x + (int64_t)st * gridDim.x;
             if (tl < full_tiles) {
-                mbar_expect_tx(&bars[st], (uint32_t)(kStreamThreads * n));
-                tma_load_1d(tiles + st * L.tile_bytes, owner + tl * kStreamThreads * n,
-                            (uint32_t)(kStreamThreads * n), &bars[st]);
+                mbar_expect_tx(&bars[st], tile_load);
+                tma_load_1d(tiles + st * L.tile_bytes, owner + tl * tile_cand * n, tile_load, &bars[st]);
             }
         }
     }
     for (int a = threadIdx.x; a <= n; a += blockDim.x) rowidx[a] = a * n - a * (a - 1) / 2 - a - 1;
     __syncthreads();
-    for (int it = threadIdx.x; it < L.npairs * P; it += blockDim.x) {
+    // ---- tables (reference arithmetic, once per CTA)
+    const int npairs = n * (n + 1) / 2;
+    for (int it = threadIdx.x; it < npairs * P; it += blockDim.x) {
         int pr = it / P, w = it % P;
         int a = 0;
         while (a + 1 < n && rowidx[a + 1] + (a + 2) <= pr) ++a;
@@ -366,21 +420,24 @@ __global__ void __launch_bounds__(kStreamThreads) eval_owner_stream_kernel(dm_ta
             v = c + rd;
         }
         if (!fits_range(t, w, a, b)) v = -v;
-        T[it] = v;
+        T[SQUARE ? ((size_t)a * (n + 1) + b) * P + w : (size_t)it] = v;
     }
     __syncthreads();
 
     const int tid = threadIdx.x;
     const int nw = (n + 3) >> 2;
-    const int last_valid = n - 4 * (nw - 1);                            // bytes of the last word in the row
-    const uint32_t last_mask = last_valid >= 4 ? 0xffffffffu : (0xffffffffu >> (8 * (4 - last_valid)));
+    const uint32_t sm_s = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t T_s = sm_s + (uint32_t)L.off_T, rowidx_s = sm_s + (uint32_t)L.off_rowidx;
+    const uint32_t uP = (uint32_t)P, Pm1 = uP - 1u, n1P8 = 8u * (uint32_t)(n + 1) * uP;
+    const uint32_t stage_mask_lo = n - 1 >= 32 ? 0xffffffffu : ((1u << (n - 1)) - 1u);
+    const uint32_t stage_mask_hi = n - 1 >= 64 ? 0xffffffffu : (n - 1 > 32 ? ((1u << (n - 33)) - 1u) : 0u);
     Win win; win_init(win);
     int64_t it_local = 0;
     for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x, ++it_local) {
-        const int st = (int)(it_local % kStreamStages);
-        const uint32_t parity = (uint32_t)((it_local / kStreamStages) & 1);
-        const int64_t c0 = tl * kStreamThreads;
-        const int cnt = (int)((n_cand - c0) < kStreamThreads ? (n_cand - c0) : kStreamThreads);
+        const int st = (int)(it_local % stages);
+        const uint32_t parity = (uint32_t)((it_local / stages) & 1);
+        const int64_t c0 = tl * tile_cand;
+        const int cnt = (int)((n_cand - c0) < tile_cand ? (n_cand - c0) : tile_cand);
         unsigned char* tile = tiles + st * L.tile_bytes;
         if (tl < full_tiles) {
             mbar_wait(&bars[st], parity);
@@ -388,75 +445,61 @@ __global__ void __launch_bounds__(kStreamThreads) eval_owner_stream_kernel(dm_ta
             for (int b = tid; b < cnt * n; b += blockDim.x) tile[b] = owner[c0 * n + b];
             __syncthreads();
         }
-        if (tid < cnt) {
-            const uint32_t row0 = (uint32_t)tid * n;
-            const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile) + (row0 >> 2);
-            const int sh = (row0 & 3) * 8;
-            // ---- run-boundary mask: bit i-1 <=> owner[i] != owner[i-1] (i >= 1)
-            uint32_t mlo = 0, mhi = 0, prevw = 0, cur = tw[0];
-            for (int j = 0; j < nw; ++j) {
-                uint32_t nxt = tw[j + 1];
-                uint32_t wd = __funnelshift_r(cur, nxt, sh);
-                cur = nxt;
-                uint32_t x = wd ^ __byte_perm(prevw, wd, 0x6543);    // byte k vs byte k-1
-                if (j == nw - 1) x &= last_mask;
-                uint32_t nz = (x | ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu)) & 0x80808080u;
-                uint32_t nib = (nz * 0x00204081u) >> 28;             // bit k <=> byte k differs
-                int pos = 4 * j - 1;                                   // bit of byte 0 (stage 4j)
-                if (j == 0) nib >>= 1, pos = 0;
-                if (pos < 32) { mlo |= nib << pos; if (pos > 28) mhi |= nib >> (32 - pos); }
-                else mhi |= nib << (pos - 32);
-                prevw = wd;
-            }
+        const uint32_t tile_s = sm_s + (uint32_t)(tile - sm);
+#pragma unroll 1
+        for (int ci = tid; ci < cnt; ci += kStreamThreads) {
+            const uint32_t row_s = tile_s + (uint32_t)ci * n;        // shared address of the row
+            const unsigned long long bm = boundary_mask_n(nw, row_s & ~3u, (int)(row_s & 3u) * 8);
             // ---- runs: b = each boundary in ascending order, then n
-            const uint8_t* row = tile + row0;
             double mk = 0.0;
-            int code = DM_V_OK, flag = 0, a = 0, prev = -1;
-            unsigned long long seen = 0;
+            int code = DM_V_OK, a = 0, prev = -1, nruns = 0;
+            uint32_t wmax = 0, seen = 0, rowb = T_s;                 // rowb: address of T[a][0][0] (square)
             auto run = [&](int b) {
-                int w = row[a];
-                flag |= (w >= P);
-                w = w < P ? w : P - 1;
-                unsigned long long bit = 1ull << w;
-                flag |= ((seen & bit) != 0) << 1;
-                seen |= bit;
-                const int pr = rowidx[a] + b;
-                const double tv = T[pr * P + w];
+                uint32_t w = lds_u8(row_s + a);
+                wmax = max(wmax, w);
+                w = min(w, Pm1);
+                seen |= 1u << w;
+                ++nruns;
+                uint32_t addr;
+                if (SQUARE) addr = rowb + 8u * ((uint32_t)b * uP + w);
+                else addr = T_s + 8u * ((lds_u32(rowidx_s + 4u * a) + b) * uP + w);
+                const double tv = lds_f64s(addr);
                 double v = fabs(tv);
                 if (PAIR && a > 0) {
                     double al, be;
-                    link_of(t, prev, w, al, be);
+                    link_of(t, prev, (int)w, al, be);
                     double rd = 0.0;
                     for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
                         rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
                     v = v + rd;
                 }
                 mk = v > mk ? v : mk;
-                if (signbit(tv) && code == DM_V_OK) code = cap_violation(t, w, a, b);
-                prev = w; a = b;
+                if (signbit(tv) && code == DM_V_OK) code = cap_violation(t, (int)w, a, b);
+                prev = (int)w; a = b;
+                if (SQUARE) rowb = T_s + (uint32_t)b * n1P8;
             };
-            for (uint32_t y = mlo; y; y &= y - 1) run(__ffs(y));
-            for (uint32_t y = mhi; y; y &= y - 1) run(32 + __ffs(y));
+            for (uint32_t y = (uint32_t)bm & stage_mask_lo; y; y &= y - 1) run(__ffs(y));
+            for (uint32_t y = (uint32_t)(bm >> 32) & stage_mask_hi; y; y &= y - 1) run(32 + __ffs(y));
             run(n);
-            bool unknown = flag & 1;
-            if (flag == 2) eval_owner_grouped(t, row, mk, code);   // a peer holds two runs
-            out_mk[c0 + tid] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
-            out_code[c0 + tid] = unknown ? (uint8_t)0xFF : (uint8_t)code;
+            const bool unknown = wmax >= uP;
+            if (!unknown && __popc(seen) != nruns) eval_owner_grouped(t, tile + (size_t)ci * n, mk, code);
+            out_mk[c0 + ci] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
+            out_code[c0 + ci] = unknown ? (uint8_t)0xFF : (uint8_t)code;
             if (partial) {                       // fused arg-min (first strict minimum by rank)
                 win.n_eval++;
                 if (!unknown && code == DM_V_OK) {
                     win.n_feas++;
                     win.csum += (uint64_t)__double_as_longlong(mk);
-                    if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank_base + c0 + tid; }
+                    if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank_base + c0 + ci; }
                 }
             }
         }
         __syncthreads();  // every thread is done with this slot
         if (tid == 0) {
-            int64_t nt = tl + (int64_t)kStreamStages * gridDim.x;
+            int64_t nt = tl + (int64_t)stages * gridDim.x;
             if (nt < full_tiles) {
-                mbar_expect_tx(&bars[st], (uint32_t)(kStreamThreads * n));
-                tma_load_1d(tile, owner + nt * kStreamThreads * n, (uint32_t)(kStreamThreads * n), &bars[st]);
+                mbar_expect_tx(&bars[st], tile_load);
+                tma_load_1d(tile, owner + nt * tile_cand * n, tile_load, &bars[st]);
             }
         }
     }
@@ -571,24 +614,35 @@ static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner
     {
         const uint32_t f = t->flags;
         bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
-        dm::StreamLayout L = dm::stream_layout(t->n, t->P);
+        // pick the largest configuration that fits: square table if possible,
+        // 4 candidates per thread, 4 stages; shrink towards 1 cand x 2 stages
+        dm::StreamLayout L{};
+        bool found = false;
+        for (int sq = 1; sq >= 0 && !found; --sq)
+            for (int cpt = 4; cpt >= 1 && !found; cpt /= 2)
+                for (int stages = 4; stages >= 2 && !found; --stages) {
+                    L = dm::stream_layout(t->n, t->P, stages, cpt, sq == 1);
+                    if (L.bytes <= (sq ? 110 * 1024 : 220 * 1024)) found = true;
+                }
         const char* dis = std::getenv("DM_DISABLE_MEMO");
         bool aligned = (((uintptr_t)owner) & 15) == 0;
-        if (owner_bytes == 1 && memo_ok && aligned && t->n <= 64 && t->P <= 64 && L.bytes <= 220 * 1024 &&
+        if (found && owner_bytes == 1 && memo_ok && aligned && t->n <= 64 && t->P <= 32 &&
             !(dis && dis[0] && dis[0] != '0')) {
             int per_sm = (int)((225 * 1024) / (L.bytes + 1024));
             if (per_sm < 1) per_sm = 1;
-            if (per_sm > 12) per_sm = 12;
-            int64_t n_tiles = (n_cand + dm::kStreamThreads - 1) / dm::kStreamThreads;
+            if (per_sm > 2) per_sm = 2;
+            const int tile_cand = dm::kStreamThreads * L.cpt;
+            int64_t n_tiles = (n_cand + tile_cand - 1) / tile_cand;
             int64_t grid = (int64_t)sm_count() * per_sm;
             if (grid > n_tiles) grid = n_tiles;
             if (out && grid > 8 * sm_count()) grid = 8 * sm_count();   // partial slots in scratch
             const bool pair = (t->flags & DM_F_INCLUDE_COMM) && (t->flags & DM_F_PAIR_LINKS);
-            auto kern = pair ? dm::eval_owner_stream_kernel<true> : dm::eval_owner_stream_kernel<false>;
+            auto kern = pair ? (L.square ? dm::eval_owner_stream_kernel<true, true> : dm::eval_owner_stream_kernel<true, false>)
+                             : (L.square ? dm::eval_owner_stream_kernel<false, true> : dm::eval_owner_stream_kernel<false, false>);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
             kern<<<(int)grid, dm::kStreamThreads, L.bytes, s>>>(*t, n_cand, (const uint8_t*)owner, out_makespan,
                                                                out_code, rank_base,
-                                                               out ? (dm_winner*)scratch : nullptr);
+                                                               out ? (dm_winner*)scratch : nullptr, L.stages, L.cpt);
             DM_CHECK_LAUNCH();
             if (out) {
                 dm::finalize_argmin_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, (int)grid, out);

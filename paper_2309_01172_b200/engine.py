@@ -124,7 +124,7 @@ def argmin_scores(mk, code, rank_base: int = 0, bufs: WinnerBuffers | None = Non
 
 
 def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | None = None,
-         index: int = 0, online=None, mults=None, seed: int = 0):
+         index: int = 0, online=None, mults=None, seed: int = 0, part: int = 0, nparts: int = 1):
     """Mode B enumeration: 'bruteforce' | 'splits' | 'random'. Returns bufs
     (call bufs.read() to synchronise and fetch the winner)."""
     lib = _lib.load()
@@ -134,7 +134,11 @@ def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | 
     if mode == "bruteforce":
         _lib.check(lib.dm_enum_bruteforce(C.byref(st), k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
     elif mode == "splits":
-        _lib.check(lib.dm_enum_splits(C.byref(st), k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
+        if nparts > 1:
+            _lib.check(lib.dm_enum_splits_part(C.byref(st), k0, k1, part, nparts, bufs.out.data_ptr(),
+                                               bufs.scratch.data_ptr(), s))
+        else:
+            _lib.check(lib.dm_enum_splits(C.byref(st), k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
     elif mode == "random":
         _lib.check(lib.dm_enum_random(C.byref(st), online.data_ptr(), online.numel(), mults.data_ptr(),
                                       mults.numel(), seed & 0xFFFFFFFFFFFFFFFF, k0, k1, bufs.out.data_ptr(),

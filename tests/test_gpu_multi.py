@@ -37,8 +37,7 @@ def _worker(rank, world, port, q):
     st, fl = big_instance(np.random.default_rng(5), 30, 24, dag=False, pressure=(0.1, 0.6))
     batch = engine.device_batch([build_host(st, fl)], device=torch.device("cuda", rank))
     total = engine.splits_total(30, 24)
-    k0, k1 = D.shard(total, rank, world)
-    bufs = engine.enum(batch, "splits", k0, k1)
+    bufs = engine.enum(batch, "splits", 0, total, part=rank, nparts=world)
     merged = D.merge_records(D.all_gather_winner(bufs.out).cpu().numpy())
     if rank == 0:
         single = engine.enum(batch, "splits", 0, total).read()

@@ -328,3 +328,24 @@ def test_materialized_stream_matches_enumeration(engine_ready):
     own = engine.materialize(9, 5, "bruteforce", 0, bf_total)
     mk, code = engine.eval_owner(batch, own)
     assert engine.argmin_scores(mk, code).read() == engine.enum(batch, "bruteforce", 0, bf_total).read()
+
+
+def test_split_parts_partition_the_population(engine_ready):
+    """dm_enum_splits_part: the interleaved parts are disjoint and cover the
+    population; merging their records equals the single sweep."""
+    import struct
+    from paper_2309_01172_b200 import dist as D
+    rng = np.random.default_rng(17)
+    for dag, links in ((False, False), (True, False), (True, True)):
+        st, fleet = big_instance(rng, 26 if not links else 20, 20 if not links else 9, dag=dag, links=links,
+                                 pressure=(0.1, 0.7))
+        batch = engine.device_batch([build_host(st, fleet)])
+        total = engine.splits_total(len(st), len(fleet.worker_ids()))
+        full = engine.enum(batch, "splits", 0, total).read()
+        for nparts in (2, 3, 8):
+            recs = []
+            for part in range(nparts):
+                w = engine.enum(batch, "splits", 0, total, part=part, nparts=nparts).read()
+                recs.append(struct.pack(D.WINNER_FMT, w["makespan"], w["rank"], w["n_evaluated"], w["n_feasible"],
+                                        w["checksum"]))
+            assert D.merge_records(np.frombuffer(b"".join(recs), np.uint8)) == full
