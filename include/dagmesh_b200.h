@@ -271,6 +271,34 @@ DM_API int dm_pipeline_epilogue(const dm_tables* tables, int32_t n_scen, int32_t
                          const int16_t* owner, int64_t n_batches,
                          int64_t samples_per_batch, double* out, void* stream);
 
+/*
+ * Operator-level PALEO cost (hardware.op_time, hardware.py:190-206) over a
+ * DAG of operators, batched over placements.  dm_ops holds, per operator i:
+ * op_flops(node) (as f64), message_bytes(node, msg_ratio) (int-valued f64),
+ * its args and users (CSR).  place[b*n_ops + i] = peer index of op i in
+ * placement b (dm_tables indexing; >= P for peers unknown to the fleet).
+ * out[(b*n_ops + i)*3 + {0,1,2}] = read_s, compute_s, write_s.
+ */
+typedef struct dm_ops {
+    int32_t n_ops;
+    int32_t pad_;
+    const double* flops;
+    const double* mbytes;
+    const int32_t* arg_ptr;    /* [n_ops+1] */
+    const int32_t* arg_idx;
+    const int32_t* user_ptr;   /* [n_ops+1] */
+    const int32_t* user_idx;
+} dm_ops;
+
+DM_API int dm_op_costs(const dm_ops* ops, const dm_tables* t, const double* write_bw,
+                       int32_t n_place, const int32_t* place, double* out, void* stream);
+
+/* hardware.subgraph_time (hardware.py:219-226) for cells sub_idx[sub_ptr[s]..]
+ * over op costs from dm_op_costs: out[(b*n_sub + s)*3] = lower, upper, sequential. */
+DM_API int dm_subgraph_times(int32_t n_ops, int32_t n_place, const double* op_out,
+                             int32_t n_sub, const int32_t* sub_ptr, const int32_t* sub_idx,
+                             double* out, void* stream);
+
 /* dm_microbench_fp64 — FP64 DMUL+DADD issue-rate microbenchmark (the
  * roofline denominator of the generated-candidate kernels).  *ops receives
  * the number of fp64 operations the launch performs; time it with events. */

@@ -667,4 +667,49 @@ EXPORT void or_epilogue(int r, const double* compute, const double* read, int64_
     free(tot);
 }
 
+/* ----------------------------------------------------------- op costs */
+
+/* hardware.op_time (hardware.py:190-206) for every op of one placement:
+ * read = naive sum over args on other peers of comm_time(link_between, M),
+ * compute = op_flops / effective_speed, write = M / write_bandwidth when any
+ * user sits on another peer. */
+EXPORT void or_op_costs(const dm_tables* t, int n_ops, const double* flops, const double* mbytes,
+                        const int32_t* aptr, const int32_t* aidx, const int32_t* uptr, const int32_t* uidx,
+                        const double* write_bw, const int32_t* place, double* out) {
+    for (int i = 0; i < n_ops; ++i) {
+        int me = place[i];
+        double* o = out + 3 * i;
+        if (me < 0 || me >= t->P) { o[0] = o[1] = o[2] = NAN; continue; }
+        double rd = 0.0;
+        for (int e = aptr[i]; e < aptr[i + 1]; ++e) {
+            int src = place[aidx[e]];
+            if (src != me) {
+                double al, be;
+                link_of(t, src, me, &al, &be);
+                rd += comm_time(al, be, mbytes[aidx[e]]);
+            }
+        }
+        double wr = 0.0;
+        for (int e = uptr[i]; e < uptr[i + 1]; ++e)
+            if (place[uidx[e]] != me) { wr = mbytes[i] / write_bw[me]; break; }
+        o[0] = rd; o[1] = flops[i] / t->speed[me]; o[2] = wr;
+    }
+}
+
+/* hardware.subgraph_time (hardware.py:219-226): max and CPython sum of the
+ * per-op totals read + compute + write. */
+EXPORT void or_subgraph(int k, const int32_t* idx, const double* op_out, double* out3) {
+    if (k == 0) { out3[0] = out3[1] = out3[2] = 0.0; return; }
+    double* tot = (double*)malloc(sizeof(double) * (size_t)k);
+    double mx = 0.0;
+    for (int q = 0; q < k; ++q) {
+        const double* o = op_out + 3 * idx[q];
+        tot[q] = o[0] + o[1] + o[2];
+        if (q == 0 || tot[q] > mx) mx = tot[q];
+    }
+    double seq = or_py_sum(tot, k);
+    out3[0] = mx; out3[1] = seq; out3[2] = seq;
+    free(tot);
+}
+
 EXPORT int or_abi_version(void) { return DM_ABI_VERSION; }

@@ -51,6 +51,11 @@ class DmTables(C.Structure):
     ]
 
 
+class DmOps(C.Structure):
+    _fields_ = [("n_ops", C.c_int32), ("pad_", C.c_int32), ("flops", _P), ("mbytes", _P), ("arg_ptr", _P),
+                ("arg_idx", _P), ("user_ptr", _P), ("user_idx", _P)]
+
+
 class DmWinner(C.Structure):
     _fields_ = [("makespan", C.c_double), ("rank", C.c_int64), ("n_evaluated", C.c_int64),
                 ("n_feasible", C.c_int64), ("checksum", C.c_uint64)]
@@ -75,6 +80,8 @@ _SIGS = {
     "dm_prop_hill": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
     "dm_pipeline_epilogue": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int64, C.c_int64, _P, _P]),
     "dm_microbench_fp64": (C.c_int, [C.c_int64, _P, _P, _P]),
+    "dm_op_costs": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, _P]),
+    "dm_subgraph_times": (C.c_int, [C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, _P, _P]),
     "dm_materialize": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64, _P, C.c_int32, _P]),
 }
 

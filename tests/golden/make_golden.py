@@ -8,7 +8,8 @@ Run in the build container (the reference is not present on the GPU box):
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
 
 Outputs (committed): tests/golden/scheduling_cases.json,
-tests/golden/pipeline_cases.json, tests/golden/stage_digests.json.
+tests/golden/pipeline_cases.json, tests/golden/stage_digests.json,
+tests/golden/opcost_cases.json.
 
 Instances are stored in a neutral JSON form (ints stay ints, floats are
 written with repr so they round-trip bit-exactly; `tests/golden_io.py` reads
@@ -206,6 +207,36 @@ def pipeline_cases():
     return out
 
 
+def opcost_cases():
+    """hardware.op_time / subgraph_time (hardware.py:190-226) on the demo job:
+    the reference's own test placements (test_hardware.py:100-129) plus
+    seeded random placements, slow-writer and msg_ratio variants."""
+    demo = ir.load_job(REF / "jobs" / "demo.json")
+    trio = hw.load_fleet(REF / "fleets" / "trio.json")
+    names = list(demo.nodes)
+    table = {"names": names,
+             "flops": [int(ir.op_flops(demo.node(n))) for n in names],
+             "out_elements": [int(demo.node(n).out_elements) for n in names],
+             "args": [[names.index(a) for a in demo.node(n).args] for n in names],
+             "users": [[names.index(u) for u in demo.node(n).users] for n in names]}
+    slow = hw.Fleet(dict(trio.peers, **{"1": hw.Peer("1", peak_flops=2e6, write_bandwidth=1024.0)}),
+                    default_link=trio.default_link, links=trio.links)
+    halfmsg = hw.Fleet(dict(trio.peers), default_link=trio.default_link, links=trio.links, msg_ratio=0.37)
+    rng = np.random.default_rng(91)
+    placements = [dict(demo.placement)]
+    for _ in range(12):
+        placements.append({n: str(int(rng.integers(1, 5))) for n in names})
+    cells = [("TensorA", "Multiply"), tuple(names), ("Conv", "Add", "Pool"), ("Label",)]
+    out = {"table": table, "placements": placements, "cells": [list(c) for c in cells], "fleets": []}
+    for fl in (trio, slow, halfmsg):
+        rows, subs = [], []
+        for pl in placements:
+            rows.append([list(hw.op_time(demo, n, fl, pl)) for n in names])
+            subs.append([list(hw.subgraph_time(demo, c, fl, pl)) for c in cells])
+        out["fleets"].append({"fleet": dump_fleet(fl), "ops": rows, "subgraphs": subs})
+    return out
+
+
 def stage_digests():
     from paper_2309_01172_b200 import configs as CF
     out = {}
@@ -229,7 +260,8 @@ def main():
     (HERE / "scheduling_cases.json").write_text(json.dumps({"python": sys.version, "cases": scheduling_cases()}))
     (HERE / "pipeline_cases.json").write_text(json.dumps(pipeline_cases()))
     (HERE / "stage_digests.json").write_text(json.dumps(stage_digests(), indent=1))
-    for f in ("scheduling_cases.json", "pipeline_cases.json", "stage_digests.json"):
+    (HERE / "opcost_cases.json").write_text(json.dumps(opcost_cases()))
+    for f in ("scheduling_cases.json", "pipeline_cases.json", "stage_digests.json", "opcost_cases.json"):
         print(f, (HERE / f).stat().st_size, "bytes")
 
 
