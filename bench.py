@@ -413,6 +413,65 @@ def random_measure(dev, which):
             "oracle_prefix_check": got == ref, "cpu_baseline_1core": cpu}
 
 
+def dp_c4b_measure(dev, n_scen=4096):
+    """Config C4b: layer-cell encoder chains (n = L + 2 <= 38) over p <= 8
+    workers, the sizes where schedule() takes the exact subset DP."""
+    import time as _t
+    import numpy as np
+    from oracle import oracle
+    from paper_2309_01172_b200 import configs as CF
+    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200.tensorize import build_host
+    rng = np.random.default_rng(7)
+    models = {L: CF.encoder_stages(4096, L, 32000, 4, 1024, cells="layer") for L in range(24, 37)}
+    insts, hosts = [], []
+    for s_ in range(n_scen):
+        L = int(rng.integers(24, 37))
+        p = int(rng.integers(5, 9))
+        peers = CF.hetero_peers(p, int(rng.integers(1 << 30)), lam=(0.3, 1.0))
+        doc = CF.fleet_doc(peers, float(rng.uniform(0, 1e-2)), float(10 ** rng.uniform(-1, 1)))
+        fl = CF.load(doc)
+        st = models[L]
+        assert len(st) ** 2 * p * 2 ** p <= 3_000_000
+        insts.append((st, fl))
+        hosts.append(build_host(st, fl, True))
+    batch = engine.device_batch(hosts, device=dev)
+    n_max = max(h.n for h in hosts)
+    ms = _time_ms(lambda: engine.subset_dp(batch, n_max, 8), steps=3)
+    own, mk, found, _ = engine.subset_dp(batch, n_max, 8)
+    own = own.cpu().numpy()
+    ok = True
+    t0 = _t.perf_counter()
+    for i in range(0, n_scen, n_scen // 8):
+        o, _ = oracle.Instance(*insts[i]).subset_dp()
+        ok &= (o is None and not int(found[i])) or (o is not None and own[i, :len(insts[i][0])].tolist() == o.tolist())
+    cpu = 8 / (_t.perf_counter() - t0)
+    return {"config": f"C4b: {n_scen} scenarios, layer-cell chains n = L+2 in [26, 38], p in [5, 8] "
+                      "(n^2 p 2^p <= 3e6: the exact subset-DP path)", "dps": n_scen, "ms": ms,
+            "value": n_scen / (ms / 1e3), "unit": "DPs/s", "oracle_spot_check": bool(ok), "cpu_baseline_1core": cpu}
+
+
+def api_latency_measure(dev):
+    """End-to-end latency of one public schedule() call (host objects in, a
+    ScheduleReport out; tensorise + H2D + DP kernel + report kernel + D2H) on C1."""
+    import time as _t
+    import torch
+    from paper_2309_01172_b200 import configs as CF
+    from paper_2309_01172_b200 import scheduling as S
+    stages = CF.model_stages("gpt2-small")
+    fleet = CF.load(CF.c1_fleet_doc(10.0, 1e-3))
+    for _ in range(3):
+        S.schedule(stages, fleet)
+    torch.cuda.synchronize()
+    t0 = _t.perf_counter()
+    for _ in range(20):
+        rep = S.schedule(stages, fleet)
+    el = (_t.perf_counter() - t0) / 20
+    return {"config": "C1 gpt2-small x 4 mixed GPUs (10 Gbit/s, 1 ms): schedule() through the public API",
+            "ms_per_call": el * 1e3, "runs": [list(r[1][:1]) + [r[1][-1], r[0]] for r in rep.runs],
+            "makespan": rep.makespan, "trace": list(rep.trace)}
+
+
 def secondary_measurements(dev):
     """FP64 peak microbenchmark (roofline denominator), CPU baseline, and the
     secondary paths of the metric: Mode A streams (HBM roofline), DPs/s, schedules/s."""
@@ -423,7 +482,8 @@ def secondary_measurements(dev):
     sec = {}
     for name, fn in (("mode_a_c1", lambda: mode_a_measure(dev, "c1")), ("mode_a_c2", lambda: mode_a_measure(dev, "c2")),
                      ("dp_c1_grid", lambda: dp_measure(dev)), ("schedule_c4", lambda: c4_measure(dev)),
-                     ("random_c5", lambda: random_measure(dev, "c5")), ("random_c3", lambda: random_measure(dev, "c3"))):
+                     ("random_c5", lambda: random_measure(dev, "c5")), ("random_c3", lambda: random_measure(dev, "c3")),
+                     ("dp_c4b", lambda: dp_c4b_measure(dev)), ("schedule_api_latency_c1", lambda: api_latency_measure(dev))):
         try:
             sec[name] = fn()
         except Exception as exc:

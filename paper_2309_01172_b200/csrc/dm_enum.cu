@@ -563,7 +563,58 @@ __device__ __forceinline__ double div_markstein(double a, double b, double rcp) 
     return __fma_rn(rem, rcp, q0);
 }
 
-__global__ void __launch_bounds__(256) enum_random_fast_kernel(dm_tables t, const int32_t* __restrict__ online,
+__device__ __forceinline__ void lds_v2(uint32_t a, double& x, double& y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+__device__ __forceinline__ double lds_d(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_i(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// Cut positions of candidate k in ascending order, then n, then -1.  The
+// (n-1)-bit cut mask (<= 4 words, n <= 257) is generated up front and
+// consumed as a 4-word shift queue, so no RNG work sits in the run loop.
+struct CutIter {
+    uint64_t cw, w1, w2, w3;
+    int base, n;
+    bool done;
+    __device__ __forceinline__ void init(uint64_t key, int64_t k, int n_) {
+        n = n_; base = 0; done = false;
+        const int nwords = (n - 1 + 63) >> 6;
+        uint64_t w[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j < nwords) {
+                uint64_t x = rng_word(key, k, j);
+                const int valid = (n - 1) - 64 * j;
+                if (valid < 64) x &= (1ull << valid) - 1ull;
+                w[j] = x;
+            }
+        }
+        cw = w[0]; w1 = w[1]; w2 = w[2]; w3 = w[3];
+    }
+    __device__ __forceinline__ int next() {
+        while (!cw) {
+            if (!(w1 | w2 | w3)) {
+                if (done) return -1;
+                done = true;
+                return n;
+            }
+            cw = w1; w1 = w2; w2 = w3; w3 = 0ull; base += 64;
+        }
+        const int b = base + __ffsll((long long)cw);
+        cw &= cw - 1;
+        return b;
+    }
+};
+
+__global__ void __launch_bounds__(256, 3) enum_random_fast_kernel(dm_tables t, const int32_t* __restrict__ online,
                                                                int32_t n_online, const int32_t* __restrict__ mults,
                                                                int32_t n_mults, uint64_t key, int64_t k0, int64_t k1,
                                                                dm_winner* partial) {
@@ -595,54 +646,53 @@ __global__ void __launch_bounds__(256) enum_random_fast_kernel(dm_tables t, cons
     for (int i = threadIdx.x; i < n_mults; i += blockDim.x) mul[i] = mults[i];
     __syncthreads();
 
+    const uint32_t SR_s = (uint32_t)__cvta_generic_to_shared(SR), PR_s = (uint32_t)__cvta_generic_to_shared(PR);
     Win w; win_init(w);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int nwords = (n - 1 + 63) >> 6;
     for (int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1; k += stride) {
-        uint64_t h4 = rng_word(key, k, 6), h5 = rng_word(key, k, 7);
+        const uint64_t h4 = rng_word(key, k, 6), h5 = rng_word(key, k, 7);
         const int am = (int)(((int64_t)mul[h4 % (uint64_t)n_mults]) % n_online);
-        int pos_peer = (int)(h5 % (uint64_t)n_online);             // (b0 + am*q) mod n_online
+        int pos = (int)(h5 % (uint64_t)n_online);                   // (b0 + am*q) mod n_online
+        CutIter it;
+        it.init(key, k, n);
         bool ok = true;
         double mk = 0.0;
         int a = 0, prev = -1;
-        StageRec ra = SR[0];
-        for (int j = 0; j <= nwords; ++j) {
-            uint64_t bits = 0;
-            if (j < nwords) {
-                bits = rng_word(key, k, j);
-                int valid = (n - 1) - 64 * j;                          // positions 64j+1 .. 64j+valid
-                if (valid < 64) bits &= (1ull << valid) - 1ull;
-            }
-            while (true) {
-                int b;
-                if (bits) { b = 64 * j + __ffsll((long long)bits); bits &= bits - 1; }
-                else if (j == nwords) b = n;
-                else break;
-                const StageRec rb = SR[b];
-                const PeerRec pr = PR[pos_peer];
-                const int pe = pr.pe;
-                pos_peer += am;
-                if (pos_peer >= n_online) pos_peer -= n_online;
-                // _fits (scheduling.py:172-176): exact prefix differences vs capacities
-                ok &= (rb.pg - ra.pg <= pr.cg) & (rb.pc - ra.pc <= pr.cc) & (rb.pd - ra.pd <= pr.cd);
-                // _run_cost: compute + crossing read from the previous run's peer
-                const double compute = div_markstein(rb.pf - ra.pf, pr.speed, pr.rcp);
-                double rd = 0.0;
-                if (comm && a > 0) {
-                    if (pair) {
-                        double al, be;
-                        link_of(t, prev, pe, al, be);
-                        for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
-                            rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
-                    } else {
-                        rd = ra.R;
-                    }
+        // previous boundary record (prefix sums at a, read of a run starting at a)
+        double af, ag, ac, ad, aR;
+        lds_v2(SR_s, af, ag); lds_v2(SR_s + 16, ac, ad); aR = lds_d(SR_s + 32);
+        int b = it.next();
+        while (b >= 0) {
+            // both records of this run are requested before any arithmetic
+            const uint32_t sb = SR_s + (uint32_t)b * (uint32_t)sizeof(StageRec);
+            const uint32_t pb = PR_s + (uint32_t)pos * (uint32_t)sizeof(PeerRec);
+            double bf, bg, bc, bd, bR, sp, rc, cg, cc, cd;
+            lds_v2(sb, bf, bg); lds_v2(sb + 16, bc, bd); bR = lds_d(sb + 32);
+            lds_v2(pb, sp, rc); lds_v2(pb + 16, cg, cc); cd = lds_d(pb + 32);
+            const int pe = pair ? lds_i(pb + 40) : 0;
+            const int bn = it.next();                                  // next boundary, off the critical path
+            pos += am;
+            if (pos >= n_online) pos -= n_online;
+            // _fits (scheduling.py:172-176): exact prefix differences vs capacities
+            ok &= (bg - ag <= cg) & (bc - ac <= cc) & (bd - ad <= cd);
+            // _run_cost: compute (Markstein-corrected quotient) + crossing read
+            const double compute = div_markstein(bf - af, sp, rc);
+            double rd = 0.0;
+            if (comm && a > 0) {
+                if (pair) {
+                    double al, be;
+                    link_of(t, prev, pe, al, be);
+                    for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
+                        rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
+                } else {
+                    rd = aR;
                 }
-                const double load = compute + rd;
-                mk = load > mk ? load : mk;
-                prev = pe; a = b; ra = rb;
-                if (b == n) break;
             }
+            const double load = compute + rd;
+            mk = load > mk ? load : mk;
+            prev = pe; a = b;
+            af = bf; ag = bg; ac = bc; ad = bd; aR = bR;
+            b = bn;
         }
         w.n_eval++;
         if (ok) win_add(w, mk, k);
@@ -773,9 +823,9 @@ int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,
     uint64_t key = dm::fmix64(seed + 0x9E3779B97F4A7C15ULL);
     dm::RandLayout L = dm::rand_layout(t->n, t->P, n_online, n_mults);
     const bool exact = (t->flags & DM_F_FLOPS_EXACT) && (t->flags & DM_F_BYTES_EXACT);
-    if (exact && L.bytes <= 200 * 1024 && !getenv_flag("DM_DISABLE_MEMO")) {
+    if (exact && t->n <= 257 && L.bytes <= 200 * 1024 && !getenv_flag("DM_DISABLE_MEMO")) {
         int per_sm = (int)((220 * 1024) / (L.bytes + 2048));
-        if (per_sm > 8) per_sm = 8;
+        if (per_sm > 3) per_sm = 3;
         if (per_sm < 1) per_sm = 1;
         grid = enum_grid() / 8 * per_sm;
         cudaFuncSetAttribute(dm::enum_random_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
