@@ -16,7 +16,7 @@ include/dagmesh_b200.h); there is no CPU fallback.
 
 from __future__ import annotations
 
-from . import _lib, engine, model, pipeline, scheduling, tensorize
+from . import _lib, engine, model, opcost, pipeline, scheduling, tensorize
 from ._lib import EngineError, EngineUnavailable
 from .model import (GPU_TABLE, DagmeshError, Fleet, FleetError, Link, Peer, PeerLoad, Role,
                     ScheduleReport, SchedulingError, Stage, ZERO_LINK, bandwidth_to_beta, comm_time,
@@ -36,8 +36,8 @@ def install(dagmesh_module=None):
 
     Rebinds ``dagmesh.scheduling.{schedule, evaluate_runs,
     brute_force_schedule, verify_assignment, reschedule_on_failure}``, the
-    early-bound re-exports in ``dagmesh/__init__.py:23-25`` and
-    ``dagmesh.pipeline.sweep``; reports are then built from the reference's
+    early-bound re-exports in ``dagmesh/__init__.py:12-25``,
+    ``dagmesh.pipeline.sweep`` and ``dagmesh.hardware.{op_time, subgraph_time}``; reports are then built from the reference's
     own ``ScheduleReport``/``PeerLoad`` classes and errors are the
     reference's ``SchedulingError``/``FleetError``.  Every reference caller
     resolves these through the module attribute at call time (pipeline.py:237,
@@ -45,6 +45,7 @@ def install(dagmesh_module=None):
     path.  Returns a callable that restores the originals."""
     if dagmesh_module is None:
         import dagmesh as dagmesh_module
+    engine.warmup()
     ref_sched = dagmesh_module.scheduling
     ref_pipe = dagmesh_module.pipeline
     ref_err = dagmesh_module.errors
@@ -72,6 +73,13 @@ def install(dagmesh_module=None):
 
     saved[(ref_pipe, "sweep")] = ref_pipe.sweep
     ref_pipe.sweep = _sweep
+    ref_hw = dagmesh_module.hardware
+    for name in ("op_time", "subgraph_time"):
+        saved[(ref_hw, name)] = getattr(ref_hw, name)
+        setattr(ref_hw, name, getattr(opcost, name))
+        if hasattr(dagmesh_module, name):
+            saved[(dagmesh_module, name)] = getattr(dagmesh_module, name)
+            setattr(dagmesh_module, name, getattr(opcost, name))
     if hasattr(dagmesh_module, "sweep"):
         saved[(dagmesh_module, "sweep")] = dagmesh_module.sweep
         dagmesh_module.sweep = _sweep

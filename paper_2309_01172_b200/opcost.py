@@ -98,7 +98,7 @@ def op_costs(table: OpTable, fleet, placements) -> np.ndarray:
             place[b, i] = host.index_of[pid] if pid in host.index_of else unknown.setdefault(pid, host.P + len(unknown))
     write_bw = np.array([float(fleet.peers[p].write_bandwidth) for p in host.peer_ids] or [1.0], np.float64)
     from .engine import device_batch
-    batch = device_batch([host])
+    batch = device_batch([host], pin=False)
     dev = batch.dev_buf.device
     arrs = [torch.from_numpy(a).to(dev) for a in (flops, mbytes, aptr, aidx, uptr, uidx, write_bw, place.reshape(-1))]
     ops = _lib.DmOps(n, 0, *[a.data_ptr() for a in arrs[:6]])

@@ -193,7 +193,7 @@ def brute_force_schedule(stages, fleet, *, include_comm: bool = True, limit: int
         raise T.SchedulingError(f"instance too large for enumeration: "
                                 f"{total} contiguous assignments > {limit}")
     host = build_host(stages, fleet, include_comm)
-    batch = engine.device_batch([host])
+    batch = engine.device_batch([host], pin=False)
     win = engine.enum(batch, "bruteforce", 0, total).read()
     if win["rank"] < 0:
         report = _evaluate(stages, fleet, ((workers[0], tuple(range(n))),), include_comm,
@@ -230,10 +230,10 @@ def schedule(stages, fleet, *, include_comm: bool = True):
         return _evaluate(stages, fleet, runs, include_comm, ("pinned runs",))
 
     host = build_host(stages, fleet, include_comm)
-    batch = engine.device_batch([host])
+    batch = engine.device_batch([host], pin=False)
     if n * n * p * (2 ** p) <= 3_000_000:
         owner, _, found, _ = engine.subset_dp(batch, n, p)
-        if not int(found.cpu()[0]):
+        if not int(found[0].item()):
             report = _evaluate(stages, fleet, ((workers[0], tuple(range(n))),), include_comm,
                                ("exact search: no feasible assignment",), host)
             return _mark_infeasible(report, "no feasible assignment under memory constraints")

@@ -225,14 +225,17 @@ class DeviceBatch:
     ``struct(i)`` is the ctypes dm_tables (device pointers) of instance i,
     ``structs_dev`` a device array of all records (for the batched kernels)."""
 
-    def __init__(self, hosts, device="cuda", stream=None):
+    def __init__(self, hosts, device="cuda", stream=None, pin: bool = True):
         import torch
 
         hosts = list(hosts)
         self.hosts = hosts
         sizes = [h.packed_size() for h in hosts]
         total = sum(sizes) + _ALIGN
-        self.host_buf = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+        # pinned staging for long-lived batches (re-uploaded every step by the
+        # end-to-end benchmark); small per-call batches use pageable memory,
+        # whose synchronous copy is cheaper than a cudaHostAlloc
+        self.host_buf = torch.empty(total, dtype=torch.uint8, pin_memory=pin)
         hb = self.host_buf.numpy()
         offs = []
         base = 0
@@ -247,7 +250,9 @@ class DeviceBatch:
         for i, (h, o) in enumerate(zip(hosts, offs)):
             recs[i] = h.struct_record(o, dev_base)
         self.records = recs
-        self.records_host = torch.from_numpy(recs.view(np.uint8).copy()).pin_memory()
+        self.records_host = torch.from_numpy(recs.view(np.uint8).copy())
+        if pin:
+            self.records_host = self.records_host.pin_memory()
         self.structs_dev = torch.empty(recs.nbytes, dtype=torch.uint8, device=device)
         self.structs_dev.copy_(self.records_host, non_blocking=True)
         self.h2d_bytes = total + recs.nbytes
