@@ -214,7 +214,9 @@ def run_b200(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(D.WINNER_BYTES * world)},
         "gpu_launches": 2 * args.steps,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": (peak / 1e12) if peak else None,
-                     "unit": "TFLOP/s", "frac": (achieved / (peak / 1e12)) if peak else None, "traffic": None,
+                     "unit": "TFLOP/s", "frac": (achieved / (peak / 1e12)) if peak else None,
+                     "traffic": (ncu_traffic("splits_memo_kernel") or {}).get("bytes"),
+                     "traffic_source": (ncu_traffic("splits_memo_kernel") or {}).get("capture"),
                      "algorithmic_ops_per_candidate": fp64_ops, "kernel_ms": kernel_ms,
                      "note": "algorithmic fp64 add/mul/div per candidate (SURVEY 8d Mode B: 6r-3, r = mean runs "
                              "of the population) / kernel time, vs the microbenchmarked fp64 op rate"},
@@ -225,6 +227,30 @@ def run_b200(args, rank, world, local_rank):
         line["clocks"] = clk
     line.update(extras)
     return line
+
+
+_UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def ncu_traffic(kernel_substr, profile_glob="r1_prof_*_raw.csv"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the newest committed
+    `ncu --set full` capture (profiles/*_raw.csv) of a kernel, with the
+    capture's duration, so callers can scale per launch / per candidate."""
+    import csv
+    best = None
+    for f in sorted((ROOT / "profiles").glob(profile_glob), key=lambda x: x.stat().st_mtime):
+        try:
+            rows = list(csv.reader(open(f)))
+            hdr, units, vals = rows[0], rows[1], rows[2]
+            name = vals[hdr.index("Kernel Name")]
+            if kernel_substr not in name:
+                continue
+            rd = float(vals[hdr.index("dram__bytes_read.sum")].replace(",", "")) * _UNITS[units[hdr.index("dram__bytes_read.sum")]]
+            wr = float(vals[hdr.index("dram__bytes_write.sum")].replace(",", "")) * _UNITS[units[hdr.index("dram__bytes_write.sum")]]
+            best = {"bytes": rd + wr, "capture": f.name, "kernel": name}
+        except Exception:
+            continue
+    return best
 
 
 def mean_runs_splits(n, p):
@@ -299,8 +325,12 @@ def mode_a_measure(dev, which):
     peak, src = _hbm_peak()
     algo = N * (n * 1 + 9)
     achieved = algo / (ms / 1e3) / 1e9
+    tr = ncu_traffic("eval_owner_stream_kernel") if which == "c1" else None
     res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                       "traffic": None, "bytes_per_candidate": n + 9, "peak_source": src}
+                       "traffic": (tr["bytes"] / (1 << 25) * N) if tr else None,
+                       "traffic_note": (f"{tr['capture']}: DRAM read+write of a 2^25-candidate launch, scaled per "
+                                        "candidate to this launch") if tr else None,
+                       "bytes_per_candidate": n + 9, "peak_source": src}
     inst = oracle.Instance(stages, fleet)
     sample = own[:20000].cpu().numpy().astype("int64")
     t0 = _t.perf_counter()

@@ -282,21 +282,22 @@ constexpr int kStreamThreads = 256;
 // The load table is square T[(a*(n+1) + b)*P + w] when it fits (no row-offset
 // lookup per run), else triangular T[(rowidx[a] + b)*P + w].
 struct StreamLayout {
-    int n, P, stages, cpt;
+    int n, P, stages, cpt, nt;
     bool square;
     size_t t_elems, off_T, off_rowidx, off_tiles, off_bar, bytes, tile_bytes;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-__host__ __device__ inline StreamLayout stream_layout(int n, int P, int stages, int cpt, bool square) {
+__host__ __device__ inline StreamLayout stream_layout(int n, int P, int stages, int cpt, bool square,
+                                                     int nt = kStreamThreads) {
     StreamLayout L;
-    L.n = n; L.P = P; L.stages = stages; L.cpt = cpt; L.square = square;
+    L.n = n; L.P = P; L.stages = stages; L.cpt = cpt; L.square = square; L.nt = nt;
     L.t_elems = square ? (size_t)n * (n + 1) * P : (size_t)n * (n + 1) / 2 * P;
     size_t off = 0;
     L.off_T = off; off = al16(off + L.t_elems * 8);
     L.off_rowidx = off; off = al16(off + (size_t)(n + 1) * 4);
-    L.tile_bytes = al16((size_t)kStreamThreads * cpt * n);
+    L.tile_bytes = al16((size_t)nt * cpt * n);
     L.off_tiles = off; off = al16(off + L.tile_bytes * stages + 16);
     L.off_bar = off; off += 8 * stages;
     L.bytes = al16(off);
@@ -371,8 +372,8 @@ __device__ __forceinline__ unsigned long long boundary_mask_n(int nw, uint32_t w
     }
 }
 
-template <bool PAIR, bool SQUARE>
-__global__ void __launch_bounds__(kStreamThreads, 2) eval_owner_stream_kernel(dm_tables t, int64_t n_cand,
+template <bool PAIR, bool SQUARE, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) eval_owner_stream_kernel(dm_tables t, int64_t n_cand,
                                                                               const uint8_t* __restrict__ owner,
                                                                               double* __restrict__ out_mk,
                                                                               uint8_t* __restrict__ out_code,
@@ -380,14 +381,14 @@ __global__ void __launch_bounds__(kStreamThreads, 2) eval_owner_stream_kernel(dm
                                                                               int stages, int cpt) {
     extern __shared__ __align__(128) unsigned char sm[];
     const int n = t.n, P = t.P;
-    const StreamLayout L = stream_layout(n, P, stages, cpt, SQUARE);
+    const StreamLayout L = stream_layout(n, P, stages, cpt, SQUARE, NT);
     // T: load of run (a, b) on w (compute only when PAIR); sign bit set when
     // the run fails _fits (|T| is the value; -0.0 keeps the flag)
     double* T = reinterpret_cast<double*>(sm + L.off_T);
     int32_t* rowidx = reinterpret_cast<int32_t*>(sm + L.off_rowidx);
     unsigned char* tiles = sm + L.off_tiles;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.off_bar);
-    const int tile_cand = kStreamThreads * cpt;
+    const int tile_cand = NT * cpt;
     const int64_t n_tiles = (n_cand + tile_cand - 1) / tile_cand;
     const int64_t full_tiles = n_cand / tile_cand;
     const uint32_t tile_load = (uint32_t)(tile_cand * n);
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) eval_owner_stream_kernel(dm
         }
         const uint32_t tile_s = sm_s + (uint32_t)(tile - sm);
 #pragma unroll 1
-        for (int ci = tid; ci < cnt; ci += kStreamThreads) {
+        for (int ci = tid; ci < cnt; ci += NT) {
             const uint32_t row_s = tile_s + (uint32_t)ci * n;        // shared address of the row
             const unsigned long long bm = boundary_mask_n(nw, row_s & ~3u, (int)(row_s & 3u) * 8);
             // ---- runs: b = each boundary in ascending order, then n
@@ -614,35 +615,38 @@ static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner
     {
         const uint32_t f = t->flags;
         bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
-        // pick the largest configuration that fits: square table if possible,
-        // 4 candidates per thread, 4 stages; shrink towards 1 cand x 2 stages
+        // pick the largest configuration that fits: a square table with
+        // 2 CTAs x 256 threads per SM when possible, else the triangular table
+        // with one 512-thread CTA per SM; 4 -> 1 candidates per thread and
+        // 4 -> 2 pipeline stages
         dm::StreamLayout L{};
         bool found = false;
-        for (int sq = 1; sq >= 0 && !found; --sq)
+        for (int sq = 1; sq >= 0 && !found; --sq) {
+            const int nt = sq ? 256 : 512;
             for (int cpt = 4; cpt >= 1 && !found; cpt /= 2)
                 for (int stages = 4; stages >= 2 && !found; --stages) {
-                    L = dm::stream_layout(t->n, t->P, stages, cpt, sq == 1);
+                    L = dm::stream_layout(t->n, t->P, stages, cpt, sq == 1, nt);
                     if (L.bytes <= (sq ? 110 * 1024 : 220 * 1024)) found = true;
                 }
+        }
         const char* dis = std::getenv("DM_DISABLE_MEMO");
         bool aligned = (((uintptr_t)owner) & 15) == 0;
         if (found && owner_bytes == 1 && memo_ok && aligned && t->n <= 64 && t->P <= 32 &&
             !(dis && dis[0] && dis[0] != '0')) {
-            int per_sm = (int)((225 * 1024) / (L.bytes + 1024));
-            if (per_sm < 1) per_sm = 1;
-            if (per_sm > 2) per_sm = 2;
-            const int tile_cand = dm::kStreamThreads * L.cpt;
+            int per_sm = L.square ? 2 : 1;
+            const int tile_cand = L.nt * L.cpt;
             int64_t n_tiles = (n_cand + tile_cand - 1) / tile_cand;
             int64_t grid = (int64_t)sm_count() * per_sm;
             if (grid > n_tiles) grid = n_tiles;
             if (out && grid > 8 * sm_count()) grid = 8 * sm_count();   // partial slots in scratch
             const bool pair = (t->flags & DM_F_INCLUDE_COMM) && (t->flags & DM_F_PAIR_LINKS);
-            auto kern = pair ? (L.square ? dm::eval_owner_stream_kernel<true, true> : dm::eval_owner_stream_kernel<true, false>)
-                             : (L.square ? dm::eval_owner_stream_kernel<false, true> : dm::eval_owner_stream_kernel<false, false>);
+            auto kern = L.square ? (pair ? dm::eval_owner_stream_kernel<true, true, 256>
+                                         : dm::eval_owner_stream_kernel<false, true, 256>)
+                                 : (pair ? dm::eval_owner_stream_kernel<true, false, 512>
+                                         : dm::eval_owner_stream_kernel<false, false, 512>);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-            kern<<<(int)grid, dm::kStreamThreads, L.bytes, s>>>(*t, n_cand, (const uint8_t*)owner, out_makespan,
-                                                               out_code, rank_base,
-                                                               out ? (dm_winner*)scratch : nullptr, L.stages, L.cpt);
+            kern<<<(int)grid, L.nt, L.bytes, s>>>(*t, n_cand, (const uint8_t*)owner, out_makespan, out_code, rank_base,
+                                                  out ? (dm_winner*)scratch : nullptr, L.stages, L.cpt);
             DM_CHECK_LAUNCH();
             if (out) {
                 dm::finalize_argmin_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, (int)grid, out);
