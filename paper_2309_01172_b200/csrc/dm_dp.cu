@@ -48,10 +48,14 @@ __device__ __forceinline__ bool key_less(double v, int sec, double bv, int bsec)
     return v < bv || (v == bv && sec < bsec);
 }
 
+// smem_mode: 0 = all tables in per-CTA global scratch, 1 = DP states and
+// break points in shared memory (chunk costs in scratch), 2 = everything in
+// shared memory.
 __global__ void __launch_bounds__(256) subset_dp_kernel(const dm_tables* __restrict__ tables, int32_t n_scen,
-                                                        int32_t n_max, int16_t* out_owner, double* out_mk,
-                                                        int32_t* out_found, unsigned char* scratch,
-                                                        size_t scratch_per_cta) {
+                                                        int32_t n_max, int32_t p_max, int16_t* out_owner,
+                                                        double* out_mk, int32_t* out_found, unsigned char* scratch,
+                                                        size_t scratch_per_cta, int smem_mode) {
+    extern __shared__ __align__(16) unsigned char dsm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     for (int sc = blockIdx.x; sc < n_scen; sc += gridDim.x) {
         __syncthreads();
@@ -60,6 +64,13 @@ __global__ void __launch_bounds__(256) subset_dp_kernel(const dm_tables* __restr
         const int64_t S = (int64_t)1 << p;
         DpScratch d = dp_carve(scratch + (size_t)blockIdx.x * scratch_per_cta, n, p);
         const int n1 = n + 1;
+        if (smem_mode >= 1) {   // states + break points (sized for this scenario) in shared memory
+            unsigned char* b = dsm;
+            d.mk = reinterpret_cast<double*>(b); b += align_up(((size_t)n1 << p) * sizeof(double));
+            d.back = reinterpret_cast<int32_t*>(b); b += align_up(((size_t)n1 << p) * sizeof(int32_t));
+            d.jlim = reinterpret_cast<int16_t*>(b); b += align_up((size_t)n1 * p * sizeof(int16_t));
+            if (smem_mode == 2) d.cc = reinterpret_cast<double*>(b);
+        }
         // ---- _fits break points (:313-315): first j with !_fits(w, range(i, j))
         for (int it = threadIdx.x; it < n * p; it += blockDim.x) {
             int i = it / p, wi = it % p;
@@ -94,21 +105,19 @@ __global__ void __launch_bounds__(256) subset_dp_kernel(const dm_tables* __restr
                 int pc = __popcll((unsigned long long)M);
                 if (pc == 0 || pc > j) continue;
                 double bv = 0.0; int bsec = 0x7fffffff; int bsrc = -1;
-                int pairs = j * pc;
-                for (int it = lane; it < pairs; it += 32) {
-                    int i = it / pc, kth = it % pc;
-                    // kth set bit of M
-                    uint64_t mm = (uint64_t)M;
-                    for (int z = 0; z < kth; ++z) mm &= mm - 1;
-                    int wi = __ffsll((long long)mm) - 1;
-                    int64_t src = (int64_t)i * S + (M ^ ((int64_t)1 << wi));
-                    if (d.back[src] < 0) continue;
-                    if (j >= d.jlim[i * p + wi]) continue;
-                    double m0 = d.mk[src];
-                    double cc = d.cc[((size_t)i * n1 + j) * p + wi];
-                    double v = cc > m0 ? cc : m0;              // max(mk, chunk_cost) :316
-                    int sec = i * 64 + (63 - wi);
-                    if (bsrc < 0 || key_less(v, sec, bv, bsec)) { bv = v; bsec = sec; bsrc = (i << 8) | wi; }
+                // lanes over the source prefix i, every worker wi of M in turn
+                for (int i = lane; i < j; i += 32) {
+                    const double* ccrow = d.cc + ((size_t)i * n1 + j) * p;
+                    for (uint32_t mm = (uint32_t)M; mm; mm &= mm - 1) {
+                        const int wi = __ffs(mm) - 1;
+                        const int64_t src = (int64_t)i * S + (M ^ ((int64_t)1 << wi));
+                        if (d.back[src] < 0 || j >= d.jlim[i * p + wi]) continue;
+                        const double m0 = d.mk[src];
+                        const double cc = ccrow[wi];
+                        const double v = cc > m0 ? cc : m0;        // max(mk, chunk_cost) :316
+                        const int sec = i * 64 + (63 - wi);
+                        if (bsrc < 0 || key_less(v, sec, bv, bsec)) { bv = v; bsec = sec; bsrc = (i << 8) | wi; }
+                    }
                 }
                 for (int off = 16; off > 0; off >>= 1) {
                     double ov = __shfl_down_sync(0xffffffffu, bv, off);
@@ -188,11 +197,22 @@ int dm_subset_dp(const dm_tables* tables, int32_t n_scen, int32_t n_max, int32_t
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int64_t grid = (int64_t)sms * 4;
+    const size_t n1 = (size_t)n_max + 1;
+    const size_t st = dm::align_up((n1 << p_max) * 8) + dm::align_up((n1 << p_max) * 4) + dm::align_up(n1 * p_max * 2);
+    const size_t cc = n1 * n1 * p_max * 8;
+    int mode = 0;
+    size_t smem = 0;
+    if (st + cc <= 110 * 1024) { mode = 2; smem = st + cc; }   // >= 2 CTAs per SM with every table on chip
+    int per_sm = mode == 0 ? 4 : (int)((220 * 1024) / (smem + 2048));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 4) per_sm = 4;
+    int64_t grid = (int64_t)sms * per_sm;
     if (grid > n_scen) grid = n_scen;
     size_t per = dm::dp_scratch_bytes(n_max, p_max);
-    dm::subset_dp_kernel<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(tables, n_scen, n_max, out_owner, out_makespan,
-                                                                        out_found, (unsigned char*)scratch, per);
+    if (smem) cudaFuncSetAttribute(dm::subset_dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dm::subset_dp_kernel<<<(int)grid, 256, smem, (cudaStream_t)stream>>>(tables, n_scen, n_max, p_max, out_owner,
+                                                                          out_makespan, out_found,
+                                                                          (unsigned char*)scratch, per, mode);
     DM_CHECK_LAUNCH();
     return DM_OK;
 }
