@@ -372,8 +372,8 @@ __device__ __forceinline__ unsigned long long boundary_mask_n(int nw, uint32_t w
     }
 }
 
-template <bool PAIR, bool SQUARE, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) eval_owner_stream_kernel(dm_tables t, int64_t n_cand,
+template <bool PAIR, bool SQUARE, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t, int64_t n_cand,
                                                                               const uint8_t* __restrict__ owner,
                                                                               double* __restrict__ out_mk,
                                                                               uint8_t* __restrict__ out_code,
@@ -615,12 +615,15 @@ static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner
     {
         const uint32_t f = t->flags;
         bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
-        // pick the largest configuration that fits: a square table with
-        // 2 CTAs x 256 threads per SM when possible, else the triangular table
-        // with one 512-thread CTA per SM; 4 -> 1 candidates per thread and
-        // 4 -> 2 pipeline stages
+        // pick a configuration: a square table with 3 CTAs x 256 threads per
+        // SM (<= 85 registers) when the table and a 2-candidate x 3-stage tile
+        // ring fit in a third of the SM, else 2 CTAs with deeper tiles, else the
+        // triangular table with one 512-thread CTA per SM
         dm::StreamLayout L{};
         bool found = false;
+        int minb = 2;
+        L = dm::stream_layout(t->n, t->P, 3, 2, true, 256);
+        if (L.bytes <= 72 * 1024) { found = true; minb = 3; }
         for (int sq = 1; sq >= 0 && !found; --sq) {
             const int nt = sq ? 256 : 512;
             for (int cpt = 4; cpt >= 1 && !found; cpt /= 2)
@@ -628,22 +631,25 @@ static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner
                     L = dm::stream_layout(t->n, t->P, stages, cpt, sq == 1, nt);
                     if (L.bytes <= (sq ? 110 * 1024 : 220 * 1024)) found = true;
                 }
+            minb = sq ? 2 : 1;
         }
         const char* dis = std::getenv("DM_DISABLE_MEMO");
         bool aligned = (((uintptr_t)owner) & 15) == 0;
         if (found && owner_bytes == 1 && memo_ok && aligned && t->n <= 64 && t->P <= 32 &&
             !(dis && dis[0] && dis[0] != '0')) {
-            int per_sm = L.square ? 2 : 1;
+            int per_sm = minb;
             const int tile_cand = L.nt * L.cpt;
             int64_t n_tiles = (n_cand + tile_cand - 1) / tile_cand;
             int64_t grid = (int64_t)sm_count() * per_sm;
             if (grid > n_tiles) grid = n_tiles;
             if (out && grid > 8 * sm_count()) grid = 8 * sm_count();   // partial slots in scratch
             const bool pair = (t->flags & DM_F_INCLUDE_COMM) && (t->flags & DM_F_PAIR_LINKS);
-            auto kern = L.square ? (pair ? dm::eval_owner_stream_kernel<true, true, 256>
-                                         : dm::eval_owner_stream_kernel<false, true, 256>)
-                                 : (pair ? dm::eval_owner_stream_kernel<true, false, 512>
-                                         : dm::eval_owner_stream_kernel<false, false, 512>);
+            auto kern = !L.square ? (pair ? dm::eval_owner_stream_kernel<true, false, 512, 1>
+                                          : dm::eval_owner_stream_kernel<false, false, 512, 1>)
+                      : minb == 3 ? (pair ? dm::eval_owner_stream_kernel<true, true, 256, 3>
+                                          : dm::eval_owner_stream_kernel<false, true, 256, 3>)
+                                  : (pair ? dm::eval_owner_stream_kernel<true, true, 256, 2>
+                                          : dm::eval_owner_stream_kernel<false, true, 256, 2>);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
             kern<<<(int)grid, L.nt, L.bytes, s>>>(*t, n_cand, (const uint8_t*)owner, out_makespan, out_code, rank_base,
                                                   out ? (dm_winner*)scratch : nullptr, L.stages, L.cpt);
