@@ -72,6 +72,13 @@ extern "C" {
 #define DM_F_CHAIN        8u   /* every in-edge of stage i has src == i-1             */
 #define DM_F_BACKWARD    16u   /* some in-edge has src >= its own stage               */
 #define DM_F_INCLUDE_COMM 32u  /* include_comm=True (scheduling.py:162)               */
+/* CPython's sum() runs its compensated fast path only over exact `float`
+ * items; numpy.float64 inputs make it a naive left-to-right sum from the first
+ * such item on (with the compensation gathered so far applied at the switch).
+ * These flags record which inputs are not exact Python floats. */
+#define DM_F_NP_FLOPS    64u   /* stage flops column            */
+#define DM_F_NP_COMM    128u   /* msg_ratio or link alpha/beta  */
+#define DM_F_NP_BYTES   256u   /* gpu/cpu/disk byte columns      */
 
 /*
  * One scheduling instance: the stage table (scheduling.Stage, :32-42) and the
@@ -114,6 +121,10 @@ typedef struct dm_tables {
        column b = reading peer, diagonal = ZERO_LINK; only with DM_F_PAIR_LINKS */
     const double* link_alpha;  /* [P*P] */
     const double* link_beta;   /* [P*P] */
+    /* peer_np[w] = 1 when effective_speed(peer w) is not an exact Python float
+       (numpy.float64 peak or lambda): CPython's sum() then leaves its
+       compensated fast path at that item (bltinmodule.c) — see dm_common.cuh */
+    const uint8_t* peer_np;    /* [P] */
 } dm_tables;
 
 /* Arg-min record shared by every enumeration: first strict minimum in rank
@@ -277,25 +288,33 @@ DM_API int dm_pipeline_epilogue(const dm_tables* tables, int32_t n_scen, int32_t
  * op_flops(node) (as f64), message_bytes(node, msg_ratio) (int-valued f64),
  * its args and users (CSR).  place[b*n_ops + i] = peer index of op i in
  * placement b (dm_tables indexing; >= P for peers unknown to the fleet).
- * out[(b*n_ops + i)*3 + {0,1,2}] = read_s, compute_s, write_s.
+ * out[(b*n_ops + i)*3 + {0,1,2}] = read_s, compute_s, write_s; out_np (optional)
+ * [b*n_ops + i] = 1 when OpCost.total_s is a numpy float in the reference
+ * (numpy speed, or a crossing read / write priced with numpy link values or
+ * write bandwidth — flags DM_OPS_NP_LINKS, write_np[peer]).
  */
+#define DM_OPS_NP_LINKS 1
+
 typedef struct dm_ops {
     int32_t n_ops;
-    int32_t pad_;
+    int32_t flags;             /* DM_OPS_* */
     const double* flops;
     const double* mbytes;
     const int32_t* arg_ptr;    /* [n_ops+1] */
     const int32_t* arg_idx;
     const int32_t* user_ptr;   /* [n_ops+1] */
     const int32_t* user_idx;
+    const uint8_t* write_np;   /* [P] write_bandwidth is a numpy value (NULL: none) */
 } dm_ops;
 
 DM_API int dm_op_costs(const dm_ops* ops, const dm_tables* t, const double* write_bw,
-                       int32_t n_place, const int32_t* place, double* out, void* stream);
+                       int32_t n_place, const int32_t* place, double* out, uint8_t* out_np,
+                       void* stream);
 
 /* hardware.subgraph_time (hardware.py:219-226) for cells sub_idx[sub_ptr[s]..]
- * over op costs from dm_op_costs: out[(b*n_sub + s)*3] = lower, upper, sequential. */
-DM_API int dm_subgraph_times(int32_t n_ops, int32_t n_place, const double* op_out,
+ * over op costs from dm_op_costs: out[(b*n_sub + s)*3] = lower, upper, sequential.
+ * op_np: dm_op_costs' out_np (NULL: every total an exact float). */
+DM_API int dm_subgraph_times(int32_t n_ops, int32_t n_place, const double* op_out, const uint8_t* op_np,
                              int32_t n_sub, const int32_t* sub_ptr, const int32_t* sub_idx,
                              double* out, void* stream);
 

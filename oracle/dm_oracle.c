@@ -34,30 +34,49 @@
  * at the end when it is non-zero and finite.  Used where the reference calls
  * sum() over Python floats: scheduling.py:160,174-176,200,295,332-333,
  * pipeline.py:43. */
-EXPORT double or_py_sum(const double* x, int64_t k) {
+/* The same sum() when some items are not exact `float` objects
+ * (numpy.float64; np_item[i] != 0): builtin_sum_impl leaves its float fast
+ * path at the first such item, adding the compensation gathered so far, and
+ * adds every later item with plain `+`.  np_item == NULL: all exact floats. */
+EXPORT double or_py_sum_items(const double* x, const uint8_t* np_item, int64_t k) {
     if (k <= 0) return 0.0;
     double f = 0.0 + x[0];
     double c = 0.0;
+    int naive = np_item && np_item[0];
     for (int64_t i = 1; i < k; ++i) {
         double v = x[i];
+        if (!naive && np_item && np_item[i]) {
+            if (c != 0.0 && isfinite(c)) f += c;
+            naive = 1;
+        }
+        if (naive) { f = f + v; continue; }
         double t = f + v;
         if (fabs(f) >= fabs(v)) c += (f - t) + v;
         else c += (v - t) + f;
         f = t;
     }
-    if (c != 0.0 && isfinite(c)) f += c;
+    if (!naive && c != 0.0 && isfinite(c)) f += c;
     return f;
+}
+
+EXPORT double or_py_sum(const double* x, int64_t k) {
+    return or_py_sum_items(x, NULL, k);
 }
 
 /* Python sum over the items col[idx[0..k)] (in that order). */
 static double col_sum_idx(const double* col, const int64_t* pre, int exact,
-                          const int32_t* idx, int k) {
+                          const int32_t* idx, int k, int np_items) {
     if (exact) {
         int64_t s = 0;
         for (int q = 0; q < k; ++q) s += (pre[idx[q] + 1] - pre[idx[q]]);
         return (double)s;
     }
     if (k <= 0) return 0.0;
+    if (np_items) {                       /* sum() over numpy items: plain + */
+        double f = 0.0 + col[idx[0]];
+        for (int q = 1; q < k; ++q) f = f + col[idx[q]];
+        return f;
+    }
     double f = 0.0 + col[idx[0]], c = 0.0;
     for (int q = 1; q < k; ++q) {
         double v = col[idx[q]], t = f + v;
@@ -70,14 +89,21 @@ static double col_sum_idx(const double* col, const int64_t* pre, int exact,
 
 /* Python sum over col[a..b) in index order. */
 static double col_sum_range(const double* col, const int64_t* pre, int exact,
-                            int a, int b) {
+                            int a, int b, int np_items) {
     if (exact) return (double)(pre[b] - pre[a]);
     if (b <= a) return 0.0;
+    if (np_items) {
+        double f = 0.0 + col[a];
+        for (int i = a + 1; i < b; ++i) f = f + col[i];
+        return f;
+    }
     return or_py_sum(col + a, b - a);
 }
 
 static inline int flops_exact(const dm_tables* t) { return (t->flags & DM_F_FLOPS_EXACT) != 0; }
 static inline int bytes_exact(const dm_tables* t) { return (t->flags & DM_F_BYTES_EXACT) != 0; }
+static inline int np_flops(const dm_tables* t) { return (t->flags & DM_F_NP_FLOPS) != 0; }
+static inline int np_bytes(const dm_tables* t) { return (t->flags & DM_F_NP_BYTES) != 0; }
 
 /* hardware.Fleet.link_between (hardware.py:136-140) resolved to indices;
  * owner indices outside [0, P) are peers unknown to the fleet (default link). */
@@ -106,7 +132,7 @@ static int run_cost(const dm_tables* t, const int32_t* peer_of, int peer,
                     double* compute, double* read) {
     if (peer < 0 || peer >= t->P) return DM_E_UNKNOWN_PEER;  /* fleet.peer :158 */
     double speed = t->speed[peer];                              /* :159 */
-    double fl = col_sum_idx(t->flops, t->pre_flops, flops_exact(t), idx, k);
+    double fl = col_sum_idx(t->flops, t->pre_flops, flops_exact(t), idx, k, np_flops(t));
     *compute = fl / speed;                                      /* :160 */
     double rd = 0.0;
     if (t->flags & DM_F_INCLUDE_COMM) {                         /* :162 */
@@ -136,9 +162,9 @@ static int run_cost(const dm_tables* t, const int32_t* peer_of, int peer,
 /* scheduling._fits (scheduling.py:172-176) over the contiguous range [a, b). */
 static int fits_range(const dm_tables* t, int peer, int a, int b) {
     int ex = bytes_exact(t);
-    return col_sum_range(t->gpu, t->pre_gpu, ex, a, b) <= t->cap_gpu[peer]
-        && col_sum_range(t->cpu, t->pre_cpu, ex, a, b) <= t->cap_cpu[peer]
-        && col_sum_range(t->disk, t->pre_disk, ex, a, b) <= t->cap_disk[peer];
+    return col_sum_range(t->gpu, t->pre_gpu, ex, a, b, np_bytes(t)) <= t->cap_gpu[peer]
+        && col_sum_range(t->cpu, t->pre_cpu, ex, a, b, np_bytes(t)) <= t->cap_cpu[peer]
+        && col_sum_range(t->disk, t->pre_disk, ex, a, b, np_bytes(t)) <= t->cap_disk[peer];
 }
 
 /* ------------------------------------------------------ verify_assignment */
@@ -180,9 +206,9 @@ EXPORT int or_verify_runs(const dm_tables* t, int nr, const int32_t* run_peer,
         }
         if (code) { *bad_run = r; break; }
         int ex = bytes_exact(t);                                  /* :199-203 */
-        if (col_sum_idx(t->gpu, t->pre_gpu, ex, sorted, k) > t->cap_gpu[peer]) code = DM_V_GPU;
-        else if (col_sum_idx(t->cpu, t->pre_cpu, ex, sorted, k) > t->cap_cpu[peer]) code = DM_V_CPU;
-        else if (col_sum_idx(t->disk, t->pre_disk, ex, sorted, k) > t->cap_disk[peer]) code = DM_V_DISK;
+        if (col_sum_idx(t->gpu, t->pre_gpu, ex, sorted, k, np_bytes(t)) > t->cap_gpu[peer]) code = DM_V_GPU;
+        else if (col_sum_idx(t->cpu, t->pre_cpu, ex, sorted, k, np_bytes(t)) > t->cap_cpu[peer]) code = DM_V_CPU;
+        else if (col_sum_idx(t->disk, t->pre_disk, ex, sorted, k, np_bytes(t)) > t->cap_disk[peer]) code = DM_V_DISK;
         if (code) *bad_run = r;
     }
     if (code == DM_V_OK && n_seen != n) code = DM_V_UNASSIGNED;  /* :204-206 */
@@ -474,7 +500,7 @@ EXPORT int or_subset_dp(const dm_tables* t, int32_t* owner, double* out_mk) {
                 for (int j = i + 1; j <= n; ++j) {                   /* :313 */
                     if (!fits_range(t, wi, i, j)) break;             /* :314-315 */
                     /* chunk_cost :294-302 */
-                    double fl = col_sum_range(t->flops, t->pre_flops, flops_exact(t), i, j);
+                    double fl = col_sum_range(t->flops, t->pre_flops, flops_exact(t), i, j, np_flops(t));
                     double compute = fl / t->speed[wi];
                     double rd = 0.0;
                     if (inc) {
@@ -519,8 +545,8 @@ EXPORT int or_subset_dp(const dm_tables* t, int32_t* owner, double* out_mk) {
  * the runs (run q on worker q) and returns the number of runs. */
 EXPORT int or_proportional(const dm_tables* t, int32_t* bounds) {
     int n = t->n, p = t->p;
-    double total_speed = or_py_sum(t->speed, p);                     /* :332 */
-    double total_flops = col_sum_range(t->flops, t->pre_flops, flops_exact(t), 0, n); /* :333 */
+    double total_speed = or_py_sum_items(t->speed, t->peer_np, p);                     /* :332 */
+    double total_flops = col_sum_range(t->flops, t->pre_flops, flops_exact(t), 0, n, np_flops(t)); /* :333 */
     if (total_flops == 0.0) total_flops = 1.0;
     double* prefix = (double*)malloc(sizeof(double) * (size_t)n);   /* :334 accumulate */
     prefix[0] = t->flops[0];
@@ -561,9 +587,9 @@ static double hill_score(const dm_tables* t, int r, const int32_t* bounds, const
     for (int q = 0; q < r; ++q) {
         int a = bounds[q], b = bounds[q + 1], pe = peers[q];
         if (b == a) continue;
-        if (col_sum_range(t->gpu, t->pre_gpu, ex, a, b) > t->cap_gpu[pe]) return INFINITY;
-        if (col_sum_range(t->cpu, t->pre_cpu, ex, a, b) > t->cap_cpu[pe]) return INFINITY;
-        if (col_sum_range(t->disk, t->pre_disk, ex, a, b) > t->cap_disk[pe]) return INFINITY;
+        if (col_sum_range(t->gpu, t->pre_gpu, ex, a, b, np_bytes(t)) > t->cap_gpu[pe]) return INFINITY;
+        if (col_sum_range(t->cpu, t->pre_cpu, ex, a, b, np_bytes(t)) > t->cap_cpu[pe]) return INFINITY;
+        if (col_sum_range(t->disk, t->pre_disk, ex, a, b, np_bytes(t)) > t->cap_disk[pe]) return INFINITY;
     }
     for (int q = 0; q < r; ++q)
         for (int i = bounds[q]; i < bounds[q + 1]; ++i) peer_of[i] = peers[q];
@@ -649,9 +675,10 @@ EXPORT int or_schedule(const dm_tables* t, int has_links, int32_t* owner) {
 /* -------------------------------------------------------------- epilogue */
 
 /* pipeline.fp_latency / bottleneck / pipeline_time / throughput
- * (pipeline.py:41-62) over profiles given in first-stage order. */
-EXPORT void or_epilogue(int r, const double* compute, const double* read, int64_t n_batches,
-                        int64_t samples_per_batch, double* out4) {
+ * (pipeline.py:41-62) over profiles given in first-stage order.  np_load[q]
+ * != 0 when profile q's compute_s + read_s is a numpy float (NULL: none). */
+EXPORT void or_epilogue(int r, const double* compute, const double* read, const uint8_t* np_load,
+                        int64_t n_batches, int64_t samples_per_batch, double* out4) {
     double* tot = (double*)malloc(sizeof(double) * (size_t)(r + 1));
     double bn = 0.0;
     for (int q = 0; q < r; ++q) {
@@ -659,7 +686,7 @@ EXPORT void or_epilogue(int r, const double* compute, const double* read, int64_
         double m = compute[q] >= read[q] ? compute[q] : read[q];
         if (q == 0 || m > bn) bn = m;
     }
-    double lat = or_py_sum(tot, r);
+    double lat = or_py_sum_items(tot, np_load, r);
     double fill = (double)(n_batches - 1) * bn;
     double pipe = lat + fill;
     double thr = (double)(n_batches * samples_per_batch) / pipe;
@@ -675,11 +702,13 @@ EXPORT void or_epilogue(int r, const double* compute, const double* read, int64_
  * user sits on another peer. */
 EXPORT void or_op_costs(const dm_tables* t, int n_ops, const double* flops, const double* mbytes,
                         const int32_t* aptr, const int32_t* aidx, const int32_t* uptr, const int32_t* uidx,
-                        const double* write_bw, const int32_t* place, double* out) {
+                        const double* write_bw, const int32_t* place, double* out,
+                        int np_links, const uint8_t* write_np, uint8_t* out_np) {
     for (int i = 0; i < n_ops; ++i) {
         int me = place[i];
         double* o = out + 3 * i;
-        if (me < 0 || me >= t->P) { o[0] = o[1] = o[2] = NAN; continue; }
+        if (me < 0 || me >= t->P) { o[0] = o[1] = o[2] = NAN; if (out_np) out_np[i] = 0; continue; }
+        int is_np = t->peer_np && t->peer_np[me];              /* compute_s type */
         double rd = 0.0;
         for (int e = aptr[i]; e < aptr[i + 1]; ++e) {
             int src = place[aidx[e]];
@@ -687,27 +716,32 @@ EXPORT void or_op_costs(const dm_tables* t, int n_ops, const double* flops, cons
                 double al, be;
                 link_of(t, src, me, &al, &be);
                 rd += comm_time(al, be, mbytes[aidx[e]]);
+                is_np |= np_links;
             }
         }
         double wr = 0.0;
         for (int e = uptr[i]; e < uptr[i + 1]; ++e)
-            if (place[uidx[e]] != me) { wr = mbytes[i] / write_bw[me]; break; }
+            if (place[uidx[e]] != me) { wr = mbytes[i] / write_bw[me]; is_np |= write_np && write_np[me]; break; }
         o[0] = rd; o[1] = flops[i] / t->speed[me]; o[2] = wr;
+        if (out_np) out_np[i] = (uint8_t)is_np;
     }
 }
 
 /* hardware.subgraph_time (hardware.py:219-226): max and CPython sum of the
  * per-op totals read + compute + write. */
-EXPORT void or_subgraph(int k, const int32_t* idx, const double* op_out, double* out3) {
+EXPORT void or_subgraph(int k, const int32_t* idx, const double* op_out, const uint8_t* op_np, double* out3) {
     if (k == 0) { out3[0] = out3[1] = out3[2] = 0.0; return; }
     double* tot = (double*)malloc(sizeof(double) * (size_t)k);
+    uint8_t* npv = (uint8_t*)malloc((size_t)k);
     double mx = 0.0;
     for (int q = 0; q < k; ++q) {
         const double* o = op_out + 3 * idx[q];
         tot[q] = o[0] + o[1] + o[2];
+        npv[q] = op_np ? op_np[idx[q]] : 0;
         if (q == 0 || tot[q] > mx) mx = tot[q];
     }
-    double seq = or_py_sum(tot, k);
+    double seq = or_py_sum_items(tot, npv, k);
+    free(npv);
     out3[0] = mx; out3[1] = seq; out3[2] = seq;
     free(tot);
 }

@@ -24,6 +24,7 @@ LIB = HERE / "liboracle.so"
 
 DM_F_FLOPS_EXACT, DM_F_BYTES_EXACT, DM_F_PAIR_LINKS = 1, 2, 4
 DM_F_CHAIN, DM_F_BACKWARD, DM_F_INCLUDE_COMM = 8, 16, 32
+DM_F_NP_FLOPS, DM_F_NP_COMM, DM_F_NP_BYTES = 64, 128, 256
 
 _P = C.c_void_p
 
@@ -37,7 +38,7 @@ class Tables(C.Structure):
         ("pre_flops", _P), ("pre_gpu", _P), ("pre_cpu", _P), ("pre_disk", _P),
         ("edge_ptr", _P), ("edge_src", _P), ("edge_m", _P),
         ("speed", _P), ("cap_gpu", _P), ("cap_cpu", _P), ("cap_disk", _P),
-        ("link_alpha", _P), ("link_beta", _P),
+        ("link_alpha", _P), ("link_beta", _P), ("peer_np", _P),
     ]
 
 
@@ -84,7 +85,9 @@ def lib():
         L.or_schedule.restype = C.c_int
         L.or_schedule.argtypes = [_P, C.c_int, _P]
         L.or_epilogue.restype = None
-        L.or_epilogue.argtypes = [C.c_int, _P, _P, C.c_int64, C.c_int64, _P]
+        L.or_epilogue.argtypes = [C.c_int, _P, _P, _P, C.c_int64, C.c_int64, _P]
+        L.or_py_sum_items.restype = C.c_double
+        L.or_py_sum_items.argtypes = [_P, _P, C.c_int64]
         _lib = L
     return _lib
 
@@ -141,7 +144,17 @@ class Instance:
         self.edge_src = np.array(src or [0], dtype=np.int32)
         self.edge_m = np.array(m or [0.0], dtype=np.float64)
         peers = [fleet.peers[q] for q in order]
-        self.speed = np.array([pe.peak_flops * pe.lam for pe in peers], dtype=np.float64)
+        sp = [pe.peak_flops * pe.lam for pe in peers]
+        self.speed = np.array(sp, dtype=np.float64)
+        self.peer_np = np.array([0 if type(v) in (int, float, bool) else 1 for v in sp] or [0], dtype=np.uint8)
+        isnp = lambda v: type(v) not in (int, float, bool)
+        np_flops = any(isnp(s.flops) for s in stages)
+        np_bytes = any(isnp(s.gpu_bytes) or isnp(s.cpu_bytes) or isnp(s.disk_bytes) for s in stages)
+        np_comm = (isnp(fleet.msg_ratio) or isnp(fleet.default_link.alpha) or isnp(fleet.default_link.beta)
+                   or any(isnp(l.alpha) or isnp(l.beta) for l in fleet.links.values())
+                   or any(isnp(nb) for s in stages for _, nb in s.in_edges))
+        self.include_comm = include_comm
+        self.np_flops, self.np_comm = np_flops, np_comm
         self.cap_gpu = np.array([float(pe.gpu_bytes) for pe in peers], dtype=np.float64)
         self.cap_cpu = np.array([float(pe.cpu_bytes) for pe in peers], dtype=np.float64)
         self.cap_disk = np.array([float(pe.disk_bytes) for pe in peers], dtype=np.float64)
@@ -150,6 +163,8 @@ class Instance:
         flags |= DM_F_BYTES_EXACT if (g_ok and c_ok and d_ok) else 0
         flags |= DM_F_CHAIN if chain else 0
         flags |= DM_F_BACKWARD if backward else 0
+        flags |= (DM_F_NP_FLOPS if np_flops else 0) | (DM_F_NP_BYTES if np_bytes else 0)
+        flags |= DM_F_NP_COMM if np_comm else 0
         self.la = self.lb = None
         if fleet.links:
             flags |= DM_F_PAIR_LINKS
@@ -167,6 +182,7 @@ class Instance:
                      "edge_src", "edge_m", "speed", "cap_gpu", "cap_cpu", "cap_disk"):
             setattr(t, name, _ptr(getattr(self, name)))
         t.link_alpha, t.link_beta = _ptr(self.la), _ptr(self.lb)
+        t.peer_np = _ptr(self.peer_np)
         self.t = t
         self.n, self.p, self.P = n, len(workers), P
 
@@ -182,6 +198,22 @@ class Instance:
             idx.extend(sorted(ids))
             ptr.append(len(idx))
         return (np.array(peer or [0], np.int32), np.array(ptr, np.int32), np.array(idx or [0], np.int32))
+
+    def load_np(self, runs):
+        """Per run (first-stage order, as eval_runs): 1 when _evaluate's
+        compute + read (scheduling.py:156-169, 220) is a numpy float — numpy
+        speed or FLOPs, or a crossing read priced with numpy link/message
+        values.  fp_latency's sum() (pipeline.py:43) turns naive there."""
+        runs = sorted(((pe, tuple(sorted(ids))) for pe, ids in runs if ids), key=lambda r: r[1][0])
+        out = []
+        for pe, ids in runs:
+            w = self.idx.get(pe)
+            f = (w is not None and bool(self.peer_np[w])) or self.np_flops
+            if self.np_comm and self.include_comm:
+                inside = set(ids)
+                f = f or any(a not in inside for i in ids for a, _ in self.stages[i].in_edges)
+            out.append(1 if f else 0)
+        return np.array(out, np.uint8)
 
     def eval_runs(self, runs):
         """(makespan, code, code_run, status, compute[], read[])"""
@@ -263,11 +295,14 @@ def py_sum(values) -> float:
     return float(lib().or_py_sum(_ptr(a), a.size))
 
 
-def epilogue(compute, read, n_batches, samples_per_batch):
+def epilogue(compute, read, n_batches, samples_per_batch, np_load=None):
+    """np_load[q]: profile q's compute_s + read_s is a numpy float
+    (Instance.load_np); None = every load is an exact float."""
     c = np.ascontiguousarray(compute, np.float64)
     r = np.ascontiguousarray(read, np.float64)
+    f = None if np_load is None else np.ascontiguousarray(np_load, np.uint8)
     out = np.zeros(4)
-    lib().or_epilogue(c.size, _ptr(c), _ptr(r), n_batches, samples_per_batch, _ptr(out))
+    lib().or_epilogue(c.size, _ptr(c), _ptr(r), _ptr(f), n_batches, samples_per_batch, _ptr(out))
     return tuple(float(x) for x in out)
 
 

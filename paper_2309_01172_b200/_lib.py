@@ -21,6 +21,7 @@ DM_V_ASSIGNED_TWICE, DM_V_GPU, DM_V_CPU, DM_V_DISK, DM_V_UNASSIGNED = 4, 5, 6, 7
 
 DM_F_FLOPS_EXACT, DM_F_BYTES_EXACT, DM_F_PAIR_LINKS = 1, 2, 4
 DM_F_CHAIN, DM_F_BACKWARD, DM_F_INCLUDE_COMM = 8, 16, 32
+DM_F_NP_FLOPS, DM_F_NP_COMM, DM_F_NP_BYTES = 64, 128, 256
 
 
 class EngineUnavailable(RuntimeError):
@@ -47,13 +48,16 @@ class DmTables(C.Structure):
         ("pre_flops", _P), ("pre_gpu", _P), ("pre_cpu", _P), ("pre_disk", _P),
         ("edge_ptr", _P), ("edge_src", _P), ("edge_m", _P),
         ("speed", _P), ("cap_gpu", _P), ("cap_cpu", _P), ("cap_disk", _P),
-        ("link_alpha", _P), ("link_beta", _P),
+        ("link_alpha", _P), ("link_beta", _P), ("peer_np", _P),
     ]
 
 
+DM_OPS_NP_LINKS = 1
+
+
 class DmOps(C.Structure):
-    _fields_ = [("n_ops", C.c_int32), ("pad_", C.c_int32), ("flops", _P), ("mbytes", _P), ("arg_ptr", _P),
-                ("arg_idx", _P), ("user_ptr", _P), ("user_idx", _P)]
+    _fields_ = [("n_ops", C.c_int32), ("flags", C.c_int32), ("flops", _P), ("mbytes", _P), ("arg_ptr", _P),
+                ("arg_idx", _P), ("user_ptr", _P), ("user_idx", _P), ("write_np", _P)]
 
 
 class DmWinner(C.Structure):
@@ -80,8 +84,8 @@ _SIGS = {
     "dm_prop_hill": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
     "dm_pipeline_epilogue": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int64, C.c_int64, _P, _P]),
     "dm_microbench_fp64": (C.c_int, [C.c_int64, _P, _P, _P]),
-    "dm_op_costs": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, _P]),
-    "dm_subgraph_times": (C.c_int, [C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, _P, _P]),
+    "dm_op_costs": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, _P, _P]),
+    "dm_subgraph_times": (C.c_int, [C.c_int32, C.c_int32, _P, _P, C.c_int32, _P, _P, _P, _P]),
     "dm_materialize": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64, _P, C.c_int32, _P]),
 }
 

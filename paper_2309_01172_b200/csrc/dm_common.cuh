@@ -21,16 +21,26 @@ __host__ __device__ inline bool bytes_exact(const dm_tables& t) { return t.flags
 __host__ __device__ inline bool include_comm(const dm_tables& t) { return t.flags & DM_F_INCLUDE_COMM; }
 __host__ __device__ inline bool pair_links(const dm_tables& t) { return t.flags & DM_F_PAIR_LINKS; }
 __host__ __device__ inline bool chain(const dm_tables& t) { return t.flags & DM_F_CHAIN; }
+__host__ __device__ inline bool np_flops(const dm_tables& t) { return t.flags & DM_F_NP_FLOPS; }
+__host__ __device__ inline bool np_bytes(const dm_tables& t) { return t.flags & DM_F_NP_BYTES; }
+__host__ __device__ inline bool np_comm(const dm_tables& t) { return t.flags & DM_F_NP_COMM; }
 
-// CPython 3.12 builtin sum() over float items (bltinmodule.c builtin_sum_impl):
-// 0 + x0, then Neumaier compensation, compensation added when non-zero and
-// finite.  The reference calls sum() over floats at scheduling.py:160,
-// 174-176, 200, 295, 332-333 and pipeline.py:43.
+// CPython 3.12 builtin sum() (bltinmodule.c builtin_sum_impl).  Over exact
+// `float` items: 0 + x0, then Neumaier compensation, compensation added when
+// non-zero and finite.  An item that is not an exact float (numpy.float64)
+// ends the fast path: the compensation gathered so far is applied and every
+// later item is added naively.  The reference calls sum() over floats at
+// scheduling.py:160, 174-176, 200, 295, 332-333 and pipeline.py:43.
 struct PySum {
     double f = 0.0, c = 0.0;
-    bool any = false;
-    __device__ __forceinline__ void add(double v) {
-        if (!any) { f = 0.0 + v; any = true; return; }
+    bool any = false, naive = false;
+    __device__ __forceinline__ void add(double v, bool exact = true) {
+        if (!any) { f = 0.0 + v; any = true; naive = !exact; return; }
+        if (!naive && !exact) {
+            if (c != 0.0 && isfinite(c)) f += c;
+            naive = true;
+        }
+        if (naive) { f = f + v; return; }
         double t = f + v;
         if (fabs(f) >= fabs(v)) c += (f - t) + v;
         else c += (v - t) + f;
@@ -38,18 +48,19 @@ struct PySum {
     }
     __device__ __forceinline__ double value() const {
         double r = f;
-        if (c != 0.0 && isfinite(c)) r += c;
+        if (!naive && c != 0.0 && isfinite(c)) r += c;
         return r;
     }
 };
 
 // Python sum over col[a..b) (index order): exact int64 prefix difference when
-// the column is integral with every prefix < 2^53, else the Neumaier restatement.
+// the column is integral with every prefix < 2^53, else the restated sum()
+// (naive when the column holds numpy floats).
 __device__ __forceinline__ double col_range(const double* col, const int64_t* pre,
-                                            bool exact, int a, int b) {
+                                            bool exact, int a, int b, bool np_items = false) {
     if (exact) return (double)(pre[b] - pre[a]);
     PySum s;
-    for (int i = a; i < b; ++i) s.add(col[i]);
+    for (int i = a; i < b; ++i) s.add(col[i], !np_items);
     return s.value();
 }
 
@@ -73,19 +84,19 @@ __device__ __forceinline__ double comm_time(double al, double be, double m) {
 
 // scheduling._fits (scheduling.py:172-176) on the contiguous range [a, b).
 __device__ __forceinline__ bool fits_range(const dm_tables& t, int w, int a, int b) {
-    bool ex = bytes_exact(t);
-    return col_range(t.gpu, t.pre_gpu, ex, a, b) <= t.cap_gpu[w]
-        && col_range(t.cpu, t.pre_cpu, ex, a, b) <= t.cap_cpu[w]
-        && col_range(t.disk, t.pre_disk, ex, a, b) <= t.cap_disk[w];
+    bool ex = bytes_exact(t), nb = np_bytes(t);
+    return col_range(t.gpu, t.pre_gpu, ex, a, b, nb) <= t.cap_gpu[w]
+        && col_range(t.cpu, t.pre_cpu, ex, a, b, nb) <= t.cap_cpu[w]
+        && col_range(t.disk, t.pre_disk, ex, a, b, nb) <= t.cap_disk[w];
 }
 
 // First failing capacity dimension of a contiguous run (verify_assignment
 // :199-203): 0 = fits, else DM_V_GPU / DM_V_CPU / DM_V_DISK.
 __device__ __forceinline__ int cap_violation(const dm_tables& t, int w, int a, int b) {
-    bool ex = bytes_exact(t);
-    if (col_range(t.gpu, t.pre_gpu, ex, a, b) > t.cap_gpu[w]) return DM_V_GPU;
-    if (col_range(t.cpu, t.pre_cpu, ex, a, b) > t.cap_cpu[w]) return DM_V_CPU;
-    if (col_range(t.disk, t.pre_disk, ex, a, b) > t.cap_disk[w]) return DM_V_DISK;
+    bool ex = bytes_exact(t), nb = np_bytes(t);
+    if (col_range(t.gpu, t.pre_gpu, ex, a, b, nb) > t.cap_gpu[w]) return DM_V_GPU;
+    if (col_range(t.cpu, t.pre_cpu, ex, a, b, nb) > t.cap_cpu[w]) return DM_V_CPU;
+    if (col_range(t.disk, t.pre_disk, ex, a, b, nb) > t.cap_disk[w]) return DM_V_DISK;
     return 0;
 }
 
@@ -97,7 +108,7 @@ __device__ __forceinline__ int cap_violation(const dm_tables& t, int w, int a, i
 template <class OwnerFn>
 __device__ __forceinline__ void run_cost_contig(const dm_tables& t, int a, int b, int w,
                                                 OwnerFn own, double& compute, double& read) {
-    double fl = col_range(t.flops, t.pre_flops, flops_exact(t), a, b);
+    double fl = col_range(t.flops, t.pre_flops, flops_exact(t), a, b, np_flops(t));
     compute = fl / t.speed[w];
     double rd = 0.0;
     if (include_comm(t)) {

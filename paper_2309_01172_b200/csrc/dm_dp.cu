@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) subset_dp_kernel(const dm_tables* __restr
         for (int it = threadIdx.x; it < n * n; it += blockDim.x) {
             int i = it / n, j = it % n + 1;
             if (j <= i) continue;
-            double fl = col_range(t.flops, t.pre_flops, flops_exact(t), i, j);
+            double fl = col_range(t.flops, t.pre_flops, flops_exact(t), i, j, np_flops(t));
             double rd = 0.0;
             if (include_comm(t)) {
                 for (int s = i; s < j; ++s)

@@ -31,14 +31,14 @@ __device__ inline bool in_run(const int32_t* idx, int k, int s) {
 }
 
 __device__ inline double col_items(const double* col, const int64_t* pre, bool exact,
-                                   const int32_t* idx, int k) {
+                                   const int32_t* idx, int k, bool np_items) {
     if (exact) {
         int64_t s = 0;
         for (int q = 0; q < k; ++q) s += pre[idx[q] + 1] - pre[idx[q]];
         return (double)s;
     }
     PySum acc;
-    for (int q = 0; q < k; ++q) acc.add(col[idx[q]]);
+    for (int q = 0; q < k; ++q) acc.add(col[idx[q]], !np_items);
     return acc.value();
 }
 
@@ -75,9 +75,10 @@ __global__ void eval_runs_kernel(dm_tables t, int32_t n_cand, const int32_t* __r
             seen[idx[q]] = 1; ++n_seen;
         }
         if (code) { bad = r - r0; break; }
-        if (col_items(t.gpu, t.pre_gpu, ex, idx, k) > t.cap_gpu[pe]) code = DM_V_GPU;
-        else if (col_items(t.cpu, t.pre_cpu, ex, idx, k) > t.cap_cpu[pe]) code = DM_V_CPU;
-        else if (col_items(t.disk, t.pre_disk, ex, idx, k) > t.cap_disk[pe]) code = DM_V_DISK;
+        const bool nb = np_bytes(t);
+        if (col_items(t.gpu, t.pre_gpu, ex, idx, k, nb) > t.cap_gpu[pe]) code = DM_V_GPU;
+        else if (col_items(t.cpu, t.pre_cpu, ex, idx, k, nb) > t.cap_cpu[pe]) code = DM_V_CPU;
+        else if (col_items(t.disk, t.pre_disk, ex, idx, k, nb) > t.cap_disk[pe]) code = DM_V_DISK;
         if (code) bad = r - r0;
     }
     if (code == DM_V_OK && n_seen != n) code = DM_V_UNASSIGNED;
@@ -109,7 +110,7 @@ __global__ void eval_runs_kernel(dm_tables t, int32_t n_cand, const int32_t* __r
         int k = run_ptr[r + 1] - run_ptr[r];
         int pe = run_peer[r];
         if (pe < 0 || pe >= t.P) { status = DM_E_UNKNOWN_PEER; break; }  // fleet.peer :158
-        double fl = col_items(t.flops, t.pre_flops, flops_exact(t), idx, k);
+        double fl = col_items(t.flops, t.pre_flops, flops_exact(t), idx, k, np_flops(t));
         double compute = fl / t.speed[pe];
         double rd = 0.0;
         if (include_comm(t)) {
@@ -167,8 +168,8 @@ __device__ void eval_owner_grouped(const dm_tables& t, const OT* row, double& mk
             last = i; ++k;
             if (ex) { sg += t.pre_gpu[i + 1] - t.pre_gpu[i]; sc += t.pre_cpu[i + 1] - t.pre_cpu[i];
                       sd += t.pre_disk[i + 1] - t.pre_disk[i]; }
-            else { pg.add(t.gpu[i]); pc.add(t.cpu[i]); pd.add(t.disk[i]); }
-            if (fex) sf += t.pre_flops[i + 1] - t.pre_flops[i]; else pf.add(t.flops[i]);
+            else { pg.add(t.gpu[i], !np_bytes(t)); pc.add(t.cpu[i], !np_bytes(t)); pd.add(t.disk[i], !np_bytes(t)); }
+            if (fex) sf += t.pre_flops[i + 1] - t.pre_flops[i]; else pf.add(t.flops[i], !np_flops(t));
         }
         if (code == DM_V_OK) {
             if (!contig) code = DM_V_NOT_CONTIGUOUS;
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
         int b = pr - rowidx[a];
         double v, c, rd;
         if (PAIR) {
-            v = col_range(t.flops, t.pre_flops, flops_exact(t), a, b) / t.speed[w];
+            v = col_range(t.flops, t.pre_flops, flops_exact(t), a, b, np_flops(t)) / t.speed[w];
         } else {
             run_cost_contig(t, a, b, w, [&](int) { return -1; }, c, rd);  // uniform link: every source is remote
             v = c + rd;

@@ -52,9 +52,9 @@ __device__ double hill_score(const dm_tables& t, int r, const int32_t* bounds, c
 __device__ int proportional(const dm_tables& t, int32_t* bounds, int32_t* peers) {
     const int n = t.n, p = t.p;
     PySum ts;
-    for (int w = 0; w < p; ++w) ts.add(t.speed[w]);
+    for (int w = 0; w < p; ++w) ts.add(t.speed[w], !(t.peer_np && t.peer_np[w]));
     double total_speed = ts.value();                                     // :332
-    double total_flops = col_range(t.flops, t.pre_flops, flops_exact(t), 0, n);  // :333
+    double total_flops = col_range(t.flops, t.pre_flops, flops_exact(t), 0, n, np_flops(t));  // :333
     if (total_flops == 0.0) total_flops = 1.0;
     int start = 0, nr = 0;
     double acc = 0.0, pf = t.flops[0];   // pf = prefix[end-1] (itertools.accumulate :334)
@@ -181,7 +181,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) epilogue_kernel(
             if (chain(t)) run_cost_contig(t, a, b, w, [&](int) { return prev; }, c, rd);
             else { BoundsOwner own{bounds, peers, r}; run_cost_contig(t, a, b, w, own, c, rd); }
             double load = c + rd;
-            loads[q] = load;
+            // Python type of p.compute_s + p.read_s: numpy when the speed, the
+            // FLOPs or (for a run with a crossing read) the link values are
+            // (sum() over them then turns naive, see PySum)
+            bool np_load = (t.peer_np && t.peer_np[w]) || np_flops(t);
+            if (np_comm(t) && include_comm(t)) {
+                if (chain(t)) np_load |= a > 0 && t.edge_ptr[a + 1] > t.edge_ptr[a];
+                else for (int i = a; i < b && !np_load; ++i)
+                    for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e)
+                        if (t.edge_src[e] < a || t.edge_src[e] >= b) { np_load = true; break; }
+            }
+            loads[q] = np_load ? -load : load;    // loads are >= 0 (or NaN): the sign bit flags a numpy item
             mk = load > mk ? load : mk;
             double m = c >= rd ? c : rd;          // max(p.compute_s, p.read_s) pipeline.py:50
             bn = m > bn ? m : bn;
@@ -196,7 +206,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) epilogue_kernel(
         __syncwarp();
         if (lane == 0) {
             PySum lat;                                 // fp_latency, builtin sum :43
-            for (int q = 0; q < r; ++q) lat.add(loads[q]);
+            for (int q = 0; q < r; ++q) {
+                const double v = loads[q];
+                lat.add(fabs(v), !signbit(v));
+            }
             double latency = lat.value();
             double fill = (double)(n_batches - 1) * bn;   // (n_b - 1) * bottleneck :56
             double pipe = latency + fill;

@@ -96,17 +96,27 @@ def op_costs(table: OpTable, fleet, placements) -> np.ndarray:
         for i, name in enumerate(table.names):
             pid = str(pl[name])
             place[b, i] = host.index_of[pid] if pid in host.index_of else unknown.setdefault(pid, host.P + len(unknown))
-    write_bw = np.array([float(fleet.peers[p].write_bandwidth) for p in host.peer_ids] or [1.0], np.float64)
+    wbw = [fleet.peers[p].write_bandwidth for p in host.peer_ids]
+    write_bw = np.array([float(v) for v in wbw] or [1.0], np.float64)
+    # CPython sum() in subgraph_time is compensated only over exact floats:
+    # record which totals the reference computes as numpy floats
+    write_np = np.array([0 if type(v) in (int, float, bool) else 1 for v in wbw] or [0], np.uint8)
+    d = fleet.default_link
+    np_links = any(type(v) not in (int, float, bool)
+                   for v in [d.alpha, d.beta, *(x for lk in fleet.links.values() for x in (lk.alpha, lk.beta))])
     from .engine import device_batch
     batch = device_batch([host], pin=False)
     dev = batch.dev_buf.device
-    arrs = [torch.from_numpy(a).to(dev) for a in (flops, mbytes, aptr, aidx, uptr, uidx, write_bw, place.reshape(-1))]
-    ops = _lib.DmOps(n, 0, *[a.data_ptr() for a in arrs[:6]])
+    arrs = [torch.from_numpy(a).to(dev)
+            for a in (flops, mbytes, aptr, aidx, uptr, uidx, write_bw, place.reshape(-1), write_np)]
+    ops = _lib.DmOps(n, _lib.DM_OPS_NP_LINKS if np_links else 0, *[a.data_ptr() for a in arrs[:6]],
+                     arrs[8].data_ptr())
     out = torch.empty(max(len(placements) * n * 3, 1), dtype=torch.float64, device=dev)
+    out_np = torch.empty(max(len(placements) * n, 1), dtype=torch.uint8, device=dev)
     st = batch.struct(0)
     _lib.check(lib.dm_op_costs(C.byref(ops), C.byref(st), arrs[6].data_ptr(), len(placements), arrs[7].data_ptr(),
-                               out.data_ptr(), _lib.stream_ptr()))
-    op_costs._last = (arrs, out, n)
+                               out.data_ptr(), out_np.data_ptr(), _lib.stream_ptr()))
+    op_costs._last = (arrs, out, out_np, n)
     return out.cpu().numpy()[: len(placements) * n * 3].reshape(len(placements), n, 3)
 
 
@@ -115,12 +125,13 @@ def subgraph_costs(table: OpTable, fleet, placements, cells) -> np.ndarray:
     import torch
     lib = _lib.load()
     op_costs(table, fleet, placements)
-    arrs, out, n = op_costs._last
+    arrs, out, out_np, n = op_costs._last
     idx = table.index
     sptr, sidx = _csr([[idx[x] for x in cell] for cell in cells])
     sp, si = torch.from_numpy(sptr).to(out.device), torch.from_numpy(sidx).to(out.device)
     res = torch.empty(max(len(placements) * len(cells) * 3, 1), dtype=torch.float64, device=out.device)
-    _lib.check(lib.dm_subgraph_times(n, len(placements), out.data_ptr(), len(cells), sp.data_ptr(), si.data_ptr(),
+    _lib.check(lib.dm_subgraph_times(n, len(placements), out.data_ptr(), out_np.data_ptr(), len(cells),
+                                     sp.data_ptr(), si.data_ptr(),
                                      res.data_ptr(), _lib.stream_ptr()))
     return res.cpu().numpy()[: len(placements) * len(cells) * 3].reshape(len(placements), len(cells), 3)
 

@@ -17,6 +17,8 @@ from __future__ import annotations
 import math
 from types import SimpleNamespace
 
+import numpy as np
+
 from . import _lib, engine
 from . import model as _model
 from .model import peer_sort_key
@@ -108,7 +110,24 @@ def _reason(stages, fleet, runs, code, bad):
     return f"peer {peer} exceeds {dim} capacity: {used:.0f} > {cap:.0f} bytes"
 
 
-def _report(stages, fleet, runs, include_comm, trace, res, c=0):
+def _cost_types(host, stages, peer, indices, include_comm):
+    """Python types of _run_cost's (compute, read) (scheduling.py:156-169):
+    numpy.float64 where the reference's arithmetic meets a numpy operand —
+    a numpy speed or FLOP count for compute, a crossing read priced with
+    numpy message/link values for read.  Later sum()s over these values
+    (fp_latency, pipeline.py:43) are compensated only over exact floats, so
+    the report carries the same types as the reference's."""
+    f = host.flags
+    pi = host.index_of.get(peer)
+    cnp = bool(f & _lib.DM_F_NP_FLOPS) or (pi is not None and bool(host.arrays["peer_np"][pi]))
+    rnp = False
+    if include_comm and f & _lib.DM_F_NP_COMM:
+        inside = set(indices)
+        rnp = any(src not in inside for i in indices for src, _ in stages[i].in_edges)
+    return cnp, rnp
+
+
+def _report(stages, fleet, runs, include_comm, trace, res, c=0, host=None):
     """Assemble the ScheduleReport of candidate c from device results
     (scheduling.py:210-232)."""
     lo = int(res["cand_ptr"][c])
@@ -120,12 +139,21 @@ def _report(stages, fleet, runs, include_comm, trace, res, c=0):
             comp[r] = (float(res["compute"][lo + r]), float(res["read"][lo + r]))
     order = sorted((r for r, (_, i) in enumerate(runs) if i), key=lambda r: min(runs[r][1]))
     rows, ordered_runs = [], []
+    typed = host is not None and (bool(host.flags & (_lib.DM_F_NP_FLOPS | _lib.DM_F_NP_COMM))
+                                  or bool(host.arrays["peer_np"].any()))
+    makespan = 0.0
     for r in order:
         peer, idxs = runs[r]
         indices = tuple(sorted(idxs))
         compute, read = comp[r]
+        if typed:
+            cnp, rnp = _cost_types(host, stages, peer, indices, include_comm)
+            compute = np.float64(compute) if cnp else compute
+            read = np.float64(read) if rnp else read
         ordered_runs.append((peer, indices))
-        rows.append(T.PeerLoad(peer, indices, compute, read, compute + read,
+        load = compute + read
+        makespan = max(makespan, load)          # :222, keeps the first maximal value's type
+        rows.append(T.PeerLoad(peer, indices, compute, read, load,
                                sum(stages[i].gpu_bytes for i in indices),
                                sum(stages[i].cpu_bytes for i in indices),
                                sum(stages[i].disk_bytes for i in indices)))
@@ -133,7 +161,10 @@ def _report(stages, fleet, runs, include_comm, trace, res, c=0):
     for peer in fleet.worker_ids():
         if peer not in assigned:
             rows.append(T.PeerLoad(peer, (), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0))
-    return T.ScheduleReport(tuple(stages), tuple(ordered_runs), tuple(rows), float(res["makespan"][c]),
+    mk = float(res["makespan"][c])
+    if typed and mk == makespan:
+        mk = makespan
+    return T.ScheduleReport(tuple(stages), tuple(ordered_runs), tuple(rows), mk,
                             feasible=(code == _lib.DM_V_OK), reason=reason,
                             include_comm=include_comm, trace=trace)
 
@@ -148,7 +179,7 @@ def _evaluate_many(stages, fleet, runs_list, include_comm, traces, host=None):
         if int(res["status"][c]) != _lib.DM_OK:
             out.append(None)
             continue
-        out.append(_report(stages, fleet, tuple(runs), include_comm, traces[c], res, c))
+        out.append(_report(stages, fleet, tuple(runs), include_comm, traces[c], res, c, host))
     return out, res
 
 

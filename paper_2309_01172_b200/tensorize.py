@@ -38,13 +38,13 @@ TABLES_DTYPE = np.dtype([
     ("pre_flops", "<u8"), ("pre_gpu", "<u8"), ("pre_cpu", "<u8"), ("pre_disk", "<u8"),
     ("edge_ptr", "<u8"), ("edge_src", "<u8"), ("edge_m", "<u8"),
     ("speed", "<u8"), ("cap_gpu", "<u8"), ("cap_cpu", "<u8"), ("cap_disk", "<u8"),
-    ("link_alpha", "<u8"), ("link_beta", "<u8"),
+    ("link_alpha", "<u8"), ("link_beta", "<u8"), ("peer_np", "<u8"),
 ])
 assert TABLES_DTYPE.itemsize == C.sizeof(_lib.DmTables)
 
 _PTR_FIELDS = ("flops", "gpu", "cpu", "disk", "pre_flops", "pre_gpu", "pre_cpu", "pre_disk",
                "edge_ptr", "edge_src", "edge_m", "speed", "cap_gpu", "cap_cpu", "cap_disk",
-               "link_alpha", "link_beta")
+               "link_alpha", "link_beta", "peer_np")
 
 
 def _exact_column(values) -> tuple[np.ndarray, np.ndarray | None]:
@@ -165,7 +165,17 @@ def build_host(stages, fleet, include_comm: bool = True) -> HostTables:
     edge_m = np.array(ms, dtype=np.float64)
 
     peers = [fleet.peers[pid] for pid in order]
-    speed = np.array([effective_speed(pe) for pe in peers], dtype=np.float64)
+    speeds = [effective_speed(pe) for pe in peers]
+    speed = np.array(speeds, dtype=np.float64)
+    # CPython's sum() is compensated only over exact `float` items
+    peer_np = np.array([0 if type(v) in (int, float, bool) else 1 for v in speeds] or [0], dtype=np.uint8)
+    def _np(v):
+        return type(v) not in (int, float, bool)
+    np_flops = any(_np(s.flops) for s in stages)
+    np_bytes = any(_np(s.gpu_bytes) or _np(s.cpu_bytes) or _np(s.disk_bytes) for s in stages)
+    np_comm = (_np(fleet.msg_ratio) or _np(fleet.default_link.alpha) or _np(fleet.default_link.beta)
+               or any(_np(lk.alpha) or _np(lk.beta) for lk in fleet.links.values())
+               or any(_np(nb) for s in stages for _, nb in s.in_edges))
     cap_gpu = np.array([float(pe.gpu_bytes) for pe in peers], dtype=np.float64)
     cap_cpu = np.array([float(pe.cpu_bytes) for pe in peers], dtype=np.float64)
     cap_disk = np.array([float(pe.disk_bytes) for pe in peers], dtype=np.float64)
@@ -204,6 +214,8 @@ def build_host(stages, fleet, include_comm: bool = True) -> HostTables:
         flags |= _lib.DM_F_BACKWARD
     if include_comm:
         flags |= _lib.DM_F_INCLUDE_COMM
+    flags |= (_lib.DM_F_NP_FLOPS if np_flops else 0) | (_lib.DM_F_NP_BYTES if np_bytes else 0)
+    flags |= _lib.DM_F_NP_COMM if np_comm else 0
 
     zero_pre = np.zeros(n + 1, dtype=np.int64)
     arrays = dict(flops=flops, gpu=gpu, cpu=cpu, disk=disk,
@@ -214,7 +226,7 @@ def build_host(stages, fleet, include_comm: bool = True) -> HostTables:
                   edge_ptr=edge_ptr, edge_src=edge_src if edge_src.size else np.zeros(1, np.int32),
                   edge_m=edge_m if edge_m.size else np.zeros(1, np.float64),
                   speed=speed, cap_gpu=cap_gpu, cap_cpu=cap_cpu, cap_disk=cap_disk,
-                  link_alpha=link_alpha, link_beta=link_beta)
+                  link_alpha=link_alpha, link_beta=link_beta, peer_np=peer_np)
     return HostTables(n=n, p=len(workers), P=P, flags=flags, def_alpha=float(d.alpha),
                       def_beta=float(d.beta), peer_ids=order, index_of=index_of, arrays=arrays)
 

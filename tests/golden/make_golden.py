@@ -96,7 +96,12 @@ def case(kind, stages, fleet, **kw):
 def solve_cases(stages, fleet, tag, brute=True, evals=()):
     """One fixture entry per instance: schedule(), brute_force_schedule() and
     evaluate_runs() of the given candidate runs."""
-    out = case("solve", stages, fleet, tag=tag, schedule=dump_report(S.schedule(stages, fleet)))
+    rep = S.schedule(stages, fleet)
+    out = case("solve", stages, fleet, tag=tag, schedule=dump_report(rep))
+    if rep.feasible:   # Eq. 3 / Eq. 4 over the schedule (pipeline.py:41-62), n_b = 64, 4 samples per batch
+        prof = PL.profiles_from_report(rep)
+        out["epilogue"] = [PL.fp_latency(prof), PL.bottleneck(prof), PL.pipeline_time(prof, 64),
+                           PL.throughput(prof, 64, 4)]
     if brute:
         try:
             out["brute_force"] = dump_report(S.brute_force_schedule(stages, fleet))
@@ -222,13 +227,25 @@ def opcost_cases():
     slow = hw.Fleet(dict(trio.peers, **{"1": hw.Peer("1", peak_flops=2e6, write_bandwidth=1024.0)}),
                     default_link=trio.default_link, links=trio.links)
     halfmsg = hw.Fleet(dict(trio.peers), default_link=trio.default_link, links=trio.links, msg_ratio=0.37)
+    # numpy-typed peer values (as the reference's own tests build fleets from
+    # rng draws): sum() over numpy totals is not compensated
+    npeers = dict(trio.peers)
+    for pid in ("2", "3"):
+        pe = npeers[pid]
+        npeers[pid] = hw.Peer(pid, role=pe.role, peak_flops=np.float64(pe.peak_flops) * np.float64(1.0 / 3.0),
+                              lam=pe.lam, gpu_bytes=pe.gpu_bytes, cpu_bytes=pe.cpu_bytes, disk_bytes=pe.disk_bytes,
+                              write_bandwidth=np.float64(pe.write_bandwidth) / 7.0)
+    numpy_fl = hw.Fleet(npeers, default_link=hw.Link(np.float64(trio.default_link.alpha) + 1e-4,
+                                                     trio.default_link.beta),
+                        links={k: hw.Link(np.float64(v.alpha), v.beta) for k, v in trio.links.items()},
+                        msg_ratio=0.61)
     rng = np.random.default_rng(91)
     placements = [dict(demo.placement)]
     for _ in range(12):
         placements.append({n: str(int(rng.integers(1, 5))) for n in names})
     cells = [("TensorA", "Multiply"), tuple(names), ("Conv", "Add", "Pool"), ("Label",)]
     out = {"table": table, "placements": placements, "cells": [list(c) for c in cells], "fleets": []}
-    for fl in (trio, slow, halfmsg):
+    for fl in (trio, slow, halfmsg, numpy_fl):
         rows, subs = [], []
         for pl in placements:
             rows.append([list(hw.op_time(demo, n, fl, pl)) for n in names])

@@ -8,34 +8,57 @@ mirror `paper_2309_01172_b200.model`)."""
 
 from __future__ import annotations
 
+import numpy as np
+
+
+def _enc(v):
+    """numpy scalars keep their type through the fixture: the reference's
+    sum() is compensated only over exact `float` items, so the type of
+    a speed or a FLOP count is part of the instance."""
+    if isinstance(v, np.floating):
+        return {"f64": float(v)}
+    if isinstance(v, np.integer):
+        return {"i64": int(v)}
+    return v
+
+
+def _dec(v):
+    if isinstance(v, dict):
+        return np.float64(v["f64"]) if "f64" in v else np.int64(v["i64"])
+    return v
+
 
 def dump_stages(stages):
-    return [[s.index, s.label, s.flops, s.gpu_bytes, s.cpu_bytes, s.disk_bytes, [list(e) for e in s.in_edges]]
+    return [[s.index, s.label, _enc(s.flops), _enc(s.gpu_bytes), _enc(s.cpu_bytes), _enc(s.disk_bytes),
+             [[e[0], _enc(e[1])] for e in s.in_edges]]
             for s in stages]
 
 
 def load_stages(rows, M):
-    return [M.Stage(r[0], r[1], r[2], r[3], r[4], r[5], tuple(tuple(e) for e in r[6])) for r in rows]
+    return [M.Stage(r[0], r[1], _dec(r[2]), _dec(r[3]), _dec(r[4]), _dec(r[5]),
+                    tuple((e[0], _dec(e[1])) for e in r[6])) for r in rows]
 
 
 def dump_fleet(f):
-    return {"peers": [[pe.id, pe.role.value, pe.peak_flops, pe.lam, pe.gpu_bytes, pe.cpu_bytes, pe.disk_bytes,
-                       pe.write_bandwidth] for pe in f.peers.values()],
-            "default_link": [f.default_link.alpha, f.default_link.beta],
-            "links": [[a, b, lk.alpha, lk.beta] for (a, b), lk in f.links.items()],
-            "backup_pool": list(f.backup_pool), "msg_ratio": f.msg_ratio,
+    return {"peers": [[pe.id, pe.role.value] + [_enc(x) for x in (pe.peak_flops, pe.lam, pe.gpu_bytes, pe.cpu_bytes,
+                                                                    pe.disk_bytes, pe.write_bandwidth)]
+                      for pe in f.peers.values()],
+            "default_link": [_enc(f.default_link.alpha), _enc(f.default_link.beta)],
+            "links": [[a, b, _enc(lk.alpha), _enc(lk.beta)] for (a, b), lk in f.links.items()],
+            "backup_pool": list(f.backup_pool), "msg_ratio": _enc(f.msg_ratio),
             "pinned_runs": None if f.pinned_runs is None else [list(r) for r in f.pinned_runs],
             "name": f.name}
 
 
 def load_fleet(d, M):
     peers = {}
-    for pid, role, pk, lam, g, c, dk, wb in d["peers"]:
+    for pid, role, *vals in d["peers"]:
+        pk, lam, g, c, dk, wb = (_dec(x) for x in vals)
         peers[pid] = M.Peer(pid, role=M.Role(role), peak_flops=pk, lam=lam, gpu_bytes=g, cpu_bytes=c,
                             disk_bytes=dk, write_bandwidth=wb)
-    fl = M.Fleet(peers=peers, default_link=M.Link(*d["default_link"]),
-                 links={(a, b): M.Link(al, be) for a, b, al, be in d["links"]},
-                 backup_pool=tuple(d["backup_pool"]), msg_ratio=d["msg_ratio"], name=d["name"])
+    fl = M.Fleet(peers=peers, default_link=M.Link(*(_dec(x) for x in d["default_link"])),
+                 links={(a, b): M.Link(_dec(al), _dec(be)) for a, b, al, be in d["links"]},
+                 backup_pool=tuple(d["backup_pool"]), msg_ratio=_dec(d["msg_ratio"]), name=d["name"])
     if d["pinned_runs"] is not None:
         fl.pinned_runs = tuple(tuple(r) for r in d["pinned_runs"])
     return fl
@@ -45,7 +68,10 @@ def dump_report(r):
     return {"runs": [[p, list(i)] for p, i in r.runs], "makespan": r.makespan, "feasible": r.feasible,
             "reason": r.reason, "trace": list(r.trace), "include_comm": r.include_comm,
             "per_peer": [[x.peer, list(x.stage_indices), x.compute_s, x.read_s, x.load_s, x.gpu_bytes, x.cpu_bytes,
-                          x.disk_bytes] for x in r.per_peer]}
+                          x.disk_bytes] for x in r.per_peer],
+            # Python types of the float fields (float vs numpy.float64)
+            "types": [type(r.makespan).__name__] + [[type(v).__name__ for v in (x.compute_s, x.read_s, x.load_s)]
+                                                    for x in r.per_peer]}
 
 
 def runs_of(d):
@@ -68,4 +94,6 @@ def report_matches(got, want) -> list:
         for a, b in zip(g["per_peer"], want["per_peer"]):
             if a[:5] != b[:5] or a[5:] != b[5:] or [type(x) for x in a[5:]] != [type(x) for x in b[5:]]:
                 bad.append(f"row {b[0]}")
+    if "types" in want and g["types"] != want["types"]:
+        bad.append("types")
     return bad

@@ -34,12 +34,13 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_agree():
     from oracle import oracle
-    assert C.sizeof(_lib.DmTables) == C.sizeof(oracle.Tables) == tensorize.TABLES_DTYPE.itemsize == 176
+    assert C.sizeof(_lib.DmTables) == C.sizeof(oracle.Tables) == tensorize.TABLES_DTYPE.itemsize == 184
     for (a, _), (b, _) in zip(_lib.DmTables._fields_, oracle.Tables._fields_):
         assert a == b
         assert getattr(_lib.DmTables, a).offset == getattr(oracle.Tables, b).offset
         assert getattr(_lib.DmTables, a).offset == tensorize.TABLES_DTYPE.fields[a][1]
     assert C.sizeof(_lib.DmWinner) == 40
+    assert C.sizeof(_lib.DmOps) == 64
 
 
 def test_engine_fails_loudly_without_device():

@@ -57,6 +57,37 @@ def test_schedule_and_brute_force_golden(engine_ready):
     assert n > 280
 
 
+def test_schedule_epilogue_golden(engine_ready):
+    """dm_pipeline_epilogue over every feasible golden schedule, batched, bit
+    for bit against the reference's Eq. 3 / Eq. 4 values (numpy-typed fleets
+    included)."""
+    import torch
+    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200.tensorize import build_host
+    hosts, owners, want = [], [], []
+    for c in CASES:
+        if c["kind"] != "solve" or "epilogue" not in c:
+            continue
+        st, fl = _inst(c)
+        h = build_host(st, fl)
+        own = [0] * len(st)
+        for pe, ix in runs_of(c["schedule"]["runs"]):
+            for i in ix:
+                own[i] = h.index_of[pe]
+        hosts.append(h)
+        owners.append(own)
+        want.append(c["epilogue"])
+    n_max = max(len(o) for o in owners)
+    own = torch.full((len(owners), n_max), -1, dtype=torch.int16)
+    for s_, o in enumerate(owners):
+        own[s_, :len(o)] = torch.tensor(o, dtype=torch.int16)
+    batch = engine.device_batch(hosts)
+    out = engine.epilogue(batch, n_max, own.cuda(), 64, 4).cpu().numpy()
+    for s_, w in enumerate(want):
+        assert out[s_, 1:5].tolist() == w, s_
+    assert len(want) > 250
+
+
 def test_reschedule_golden(engine_ready):
     for c in CASES:
         if c["kind"] != "reschedule":

@@ -112,3 +112,43 @@ def test_reference_fleet_files_parse_identically(dagmesh_ref):
         a = dump_fleet(dagmesh_ref.hardware.load_fleet(f))
         b = dump_fleet(M.load_fleet(f))
         assert a == b, f
+
+
+def test_report_assembly_types_golden():
+    """scheduling._report (host-side report assembly) fed with the oracle's
+    per-run costs reproduces the reference's reports field for field —
+    including which floats are numpy.float64 (fleets built from rng draws):
+    CPython's sum() over report values is compensated only over exact floats,
+    so the types are part of parity."""
+    import json
+    import pathlib
+
+    import numpy as np
+
+    from golden_io import load_fleet, load_stages, report_matches, runs_of
+    from oracle import oracle as O
+    from paper_2309_01172_b200 import model as M
+    from paper_2309_01172_b200 import scheduling as S
+    from paper_2309_01172_b200.tensorize import build_host
+
+    O.build()
+    cases = json.loads((pathlib.Path(__file__).parent / "golden" / "scheduling_cases.json").read_text())["cases"]
+    n_np = n = 0
+    for c in cases:
+        if c["kind"] != "solve":
+            continue
+        st, fl = load_stages(c["stages"], M), load_fleet(c["fleet"], M)
+        want = c["schedule"]
+        if not want["feasible"]:
+            continue
+        runs = runs_of(want["runs"])
+        inst = O.Instance(st, fl)
+        mk, code, bad, status, comp, read = inst.eval_runs(runs)
+        res = dict(compute=np.asarray(comp), read=np.asarray(read), makespan=np.array([mk]),
+                   code=np.array([code]), code_run=np.array([bad]), status=np.array([status]),
+                   cand_ptr=np.array([0, len(runs)]))
+        rep = S._report(st, fl, runs, True, tuple(want["trace"]), res, 0, build_host(st, fl))
+        assert report_matches(rep, want) == [], c["tag"]
+        n += 1
+        n_np += "float64" in json.dumps(want["types"])
+    assert n > 250 and n_np > 200

@@ -127,3 +127,22 @@ def test_py_sum_restatement(oracle_mod):
         k = int(rng.integers(1, 40))
         v = [float(x) for x in rng.standard_normal(k) * 10.0 ** rng.integers(-5, 20, k)]
         assert oracle_mod.py_sum(v) == sum(v)
+
+
+def test_oracle_schedule_epilogue(oracle_mod):
+    """Eq. 3 / Eq. 4 over every feasible golden schedule, against the
+    reference's fp_latency / bottleneck / pipeline_time / throughput
+    (pipeline.py:41-62) — fleets with numpy speeds included, where fp_latency's
+    sum() runs uncompensated."""
+    n = 0
+    for c in CASES:
+        if c["kind"] != "solve" or "epilogue" not in c:
+            continue
+        _, _, inst = _inst(oracle_mod, c)
+        runs = runs_of(c["schedule"]["runs"])
+        mk, code, _, _, comp, read = inst.eval_runs(runs)
+        assert code == 0
+        got = oracle_mod.epilogue(comp, read, 64, 4, inst.load_np(runs))
+        assert list(got) == c["epilogue"], c["tag"]
+        n += 1
+    assert n > 250
