@@ -201,10 +201,9 @@ def run_b200(args, rank, world, local_rank):
         return None
     value = total * args.steps / (ms / 1e3)
     e2e_val = total * args.steps / (e2e_ms / 1e3)
-    mean_runs = mean_runs_splits(n, p)
-    fp64_ops = 6 * mean_runs - 3
-    peak = extras.get("fp64_peak_ops_per_s")
-    achieved = total / (kernel_ms / 1e3) * fp64_ops / 1e12
+    cross = extras.get("cross_peak_pairs_per_s")
+    achieved = res["n_feasible"] / world / (kernel_ms / 1e3) / 1e9      # per GPU
+    traffic = ncu_traffic("splits_mitm_kernel") or {}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -213,13 +212,16 @@ def run_b200(args, rank, world, local_rank):
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(batch.h2d_bytes),
                 "d2h_bytes_per_step": int(D.WINNER_BYTES * world)},
         "gpu_launches": 2 * args.steps,
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": (peak / 1e12) if peak else None,
-                     "unit": "TFLOP/s", "frac": (achieved / (peak / 1e12)) if peak else None,
-                     "traffic": (ncu_traffic("splits_memo_kernel") or {}).get("bytes"),
-                     "traffic_source": (ncu_traffic("splits_memo_kernel") or {}).get("capture"),
-                     "algorithmic_ops_per_candidate": fp64_ops, "kernel_ms": kernel_ms,
-                     "note": "algorithmic fp64 add/mul/div per candidate (SURVEY 8d Mode B: 6r-3, r = mean runs "
-                             "of the population) / kernel time, vs the microbenchmarked fp64 op rate"},
+        "roofline": {"bound": "issue", "achieved": achieved, "peak": (cross / 1e9) if cross else None,
+                     "unit": "Gcand/s", "frac": (achieved / (cross / 1e9)) if cross else None,
+                     "traffic": traffic.get("bytes"), "traffic_source": traffic.get("capture"),
+                     "kernel_ms": kernel_ms,
+                     "algorithmic_work_per_candidate": "one fp64 max (DSETP + 64-bit select) and one 64-bit "
+                                                       "checksum add per feasible candidate",
+                     "note": "splits_mitm_kernel: feasible candidates per second vs dm_microbench_cross (the "
+                             "same inner loop alone, same grid and occupancy: the instruction-issue bound); "
+                             "infeasible candidates are resolved per side element (an unfit run), as the "
+                             "reference's `continue` skips them"},
         "winner": {"makespan": res["makespan"], "rank": res["rank"], "n_feasible": res["n_feasible"],
                    "checksum": res["checksum"]},
     }
@@ -251,12 +253,6 @@ def ncu_traffic(kernel_substr, profile_glob="r1_prof_*_raw.csv"):
         except Exception:
             continue
     return best
-
-
-def mean_runs_splits(n, p):
-    import math
-    tot = sum(math.comb(n - 1, r - 1) for r in range(1, min(n, p) + 1))
-    return sum(r * math.comb(n - 1, r - 1) for r in range(1, min(n, p) + 1)) / tot
 
 
 def _hbm_peak():
@@ -508,6 +504,7 @@ def secondary_measurements(dev):
     out = {}
     from paper_2309_01172_b200 import engine
     out["fp64_peak_ops_per_s"] = engine.fp64_peak()
+    out["cross_peak_pairs_per_s"] = engine.cross_peak()
     out["cpu_baseline"] = cpu_baseline(threads=1, seconds=10.0)
     sec = {}
     for name, fn in (("mode_a_c1", lambda: mode_a_measure(dev, "c1")), ("mode_a_c2", lambda: mode_a_measure(dev, "c2")),

@@ -323,6 +323,12 @@ DM_API int dm_subgraph_times(int32_t n_ops, int32_t n_place, const double* op_ou
  * the number of fp64 operations the launch performs; time it with events. */
 DM_API int dm_microbench_fp64(int64_t iters, double* sink, int64_t* ops, void* stream);
 
+/* dm_microbench_cross — the whole-population split sweep's inner loop alone
+ * (one fp64 max + checksum add per candidate pair, register x shared-memory
+ * operands, the sweep's grid and occupancy): the issue-bound roofline of the
+ * sweep.  *pairs receives the candidate pairs the launch evaluates. */
+DM_API int dm_microbench_cross(int64_t iters, uint64_t* sink, int64_t* pairs, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,22 +9,12 @@
 // single-CTA pass merges the partials (deterministic: the key is
 // (makespan, global rank), independent of grid shape and GPU count).
 #include "dm_common.cuh"
+#include "dm_memo.cuh"
+#include "dm_mitm.cuh"
 
 namespace dm {
 
 // ----------------------------------------------------------- combinatorics
-// Saturating binomial C(a, b) (int64 max on overflow) — only used when a
-// thread unranks its first candidate.
-__device__ inline int64_t binom_sat(int a, int b) {
-    if (b < 0 || b > a) return 0;
-    if (b > a - b) b = a - b;
-    unsigned __int128 r = 1;
-    for (int i = 1; i <= b; ++i) {
-        r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
-        if (r > (unsigned __int128)INT64_MAX) return INT64_MAX;
-    }
-    return (int64_t)r;
-}
 
 __device__ inline int64_t perm_sat(int p, int r) {
     unsigned __int128 v = 1;
@@ -190,16 +180,8 @@ __global__ void __launch_bounds__(256) enum_kernel(dm_tables t, int64_t k0, int6
 }
 
 // ------------------------------------------------ memoised identity splits
-// For the identity-order split population (run q on worker q) the load of a
-// run depends only on (q, a, b) whenever the crossing read does not depend on
-// which run owns a source stage: include_comm off, a uniform link (no pair
-// overrides: every crossing source sits on another worker), or
-// chain-structured stages (the source of run q's crossing edges is stage a-1,
-// owned by worker q-1).  Each CTA then tabulates
-//     T[q][a][b] = _fits(q, a..b) ? compute + read : +inf
-// once in shared memory (n(n+1)(n+2)/6 doubles at most, 57 KB for n = 34)
-// with exactly the reference's arithmetic, and every candidate is scored
-// from scratch as the max over its r runs of T.
+// Rank-range form (any [k0, k1)): every candidate is scored from scratch as
+// the max over its r runs of the memo table T (dm_memo.cuh).
 //
 // Each thread keeps its current combination as cut bytes in shared memory
 // (column-major per thread, 4 cuts per 32-bit word, the final boundary n
@@ -211,38 +193,8 @@ __global__ void __launch_bounds__(256) enum_kernel(dm_tables t, int64_t k0, int6
 constexpr int kMemoThreads = 512;
 constexpr int kMemoChunk = 64;
 
-// Shared-memory layout of the memo kernel.  rowoff[q * S + a] is the byte
-// offset of T[q][a][0] (so &T[q][a][b] = sm + rowoff + 8b); row a = n of
-// every q points at a row of -inf so that runs past the final boundary
-// (groups of 4 are scored unconditionally) never change the max.
-struct MemoLayout {
-    int n, rmax, W, S;
-    int t_elems;
-    size_t off_dummy, off_rowoff, off_binom, off_cum, off_cuts, bytes;
-};
-
-__host__ __device__ inline MemoLayout memo_layout(int n, int p) {
-    MemoLayout L;
-    L.n = n; L.rmax = n < p ? n : p; L.W = n - 1; L.S = n < 64 ? 64 : 256;
-    int tot = 0;
-    for (int q = 0; q < L.rmax; ++q) { int Lq = n - q; tot += Lq * (Lq + 1) / 2; }
-    L.t_elems = tot;
-    size_t off = (size_t)tot * 8;
-    L.off_dummy = off; off += (size_t)(n + 1) * 8;
-    off = (off + 15) & ~(size_t)15;
-    L.off_rowoff = off; off += (size_t)(L.rmax + 4) * L.S * 4;
-    L.off_binom = off; off += (size_t)n * (L.rmax + 1) * 8;
-    L.off_cum = off; off += (size_t)(L.rmax + 2) * 8;
-    off = (off + 15) & ~(size_t)15;
-    L.off_cuts = off; off += (size_t)((L.rmax + 4) / 4 + 2) * kMemoThreads * 4;
-    L.bytes = off;
-    return L;
-}
-
-__device__ __forceinline__ double lds_f64(uint32_t addr) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-    return v;
+__host__ __device__ inline size_t memo_cut_bytes(const MemoLayout& L) {
+    return (size_t)((L.rmax + 4) / 4 + 2) * kMemoThreads * 4;
 }
 
 template <int S>
@@ -255,44 +207,9 @@ __global__ void __launch_bounds__(kMemoThreads, 2) splits_memo_kernel(dm_tables 
     int32_t* rowoff = reinterpret_cast<int32_t*>(sm + L.off_rowoff);
     int64_t* binom = reinterpret_cast<int64_t*>(sm + L.off_binom);   // C(a, b), a < n, b <= rmax
     int64_t* cum = reinterpret_cast<int64_t*>(sm + L.off_cum);       // cum[m] = first rank with m cuts
-    unsigned char* cutb = sm + L.off_cuts;                            // byte z of thread t: ((z>>2)*BS+t)*4+(z&3)
+    unsigned char* cutb = sm + L.off_tail;                            // byte z of thread t: ((z>>2)*BS+t)*4+(z&3)
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
-
-    const uint32_t sm_base = (uint32_t)__cvta_generic_to_shared(sm);
-    for (int i = threadIdx.x; i < (rmax + 4) * S; i += blockDim.x) {
-        int q = i / S, a = i % S;
-        int32_t v = (int32_t)L.off_dummy;
-        if (q < rmax && a >= q && a < n) {
-            int base = 0;
-            for (int qq = 0; qq < q; ++qq) { int Lq = n - qq; base += Lq * (Lq + 1) / 2; }
-            int within = (a - q) * n - ((a - q) * (a + q - 1)) / 2;
-            v = (base + within - (a + 1)) * 8;
-        }
-        rowoff[i] = (int32_t)(sm_base + (uint32_t)v);   // absolute shared address of T[q][a][0]
-    }
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) reinterpret_cast<double*>(sm + L.off_dummy)[i] = -inf;
-    for (int i = threadIdx.x; i < n * R1; i += blockDim.x) binom[i] = binom_sat(i / R1, i % R1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cum[0] = 0;
-        for (int m = 1; m <= rmax; ++m) cum[m] = cum[m - 1] + binom[(n - 1) * R1 + (m - 1)];
-    }
-    for (int row = threadIdx.x; row < rmax * n; row += blockDim.x) {
-        int q = row / n, a = row % n;
-        if (a < q) continue;
-        double* Trow = reinterpret_cast<double*>(sm + ((uint32_t)rowoff[q * S + a] - sm_base));
-        for (int b = a + 1; b <= n; ++b) {
-            double v = inf;
-            if ((q > 0 || a == 0) && fits_range(t, q, a, b)) {
-                double c, rd;
-                if (chain(t)) run_cost_contig(t, a, b, q, [&](int) { return q - 1; }, c, rd);
-                else run_cost_contig(t, a, b, q, [&](int s) { return s < a ? -1 : q + 1; }, c, rd);
-                v = c + rd;
-            }
-            Trow[b] = v;
-        }
-    }
-    __syncthreads();
+    memo_build(t, L, sm);
 
     const int BS = blockDim.x, tid = threadIdx.x;
     uint32_t* cutw = reinterpret_cast<uint32_t*>(cutb) + tid;   // word j at cutw[j * BS]
@@ -760,23 +677,46 @@ int launch_enum(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts
     return DM_OK;
 }
 
+// The meet-in-the-middle sweep covers whole populations only: [k0, k1) must
+// be every split of the instance (its parts are tile sets, not rank ranges).
+bool nparts_full_range(const dm_tables* t, int64_t k0, int64_t k1) {
+    if (k0 != 0) return false;
+    const int n = t->n, rmax = t->n < t->p ? t->n : t->p;
+    unsigned __int128 tot = 0, c = 1;   // C(n-1, m) for m = 0..rmax-1
+    for (int m = 0; m < rmax; ++m) {
+        tot += c;
+        if (tot > (unsigned __int128)INT64_MAX) return false;
+        c = c * (unsigned __int128)(n - 1 - m) / (unsigned __int128)(m + 1);
+    }
+    return (unsigned __int128)k1 == tot;
+}
+
 int enum_splits_impl(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts, dm_winner* out,
                      void* scratch, void* stream) {
     if (!t || !out || !scratch || t->n <= 0 || t->p <= 0 || nparts < 1 || part < 0 || part >= nparts)
         return dmabi::fail(DM_E_ARG, "bad arguments");
     cudaStream_t s = (cudaStream_t)stream;
-    const uint32_t f = t->flags;
-    bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
+    const bool memo_ok = dm::memo_valid(*t) && !getenv_flag("DM_DISABLE_MEMO");
+    if (memo_ok && nparts_full_range(t, k0, k1) && !getenv_flag("DM_DISABLE_MITM")) {
+        int rc = dm::launch_splits_mitm(*t, part, nparts, (dm_winner*)scratch, enum_grid() / 8, s);
+        if (rc != DM_E_TOO_LARGE) {
+            if (rc != DM_OK) return rc;
+            dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, dm::mitm_grid(enum_grid() / 8), out);
+            DM_CHECK_LAUNCH();
+            return DM_OK;
+        }
+    }
     dm::MemoLayout L = dm::memo_layout(t->n, t->p);
-    if (memo_ok && t->n <= 64 && L.bytes <= 110 * 1024 && !getenv_flag("DM_DISABLE_MEMO")) {
+    const size_t memo_bytes = L.off_tail + dm::memo_cut_bytes(L);
+    if (memo_ok && t->n <= 64 && memo_bytes <= 110 * 1024) {
         int grid = enum_grid() / 8 * 2;  // 2 CTAs x 512 threads per SM
         if (L.S == 64) {
-            cudaFuncSetAttribute(dm::splits_memo_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-            dm::splits_memo_kernel<64><<<grid, dm::kMemoThreads, L.bytes, s>>>(*t, k0, k1, part, nparts,
+            cudaFuncSetAttribute(dm::splits_memo_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)memo_bytes);
+            dm::splits_memo_kernel<64><<<grid, dm::kMemoThreads, memo_bytes, s>>>(*t, k0, k1, part, nparts,
                                                                               (dm_winner*)scratch);
         } else {
-            cudaFuncSetAttribute(dm::splits_memo_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-            dm::splits_memo_kernel<256><<<grid, dm::kMemoThreads, L.bytes, s>>>(*t, k0, k1, part, nparts,
+            cudaFuncSetAttribute(dm::splits_memo_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)memo_bytes);
+            dm::splits_memo_kernel<256><<<grid, dm::kMemoThreads, memo_bytes, s>>>(*t, k0, k1, part, nparts,
                                                                                (dm_winner*)scratch);
         }
         DM_CHECK_LAUNCH();

@@ -244,6 +244,26 @@ def unrank(n: int, p: int, k: int, mode: str):
     raise IndexError(k)
 
 
+def cross_peak(iters: int = 400, repeats: int = 3) -> float:
+    """Measured candidate pairs per second of the split sweep's inner loop
+    alone (dm_microbench_cross): the sweep's issue-bound roofline."""
+    lib = _lib.load()
+    torch = _torch()
+    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+    pairs = C.c_int64(0)
+    s = _lib.stream_ptr()
+    _lib.check(lib.dm_microbench_cross(4, sink.data_ptr(), C.byref(pairs), s))
+    best = 0.0
+    for _ in range(repeats):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.check(lib.dm_microbench_cross(iters, sink.data_ptr(), C.byref(pairs), s))
+        b.record()
+        b.synchronize()
+        best = max(best, pairs.value / (a.elapsed_time(b) / 1e3))
+    return best
+
+
 def fp64_peak(iters: int = 20000, repeats: int = 3) -> float:
     """Measured fp64 (DMUL/DADD) operations per second on the current device."""
     lib = _lib.load()

@@ -349,3 +349,36 @@ def test_split_parts_partition_the_population(engine_ready):
                 recs.append(struct.pack(D.WINNER_FMT, w["makespan"], w["rank"], w["n_evaluated"], w["n_feasible"],
                                         w["checksum"]))
             assert D.merge_records(np.frombuffer(b"".join(recs), np.uint8)) == full
+
+
+def test_splits_mitm_matches_memo_and_oracle(oracle_mod, engine_ready, monkeypatch):
+    """The whole-population meet-in-the-middle sweep (dm_mitm.cu) against the
+    oracle (small shapes, incl. n = 1, p = 1, n < p, n > p) and against the
+    rank-range memo kernel (larger shapes, memory pressure, DAG with a uniform
+    link, no-comm); part-wise sweeps merge to the same record."""
+    import struct
+    from paper_2309_01172_b200 import dist as D
+    rng = np.random.default_rng(2309)
+    shapes = [(1, 1), (1, 4), (2, 1), (2, 2), (3, 5), (6, 3), (9, 9), (12, 5), (16, 16), (18, 7)]
+    for i, (n, p) in enumerate(shapes):
+        st, fleet = big_instance(rng, n, p, dag=i % 3 == 1, links=False, pressure=(0.05, 0.9))
+        inst = oracle_mod.Instance(st, fleet)
+        batch = engine.device_batch([build_host(st, fleet)])
+        total = engine.splits_total(n, p)
+        assert engine.enum(batch, "splits", 0, total).read() == inst.enum("splits", 0, total), (n, p)
+    for n, p, dag, links, inc, pr in [(30, 24, False, True, True, (0.1, 0.6)), (28, 28, True, False, True, (0.05, 0.5)),
+                                      (26, 12, True, True, False, (0.2, 0.9)), (34, 32, False, False, True, (0.3, 1.2))]:
+        st, fleet = big_instance(rng, n, p, dag=dag, links=links, pressure=pr)
+        batch = engine.device_batch([build_host(st, fleet, inc)])
+        total = engine.splits_total(n, p)
+        a = engine.enum(batch, "splits", 0, total).read()
+        monkeypatch.setenv("DM_DISABLE_MITM", "1")
+        b = engine.enum(batch, "splits", 0, total).read()
+        monkeypatch.delenv("DM_DISABLE_MITM")
+        assert a == b and a["n_evaluated"] == total, (n, p)
+        recs = []
+        for part in range(3):
+            w = engine.enum(batch, "splits", 0, total, part=part, nparts=3).read()
+            recs.append(struct.pack(D.WINNER_FMT, w["makespan"], w["rank"], w["n_evaluated"], w["n_feasible"],
+                                    w["checksum"]))
+        assert D.merge_records(np.frombuffer(b"".join(recs), np.uint8)) == a
