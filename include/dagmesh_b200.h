@@ -217,6 +217,19 @@ DM_API int dm_enum_splits(const dm_tables* t, int64_t k0, int64_t k1,
 DM_API int dm_enum_splits_part(const dm_tables* t, int64_t k0, int64_t k1, int32_t part,
                                int32_t nparts, dm_winner* out, void* scratch, void* stream);
 
+/* Whole-population split sweeps (k0 = 0, k1 = every split) run as a
+ * meet-in-the-middle cross product over per-sweep side tables held in a
+ * device workspace.  dm_splits_workspace_bytes: bytes that workspace needs
+ * (-1: the instance takes the rank-range kernels).  dm_enum_splits_ws: as
+ * dm_enum_splits_part with a caller-provided workspace (NULL or smaller than
+ * required: allocated stream-ordered inside the call, as dm_enum_splits and
+ * dm_enum_splits_part do).  Replaces the same brute_force_schedule loop
+ * (scheduling.py:245-278) for the identity worker order. */
+DM_API int64_t dm_splits_workspace_bytes(const dm_tables* t);
+DM_API int dm_enum_splits_ws(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts,
+                             dm_winner* out, void* scratch, void* workspace, int64_t workspace_bytes,
+                             void* stream);
+
 /*
  * dm_enum_random — counter-RNG random contiguous placements (config C5):
  * candidate k (k0 <= k < k1) is generated from SplitMix64 keyed (seed, k):

@@ -692,16 +692,18 @@ bool nparts_full_range(const dm_tables* t, int64_t k0, int64_t k1) {
 }
 
 int enum_splits_impl(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts, dm_winner* out,
-                     void* scratch, void* stream) {
+                     void* scratch, void* ws, int64_t ws_bytes, void* stream) {
     if (!t || !out || !scratch || t->n <= 0 || t->p <= 0 || nparts < 1 || part < 0 || part >= nparts)
         return dmabi::fail(DM_E_ARG, "bad arguments");
     cudaStream_t s = (cudaStream_t)stream;
     const bool memo_ok = dm::memo_valid(*t) && !getenv_flag("DM_DISABLE_MEMO");
     if (memo_ok && nparts_full_range(t, k0, k1) && !getenv_flag("DM_DISABLE_MITM")) {
-        int rc = dm::launch_splits_mitm(*t, part, nparts, (dm_winner*)scratch, enum_grid() / 8, s);
+        int n_partials = 0;
+        int rc = dm::launch_splits_mitm(*t, part, nparts, (dm_winner*)scratch, enum_grid() / 8, ws, ws_bytes,
+                                        &n_partials, s);
         if (rc != DM_E_TOO_LARGE) {
             if (rc != DM_OK) return rc;
-            dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, dm::mitm_grid(enum_grid() / 8), out);
+            dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, n_partials, out);
             DM_CHECK_LAUNCH();
             return DM_OK;
         }
@@ -741,12 +743,22 @@ int dm_enum_bruteforce(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* ou
 
 int dm_enum_splits(const dm_tables* t, int64_t k0, int64_t k1, dm_winner* out,
                    void* scratch, void* stream) {
-    return enum_splits_impl(t, k0, k1, 0, 1, out, scratch, stream);
+    return enum_splits_impl(t, k0, k1, 0, 1, out, scratch, nullptr, 0, stream);
 }
 
 int dm_enum_splits_part(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts,
                         dm_winner* out, void* scratch, void* stream) {
-    return enum_splits_impl(t, k0, k1, part, nparts, out, scratch, stream);
+    return enum_splits_impl(t, k0, k1, part, nparts, out, scratch, nullptr, 0, stream);
+}
+
+int64_t dm_splits_workspace_bytes(const dm_tables* t) {
+    if (!t) return -1;
+    return dm::mitm_workspace_bytes(*t);
+}
+
+int dm_enum_splits_ws(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts, dm_winner* out,
+                      void* scratch, void* workspace, int64_t workspace_bytes, void* stream) {
+    return enum_splits_impl(t, k0, k1, part, nparts, out, scratch, workspace, workspace_bytes, stream);
 }
 
 int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,

@@ -120,6 +120,15 @@ class WinnerBuffers:
         torch = _torch()
         self.scratch = torch.empty(int(lib.dm_enum_scratch_bytes()) + 256, dtype=torch.uint8, device=device)
         self.out = torch.empty(_WINNER_BYTES, dtype=torch.uint8, device=device)
+        self.device = device
+        self.workspace = None      # split-sweep side tables (dm_splits_workspace_bytes), grown on demand
+
+    def workspace_for(self, nbytes: int):
+        if nbytes <= 0:
+            return None
+        if self.workspace is None or self.workspace.numel() < nbytes:
+            self.workspace = _torch().empty(nbytes, dtype=_torch().uint8, device=self.device)
+        return self.workspace
 
     def read(self) -> dict:
         raw = self.out.cpu().numpy().tobytes()
@@ -147,11 +156,11 @@ def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | 
     if mode == "bruteforce":
         _lib.check(lib.dm_enum_bruteforce(C.byref(st), k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
     elif mode == "splits":
-        if nparts > 1:
-            _lib.check(lib.dm_enum_splits_part(C.byref(st), k0, k1, part, nparts, bufs.out.data_ptr(),
-                                               bufs.scratch.data_ptr(), s))
-        else:
-            _lib.check(lib.dm_enum_splits(C.byref(st), k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
+        need = int(lib.dm_splits_workspace_bytes(C.byref(st)))
+        ws = bufs.workspace_for(need)
+        _lib.check(lib.dm_enum_splits_ws(C.byref(st), k0, k1, part, nparts, bufs.out.data_ptr(),
+                                         bufs.scratch.data_ptr(), ws.data_ptr() if ws is not None else None,
+                                         max(need, 0), s))
     elif mode == "random":
         _lib.check(lib.dm_enum_random(C.byref(st), online.data_ptr(), online.numel(), mults.data_ptr(),
                                       mults.numel(), seed & 0xFFFFFFFFFFFFFFFF, k0, k1, bufs.out.data_ptr(),
