@@ -1,6 +1,6 @@
 // dm_mitm.cu — the exhaustive identity-split sweep (the split population of
 // brute_force_schedule, scheduling.py:245-278, run q on worker q) as a
-// meet-in-the-middle cross product, in ONE cooperative kernel.
+// meet-in-the-middle cross product.
 //
 // Splits with m cuts are grouped into blocks by the position c of cut
 // j = ceil(m/2) (m = 0: one block).  Within a block a split is a pair
@@ -13,41 +13,53 @@
 // runs; the winner key (makespan, rank) is the reference's first strict
 // minimum in itertools order.
 //
-// Phases (grid-wide barriers between them):
-//  0. T once for the grid into a global image (one entry per thread);
-//  1. every CTA copies T into shared memory (+ row offsets, binomials);
-//  2. side tables, one level (number of cuts) per barrier.  Left sides: the
-//     k = j-1 left cuts as a colex-ordered subset of positions 1.. form
-//     table L_k, and the left side of block (m, c) is its first C(c-1, j-1)
+// Three launches:
+//  1. memo_image_kernel: T once into a global image (one entry per thread);
+//  2. side_tables_kernel: the side tables, every entry evaluated directly from
+//     its cut mask at full occupancy (T read through L1).  Left sides: the
+//     k = j-1 left cuts as a colex-ordered subset of positions 1.. form table
+//     L_k, and the left side of block (m, c) is its first C(c-1, j-1)
 //     entries; an entry holds PV = max over the runs ending at one of its
 //     cuts and its top cut, so L = max(PV, T[j-1][top][c]).  Right sides:
-//     table R(m, j) over the m-j right cuts in colex order of MIRRORED
-//     positions (W, W-1, ...), prefix C(W-c, m-j) for block c; an entry holds
-//     SV = max over the runs starting at one of its cuts and its lowest cut,
-//     so R = max(T[j][c][first], SV).  Each entry is one step of a dynamic
-//     program over its top bit: L_k[e] = max(L_{k-1}[e'], T[k-1][top'][c+1]),
-//     R(m, j')[e] = max(R(m, j'+1)[e'], T[j'+1][v][first']), with e' = e minus
-//     the colex weight of the removed bit;
-//  3. tiles of the cross products: TX elements of the larger side (registers,
-//     8 per thread, compacted to the feasible ones) x TY elements of the
-//     smaller side (shared memory, compacted).  Each candidate costs one fp64
-//     max and its checksum add.  The tile's minimum and first rank follow in
-//     closed form: the minimum over the tile is tm = max(min X, min Y), every
-//     pair with X_x <= tm and Y_y <= tm has makespan exactly tm, so the
-//     smallest rank at tm is min RX + min RY over those elements (ranks are
-//     derived from the elements' cut masks, only for tiles that can hold the
+//     table R(m) over the m-j right cuts in colex order of MIRRORED positions
+//     (W, W-1, ...), prefix C(W-c, m-j) for block c; an entry holds SV = max
+//     over the runs starting at one of its cuts and its lowest cut, so
+//     R = max(T[j][c][first], SV).  A side element then costs two loads and a
+//     max in the sweep;
+//  3. splits_sweep_kernel: tiles of the cross products, largest blocks first
+//     from a dynamic queue: TX elements of the larger side (registers, 8 per
+//     thread, compacted to the feasible ones) x TY elements of the smaller
+//     side (shared memory, compacted).  Each candidate costs one fp64 max and
+//     its checksum add.  The tile's minimum and first rank follow in closed
+//     form: the minimum over the tile is tm = max(min X, min Y), every pair
+//     with X_x <= tm and Y_y <= tm has makespan exactly tm, so the smallest
+//     rank at tm is min RX + min RY over those elements (ranks are derived
+//     from the elements' cut masks, only for tiles that can hold the
 //     incumbent).  Infeasible pairs (a run that does not fit: T = +inf) are
 //     counted and their +inf contributions removed from the checksum.
-#include <cooperative_groups.h>
-
 #include "dm_common.cuh"
 #include "dm_memo.cuh"
 #include "dm_mitm.cuh"
 #include "dm_abi_util.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace dm {
+
+#ifdef DM_MITM_TIMING
+// phase timestamps of every CTA (globaltimer ns): debug builds only
+__device__ unsigned long long g_mitm_times[1024][8];
+#define MITM_MARK(i)                                                                               \
+    do {                                                                                           \
+        if (threadIdx.x == 0) {                                                                    \
+            unsigned long long t_;                                                                 \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                 \
+            g_mitm_times[blockIdx.x][i] = t_;                                                      \
+        }                                                                                          \
+    } while (0)
+#define MITM_COUNT(i, v) atomicAdd(&g_mitm_times[blockIdx.x][i], (unsigned long long)(v))
+#else
+#define MITM_MARK(i) do { } while (0)
+#define MITM_COUNT(i, v) do { } while (0)
+#endif
 
 constexpr int kMitmThreads = 256;
 constexpr int kMitmNR = 8;                           // X elements per thread (register slots)
@@ -56,28 +68,32 @@ constexpr int kMitmTX = kMitmThreads * kMitmNR;      // 2048
 constexpr int kMitmTY = kMitmThreads * kMitmNY;      // 1024
 constexpr int kMitmCtasPerSm = 2;
 constexpr int kMitmMaxM = 64;
-constexpr int kTableChunk = 8;
+constexpr int kMitmMaxBlocks = 2048;                 // blocks of one sweep (size order in the launch parameters)
+constexpr int kTabPass = 16;                         // side-table entries per thread and pass
+constexpr int kThinY = 256;                          // blocks with a smaller side below this are "thin":
+constexpr int kThinPairs = 1 << 21;                  // their tiles span ~kThinPairs pairs in rounds of kMitmTX
+constexpr int kThinRounds = 8;                       // X elements, at most this many rounds per tile
 constexpr uint64_t kInfBits = 0x7ff0000000000000ULL;
 
 __host__ __device__ inline int mitm_j(int m) { return (m + 1) >> 1; }
 __host__ __device__ inline int mitm_blocks_of(int m, int W) { return m == 0 ? 1 : W - m + 1; }
-// table levels k = 0 .. floor((rmax-1)/2); left tables exist for k <= j(rmax-1) - 1
-__host__ __device__ inline int tab_levels(int rmax) { return rmax >= 2 ? (rmax - 1) / 2 + 1 : 0; }
-__host__ __device__ inline int tab_kl(int rmax) { return rmax >= 2 ? mitm_j(rmax - 1) - 1 : -1; }
 
-// Relative double index of T[q][a][0] in the memo layout (dm_memo.cuh).
+// Relative double index of T[q][a][0] in the memo layout (dm_memo.cuh):
+// rows of q start after sum_{qq<q} (n-qq)(n-qq+1)/2 = S3(n) - S3(n-q),
+// S3(N) = N(N+1)(N+2)/6.
 __host__ __device__ inline int memo_row(int q, int a, int n) {
-    int base = 0;
-    for (int qq = 0; qq < q; ++qq) { const int Lq = n - qq; base += Lq * (Lq + 1) / 2; }
+    const int N = n - q;
+    const int base = (n * (n + 1) * (n + 2) - N * (N + 1) * (N + 2)) / 6;
     return base + (a - q) * n - ((a - q) * (a + q - 1)) / 2 - (a + 1);
 }
 
-// Shared memory: the memo tables, the block plan (mbase[m], per-block m and
-// c, tile prefix tstart), the compacted X and Y values, reduction space.
+// Shared memory of the sweep: the memo tables, the block plan (mbase[m], per
+// block m and c, size-order position -> block, tile prefix tstart), the
+// compacted X and Y values, reduction space.
 struct MitmLayout {
     MemoLayout M;
     int n_blocks;
-    size_t off_mbase, off_bm, off_bc, off_tstart, off_bx, off_by, off_red, bytes;
+    size_t off_mbase, off_bm, off_bc, off_pos, off_tstart, off_bx, off_by, off_red, bytes;
 };
 
 __host__ __device__ inline MitmLayout mitm_layout(int n, int p) {
@@ -92,6 +108,8 @@ __host__ __device__ inline MitmLayout mitm_layout(int n, int p) {
     L.off_tstart = off; off += (size_t)(nb + 1) * 4;
     L.off_bm = off; off += (size_t)nb;
     L.off_bc = off; off += (size_t)nb;
+    off = (off + 1) & ~(size_t)1;
+    L.off_pos = off; off += (size_t)nb * 2;
     off = (off + 15) & ~(size_t)15;
     L.off_bx = off; off += (size_t)kMitmTX * 8;
     L.off_by = off; off += (size_t)kMitmTY * 8;
@@ -100,36 +118,28 @@ __host__ __device__ inline MitmLayout mitm_layout(int n, int p) {
     return L;
 }
 
-// Global workspace: T image, then the side-table values and boundary bytes.
-struct MitmWorkspace {
-    size_t off_val, off_bnd, bytes;
-    int64_t entries;
+// Side tables of one sweep (host-computed, passed by value): L_k for
+// k = 0..KL, then R(m) for m = 1..rmax-1; tables the tiles read by m.
+struct SideTables {
+    int n_tab;
+    int8_t kind[2 * kMitmMaxM];       // 0: L_k, 1: R(m)
+    int8_t km[2 * kMitmMaxM];         // k for L_k, m for R(m)
+    int64_t start[2 * kMitmMaxM + 1]; // entry prefix
+    int64_t offL[kMitmMaxM], offR[kMitmMaxM];
 };
 
-__host__ inline bool mitm_workspace(int n, int p, MitmWorkspace& ws) {
-    const int W = n - 1, rmax = n < p ? n : p;
-    if (rmax > kMitmMaxM) return false;
-    auto C = [](int a, int b) -> unsigned __int128 {
-        if (b < 0 || b > a) return 0;
-        unsigned __int128 r = 1;
-        for (int i = 1; i <= b; ++i) r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
-        return r;
-    };
-    unsigned __int128 e = 0;
-    const int NL = tab_levels(rmax), KL = tab_kl(rmax);
-    for (int k = 0; k < NL; ++k) {
-        if (k <= KL) e += C(W - k - 1, k);
-        for (int m = 1; m < rmax; ++m)
-            if (k <= m - mitm_j(m)) e += C(W - m + k, k);
-    }
-    if (e > ((unsigned __int128)1 << 36)) return false;
-    ws.entries = (int64_t)e;
-    const size_t timg = (size_t)memo_layout(n, p).t_elems * 8;
-    ws.off_val = (timg + 255) & ~(size_t)255;
-    ws.off_bnd = ws.off_val + (((size_t)ws.entries * 8 + 255) & ~(size_t)255);
-    ws.bytes = ws.off_bnd + (((size_t)ws.entries + 255) & ~(size_t)255);
-    return true;
-}
+// Launch parameters of the sweep: table offsets by m and the block order by
+// decreasing number of candidates.
+struct SweepParams {
+    int64_t offL[kMitmMaxM], offR[kMitmMaxM];
+    int16_t order[kMitmMaxBlocks];
+};
+
+// Global workspace: tile counter, T image, side-table values, boundary bytes.
+struct MitmWorkspace {
+    size_t off_timg, off_val, off_bnd, bytes;
+    int64_t entries;
+};
 
 // One side of a block for rank derivation: k cuts among positions lo..hi
 // (bit b <-> position lo + b), rank terms i0.. between the boundaries start,
@@ -171,6 +181,13 @@ __device__ __forceinline__ uint64_t colex_unrank(const MitmCtx& x, int k, int P,
     return mask;
 }
 
+// colex successor (Gosper): the next mask with the same popcount.
+__device__ __forceinline__ uint64_t side_next(uint64_t mk) {
+    const uint64_t low = mk & (0ull - mk);
+    const uint64_t r = mk + low;
+    return r | (((mk ^ r) >> 2) >> (__ffsll((long long)mk) - 1));
+}
+
 // the side's share of the global rank: sum of term_i over its cuts
 __device__ __forceinline__ int64_t side_rank(const MitmCtx& x, int m, const Side& d, uint64_t mk) {
     int64_t r = d.base;
@@ -203,105 +220,12 @@ __device__ __forceinline__ void append_if(bool keep, double v, double* buf, int*
 }
 
 
-
-// largest b in [k-1, maxb] with C(b, k) <= e (k >= 1)
-__device__ __forceinline__ int top_bit(const MitmCtx& x, int k, int maxb, int64_t e) {
-    int lo = k - 1, hi = maxb;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (x.binom[mid * x.R1 + k] <= e) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-// ---- phase 0: T entry i of the flat (q, a, b) range into the global image
-__device__ __forceinline__ void memo_image_entry(const dm_tables& t, int rmax, int64_t i, double* timg) {
-    const int n = t.n;
-    const int q = (int)(i / ((int64_t)n * n)), a = (int)((i / n) % n), b = (int)(i % n) + 1;
-    if (q >= rmax || a < q || b <= a) return;
-    double v = __longlong_as_double(0x7ff0000000000000LL);
-    if ((q > 0 || a == 0) && fits_range(t, q, a, b)) {
-        double c, rd;
-        if (chain(t)) run_cost_contig(t, a, b, q, [&](int) { return q - 1; }, c, rd);
-        else run_cost_contig(t, a, b, q, [&](int s) { return s < a ? -1 : q + 1; }, c, rd);
-        v = c + rd;
-    }
-    timg[memo_row(q, a, n) + b] = v;
-}
-
-// ---- phase 1: shared copy of T, row offsets, the -inf row, binomials
-//      (Pascal's triangle in warp 0: exact for n <= 64) and cum.
-__device__ inline void memo_load(const MemoLayout& L, const double* __restrict__ timg, unsigned char* sm) {
-    const int n = L.n, rmax = L.rmax, S = L.S, R1 = rmax + 1;
-    double* T = reinterpret_cast<double*>(sm);
-    for (int i = threadIdx.x; i < L.t_elems; i += blockDim.x) T[i] = timg[i];
-    int32_t* rowoff = reinterpret_cast<int32_t*>(sm + L.off_rowoff);
-    const uint32_t sm_base = (uint32_t)__cvta_generic_to_shared(sm);
-    for (int i = threadIdx.x; i < (rmax + 4) * S; i += blockDim.x) {
-        const int q = i / S, a = i % S;
-        const int32_t v = (q < rmax && a >= q && a < n) ? memo_row(q, a, n) * 8 : (int32_t)L.off_dummy;
-        rowoff[i] = (int32_t)(sm_base + (uint32_t)v);
-    }
-    for (int i = threadIdx.x; i <= n; i += blockDim.x)
-        reinterpret_cast<double*>(sm + L.off_dummy)[i] = -__longlong_as_double(0x7ff0000000000000LL);
-    if (threadIdx.x < 32) {
-        int64_t* binom = reinterpret_cast<int64_t*>(sm + L.off_binom);
-        const int lane = threadIdx.x;
-        int64_t v0 = lane == 0, v1 = 0, v2 = 0;      // row 0 at b = lane, lane + 32, lane + 64
-        for (int a = 0; a < n; ++a) {
-            if (a > 0) {
-                const int64_t u0 = __shfl_up_sync(0xffffffffu, v0, 1), u1 = __shfl_up_sync(0xffffffffu, v1, 1),
-                              u2 = __shfl_up_sync(0xffffffffu, v2, 1);
-                const int64_t t0 = __shfl_sync(0xffffffffu, v0, 31), t1 = __shfl_sync(0xffffffffu, v1, 31);
-                v2 += lane ? u2 : t1;
-                v1 += lane ? u1 : t0;
-                v0 += lane ? u0 : 0;
-            }
-            if (lane < R1) binom[a * R1 + lane] = v0;
-            if (lane + 32 < R1) binom[a * R1 + lane + 32] = v1;
-            if (lane + 64 < R1) binom[a * R1 + lane + 64] = v2;
-        }
-        __syncwarp();
-        if (lane == 0) {
-            int64_t* cum = reinterpret_cast<int64_t*>(sm + L.off_cum);
-            cum[0] = 0;
-            for (int m = 1; m <= rmax; ++m) cum[m] = cum[m - 1] + binom[(n - 1) * R1 + (m - 1)];
-        }
-    }
-    __syncthreads();
-}
-
-// ---- phase 2 helpers: the tables of level k in order (L_k first when it
-//      exists, then R(m, m-k) by m): sizes and chunk prefix (thread 0).
-struct LevelPlan {
-    int n_tab;
-    int8_t tm[kMitmMaxM + 1];        // -1: L_k, else m
-    int64_t ent[kMitmMaxM + 2];      // entry prefix
-    int64_t chk[kMitmMaxM + 2];      // chunk prefix
-};
-
-__device__ inline void level_plan(const MitmCtx& x, int rmax, int k, LevelPlan& P) {
-    const int W = x.W, KL = tab_kl(rmax);
-    int nt = 0;
-    P.ent[0] = P.chk[0] = 0;
-    auto add = [&](int m, int64_t sz) {
-        P.tm[nt] = (int8_t)m;
-        P.ent[nt + 1] = P.ent[nt] + sz;
-        P.chk[nt + 1] = P.chk[nt] + (sz + kTableChunk - 1) / kTableChunk;
-        ++nt;
-    };
-    if (k <= KL) add(-1, x.binom[(W - k - 1) * x.R1 + k]);
-    for (int m = 1; m < rmax; ++m)
-        if (k <= m - mitm_j(m)) add(m, x.binom[(W - m + k) * x.R1 + k]);
-    P.n_tab = nt;
-}
-
 // ------------------------------------------------------------- the sweep
 // A block's two sides: m, c, j and table offsets; element values from the
 // side tables (m = 0: the single split [0, n) as an empty left side and a
 // right side without cuts).
 struct Blk {
-    int m, j, c;
+    int m, j, c, R;    // R: rounds of kMitmTX X elements per tile (thin blocks)
     int64_t nl, nr, offl, offr;
     uint32_t rbase;    // shared address of T[j][c][0] (right sides)
 };
@@ -410,19 +334,246 @@ __device__ __forceinline__ void mitm_cross(const double (&xv)[kMitmNR], const do
     }
 }
 
+
+}  // namespace dm
+
+#include <algorithm>
+#include <utility>
+#include <vector>
+
+namespace dm {
+
+namespace {
+unsigned __int128 binom128(int a, int b) {
+    if (b < 0 || b > a) return 0;
+    unsigned __int128 r = 1;
+    for (int i = 1; i <= b; ++i) r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
+    return r;
+}
+}  // namespace
+
+// The sweep's side-table plan and workspace layout; false when it does not
+// apply (more than kMitmMaxBlocks blocks, 2^36 table entries or 2^30 tiles).
+inline bool mitm_plan(int n, int p, SideTables& st, MitmWorkspace& ws, SweepParams* sp) {
+    const int W = n - 1, rmax = n < p ? n : p;
+    if (n < 1 || n > 64 || p < 1 || rmax > kMitmMaxM) return false;
+    const MitmLayout L = mitm_layout(n, p);
+    if (L.n_blocks > kMitmMaxBlocks || L.bytes > 108 * 1024) return false;
+    const int KL = rmax >= 2 ? mitm_j(rmax - 1) - 1 : -1;
+    unsigned __int128 e = 0;
+    st.n_tab = 0;
+    for (int m = 0; m < kMitmMaxM; ++m) st.offL[m] = st.offR[m] = 0;
+    for (int k = 0; k <= KL; ++k) {
+        st.kind[st.n_tab] = 0; st.km[st.n_tab] = (int8_t)k; st.start[st.n_tab++] = (int64_t)e;
+        for (int m = 1; m < rmax; ++m) if (mitm_j(m) - 1 == k) st.offL[m] = (int64_t)e;
+        e += binom128(W - k - 1, k);
+        if (e > ((unsigned __int128)1 << 36)) return false;
+    }
+    for (int m = 1; m < rmax; ++m) {
+        st.kind[st.n_tab] = 1; st.km[st.n_tab] = (int8_t)m; st.start[st.n_tab++] = (int64_t)e;
+        st.offR[m] = (int64_t)e;
+        e += binom128(W - mitm_j(m), m - mitm_j(m));
+        if (e > ((unsigned __int128)1 << 36)) return false;
+    }
+    st.start[st.n_tab] = (int64_t)e;
+    ws.entries = (int64_t)e;
+    ws.off_timg = 256;
+    ws.off_val = ws.off_timg + ((((size_t)L.M.t_elems * 8) + 255) & ~(size_t)255);
+    ws.off_bnd = ws.off_val + (((size_t)ws.entries * 8 + 255) & ~(size_t)255);
+    ws.bytes = ws.off_bnd + (((size_t)ws.entries + 255) & ~(size_t)255);
+    // blocks by decreasing number of candidates; total tiles bounded
+    const int nb = L.n_blocks;
+    std::vector<std::pair<unsigned __int128, int>> key(nb);
+    unsigned __int128 tiles = 0;
+    for (int m = 0, b = 0; m < rmax; ++m)
+        for (int i = 0; i < mitm_blocks_of(m, W); ++i, ++b) {
+            const int j = mitm_j(m), c = m == 0 ? 0 : j + i;
+            const unsigned __int128 nl = m == 0 ? 1 : binom128(c - 1, j - 1), nr = m == 0 ? 1 : binom128(W - c, m - j);
+            const unsigned __int128 nX = nl >= nr ? nl : nr, nY = nl >= nr ? nr : nl;
+            // tiles of the block (thin blocks: rounds of kMitmTX X elements),
+            // ordered by the estimated duration of one tile: its pairs plus
+            // ~256 pair-equivalents per element it builds
+            unsigned __int128 R = 1;
+            if (nY < (unsigned __int128)kThinY) {
+                R = (unsigned __int128)kThinPairs / ((unsigned __int128)kMitmTX * nY);
+                R = R < 1 ? 1 : (R > (unsigned __int128)kThinRounds ? kThinRounds : R);
+            }
+            const unsigned __int128 txs = (unsigned __int128)kMitmTX * R;
+            const unsigned __int128 tx = nX < txs ? nX : txs, ty = nY < kMitmTY ? nY : kMitmTY;
+            tiles += ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
+            key[b] = {tx * ty + 256 * (tx + ty), b};
+        }
+    if (tiles > ((unsigned __int128)1 << 30)) return false;
+    if (sp) {
+        std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+        for (int i = 0; i < nb; ++i) sp->order[i] = (int16_t)key[i].second;
+        for (int m = 0; m < kMitmMaxM; ++m) { sp->offL[m] = st.offL[m]; sp->offR[m] = st.offR[m]; }
+    }
+    return true;
+}
+
+
+// ------------------------------------------------------------ 1. T image
+__global__ void __launch_bounds__(256) memo_image_kernel(const dm_tables tp, double* __restrict__ timg) {
+    const dm_tables t = tp;
+    const int n = t.n, rmax = n < t.p ? n : t.p;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)rmax * n * n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(i / ((int64_t)n * n)), a = (int)((i / n) % n), b = (int)(i % n) + 1;
+        if (a < q || b <= a) continue;
+        double v = __longlong_as_double(0x7ff0000000000000LL);
+        if ((q > 0 || a == 0) && fits_range(t, q, a, b)) {
+            double c, rd;
+            if (chain(t)) run_cost_contig(t, a, b, q, [&](int) { return q - 1; }, c, rd);
+            else run_cost_contig(t, a, b, q, [&](int s) { return s < a ? -1 : q + 1; }, c, rd);
+            v = c + rd;
+        }
+        timg[memo_row(q, a, n) + b] = v;
+    }
+}
+
+// -------------------------------------------------------- 2. side tables
+// One thread per kTabPass consecutive entries of the concatenated tables:
+// colex unrank of the first, Gosper successor for the rest, then the runs
+// the entry covers (T from the global image through L1).  Binomials in
+// shared memory (Pascal's triangle).  CTA 0 also resets the tile counter.
+__global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, const double* __restrict__ timg,
+                                                          const __grid_constant__ SideTables st,
+                                                          double* __restrict__ val, uint8_t* __restrict__ bnd,
+                                                          int* __restrict__ counter) {
+    extern __shared__ __align__(16) int64_t binom_s[];
+    const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, R1 = rmax + 1;
+    int32_t* rowrel = reinterpret_cast<int32_t*>(binom_s + n * R1);       // memo_row(q, a) for a < n
+    for (int i = threadIdx.x; i < rmax * n; i += blockDim.x) {
+        const int q = i / n, a = i % n;
+        rowrel[i] = a >= q ? memo_row(q, a, n) : 0;
+    }
+    if (threadIdx.x < 32) {                      // Pascal's triangle, exact for n <= 64
+        const int lane = threadIdx.x;
+        int64_t v0 = lane == 0, v1 = 0, v2 = 0;
+        for (int a = 0; a < n; ++a) {
+            if (a > 0) {
+                const int64_t u0 = __shfl_up_sync(0xffffffffu, v0, 1), u1 = __shfl_up_sync(0xffffffffu, v1, 1),
+                              u2 = __shfl_up_sync(0xffffffffu, v2, 1);
+                const int64_t t0 = __shfl_sync(0xffffffffu, v0, 31), t1 = __shfl_sync(0xffffffffu, v1, 31);
+                v2 += lane ? u2 : t1;
+                v1 += lane ? u1 : t0;
+                v0 += lane ? u0 : 0;
+            }
+            if (lane < R1) binom_s[a * R1 + lane] = v0;
+            if (lane + 32 < R1) binom_s[a * R1 + lane + 32] = v1;
+            if (lane + 64 < R1) binom_s[a * R1 + lane + 64] = v2;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0;
+    __syncthreads();
+    const MitmCtx x{n, W, 0, R1, binom_s, nullptr};
+    auto T = [&](int q, int a, int b) { return __ldg(timg + rowrel[q * n + a] + b); };
+    const double ninf = -__longlong_as_double(0x7ff0000000000000LL);
+    const int64_t E = st.start[st.n_tab];
+    for (int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTabPass; e0 < E;
+         e0 += (int64_t)gridDim.x * blockDim.x * kTabPass) {
+        int ti;
+        {
+            int lo = 0, hi = st.n_tab - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (st.start[mid] <= e0) lo = mid; else hi = mid - 1;
+            }
+            ti = lo;
+        }
+        uint64_t mk = 0;
+        for (int u = 0; u < kTabPass; ++u) {
+            const int64_t e = e0 + u;
+            if (e >= E) break;
+            bool fresh = u == 0;
+            while (st.start[ti + 1] <= e) { ++ti; fresh = true; }
+            const bool right = st.kind[ti];
+            const int km = st.km[ti];
+            const int k = right ? km - mitm_j(km) : km;               // cuts per entry
+            const int P = right ? W - mitm_j(km) : W - km - 1;        // positions
+            if (fresh) mk = colex_unrank(x, k, P, e - st.start[ti]);
+            else mk = side_next(mk);
+            double v = ninf;
+            int prev;
+            if (!right) {                // L_k: runs q = 0..k-1 ending at the cuts (position 1 + b)
+                prev = 0;
+                int q = 0;
+                for (uint64_t r = mk; r; r &= r - 1, ++q) {
+                    const int c = __ffsll((long long)r);
+                    const double tv = T(q, prev, c);
+                    v = tv > v ? tv : v;
+                    prev = c;
+                }
+            } else {                     // R(m): runs q = m, m-1, .. starting at the cuts (position W - b)
+                prev = n;
+                int q = km;
+                for (uint64_t r = mk; r; r &= r - 1, --q) {
+                    const int c = W - (__ffsll((long long)r) - 1);
+                    const double tv = T(q, c, prev);
+                    v = tv > v ? tv : v;
+                    prev = c;
+                }
+            }
+            val[e] = v;
+            bnd[e] = (uint8_t)prev;
+        }
+    }
+}
+
+// ------------------------------------------------------------- 3. sweep
+// shared copy of T from the image, row offsets, the -inf row, binomials
+// (Pascal's triangle in warp 0) and cum.
+__device__ inline void memo_load(const MemoLayout& L, const double* __restrict__ timg, unsigned char* sm) {
+    const int n = L.n, rmax = L.rmax, S = L.S, R1 = rmax + 1;
+    double* Tm = reinterpret_cast<double*>(sm);
+    for (int i = threadIdx.x; i < L.t_elems; i += blockDim.x) Tm[i] = timg[i];
+    int32_t* rowoff = reinterpret_cast<int32_t*>(sm + L.off_rowoff);
+    const uint32_t sm_base = (uint32_t)__cvta_generic_to_shared(sm);
+    for (int i = threadIdx.x; i < (rmax + 4) * S; i += blockDim.x) {
+        const int q = i / S, a = i % S;
+        const int32_t v = (q < rmax && a >= q && a < n) ? memo_row(q, a, n) * 8 : (int32_t)L.off_dummy;
+        rowoff[i] = (int32_t)(sm_base + (uint32_t)v);
+    }
+    for (int i = threadIdx.x; i <= n; i += blockDim.x)
+        reinterpret_cast<double*>(sm + L.off_dummy)[i] = -__longlong_as_double(0x7ff0000000000000LL);
+    if (threadIdx.x < 32) {
+        int64_t* binom = reinterpret_cast<int64_t*>(sm + L.off_binom);
+        const int lane = threadIdx.x;
+        int64_t v0 = lane == 0, v1 = 0, v2 = 0;
+        for (int a = 0; a < n; ++a) {
+            if (a > 0) {
+                const int64_t u0 = __shfl_up_sync(0xffffffffu, v0, 1), u1 = __shfl_up_sync(0xffffffffu, v1, 1),
+                              u2 = __shfl_up_sync(0xffffffffu, v2, 1);
+                const int64_t t0 = __shfl_sync(0xffffffffu, v0, 31), t1 = __shfl_sync(0xffffffffu, v1, 31);
+                v2 += lane ? u2 : t1;
+                v1 += lane ? u1 : t0;
+                v0 += lane ? u0 : 0;
+            }
+            if (lane < R1) binom[a * R1 + lane] = v0;
+            if (lane + 32 < R1) binom[a * R1 + lane + 32] = v1;
+            if (lane + 64 < R1) binom[a * R1 + lane + 64] = v2;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            int64_t* cum = reinterpret_cast<int64_t*>(sm + L.off_cum);
+            cum[0] = 0;
+            for (int m = 1; m <= rmax; ++m) cum[m] = cum[m - 1] + binom[(n - 1) * R1 + (m - 1)];
+        }
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_kernel(
-        const dm_tables tp, double* __restrict__ timg, double* __restrict__ val, uint8_t* __restrict__ bnd, int part,
+        const dm_tables tp, const __grid_constant__ SweepParams P, int* __restrict__ ctl,
+        const double* __restrict__ timg, const double* __restrict__ val, const uint8_t* __restrict__ bnd, int part,
         int nparts, dm_winner* partial) {
     const dm_tables t = tp;   // register copy (no param-space references)
-    cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int s_cnt[2][2];       // [tile parity][X, Y] feasible counts
     __shared__ int s_flag[2];         // [tile parity] bit 0: an X <= best, bit 1: a Y <= best
+    __shared__ int s_g[2];            // [tile parity] tile index
     __shared__ double s_best;
-    __shared__ LevelPlan s_lp;
-    __shared__ int64_t s_lvl;                      // first entry of the current level
-    __shared__ int64_t s_roff[2][kMitmMaxM];       // R(m, m-k) entry offsets, [level parity][m]
-    __shared__ int64_t s_offL[kMitmMaxM], s_offR[kMitmMaxM];
     const int n = t.n;
     const MitmLayout L = mitm_layout(n, t.p);
     const int rmax = L.M.rmax, nb = L.n_blocks;
@@ -433,99 +584,18 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     int32_t* tstart = reinterpret_cast<int32_t*>(sm + L.off_tstart);
     uint8_t* bm = sm + L.off_bm;
     uint8_t* bc = sm + L.off_bc;
+    int16_t* pos_blk = reinterpret_cast<int16_t*>(sm + L.off_pos);
     double* bx = reinterpret_cast<double*>(sm + L.off_bx);
     double* by = reinterpret_cast<double*>(sm + L.off_by);
     double* red = reinterpret_cast<double*>(sm + L.off_red);
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
 
-    // ---- phase 0: T image
-    for (int64_t i = gtid; i < (int64_t)rmax * n * n; i += gthreads) memo_image_entry(t, rmax, i, timg);
-    grid.sync();
-    // ---- phase 1: shared T, binomials
+    MITM_MARK(0);
+#ifdef DM_MITM_TIMING
+    if (threadIdx.x == 0) { g_mitm_times[blockIdx.x][4] = 0; g_mitm_times[blockIdx.x][5] = 0; }
+#endif
     memo_load(L.M, timg, sm);
-
-    // ---- phase 2: side tables, level by level
-    const int NL = tab_levels(rmax), KL = tab_kl(rmax);
-    int64_t lvl_base = 0, prev_base = 0;   // first entries of levels k and k-1
-    for (int k = 0; k < NL; ++k) {
-        if (threadIdx.x == 0) {
-            level_plan(x, rmax, k, s_lp);
-            s_lvl = lvl_base;
-            for (int i = 0; i < s_lp.n_tab; ++i) {
-                const int m = s_lp.tm[i];
-                const int64_t off = lvl_base + s_lp.ent[i];
-                if (m < 0) {
-                    for (int mm = 1; mm < rmax; ++mm) if (mitm_j(mm) - 1 == k) s_offL[mm] = off;
-                } else {
-                    s_roff[k & 1][m] = off;
-                    if (k == m - mitm_j(m)) s_offR[m] = off;
-                }
-            }
-        }
-        __syncthreads();
-        const int64_t nchunks = s_lp.chk[s_lp.n_tab];
-        for (int64_t ch = gtid; ch < nchunks; ch += gthreads) {
-            int lo = 0, hi = s_lp.n_tab - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_lp.chk[mid] <= ch) lo = mid; else hi = mid - 1;
-            }
-            const int m = s_lp.tm[lo];
-            const int64_t e0 = (ch - s_lp.chk[lo]) * kTableChunk;
-            const int64_t size = s_lp.ent[lo + 1] - s_lp.ent[lo];
-            const int cnt = (int)(size - e0 < kTableChunk ? size - e0 : kTableChunk);
-            const int64_t dst = s_lvl + s_lp.ent[lo];
-            if (k == 0) {                                   // no cuts: L_0 = (-inf, 0), R(m, m) = (-inf, n)
-                val[dst] = -inf;
-                bnd[dst] = (uint8_t)(m < 0 ? 0 : n);
-                continue;
-            }
-            const int jp = m < 0 ? 0 : m - k;              // R(m, jp)
-            const int maxb = m < 0 ? x.W - k - 2 : x.W - jp - 1;
-            // the chunk's entries: top bits and source indices, then all
-            // source loads in flight, then the T lookups and stores
-            const int64_t sbase = m < 0 ? prev_base : s_roff[(k - 1) & 1][m];
-            int bs[kTableChunk];
-            int64_t src[kTableChunk];
-            int b = top_bit(x, k, maxb, e0);
-#pragma unroll
-            for (int u = 0; u < kTableChunk; ++u) {
-                const int64_t e = e0 + u;
-                if (u < cnt) while (b < maxb && x.binom[(b + 1) * x.R1 + k] <= e) ++b;
-                bs[u] = b;
-                src[u] = sbase + (e - x.binom[b * x.R1 + k]);
-            }
-            double sv[kTableChunk];
-            int sb[kTableChunk];
-#pragma unroll
-            for (int u = 0; u < kTableChunk; ++u) {
-                if (u < cnt) { sv[u] = val[src[u]]; sb[u] = bnd[src[u]]; }
-            }
-#pragma unroll
-            for (int u = 0; u < kTableChunk; ++u) {
-                if (u >= cnt) break;
-                double tv;
-                int nb8;
-                if (m < 0) {                    // L_k: the top cut (position b + 1) extends L_{k-1}
-                    nb8 = bs[u] + 1;
-                    tv = tval(x, k - 1, sb[u], nb8);
-                } else {                        // R(m, jp): the first cut (position W - b) extends R(m, jp+1)
-                    nb8 = x.W - bs[u];
-                    tv = tval(x, jp + 1, nb8, sb[u]);
-                }
-                val[dst + e0 + u] = tv > sv[u] ? tv : sv[u];
-                bnd[dst + e0 + u] = (uint8_t)nb8;
-            }
-        }
-        prev_base = lvl_base;
-        lvl_base += s_lp.ent[s_lp.n_tab];
-        __syncthreads();        // s_lp reuse
-        grid.sync();
-    }
-
-    // ---- phase 3: tiles
+    MITM_MARK(1);
     if (threadIdx.x == 0) {
         int b = 0;
         for (int m = 0; m < rmax; ++m) { mbase[m] = b; b += mitm_blocks_of(m, x.W); }
@@ -542,21 +612,30 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         else {
             B.nl = x.binom[(c - 1) * x.R1 + (B.j - 1)];
             B.nr = x.binom[(x.W - c) * x.R1 + (m - B.j)];
-            B.offl = s_offL[m]; B.offr = s_offR[m];
+            B.offl = P.offL[m]; B.offr = P.offR[m];
         }
         B.rbase = (uint32_t)x.rowoff[B.j * x.S + c];
+        const int64_t nY = B.nl >= B.nr ? B.nr : B.nl;
+        int64_t R = nY >= kThinY ? 1 : kThinPairs / (kMitmTX * nY);
+        B.R = (int)(R < 1 ? 1 : (R > kThinRounds ? kThinRounds : R));
         return B;
     };
-    // ---- plan: (m, c) and tiles per block, inclusive prefix in tstart[1..nb]
+    // ---- plan: (m, c) per block; tiles per position of the size order,
+    //      inclusive prefix in tstart[1..nb] (positions)
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
         int m = 0;
         while (m + 1 < rmax && mbase[m + 1] <= b) ++m;
-        const int c = m == 0 ? 0 : mitm_j(m) + (b - mbase[m]);
         bm[b] = (uint8_t)m;
-        bc[b] = (uint8_t)c;
-        const Blk B = block_of(b, m, c);
+        bc[b] = (uint8_t)(m == 0 ? 0 : mitm_j(m) + (b - mbase[m]));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const int b = P.order[i];
+        pos_blk[i] = (int16_t)b;
+        const Blk B = block_of(b, bm[b], bc[b]);
         const int64_t nX = B.nl >= B.nr ? B.nl : B.nr, nY = B.nl >= B.nr ? B.nr : B.nl;
-        tstart[b + 1] = (int32_t)(((nX + kMitmTX - 1) / kMitmTX) * ((nY + kMitmTY - 1) / kMitmTY));
+        const int64_t txs = (int64_t)kMitmTX * B.R;
+        tstart[i + 1] = (int32_t)(((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -573,8 +652,10 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         for (int b = b0; b < b1; ++b) { run += tstart[b + 1]; tstart[b + 1] = run; }
         if (lane == 0) tstart[0] = 0;
     }
+    if (threadIdx.x == 0) s_g[0] = part + nparts * atomicAdd(ctl, 1);   // dynamic tile queue
     __syncthreads();
     const int n_tiles = tstart[nb];
+    MITM_MARK(2);
 
     Win w;
     win_init(w);
@@ -583,115 +664,200 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     for (int u = 0; u < kMitmNR; ++u) cs[u] = 0;
     uint64_t corr = 0;   // +inf contributions to remove (counted in units of kInfBits)
 
-    int par = 0;
-    for (int g = part + nparts * blockIdx.x; g < n_tiles; g += nparts * gridDim.x, par ^= 1) {
+    for (int par = 0;; par ^= 1) {
+        const int g = s_g[par];
+        if (g >= n_tiles) break;           // uniform
+        if (threadIdx.x == 0) s_g[par ^ 1] = part + nparts * atomicAdd(ctl, 1);   // read after the end barrier
         int lo = 0, hi = nb - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (tstart[mid] <= g) lo = mid; else hi = mid - 1;
         }
-        const Blk B = block_of(lo, bm[lo], bc[lo]);
+        const int blk = pos_blk[lo];
+        const Blk B = block_of(blk, bm[blk], bc[blk]);
         const bool xl = B.nl >= B.nr;
         const int64_t nX = xl ? B.nl : B.nr, nY = xl ? B.nr : B.nl;
         const int64_t nty = (nY + kMitmTY - 1) / kMitmTY;
         const int64_t local = g - tstart[lo];
-        const int64_t x0 = (local / nty) * kMitmTX, y0 = (local % nty) * kMitmTY;
-        const int nXr = (int)(nX - x0 < kMitmTX ? nX - x0 : kMitmTX);
+        const int64_t txs = (int64_t)kMitmTX * B.R;
+        const int64_t x0 = (local / nty) * txs, y0 = (local % nty) * kMitmTY;
+        const int nXr = (int)(nX - x0 < txs ? nX - x0 : txs);
         const int nYr = (int)(nY - y0 < kMitmTY ? nY - y0 : kMitmTY);
-
-        // ---- both sides' feasible elements, compacted into shared memory
         const double best = s_best;
-        // element raw data (table value, boundary cut) for every slot first,
-        // so all global loads are in flight together
         const int64_t xoff = xl ? B.offl : B.offr, yoff = xl ? B.offr : B.offl;
-        double xr[kMitmNR], yr[kMitmNY];
-        int xb[kMitmNR], yb[kMitmNY];
-#pragma unroll
-        for (int u = 0; u < kMitmNR; ++u) {
-            const int e = u * kMitmThreads + threadIdx.x;
-            if (e < nXr && B.m) { xr[u] = val[xoff + x0 + e]; xb[u] = bnd[xoff + x0 + e]; }
-        }
-#pragma unroll
-        for (int u = 0; u < kMitmNY; ++u) {
-            const int e = u * kMitmThreads + threadIdx.x;
-            if (e < nYr && B.m) { yr[u] = val[yoff + y0 + e]; yb[u] = bnd[yoff + y0 + e]; }
-        }
+        bool maybe_best = false;
         double xmin = inf, ymin = inf;
+        int nyf = 0;
+        if (B.R > 1) {
+            // ---- thin tile: the few feasible Y once in shared memory, then
+            //      rounds of kMitmTX X elements straight into registers
+            //      (infeasible X slots stay +inf and are counted)
 #pragma unroll
-        for (int u = 0; u < kMitmNR; ++u) {
-            const int e = u * kMitmThreads + threadIdx.x;
-            double v = inf;
-            if (e < nXr) { v = side_finish(x, B, xl, xr[u], xb[u]); xmin = v < xmin ? v : xmin; }
-            append_if(v != inf, v, bx, &s_cnt[par][0]);
-        }
+            for (int u = 0; u < kMitmNY; ++u) {
+                const int e = u * kMitmThreads + threadIdx.x;
+                double v = inf;
+                if (e < nYr) {
+                    v = side_finish(x, B, !xl, B.m ? val[yoff + y0 + e] : 0.0, B.m ? bnd[yoff + y0 + e] : 0);
+                    ymin = v < ymin ? v : ymin;
+                }
+                append_if(v != inf, v, by, &s_cnt[par][1]);
+            }
+            if (ymin <= best) atomicOr(&s_flag[par], 2);
+            __syncthreads();
+            nyf = s_cnt[par][1];
+            const bool yb_ok = s_flag[par] & 2;
+            if (threadIdx.x == 0) {
+                s_cnt[par ^ 1][0] = s_cnt[par ^ 1][1] = 0;
+                s_flag[par ^ 1] = 0;
+                w.n_eval += (int64_t)nXr * nYr;
+            }
+            int64_t nxf_all = 0;
+            if (nyf > 0) {
+                // warp-private compaction of each round's feasible X
+                double* wbuf = bx + (threadIdx.x >> 5) * (kMitmNR * 32);
+                const int lane = threadIdx.x & 31;
+                for (int r0 = 0; r0 < nXr; r0 += kMitmTX) {
+                    double xr[kMitmNR];
+                    int xb[kMitmNR];
 #pragma unroll
-        for (int u = 0; u < kMitmNY; ++u) {
-            const int e = u * kMitmThreads + threadIdx.x;
-            double v = inf;
-            if (e < nYr) { v = side_finish(x, B, !xl, yr[u], yb[u]); ymin = v < ymin ? v : ymin; }
-            append_if(v != inf, v, by, &s_cnt[par][1]);
-        }
-        const int fl = (xmin <= best ? 1 : 0) | (ymin <= best ? 2 : 0);
-        if (fl) atomicOr(&s_flag[par], fl);
-        __syncthreads();
-        const int nxf_tot = s_cnt[par][0], nyf = s_cnt[par][1];
-        const bool maybe_best = s_flag[par] == 3;
-        if (threadIdx.x == 0) {       // the other parity's slots are free until the end barrier
-            s_cnt[par ^ 1][0] = s_cnt[par ^ 1][1] = 0;
-            s_flag[par ^ 1] = 0;
-            w.n_eval += (int64_t)nXr * nYr;
-            w.n_feas += (int64_t)nxf_tot * nyf;
-        }
-        if (nxf_tot > 0 && nyf > 0) {     // uniform
-            const int nsl = (nxf_tot + kMitmThreads - 1) / kMitmThreads;
-            double xv[kMitmNR];
-            int nxf = 0;
+                    for (int u = 0; u < kMitmNR; ++u) {
+                        const int e = r0 + u * kMitmThreads + threadIdx.x;
+                        if (e < nXr && B.m) { xr[u] = val[xoff + x0 + e]; xb[u] = bnd[xoff + x0 + e]; }
+                    }
+                    int f = 0;
 #pragma unroll
+                    for (int u = 0; u < kMitmNR; ++u) {
+                        const int e = r0 + u * kMitmThreads + threadIdx.x;
+                        const double v = e < nXr ? side_finish(x, B, xl, xr[u], xb[u]) : inf;
+                        xmin = v < xmin ? v : xmin;
+                        const unsigned bal = __ballot_sync(0xffffffffu, v != inf);
+                        if (v != inf) wbuf[f + __popc(bal & ((1u << lane) - 1u))] = v;
+                        f += __popc(bal);
+                    }
+                    __syncwarp();
+                    const int nsl = (f + 31) >> 5;
+                    double xv[kMitmNR];
+                    int nxf = 0;
+#pragma unroll
+                    for (int u = 0; u < kMitmNR; ++u) {
+                        const int e = u * 32 + lane;
+                        xv[u] = e < f ? wbuf[e] : inf;
+                        nxf += e < f;
+                    }
+                    switch (nsl) {
+                        case 0: break;
+                        case 1: mitm_cross<1>(xv, by, nyf, cs); break;
+                        case 2: mitm_cross<2>(xv, by, nyf, cs); break;
+                        case 3: mitm_cross<3>(xv, by, nyf, cs); break;
+                        case 4: mitm_cross<4>(xv, by, nyf, cs); break;
+                        case 5: mitm_cross<5>(xv, by, nyf, cs); break;
+                        case 6: mitm_cross<6>(xv, by, nyf, cs); break;
+                        case 7: mitm_cross<7>(xv, by, nyf, cs); break;
+                        default: mitm_cross<8>(xv, by, nyf, cs); break;
+                    }
+                    corr += (uint64_t)(nsl - nxf) * (uint64_t)nyf;
+                    nxf_all += nxf;
+                    MITM_COUNT(5, nsl * nyf);
+                    __syncwarp();
+                }
+            }
+            w.n_feas += nxf_all * nyf;
+            maybe_best = __syncthreads_or(xmin <= best) && yb_ok && nyf > 0;
+        } else {
+            // ---- both sides' feasible elements, compacted into shared memory;
+            //      element raw data (table value, boundary cut) for every slot
+            //      first, so all global loads are in flight together
+            double xr[kMitmNR], yr[kMitmNY];
+            int xb[kMitmNR], yb[kMitmNY];
+    #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                xv[u] = e < nxf_tot ? bx[e] : inf;
-                nxf += e < nxf_tot;
+                if (e < nXr && B.m) { xr[u] = val[xoff + x0 + e]; xb[u] = bnd[xoff + x0 + e]; }
             }
-            // ---- cross product: one max + checksum add per candidate
-            switch (nsl) {
-                case 1: mitm_cross<1>(xv, by, nyf, cs); break;
-                case 2: mitm_cross<2>(xv, by, nyf, cs); break;
-                case 3: mitm_cross<3>(xv, by, nyf, cs); break;
-                case 4: mitm_cross<4>(xv, by, nyf, cs); break;
-                case 5: mitm_cross<5>(xv, by, nyf, cs); break;
-                case 6: mitm_cross<6>(xv, by, nyf, cs); break;
-                case 7: mitm_cross<7>(xv, by, nyf, cs); break;
-                default: mitm_cross<8>(xv, by, nyf, cs); break;
+    #pragma unroll
+            for (int u = 0; u < kMitmNY; ++u) {
+                const int e = u * kMitmThreads + threadIdx.x;
+                if (e < nYr && B.m) { yr[u] = val[yoff + y0 + e]; yb[u] = bnd[yoff + y0 + e]; }
             }
-            corr += (uint64_t)(nsl - nxf) * (uint64_t)nyf;
-            // ---- rare: the tile can hold the incumbent. Its minimum is
-            //      tm = max(min X, min Y); the first rank at tm is the sum of
-            //      the smallest ranks of the elements at or below tm.
-            if (maybe_best) {
-                const double txmin = block_min_f64(xmin, red);
-                const double tymin = block_min_f64(ymin, red);
-                const double tm = txmin > tymin ? txmin : tymin;
-                if (tm <= best) {
-                    int64_t rx = INT64_MAX, ry = INT64_MAX;
-                    for (int e = threadIdx.x; e < nXr; e += kMitmThreads) {
-                        if (side_value(x, B, xl, val, bnd, x0 + e) <= tm) {
-                            const int64_t r = xl ? left_rank(x, B, x0 + e) : right_rank(x, B, cum, x0 + e);
-                            rx = r < rx ? r : rx;
-                        }
+    #pragma unroll
+            for (int u = 0; u < kMitmNR; ++u) {
+                const int e = u * kMitmThreads + threadIdx.x;
+                double v = inf;
+                if (e < nXr) { v = side_finish(x, B, xl, xr[u], xb[u]); xmin = v < xmin ? v : xmin; }
+                append_if(v != inf, v, bx, &s_cnt[par][0]);
+            }
+    #pragma unroll
+            for (int u = 0; u < kMitmNY; ++u) {
+                const int e = u * kMitmThreads + threadIdx.x;
+                double v = inf;
+                if (e < nYr) { v = side_finish(x, B, !xl, yr[u], yb[u]); ymin = v < ymin ? v : ymin; }
+                append_if(v != inf, v, by, &s_cnt[par][1]);
+            }
+            const int fl = (xmin <= best ? 1 : 0) | (ymin <= best ? 2 : 0);
+            if (fl) atomicOr(&s_flag[par], fl);
+            __syncthreads();
+            const int nxf_tot = s_cnt[par][0];
+            nyf = s_cnt[par][1];
+            maybe_best = s_flag[par] == 3;
+            if (threadIdx.x == 0) {       // the other parity's slots are free until the end barrier
+                s_cnt[par ^ 1][0] = s_cnt[par ^ 1][1] = 0;
+                s_flag[par ^ 1] = 0;
+                w.n_eval += (int64_t)nXr * nYr;
+                w.n_feas += (int64_t)nxf_tot * nyf;
+            }
+            if (nxf_tot > 0 && nyf > 0) {     // uniform
+                const int nsl = (nxf_tot + kMitmThreads - 1) / kMitmThreads;
+                double xv[kMitmNR];
+                int nxf = 0;
+#pragma unroll
+                for (int u = 0; u < kMitmNR; ++u) {
+                    const int e = u * kMitmThreads + threadIdx.x;
+                    xv[u] = e < nxf_tot ? bx[e] : inf;
+                    nxf += e < nxf_tot;
+                }
+                // ---- cross product: one max + checksum add per candidate
+                switch (nsl) {
+                    case 1: mitm_cross<1>(xv, by, nyf, cs); break;
+                    case 2: mitm_cross<2>(xv, by, nyf, cs); break;
+                    case 3: mitm_cross<3>(xv, by, nyf, cs); break;
+                    case 4: mitm_cross<4>(xv, by, nyf, cs); break;
+                    case 5: mitm_cross<5>(xv, by, nyf, cs); break;
+                    case 6: mitm_cross<6>(xv, by, nyf, cs); break;
+                    case 7: mitm_cross<7>(xv, by, nyf, cs); break;
+                    default: mitm_cross<8>(xv, by, nyf, cs); break;
+                }
+                corr += (uint64_t)(nsl - nxf) * (uint64_t)nyf;
+                MITM_COUNT(4, nsl * nyf);
+            }
+            maybe_best = maybe_best && nxf_tot > 0 && nyf > 0;
+        }
+        // ---- rare: the tile can hold the incumbent. Its minimum is
+        //      tm = max(min X, min Y); the first rank at tm is the sum of
+        //      the smallest ranks of the elements at or below tm.
+        if (maybe_best) {
+            const double txmin = block_min_f64(xmin, red);
+            const double tymin = block_min_f64(ymin, red);
+            const double tm = txmin > tymin ? txmin : tymin;
+            if (tm <= best && tm < inf) {
+                int64_t rx = INT64_MAX, ry = INT64_MAX;
+                for (int e = threadIdx.x; e < nXr; e += kMitmThreads) {
+                    if (side_value(x, B, xl, val, bnd, x0 + e) <= tm) {
+                        const int64_t r = xl ? left_rank(x, B, x0 + e) : right_rank(x, B, cum, x0 + e);
+                        rx = r < rx ? r : rx;
                     }
-                    for (int e = threadIdx.x; e < nYr; e += kMitmThreads) {
-                        if (side_value(x, B, !xl, val, bnd, y0 + e) <= tm) {
-                            const int64_t r = xl ? right_rank(x, B, cum, y0 + e) : left_rank(x, B, y0 + e);
-                            ry = r < ry ? r : ry;
-                        }
+                }
+                for (int e = threadIdx.x; e < nYr; e += kMitmThreads) {
+                    if (side_value(x, B, !xl, val, bnd, y0 + e) <= tm) {
+                        const int64_t r = xl ? right_rank(x, B, cum, y0 + e) : left_rank(x, B, y0 + e);
+                        ry = r < ry ? r : ry;
                     }
-                    rx = block_min_i64(rx, red);
-                    ry = block_min_i64(ry, red);
-                    if (threadIdx.x == 0 && win_better(tm, rx + ry, w.mk, w.rank)) {
-                        w.mk = tm;
-                        w.rank = rx + ry;
-                        s_best = tm;
-                    }
+                }
+                rx = block_min_i64(rx, red);
+                ry = block_min_i64(ry, red);
+                if (threadIdx.x == 0 && win_better(tm, rx + ry, w.mk, w.rank)) {
+                    w.mk = tm;
+                    w.rank = rx + ry;
+                    s_best = tm;
                 }
             }
         }
@@ -701,6 +867,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
     for (int u = 0; u < kMitmNR; ++u) c += cs[u];
     w.csum = c - corr * kInfBits;
+    MITM_MARK(3);
     block_reduce_win_store(w, partial);
 }
 
@@ -723,63 +890,65 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) cross_peak_kerne
     if (c == 42) sink[0] = c;
 }
 
+
 int mitm_grid(int sms) { return sms * kMitmCtasPerSm; }
 
 int64_t mitm_workspace_bytes(const dm_tables& t) {
-    if (t.n < 1 || t.n > 64 || t.p < 1 || !memo_valid(t)) return -1;
-    const MitmLayout L = mitm_layout(t.n, t.p);
-    if (L.bytes > 108 * 1024) return -1;
+    if (!memo_valid(t)) return -1;
+    SideTables st;
     MitmWorkspace ws;
-    if (!mitm_workspace(t.n, t.p, ws)) return -1;
+    if (!mitm_plan(t.n, t.p, st, ws, nullptr)) return -1;
     return (int64_t)ws.bytes;
 }
 
 int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* partial, int sms, void* ws,
                        int64_t ws_bytes, int* n_partials, cudaStream_t s) {
-    const int64_t need = mitm_workspace_bytes(t);
-    if (need < 0) return DM_E_TOO_LARGE;
-    const MitmLayout L = mitm_layout(t.n, t.p);
-    {   // tile count must fit the kernel's int32 tile indices
-        const int W = t.n - 1, rmax = t.n < t.p ? t.n : t.p;
-        auto C = [](int a, int b) -> unsigned __int128 {
-            if (b < 0 || b > a) return 0;
-            unsigned __int128 r = 1;
-            for (int i = 1; i <= b; ++i) r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
-            return r;
-        };
-        unsigned __int128 tiles = 1;
-        for (int m = 1; m < rmax; ++m) {
-            const int j = mitm_j(m);
-            for (int c = j; c <= W - (m - j); ++c) {
-                const unsigned __int128 nl = C(c - 1, j - 1), nr = C(W - c, m - j);
-                const unsigned __int128 nX = nl >= nr ? nl : nr, nY = nl >= nr ? nr : nl;
-                tiles += ((nX + kMitmTX - 1) / kMitmTX) * ((nY + kMitmTY - 1) / kMitmTY);
-            }
-        }
-        if (tiles > (unsigned __int128)(INT32_MAX / 2)) return DM_E_TOO_LARGE;
-    }
+    if (!memo_valid(t)) return DM_E_TOO_LARGE;
+    SideTables st;
     MitmWorkspace W;
-    mitm_workspace(t.n, t.p, W);
+    static thread_local SweepParams sp;
+    if (!mitm_plan(t.n, t.p, st, W, &sp)) return DM_E_TOO_LARGE;
+    const MitmLayout L = mitm_layout(t.n, t.p);
     void* buf = ws;
-    const bool own = !ws || ws_bytes < need;
-    if (own) DM_CUDA(cudaMallocAsync(&buf, (size_t)need, s));
-    double* timg = static_cast<double*>(buf);
-    double* val = reinterpret_cast<double*>(static_cast<unsigned char*>(buf) + W.off_val);
-    uint8_t* bnd = static_cast<uint8_t*>(buf) + W.off_bnd;
+    const bool own = !ws || ws_bytes < (int64_t)W.bytes;
+    if (own) DM_CUDA(cudaMallocAsync(&buf, W.bytes, s));
+    unsigned char* b8 = static_cast<unsigned char*>(buf);
+    int* ctl = reinterpret_cast<int*>(b8);
+    double* timg = reinterpret_cast<double*>(b8 + W.off_timg);
+    double* val = reinterpret_cast<double*>(b8 + W.off_val);
+    uint8_t* bnd = b8 + W.off_bnd;
+    const int rmax = t.n < t.p ? t.n : t.p;
+    {
+        const int64_t work = (int64_t)rmax * t.n * t.n;
+        int blocks = (int)((work + 255) / 256);
+        memo_image_kernel<<<blocks, 256, 0, s>>>(t, timg);
+        DM_CHECK_LAUNCH();
+    }
+    {
+        const size_t smem = (size_t)t.n * (rmax + 1) * 8 + (size_t)rmax * t.n * 4;
+        const int64_t per = (int64_t)256 * kTabPass;
+        int64_t blocks = (W.entries + per - 1) / per;
+        if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+        if (blocks < 1) blocks = 1;
+        side_tables_kernel<<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl);
+        DM_CHECK_LAUNCH();
+    }
     DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
-    int per_sm = 0;
-    DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splits_sweep_kernel, kMitmThreads, L.bytes));
-    if (per_sm < 1) return DM_E_TOO_LARGE;
-    int grid = sms * (per_sm < kMitmCtasPerSm ? per_sm : kMitmCtasPerSm);
-    dm_tables tv = t;
-    void* args[] = {&tv, &timg, &val, &bnd, &part, &nparts, &partial};
-    DM_CUDA(cudaLaunchCooperativeKernel((void*)splits_sweep_kernel, grid, kMitmThreads, args, L.bytes, s));
+    const int grid = mitm_grid(sms);
+    splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, part, nparts, partial);
+    DM_CHECK_LAUNCH();
     if (own) DM_CUDA(cudaFreeAsync(buf, s));
     *n_partials = grid;
     return DM_OK;
 }
 
 }  // namespace dm
+
+#ifdef DM_MITM_TIMING
+extern "C" __attribute__((visibility("default"))) int dm_debug_mitm_times(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, dm::g_mitm_times, sizeof(dm::g_mitm_times));
+}
+#endif
 
 extern "C" int dm_microbench_cross(int64_t iters, uint64_t* sink, int64_t* pairs, void* stream) {
     if (iters <= 0 || iters > INT32_MAX || !sink) return dmabi::fail(DM_E_ARG, "dm_microbench_cross: bad arguments");

@@ -1,0 +1,72 @@
+// Inner-loop variants of the split sweep's cross product (experiment, not
+// part of the library): pairs/s for each formulation at 2 CTAs x 256 thr/SM.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+constexpr int NR = 8, TY = 1024;
+
+template <int V, int CPS>
+__global__ void __launch_bounds__(256, CPS) k(int iters, uint64_t* sink) {
+    __shared__ __align__(16) double ys[TY];
+    for (int i = threadIdx.x; i < TY; i += blockDim.x) ys[i] = 1.0 + 1e-3 * ((i * 37) % 101);
+    __syncthreads();
+    double xv[NR]; uint64_t cs[NR]; uint32_t c32[NR];
+#pragma unroll
+    for (int u = 0; u < NR; ++u) { xv[u] = 1.0 + 1e-3 * ((threadIdx.x + 13 * u) % 101); cs[u] = 0; c32[u] = 0; }
+    const double2* y2 = reinterpret_cast<const double2*>(ys);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll 2
+        for (int y = 0; y < TY / 2; ++y) {
+            const double2 yy = y2[y];
+#pragma unroll
+            for (int u = 0; u < NR; ++u) {
+                if (V == 0) {
+                    const double a = xv[u] > yy.x ? xv[u] : yy.x;
+                    const double b = xv[u] > yy.y ? xv[u] : yy.y;
+                    cs[u] += (uint64_t)__double_as_longlong(a) + (uint64_t)__double_as_longlong(b);
+                } else if (V == 1) {
+                    const uint64_t xa = __double_as_longlong(xv[u]);
+                    const uint64_t a = xa > (uint64_t)__double_as_longlong(yy.x) ? xa : (uint64_t)__double_as_longlong(yy.x);
+                    const uint64_t b = xa > (uint64_t)__double_as_longlong(yy.y) ? xa : (uint64_t)__double_as_longlong(yy.y);
+                    cs[u] += a + b;
+                } else if (V == 2) {
+                    const int xh = __double2hiint(xv[u]);
+                    c32[u] += max(xh, __double2hiint(yy.x)) + max(xh, __double2hiint(yy.y));
+                } else if (V == 3) {
+                    const double a = fmax(xv[u], yy.x);
+                    const double b = fmax(xv[u], yy.y);
+                    cs[u] += (uint64_t)__double_as_longlong(a) + (uint64_t)__double_as_longlong(b);
+                }
+            }
+        }
+    }
+    uint64_t c = 0;
+#pragma unroll
+    for (int u = 0; u < NR; ++u) c += cs[u] + c32[u];
+    if (c == 42) sink[0] = c;
+}
+
+template <int V, int CPS>
+void run(const char* name) {
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    uint64_t* sink; cudaMalloc(&sink, 8);
+    int grid = sms * CPS, iters = 200;
+    k<V, CPS><<<grid, 256>>>(4, sink);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    k<V, CPS><<<grid, 256>>>(iters, sink);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    double pairs = (double)grid * 256 * NR * TY * iters;
+    printf("%-28s CPS=%d  %.3e pairs/s\n", name, CPS, pairs / (ms / 1e3));
+}
+
+int main() {
+    run<0, 2>("dsetp+fsel+sel+iadd3");
+    run<0, 4>("dsetp+fsel+sel+iadd3");
+    run<1, 2>("u64 isetp+sel+iadd3");
+    run<1, 4>("u64 isetp+sel+iadd3");
+    run<2, 2>("hi32 imnmx+iadd3");
+    run<3, 2>("fmax (dsetp.max)");
+    return 0;
+}
