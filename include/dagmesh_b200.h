@@ -342,6 +342,12 @@ DM_API int dm_microbench_fp64(int64_t iters, double* sink, int64_t* ops, void* s
  * sweep.  *pairs receives the candidate pairs the launch evaluates. */
 DM_API int dm_microbench_cross(int64_t iters, uint64_t* sink, int64_t* pairs, void* stream);
 
+/* dm_sweep_timing — CUDA-event timing of the whole-population split sweep's
+ * kernels on the calling thread: enable = 1 / 0 switches it (-1: unchanged);
+ * when ms_tables / ms_sweep are given, waits for the last timed sweep and
+ * returns its table phase (T image + side tables) and sweep kernel times. */
+DM_API int dm_sweep_timing(int32_t enable, float* ms_tables, float* ms_sweep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(256) memo_image_kernel(const dm_tables tp, dou
 // colex unrank of the first, Gosper successor for the rest, then the runs
 // the entry covers (T from the global image through L1).  Binomials in
 // shared memory (Pascal's triangle).  CTA 0 also resets the tile counter.
+template <typename Mask>   // uint32_t when every cut position fits 32 bits (n <= 34), else uint64_t
 __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, const double* __restrict__ timg,
                                                           const __grid_constant__ SideTables st,
                                                           double* __restrict__ val, uint8_t* __restrict__ bnd,
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
             }
             ti = lo;
         }
-        uint64_t mk = 0;
+        Mask mk = 0;
         for (int u = 0; u < kTabPass; ++u) {
             const int64_t e = e0 + u;
             if (e >= E) break;
@@ -492,15 +493,18 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
             const int km = st.km[ti];
             const int k = right ? km - mitm_j(km) : km;               // cuts per entry
             const int P = right ? W - mitm_j(km) : W - km - 1;        // positions
-            if (fresh) mk = colex_unrank(x, k, P, e - st.start[ti]);
-            else mk = side_next(mk);
+            if (fresh) mk = (Mask)colex_unrank(x, k, P, e - st.start[ti]);
+            else mk = (Mask)side_next((uint64_t)mk);
             double v = ninf;
             int prev;
+            auto low_bit = [](Mask r) {
+                if constexpr (sizeof(Mask) == 4) return __ffs((int)r); else return __ffsll((long long)r);
+            };
             if (!right) {                // L_k: runs q = 0..k-1 ending at the cuts (position 1 + b)
                 prev = 0;
                 int q = 0;
-                for (uint64_t r = mk; r; r &= r - 1, ++q) {
-                    const int c = __ffsll((long long)r);
+                for (Mask r = mk; r; r &= r - 1, ++q) {
+                    const int c = low_bit(r);
                     const double tv = T(q, prev, c);
                     v = tv > v ? tv : v;
                     prev = c;
@@ -508,8 +512,8 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
             } else {                     // R(m): runs q = m, m-1, .. starting at the cuts (position W - b)
                 prev = n;
                 int q = km;
-                for (uint64_t r = mk; r; r &= r - 1, --q) {
-                    const int c = W - (__ffsll((long long)r) - 1);
+                for (Mask r = mk; r; r &= r - 1, --q) {
+                    const int c = W + 1 - low_bit(r);
                     const double tv = T(q, c, prev);
                     v = tv > v ? tv : v;
                     prev = c;
@@ -901,6 +905,17 @@ int64_t mitm_workspace_bytes(const dm_tables& t) {
     return (int64_t)ws.bytes;
 }
 
+// Optional per-launch event timing of the sweep's kernels (dm_sweep_timing).
+struct SweepTiming {
+    bool on = false;
+    bool pending = false;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+};
+inline SweepTiming& sweep_timing() {
+    static thread_local SweepTiming st;
+    return st;
+}
+
 int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* partial, int sms, void* ws,
                        int64_t ws_bytes, int* n_partials, cudaStream_t s) {
     if (!memo_valid(t)) return DM_E_TOO_LARGE;
@@ -918,6 +933,11 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
     double* val = reinterpret_cast<double*>(b8 + W.off_val);
     uint8_t* bnd = b8 + W.off_bnd;
     const int rmax = t.n < t.p ? t.n : t.p;
+    SweepTiming& tm = sweep_timing();
+    if (tm.on) {
+        for (auto& e : tm.ev) if (!e) DM_CUDA(cudaEventCreate(&e));
+        DM_CUDA(cudaEventRecord(tm.ev[0], s));
+    }
     {
         const int64_t work = (int64_t)rmax * t.n * t.n;
         int blocks = (int)((work + 255) / 256);
@@ -930,19 +950,40 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         int64_t blocks = (W.entries + per - 1) / per;
         if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
         if (blocks < 1) blocks = 1;
-        side_tables_kernel<<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl);
+        if (t.n <= 34) side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl);
+        else side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl);
         DM_CHECK_LAUNCH();
     }
     DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
     const int grid = mitm_grid(sms);
+    if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
     splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, part, nparts, partial);
     DM_CHECK_LAUNCH();
+    if (tm.on) {
+        DM_CUDA(cudaEventRecord(tm.ev[2], s));
+        tm.pending = true;
+    }
     if (own) DM_CUDA(cudaFreeAsync(buf, s));
     *n_partials = grid;
     return DM_OK;
 }
 
 }  // namespace dm
+
+extern "C" int dm_sweep_timing(int32_t enable, float* ms_tables, float* ms_sweep) {
+    dm::SweepTiming& tm = dm::sweep_timing();
+    if (ms_tables || ms_sweep) {
+        if (!tm.pending) return dmabi::fail(DM_E_ARG, "dm_sweep_timing: no timed sweep since it was enabled");
+        DM_CUDA(cudaEventSynchronize(tm.ev[2]));
+        float a = 0, b = 0;
+        DM_CUDA(cudaEventElapsedTime(&a, tm.ev[0], tm.ev[1]));
+        DM_CUDA(cudaEventElapsedTime(&b, tm.ev[1], tm.ev[2]));
+        if (ms_tables) *ms_tables = a;
+        if (ms_sweep) *ms_sweep = b;
+    }
+    if (enable >= 0) tm.on = enable != 0;
+    return DM_OK;
+}
 
 #ifdef DM_MITM_TIMING
 extern "C" __attribute__((visibility("default"))) int dm_debug_mitm_times(unsigned long long* host) {

@@ -273,6 +273,26 @@ def cross_peak(iters: int = 400, repeats: int = 3) -> float:
     return best
 
 
+def sweep_kernel_times(batch: DeviceBatch, total: int, steps: int = 5, bufs: WinnerBuffers | None = None,
+                       part: int = 0, nparts: int = 1) -> tuple:
+    """Average (table phase ms, sweep kernel ms) of `steps` whole-population
+    split sweeps, from CUDA events the library records around its kernels."""
+    lib = _lib.load()
+    bufs = bufs or WinnerBuffers(batch.dev_buf.device)
+    _lib.check(lib.dm_sweep_timing(1, None, None))
+    ta = tb = 0.0
+    try:
+        for _ in range(steps):
+            enum(batch, "splits", 0, total, bufs, part=part, nparts=nparts)
+            a, b = C.c_float(0), C.c_float(0)
+            _lib.check(lib.dm_sweep_timing(-1, C.byref(a), C.byref(b)))
+            ta += a.value
+            tb += b.value
+    finally:
+        lib.dm_sweep_timing(0, None, None)
+    return ta / steps, tb / steps
+
+
 def fp64_peak(iters: int = 20000, repeats: int = 3) -> float:
     """Measured fp64 (DMUL/DADD) operations per second on the current device."""
     lib = _lib.load()
