@@ -194,6 +194,15 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te[0])
 
+    # the dominant kernel's own duration on every rank: CUDA events the library
+    # records around its launches (separate pass after the timed region)
+    tab_ms, sweep_ms = engine.sweep_kernel_times(batch, total, steps=args.steps, bufs=bufs, part=rank, nparts=world)
+    per_rank = torch.tensor([tab_ms, sweep_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        gathered = torch.empty(2 * world, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(gathered, per_rank)
+        per_rank = gathered
+    per_rank = per_rank.view(-1, 2).cpu().tolist()
     extras = {}
     if rank == 0 and not args.no_extras and world == 1:
         extras = secondary_measurements(dev)
@@ -202,9 +211,6 @@ def run_b200(args, rank, world, local_rank):
     value = total * args.steps / (ms / 1e3)
     e2e_val = total * args.steps / (e2e_ms / 1e3)
     cross = extras.get("cross_peak_pairs_per_s")
-    # the dominant kernel's own duration: CUDA events the library records
-    # around its launches (separate pass after the timed region)
-    tab_ms, sweep_ms = engine.sweep_kernel_times(batch, total, steps=args.steps, bufs=bufs, part=rank, nparts=world)
     achieved = res["n_feasible"] / world / (sweep_ms / 1e3) / 1e9      # per GPU
     traffic = ncu_traffic("splits_sweep_kernel") or {}
     line = {
@@ -219,6 +225,7 @@ def run_b200(args, rank, world, local_rank):
                      "unit": "Gcand/s", "frac": (achieved / (cross / 1e9)) if cross else None,
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("capture"),
                      "kernel": "splits_sweep_kernel", "kernel_ms": sweep_ms, "table_phase_ms": tab_ms,
+                     "per_rank_table_sweep_ms": per_rank,
                      "step_kernels_ms": kernel_ms,
                      "algorithmic_work_per_candidate": "one fp64 max (DSETP + 64-bit select) and one 64-bit "
                                                        "checksum add per feasible candidate",

@@ -132,7 +132,8 @@ struct SideTables {
 // decreasing number of candidates.
 struct SweepParams {
     int64_t offL[kMitmMaxM], offR[kMitmMaxM];
-    int16_t order[kMitmMaxBlocks];
+    int nbp;                          // blocks of this part
+    int16_t order[kMitmMaxBlocks];    // the part's blocks, largest tiles first
 };
 
 // Global workspace: tile counter, T image, side-table values, boundary bytes.
@@ -338,6 +339,8 @@ __device__ __forceinline__ void mitm_cross(const double (&xv)[kMitmNR], const do
 }  // namespace dm
 
 #include <algorithm>
+#include <array>
+#include <memory>
 #include <utility>
 #include <vector>
 
@@ -352,24 +355,90 @@ unsigned __int128 binom128(int a, int b) {
 }
 }  // namespace
 
-// The sweep's side-table plan and workspace layout; false when it does not
-// apply (more than kMitmMaxBlocks blocks, 2^36 table entries or 2^30 tiles).
-inline bool mitm_plan(int n, int p, SideTables& st, MitmWorkspace& ws, SweepParams* sp) {
+// The sweep's plan for part `part` of `nparts` and its workspace layout;
+// false when the sweep does not apply (more than kMitmMaxBlocks blocks, 2^36
+// table entries or 2^30 tiles).
+//
+// Parts own whole blocks, dealt largest first to the part where the block
+// adds the least load: its tiles plus the tables it reads (R(m), L_{j-1})
+// when the part does not hold them yet.  Each part builds only the tables of
+// its blocks, so the table phase splits across GPUs with the tiles.  Within a
+// part, blocks are ordered by the estimated duration of one of their tiles
+// (its pairs plus ~256 pair-equivalents per element it builds), largest
+// first, for the dynamic tile queue.
+inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWorkspace& ws, SweepParams* sp) {
     const int W = n - 1, rmax = n < p ? n : p;
-    if (n < 1 || n > 64 || p < 1 || rmax > kMitmMaxM) return false;
+    if (n < 1 || n > 64 || p < 1 || rmax > kMitmMaxM || nparts < 1 || part < 0 || part >= nparts) return false;
     const MitmLayout L = mitm_layout(n, p);
     if (L.n_blocks > kMitmMaxBlocks || L.bytes > 108 * 1024) return false;
-    const int KL = rmax >= 2 ? mitm_j(rmax - 1) - 1 : -1;
+    const int nb = L.n_blocks;
+    struct BlockCost { double tile, total; int m, b; };
+    std::vector<BlockCost> blk(nb);
+    unsigned __int128 tiles = 0;
+    for (int m = 0, b = 0; m < rmax; ++m)
+        for (int i = 0; i < mitm_blocks_of(m, W); ++i, ++b) {
+            const int j = mitm_j(m), c = m == 0 ? 0 : j + i;
+            const unsigned __int128 nl = m == 0 ? 1 : binom128(c - 1, j - 1), nr = m == 0 ? 1 : binom128(W - c, m - j);
+            const unsigned __int128 nX = nl >= nr ? nl : nr, nY = nl >= nr ? nr : nl;
+            unsigned __int128 R = 1;                     // thin blocks: rounds of kMitmTX X elements per tile
+            if (nY < (unsigned __int128)kThinY) {
+                R = (unsigned __int128)kThinPairs / ((unsigned __int128)kMitmTX * nY);
+                R = R < 1 ? 1 : (R > (unsigned __int128)kThinRounds ? kThinRounds : R);
+            }
+            const unsigned __int128 txs = (unsigned __int128)kMitmTX * R;
+            const unsigned __int128 tx = nX < txs ? nX : txs, ty = nY < kMitmTY ? nY : kMitmTY;
+            const unsigned __int128 nt = ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
+            tiles += nt;
+            const double tc = (double)(tx * ty + 256 * (tx + ty));
+            blk[b] = {tc, tc * (double)nt, m, b};
+        }
+    if (tiles > ((unsigned __int128)1 << 30)) return false;
+    // ---- blocks of this part
+    std::vector<int> mine;
+    if (nparts == 1) {
+        for (int b = 0; b < nb; ++b) mine.push_back(b);
+    } else {
+        // LPT over blocks, largest first; a block costs its tiles plus the
+        // tables (R(m), L_{j-1}) its part does not hold yet, at ~270
+        // pair-equivalents per table entry
+        std::vector<double> load(nparts, 0.0);
+        std::vector<std::vector<char>> hasR(nparts, std::vector<char>(rmax, 0)), hasL = hasR;
+        std::vector<int> order(nb);
+        for (int b = 0; b < nb; ++b) order[b] = b;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return blk[a].total > blk[b].total; });
+        std::vector<int> owner(nb, 0);
+        for (int b : order) {
+            const int m = blk[b].m, k = m >= 1 ? mitm_j(m) - 1 : 0;
+            const double tR = m >= 1 ? 270.0 * (double)binom128(W - mitm_j(m), m - mitm_j(m)) : 0.0;
+            const double tL = m >= 1 ? 270.0 * (double)binom128(W - k - 1, k) : 0.0;
+            int best = 0;
+            double best_load = 0;
+            for (int q = 0; q < nparts; ++q) {
+                const double l = load[q] + blk[b].total + (m >= 1 && !hasR[q][m] ? tR : 0.0) +
+                                 (m >= 1 && !hasL[q][k] ? tL : 0.0);
+                if (q == 0 || l < best_load) { best = q; best_load = l; }
+            }
+            owner[b] = best;
+            load[best] = best_load;
+            if (m >= 1) { hasR[best][m] = 1; hasL[best][k] = 1; }
+        }
+        for (int b = 0; b < nb; ++b) if (owner[b] == part) mine.push_back(b);
+    }
+    // ---- the tables those blocks read
+    std::vector<char> needR(rmax, 0), needL(rmax, 0);
+    for (int b : mine) if (blk[b].m >= 1) { needR[blk[b].m] = 1; needL[mitm_j(blk[b].m) - 1] = 1; }
     unsigned __int128 e = 0;
     st.n_tab = 0;
     for (int m = 0; m < kMitmMaxM; ++m) st.offL[m] = st.offR[m] = 0;
-    for (int k = 0; k <= KL; ++k) {
+    for (int k = 0; k < rmax; ++k) {
+        if (!needL[k]) continue;
         st.kind[st.n_tab] = 0; st.km[st.n_tab] = (int8_t)k; st.start[st.n_tab++] = (int64_t)e;
         for (int m = 1; m < rmax; ++m) if (mitm_j(m) - 1 == k) st.offL[m] = (int64_t)e;
         e += binom128(W - k - 1, k);
         if (e > ((unsigned __int128)1 << 36)) return false;
     }
     for (int m = 1; m < rmax; ++m) {
+        if (!needR[m]) continue;
         st.kind[st.n_tab] = 1; st.km[st.n_tab] = (int8_t)m; st.start[st.n_tab++] = (int64_t)e;
         st.offR[m] = (int64_t)e;
         e += binom128(W - mitm_j(m), m - mitm_j(m));
@@ -381,37 +450,14 @@ inline bool mitm_plan(int n, int p, SideTables& st, MitmWorkspace& ws, SweepPara
     ws.off_val = ws.off_timg + ((((size_t)L.M.t_elems * 8) + 255) & ~(size_t)255);
     ws.off_bnd = ws.off_val + (((size_t)ws.entries * 8 + 255) & ~(size_t)255);
     ws.bytes = ws.off_bnd + (((size_t)ws.entries + 255) & ~(size_t)255);
-    // blocks by decreasing number of candidates; total tiles bounded
-    const int nb = L.n_blocks;
-    std::vector<std::pair<unsigned __int128, int>> key(nb);
-    unsigned __int128 tiles = 0;
-    for (int m = 0, b = 0; m < rmax; ++m)
-        for (int i = 0; i < mitm_blocks_of(m, W); ++i, ++b) {
-            const int j = mitm_j(m), c = m == 0 ? 0 : j + i;
-            const unsigned __int128 nl = m == 0 ? 1 : binom128(c - 1, j - 1), nr = m == 0 ? 1 : binom128(W - c, m - j);
-            const unsigned __int128 nX = nl >= nr ? nl : nr, nY = nl >= nr ? nr : nl;
-            // tiles of the block (thin blocks: rounds of kMitmTX X elements),
-            // ordered by the estimated duration of one tile: its pairs plus
-            // ~256 pair-equivalents per element it builds
-            unsigned __int128 R = 1;
-            if (nY < (unsigned __int128)kThinY) {
-                R = (unsigned __int128)kThinPairs / ((unsigned __int128)kMitmTX * nY);
-                R = R < 1 ? 1 : (R > (unsigned __int128)kThinRounds ? kThinRounds : R);
-            }
-            const unsigned __int128 txs = (unsigned __int128)kMitmTX * R;
-            const unsigned __int128 tx = nX < txs ? nX : txs, ty = nY < kMitmTY ? nY : kMitmTY;
-            tiles += ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
-            key[b] = {tx * ty + 256 * (tx + ty), b};
-        }
-    if (tiles > ((unsigned __int128)1 << 30)) return false;
     if (sp) {
-        std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
-        for (int i = 0; i < nb; ++i) sp->order[i] = (int16_t)key[i].second;
+        std::stable_sort(mine.begin(), mine.end(), [&](int a, int b) { return blk[a].tile > blk[b].tile; });
+        sp->nbp = (int)mine.size();
+        for (int i = 0; i < sp->nbp; ++i) sp->order[i] = (int16_t)mine[i];
         for (int m = 0; m < kMitmMaxM; ++m) { sp->offL[m] = st.offL[m]; sp->offR[m] = st.offR[m]; }
     }
     return true;
 }
-
 
 // ------------------------------------------------------------ 1. T image
 __global__ void __launch_bounds__(256) memo_image_kernel(const dm_tables tp, double* __restrict__ timg) {
@@ -570,8 +616,8 @@ __device__ inline void memo_load(const MemoLayout& L, const double* __restrict__
 
 __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_kernel(
         const dm_tables tp, const __grid_constant__ SweepParams P, int* __restrict__ ctl,
-        const double* __restrict__ timg, const double* __restrict__ val, const uint8_t* __restrict__ bnd, int part,
-        int nparts, dm_winner* partial) {
+        const double* __restrict__ timg, const double* __restrict__ val, const uint8_t* __restrict__ bnd,
+        dm_winner* partial) {
     const dm_tables t = tp;   // register copy (no param-space references)
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int s_cnt[2][2];       // [tile parity][X, Y] feasible counts
@@ -633,7 +679,8 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         bc[b] = (uint8_t)(m == 0 ? 0 : mitm_j(m) + (b - mbase[m]));
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    const int nbp = P.nbp;
+    for (int i = threadIdx.x; i < nbp; i += blockDim.x) {
         const int b = P.order[i];
         pos_blk[i] = (int16_t)b;
         const Blk B = block_of(b, bm[b], bc[b]);
@@ -643,8 +690,8 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     }
     __syncthreads();
     if (threadIdx.x < 32) {
-        const int lane = threadIdx.x, per = (nb + 31) / 32;
-        const int b0 = lane * per, b1 = b0 + per < nb ? b0 + per : nb;
+        const int lane = threadIdx.x, per = (nbp + 31) / 32;
+        const int b0 = lane * per, b1 = b0 + per < nbp ? b0 + per : nbp;
         int s = 0;
         for (int b = b0; b < b1; ++b) s += tstart[b + 1];
         int incl = s;
@@ -656,9 +703,9 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         for (int b = b0; b < b1; ++b) { run += tstart[b + 1]; tstart[b + 1] = run; }
         if (lane == 0) tstart[0] = 0;
     }
-    if (threadIdx.x == 0) s_g[0] = part + nparts * atomicAdd(ctl, 1);   // dynamic tile queue
+    if (threadIdx.x == 0) s_g[0] = atomicAdd(ctl, 1);   // dynamic tile queue over the part's blocks
     __syncthreads();
-    const int n_tiles = tstart[nb];
+    const int n_tiles = tstart[nbp];
     MITM_MARK(2);
 
     Win w;
@@ -671,8 +718,8 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     for (int par = 0;; par ^= 1) {
         const int g = s_g[par];
         if (g >= n_tiles) break;           // uniform
-        if (threadIdx.x == 0) s_g[par ^ 1] = part + nparts * atomicAdd(ctl, 1);   // read after the end barrier
-        int lo = 0, hi = nb - 1;
+        if (threadIdx.x == 0) s_g[par ^ 1] = atomicAdd(ctl, 1);   // read after the end barrier
+        int lo = 0, hi = nbp - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (tstart[mid] <= g) lo = mid; else hi = mid - 1;
@@ -897,12 +944,31 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) cross_peak_kerne
 
 int mitm_grid(int sms) { return sms * kMitmCtasPerSm; }
 
-int64_t mitm_workspace_bytes(const dm_tables& t) {
-    if (!memo_valid(t)) return -1;
+// Plans depend only on (n, p, part, nparts): computed once per thread and
+// shape, then reused (host-side combinatorics, no instance data).
+struct PlanEntry {
+    bool ok;
     SideTables st;
     MitmWorkspace ws;
-    if (!mitm_plan(t.n, t.p, st, ws, nullptr)) return -1;
-    return (int64_t)ws.bytes;
+    SweepParams sp;
+};
+
+inline const PlanEntry& cached_plan(int n, int p, int part, int nparts) {
+    static thread_local std::vector<std::pair<std::array<int, 4>, std::unique_ptr<PlanEntry>>> cache;
+    const std::array<int, 4> key{n, p, part, nparts};
+    for (auto& kv : cache)
+        if (kv.first == key) return *kv.second;
+    auto e = std::make_unique<PlanEntry>();
+    e->ok = mitm_plan(n, p, part, nparts, e->st, e->ws, &e->sp);
+    if (cache.size() > 64) cache.erase(cache.begin());
+    cache.emplace_back(key, std::move(e));
+    return *cache.back().second;
+}
+
+int64_t mitm_workspace_bytes(const dm_tables& t) {
+    if (!memo_valid(t)) return -1;
+    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1);
+    return pe.ok ? (int64_t)pe.ws.bytes : -1;
 }
 
 // Optional per-launch event timing of the sweep's kernels (dm_sweep_timing).
@@ -919,10 +985,11 @@ inline SweepTiming& sweep_timing() {
 int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* partial, int sms, void* ws,
                        int64_t ws_bytes, int* n_partials, cudaStream_t s) {
     if (!memo_valid(t)) return DM_E_TOO_LARGE;
-    SideTables st;
-    MitmWorkspace W;
-    static thread_local SweepParams sp;
-    if (!mitm_plan(t.n, t.p, st, W, &sp)) return DM_E_TOO_LARGE;
+    const PlanEntry& pe = cached_plan(t.n, t.p, part, nparts);
+    if (!pe.ok) return DM_E_TOO_LARGE;
+    const SideTables& st = pe.st;
+    const MitmWorkspace& W = pe.ws;
+    const SweepParams& sp = pe.sp;
     const MitmLayout L = mitm_layout(t.n, t.p);
     void* buf = ws;
     const bool own = !ws || ws_bytes < (int64_t)W.bytes;
@@ -957,7 +1024,7 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
     DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
     const int grid = mitm_grid(sms);
     if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
-    splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, part, nparts, partial);
+    splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial);
     DM_CHECK_LAUNCH();
     if (tm.on) {
         DM_CUDA(cudaEventRecord(tm.ev[2], s));
