@@ -398,29 +398,46 @@ inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWo
     if (nparts == 1) {
         for (int b = 0; b < nb; ++b) mine.push_back(b);
     } else {
-        // LPT over blocks, largest first; a block costs its tiles plus the
-        // tables (R(m), L_{j-1}) its part does not hold yet, at ~270
-        // pair-equivalents per table entry
-        std::vector<double> load(nparts, 0.0);
-        std::vector<std::vector<char>> hasR(nparts, std::vector<char>(rmax, 0)), hasL = hasR;
-        std::vector<int> order(nb);
-        for (int b = 0; b < nb; ++b) order[b] = b;
-        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return blk[a].total > blk[b].total; });
+        // m-groups (a group shares R(m) and L_{j-1}) whole to the least-loaded
+        // part, largest first; a group above 3/4 of a part's share is dealt
+        // block by block (LPT) and its tables are built by every part it
+        // touches.  Costs: tiles plus ~270 pair-equivalents per table entry.
+        std::vector<double> load(nparts, 0.0), gcost(rmax, 0.0), gtab(rmax, 0.0);
+        double total = 0;
+        for (const auto& x : blk) { gcost[x.m] += x.total; total += x.total; }
+        for (int m = 1; m < rmax; ++m) {
+            const int k = mitm_j(m) - 1;
+            gtab[m] = 270.0 * (double)(binom128(W - mitm_j(m), m - mitm_j(m)) + binom128(W - k - 1, k));
+            total += gtab[m];
+        }
+        std::vector<int> ms(rmax);
+        for (int m = 0; m < rmax; ++m) ms[m] = m;
+        std::stable_sort(ms.begin(), ms.end(),
+                         [&](int a, int b) { return gcost[a] + gtab[a] > gcost[b] + gtab[b]; });
+        auto least = [&]() { return (int)(std::min_element(load.begin(), load.end()) - load.begin()); };
         std::vector<int> owner(nb, 0);
-        for (int b : order) {
-            const int m = blk[b].m, k = m >= 1 ? mitm_j(m) - 1 : 0;
-            const double tR = m >= 1 ? 270.0 * (double)binom128(W - mitm_j(m), m - mitm_j(m)) : 0.0;
-            const double tL = m >= 1 ? 270.0 * (double)binom128(W - k - 1, k) : 0.0;
-            int best = 0;
-            double best_load = 0;
-            for (int q = 0; q < nparts; ++q) {
-                const double l = load[q] + blk[b].total + (m >= 1 && !hasR[q][m] ? tR : 0.0) +
-                                 (m >= 1 && !hasL[q][k] ? tL : 0.0);
-                if (q == 0 || l < best_load) { best = q; best_load = l; }
+        for (int m : ms) {
+            std::vector<int> bs;
+            for (int b = 0; b < nb; ++b) if (blk[b].m == m) bs.push_back(b);
+            if (gcost[m] + gtab[m] <= 0.75 * total / nparts) {
+                const int q = least();
+                for (int b : bs) owner[b] = q;
+                load[q] += gcost[m] + gtab[m];
+            } else {
+                std::vector<char> has(nparts, 0);
+                std::stable_sort(bs.begin(), bs.end(), [&](int a, int b) { return blk[a].total > blk[b].total; });
+                for (int b : bs) {
+                    int best = 0;
+                    double bl = 0;
+                    for (int q = 0; q < nparts; ++q) {
+                        const double l = load[q] + blk[b].total + (has[q] ? 0.0 : gtab[m]);
+                        if (q == 0 || l < bl) { best = q; bl = l; }
+                    }
+                    owner[b] = best;
+                    load[best] = bl;
+                    has[best] = 1;
+                }
             }
-            owner[b] = best;
-            load[best] = best_load;
-            if (m >= 1) { hasR[best][m] = 1; hasL[best][k] = 1; }
         }
         for (int b = 0; b < nb; ++b) if (owner[b] == part) mine.push_back(b);
     }
