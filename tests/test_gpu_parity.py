@@ -382,3 +382,27 @@ def test_splits_mitm_matches_memo_and_oracle(oracle_mod, engine_ready, monkeypat
             recs.append(struct.pack(D.WINNER_FMT, w["makespan"], w["rank"], w["n_evaluated"], w["n_feasible"],
                                     w["checksum"]))
         assert D.merge_records(np.frombuffer(b"".join(recs), np.uint8)) == a
+
+
+def test_splits_c_abi_without_workspace(engine_ready):
+    """dm_enum_splits / dm_enum_splits_part called directly through the C ABI
+    (no caller workspace: the library allocates its side tables
+    stream-ordered) return the same record as the engine's workspace path."""
+    import ctypes as C
+    import torch
+    from paper_2309_01172_b200 import _lib
+    rng = np.random.default_rng(5)
+    st, fleet = big_instance(rng, 24, 20, dag=False, links=True, pressure=(0.1, 0.7))
+    batch = engine.device_batch([build_host(st, fleet)])
+    total = engine.splits_total(24, 20)
+    want = engine.enum(batch, "splits", 0, total).read()
+    lib = _lib.load()
+    bufs = engine.WinnerBuffers(batch.dev_buf.device)
+    stt = batch.struct(0)
+    _lib.check(lib.dm_enum_splits(C.byref(stt), 0, total, bufs.out.data_ptr(), bufs.scratch.data_ptr(),
+                                  _lib.stream_ptr()))
+    assert bufs.read() == want
+    _lib.check(lib.dm_enum_splits_part(C.byref(stt), 0, total, 0, 1, bufs.out.data_ptr(), bufs.scratch.data_ptr(),
+                                       _lib.stream_ptr()))
+    assert bufs.read() == want
+    torch.cuda.synchronize()
