@@ -56,9 +56,13 @@ def c2_instance():
 def workload_config(total):
     return {"workload": "C2 llama2-7b (34 layer cells) x 32 heterogeneous workers, exhaustive split sweep",
             "candidates_per_step": total, "stages": 34, "workers": 32,
-            "candidate_source": "in-kernel enumeration (rank -> splits), ~0 HBM bytes per candidate",
-            "l2_policy": "inputs are generated on chip; no HBM-resident candidate stream to flush",
-            "parallelism": "rank tasks interleaved across GPUs (task mod world) + 1 NCCL all-gather of 40-byte winner records"}
+            "candidate_source": "generated on chip: splits grouped by (cut count, middle-cut position) as cross "
+                                "products of left x right cut sets; each feasible candidate's makespan = "
+                                "max(L, R) folded into the checksum, infeasible ones resolved per side element",
+            "l2_policy": "no HBM-resident candidate stream; the per-sweep side tables (134 MB) exceed L2 and are "
+                         "rebuilt every step",
+            "parallelism": "whole blocks per GPU (each builds the side tables of its blocks) + 1 NCCL all-gather "
+                           "of 40-byte winner records"}
 
 
 # ---------------------------------------------------------------- clocks
