@@ -285,7 +285,7 @@ constexpr int kStreamThreads = 256;
 struct StreamLayout {
     int n, P, stages, cpt, nt;
     bool square;
-    size_t t_elems, off_T, off_rowidx, off_tiles, off_bar, bytes, tile_bytes;
+    size_t t_elems, off_T, off_code, off_rowidx, off_tiles, off_bar, bytes, tile_bytes;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -297,6 +297,7 @@ __host__ __device__ inline StreamLayout stream_layout(int n, int P, int stages, 
     L.t_elems = square ? (size_t)n * (n + 1) * P : (size_t)n * (n + 1) / 2 * P;
     size_t off = 0;
     L.off_T = off; off = al16(off + L.t_elems * 8);
+    L.off_code = off; off = al16(off + L.t_elems);          // first failing capacity of the run (0: fits)
     L.off_rowidx = off; off = al16(off + (size_t)(n + 1) * 4);
     L.tile_bytes = al16((size_t)nt * cpt * n);
     L.off_tiles = off; off = al16(off + L.tile_bytes * stages + 16);
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
     // T: load of run (a, b) on w (compute only when PAIR); sign bit set when
     // the run fails _fits (|T| is the value; -0.0 keeps the flag)
     double* T = reinterpret_cast<double*>(sm + L.off_T);
+    uint8_t* C8 = sm + L.off_code;
     int32_t* rowidx = reinterpret_cast<int32_t*>(sm + L.off_rowidx);
     unsigned char* tiles = sm + L.off_tiles;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.off_bar);
@@ -421,8 +423,11 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
             run_cost_contig(t, a, b, w, [&](int) { return -1; }, c, rd);  // uniform link: every source is remote
             v = c + rd;
         }
-        if (!fits_range(t, w, a, b)) v = -v;
-        T[SQUARE ? ((size_t)a * (n + 1) + b) * P + w : (size_t)it] = v;
+        const int code = cap_violation(t, w, a, b);
+        if (code) v = -v;
+        const size_t ti = SQUARE ? ((size_t)a * (n + 1) + b) * P + w : (size_t)it;
+        T[ti] = v;
+        C8[ti] = (uint8_t)code;
     }
     __syncthreads();
 
@@ -430,6 +435,7 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
     const int nw = (n + 3) >> 2;
     const uint32_t sm_s = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t T_s = sm_s + (uint32_t)L.off_T, rowidx_s = sm_s + (uint32_t)L.off_rowidx;
+    const uint32_t C_s = sm_s + (uint32_t)L.off_code;
     const uint32_t uP = (uint32_t)P, Pm1 = uP - 1u, n1P8 = 8u * (uint32_t)(n + 1) * uP;
     const uint32_t stage_mask_lo = n - 1 >= 32 ? 0xffffffffu : ((1u << (n - 1)) - 1u);
     const uint32_t stage_mask_hi = n - 1 >= 64 ? 0xffffffffu : (n - 1 > 32 ? ((1u << (n - 33)) - 1u) : 0u);
@@ -476,7 +482,7 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
                     v = v + rd;
                 }
                 mk = v > mk ? v : mk;
-                if (signbit(tv) && code == DM_V_OK) code = cap_violation(t, (int)w, a, b);
+                if (signbit(tv) && code == DM_V_OK) code = lds_u8(C_s + ((addr - T_s) >> 3));
                 prev = (int)w; a = b;
                 if (SQUARE) rowb = T_s + (uint32_t)b * n1P8;
             };
