@@ -175,21 +175,24 @@ def run_b200(args, rank, world, local_rank):
     ms, kernel_ms = float(t[0]), float(t[1])
     res = D.merge_records(step().cpu().numpy()) if world > 1 else bufs.read()
 
-    # ---- e2e: public API with host buffers, copies inside the timed region
-    import numpy as np
-    host_rec = batch.host_buf
+    # ---- e2e: the engine's serving form of the sweep (engine.SweepGraph: one
+    #      CUDA graph with the H2D copy of the instance tables from pinned
+    #      host memory, the sweep's kernels and the D2H of the winner record),
+    #      host synchronisation and the winner read every step
+    sweep = engine.SweepGraph(batch, total, bufs=engine.WinnerBuffers(dev), part=rank, nparts=world)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pinned_out = torch.empty(bufs.out.numel() * world, dtype=torch.uint8, pin_memory=True)
     e0.record(stream)
     for _ in range(args.steps):
-        batch.dev_buf.copy_(host_rec, non_blocking=True)
-        batch.structs_dev.copy_(batch.records_host, non_blocking=True)
-        engine.enum(batch, "splits", k0, k1, bufs, part=rank, nparts=world)
-        out = D.all_gather_winner(bufs.out).view(-1) if world > 1 else bufs.out
-        pinned_out.narrow(0, 0, out.numel()).copy_(out, non_blocking=True)
-        stream.synchronize()
-        D.merge_records(pinned_out.numpy()[: out.numel()])
+        sweep.launch()
+        if world > 1:
+            out = D.all_gather_winner(sweep.bufs.out).view(-1)
+            pinned_out.copy_(out, non_blocking=True)
+            stream.synchronize()
+            D.merge_records(pinned_out.numpy())
+        else:
+            sweep.read()
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1)

@@ -273,6 +273,53 @@ def cross_peak(iters: int = 400, repeats: int = 3) -> float:
     return best
 
 
+class SweepGraph:
+    """A whole-population split sweep of one instance captured as a CUDA
+    graph (the serving form of `enum(batch, "splits", 0, total)`): the H2D
+    copy of the instance tables from pinned host memory, the sweep's kernels
+    and — single GPU — the D2H copy of the winner record into pinned host
+    memory.  `launch()` replays it on the current stream; `read()` waits and
+    returns the winner.  For a multi-GPU part (nparts > 1) the record stays
+    on the device (`bufs.out`) for the caller's all-gather."""
+
+    def __init__(self, batch: DeviceBatch, total: int, bufs: WinnerBuffers | None = None, part: int = 0,
+                 nparts: int = 1):
+        torch = _torch()
+        lib = _lib.load()
+        self.batch, self.total, self.part, self.nparts = batch, total, part, nparts
+        self.bufs = bufs or WinnerBuffers(batch.dev_buf.device)
+        self.bufs.workspace_for(int(lib.dm_splits_workspace_bytes(C.byref(batch.struct(0)))))
+        self.host_out = torch.empty(_WINNER_BYTES, dtype=torch.uint8, pin_memory=True)
+        self.h2d_bytes = int(batch.h2d_bytes)
+        self.d2h_bytes = _WINNER_BYTES if nparts == 1 else 0
+        side = torch.cuda.Stream(device=batch.dev_buf.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):          # warm the plan cache and the kernels' attributes
+            self._body()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._body()
+
+    def _body(self):
+        b = self.batch
+        b.dev_buf.copy_(b.host_buf, non_blocking=True)
+        b.structs_dev.copy_(b.records_host, non_blocking=True)
+        enum(b, "splits", 0, self.total, self.bufs, part=self.part, nparts=self.nparts)
+        if self.nparts == 1:
+            self.host_out.copy_(self.bufs.out, non_blocking=True)
+
+    def launch(self):
+        self.graph.replay()
+
+    def read(self) -> dict:
+        _torch().cuda.current_stream().synchronize()
+        w = _lib.DmWinner.from_buffer_copy(self.host_out.numpy().tobytes())
+        return dict(makespan=w.makespan, rank=w.rank, n_evaluated=w.n_evaluated,
+                    n_feasible=w.n_feasible, checksum=w.checksum)
+
+
 def sweep_kernel_times(batch: DeviceBatch, total: int, steps: int = 5, bufs: WinnerBuffers | None = None,
                        part: int = 0, nparts: int = 1) -> tuple:
     """Average (table phase ms, sweep kernel ms) of `steps` whole-population

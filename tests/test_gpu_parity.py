@@ -406,3 +406,17 @@ def test_splits_c_abi_without_workspace(engine_ready):
                                        _lib.stream_ptr()))
     assert bufs.read() == want
     torch.cuda.synchronize()
+
+
+def test_sweep_graph_matches_enum(engine_ready):
+    """engine.SweepGraph (H2D + sweep kernels + D2H captured as one CUDA graph)
+    returns the enumeration's record on every replay."""
+    rng = np.random.default_rng(9)
+    st, fleet = big_instance(rng, 22, 16, dag=False, links=True, pressure=(0.1, 0.7))
+    batch = engine.device_batch([build_host(st, fleet)])
+    total = engine.splits_total(22, 16)
+    want = engine.enum(batch, "splits", 0, total).read()
+    g = engine.SweepGraph(batch, total)
+    for _ in range(3):
+        g.launch()
+        assert g.read() == want

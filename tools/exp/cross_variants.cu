@@ -3,9 +3,9 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-constexpr int NR = 8, TY = 1024;
+constexpr int TY = 1024;
 
-template <int V, int CPS>
+template <int V, int CPS, int NR>
 __global__ void __launch_bounds__(256, CPS) k(int iters, uint64_t* sink) {
     __shared__ __align__(16) double ys[TY];
     for (int i = threadIdx.x; i < TY; i += blockDim.x) ys[i] = 1.0 + 1e-3 * ((i * 37) % 101);
@@ -46,24 +46,27 @@ __global__ void __launch_bounds__(256, CPS) k(int iters, uint64_t* sink) {
     if (c == 42) sink[0] = c;
 }
 
-template <int V, int CPS>
+template <int V, int CPS, int NR = 8>
 void run(const char* name) {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     uint64_t* sink; cudaMalloc(&sink, 8);
     int grid = sms * CPS, iters = 200;
-    k<V, CPS><<<grid, 256>>>(4, sink);
+    k<V, CPS, NR><<<grid, 256>>>(4, sink);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
-    k<V, CPS><<<grid, 256>>>(iters, sink);
+    k<V, CPS, NR><<<grid, 256>>>(iters, sink);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     double pairs = (double)grid * 256 * NR * TY * iters;
-    printf("%-28s CPS=%d  %.3e pairs/s\n", name, CPS, pairs / (ms / 1e3));
+    printf("%-28s CPS=%d NR=%d %.3e pairs/s\n", name, CPS, NR, pairs / (ms / 1e3));
 }
 
 int main() {
     run<0, 2>("dsetp+fsel+sel+iadd3");
     run<0, 4>("dsetp+fsel+sel+iadd3");
+    run<0, 3, 4>("dsetp+fsel+sel+iadd3");
+    run<0, 4, 4>("dsetp+fsel+sel+iadd3");
+    run<0, 2, 16>("dsetp+fsel+sel+iadd3");
     run<1, 2>("u64 isetp+sel+iadd3");
     run<1, 4>("u64 isetp+sel+iadd3");
     run<2, 2>("hi32 imnmx+iadd3");
