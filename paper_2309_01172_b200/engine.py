@@ -280,18 +280,21 @@ class SweepGraph:
     and — single GPU — the D2H copy of the winner record into pinned host
     memory.  `launch()` replays it on the current stream; `read()` waits and
     returns the winner.  For a multi-GPU part (nparts > 1) the record stays
-    on the device (`bufs.out`) for the caller's all-gather."""
+    on the device (`bufs.out`) for the caller's all-gather.  copy_inputs=False
+    captures the kernels alone (tables already resident, record left in
+    `bufs.out`)."""
 
     def __init__(self, batch: DeviceBatch, total: int, bufs: WinnerBuffers | None = None, part: int = 0,
-                 nparts: int = 1):
+                 nparts: int = 1, copy_inputs: bool = True):
         torch = _torch()
         lib = _lib.load()
         self.batch, self.total, self.part, self.nparts = batch, total, part, nparts
+        self.copy_inputs = copy_inputs
         self.bufs = bufs or WinnerBuffers(batch.dev_buf.device)
         self.bufs.workspace_for(int(lib.dm_splits_workspace_bytes(C.byref(batch.struct(0)))))
         self.host_out = torch.empty(_WINNER_BYTES, dtype=torch.uint8, pin_memory=True)
-        self.h2d_bytes = int(batch.h2d_bytes)
-        self.d2h_bytes = _WINNER_BYTES if nparts == 1 else 0
+        self.h2d_bytes = int(batch.h2d_bytes) if copy_inputs else 0
+        self.d2h_bytes = _WINNER_BYTES if nparts == 1 and copy_inputs else 0
         side = torch.cuda.Stream(device=batch.dev_buf.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):          # warm the plan cache and the kernels' attributes
@@ -304,10 +307,11 @@ class SweepGraph:
 
     def _body(self):
         b = self.batch
-        b.dev_buf.copy_(b.host_buf, non_blocking=True)
-        b.structs_dev.copy_(b.records_host, non_blocking=True)
+        if self.copy_inputs:
+            b.dev_buf.copy_(b.host_buf, non_blocking=True)
+            b.structs_dev.copy_(b.records_host, non_blocking=True)
         enum(b, "splits", 0, self.total, self.bufs, part=self.part, nparts=self.nparts)
-        if self.nparts == 1:
+        if self.nparts == 1 and self.copy_inputs:
             self.host_out.copy_(self.bufs.out, non_blocking=True)
 
     def launch(self):
