@@ -124,6 +124,7 @@ struct SideTables {
     int n_tab;
     int8_t kind[2 * kMitmMaxM];       // 0: L_k, 1: R(m)
     int8_t km[2 * kMitmMaxM];         // k for L_k, m for R(m)
+    int8_t pos[2 * kMitmMaxM];        // positions the table's cuts range over
     int64_t start[2 * kMitmMaxM + 1]; // entry prefix
     int64_t offL[kMitmMaxM], offR[kMitmMaxM];
 };
@@ -355,6 +356,15 @@ unsigned __int128 binom128(int a, int b) {
 }
 }  // namespace
 
+// Positions the left table L_k ranges over: the largest left prefix any block
+// reading it needs (cuts below c <= cmax(m) = W - (m - j), j = k + 1).
+inline int left_positions(int W, int rmax, int k) {
+    int P = 0;
+    for (int m = 1; m < rmax; ++m)
+        if (mitm_j(m) - 1 == k) P = std::max(P, W - (m - mitm_j(m)) - 1);
+    return P;
+}
+
 // The sweep's plan for part `part` of `nparts` and its workspace layout;
 // false when the sweep does not apply (more than kMitmMaxBlocks blocks, 2^36
 // table entries or 2^30 tiles).
@@ -407,7 +417,8 @@ inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWo
         for (const auto& x : blk) { gcost[x.m] += x.total; total += x.total; }
         for (int m = 1; m < rmax; ++m) {
             const int k = mitm_j(m) - 1;
-            gtab[m] = 270.0 * (double)(binom128(W - mitm_j(m), m - mitm_j(m)) + binom128(W - k - 1, k));
+            gtab[m] = 270.0 * (double)(binom128(W - mitm_j(m), m - mitm_j(m)) +
+                                       binom128(left_positions(W, rmax, k), k));
             total += gtab[m];
         }
         std::vector<int> ms(rmax);
@@ -449,14 +460,17 @@ inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWo
     for (int m = 0; m < kMitmMaxM; ++m) st.offL[m] = st.offR[m] = 0;
     for (int k = 0; k < rmax; ++k) {
         if (!needL[k]) continue;
-        st.kind[st.n_tab] = 0; st.km[st.n_tab] = (int8_t)k; st.start[st.n_tab++] = (int64_t)e;
+        const int Pk = left_positions(W, rmax, k);
+        st.kind[st.n_tab] = 0; st.km[st.n_tab] = (int8_t)k; st.pos[st.n_tab] = (int8_t)Pk;
+        st.start[st.n_tab++] = (int64_t)e;
         for (int m = 1; m < rmax; ++m) if (mitm_j(m) - 1 == k) st.offL[m] = (int64_t)e;
-        e += binom128(W - k - 1, k);
+        e += binom128(Pk, k);
         if (e > ((unsigned __int128)1 << 36)) return false;
     }
     for (int m = 1; m < rmax; ++m) {
         if (!needR[m]) continue;
-        st.kind[st.n_tab] = 1; st.km[st.n_tab] = (int8_t)m; st.start[st.n_tab++] = (int64_t)e;
+        st.kind[st.n_tab] = 1; st.km[st.n_tab] = (int8_t)m; st.pos[st.n_tab] = (int8_t)(W - mitm_j(m));
+        st.start[st.n_tab++] = (int64_t)e;
         st.offR[m] = (int64_t)e;
         e += binom128(W - mitm_j(m), m - mitm_j(m));
         if (e > ((unsigned __int128)1 << 36)) return false;
@@ -555,7 +569,7 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
             const bool right = st.kind[ti];
             const int km = st.km[ti];
             const int k = right ? km - mitm_j(km) : km;               // cuts per entry
-            const int P = right ? W - mitm_j(km) : W - km - 1;        // positions
+            const int P = st.pos[ti];                                  // positions
             if (fresh) mk = (Mask)colex_unrank(x, k, P, e - st.start[ti]);
             else mk = (Mask)side_next((uint64_t)mk);
             double v = ninf;
