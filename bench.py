@@ -151,6 +151,9 @@ def run_b200(args, rank, world, local_rank):
 
     for _ in range(max(args.warmup, 3)):
         step()
+    # the sweep's kernels as one graph (tables resident in HBM).  Multi-GPU:
+    # the winner all-gather follows each sweep and the host waits for it, so
+    # NCCL's kernels never share the SMs with a running sweep
     kernels = engine.SweepGraph(batch, total, bufs=bufs, part=rank, nparts=world, copy_inputs=False)
     barrier()
     clocks = ClockSampler(local_rank)
@@ -161,10 +164,11 @@ def run_b200(args, rank, world, local_rank):
     ev0.record(stream)
     for s in range(args.steps):
         kev[s][0].record(stream)
-        kernels.launch()                  # the sweep's kernels, tables resident in HBM
+        kernels.launch()
         kev[s][1].record(stream)
         if world > 1:
             D.all_gather_winner(bufs.out)
+            stream.synchronize()
     ev1.record(stream)
     barrier()
     clk = clocks.stop() if rank == 0 else None
