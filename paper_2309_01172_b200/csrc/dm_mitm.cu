@@ -302,17 +302,6 @@ __device__ __forceinline__ int64_t block_min_i64(int64_t v, double* red) {
     return v;
 }
 
-__device__ __forceinline__ int block_sum_i32(int v, double* red) {
-    int* r = reinterpret_cast<int*>(red);
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
-    __syncthreads();
-    v = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) v += r[i];
-    return v;
-}
-
 // Cross product of NS register slots with the feasible Y values in shared
 // memory (pairs; the pad is +inf): one max and one checksum add per pair.
 template <int NS>
