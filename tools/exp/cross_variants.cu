@@ -32,6 +32,12 @@ __global__ void __launch_bounds__(256, CPS) k(int iters, uint64_t* sink) {
                 } else if (V == 2) {
                     const int xh = __double2hiint(xv[u]);
                     c32[u] += max(xh, __double2hiint(yy.x)) + max(xh, __double2hiint(yy.y));
+                } else if (V == 4) {           // lo words into a 64-bit sum (IMAD.WIDE, FMA pipe), hi words mod 2^32
+                    const double a = xv[u] > yy.x ? xv[u] : yy.x;
+                    const double b = xv[u] > yy.y ? xv[u] : yy.y;
+                    cs[u] += (uint64_t)(uint32_t)__double2loint(a);
+                    cs[u] += (uint64_t)(uint32_t)__double2loint(b);
+                    c32[u] += (uint32_t)__double2hiint(a) + (uint32_t)__double2hiint(b);
                 } else if (V == 3) {
                     const double a = fmax(xv[u], yy.x);
                     const double b = fmax(xv[u], yy.y);
@@ -63,6 +69,8 @@ void run(const char* name) {
 
 int main() {
     run<0, 2>("dsetp+fsel+sel+iadd3");
+    run<4, 2>("lo imad.wide + hi iadd3");
+    run<4, 2, 16>("lo imad.wide + hi iadd3");
     run<0, 4>("dsetp+fsel+sel+iadd3");
     run<0, 3, 4>("dsetp+fsel+sel+iadd3");
     run<0, 4, 4>("dsetp+fsel+sel+iadd3");
