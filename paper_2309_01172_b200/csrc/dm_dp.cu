@@ -16,6 +16,7 @@
 // n*n*p*2^p <= 3e6).
 #include "dm_common.cuh"
 #include "dm_abi_util.cuh"
+#include <cstdlib>
 
 namespace dm {
 
@@ -78,21 +79,18 @@ __global__ void __launch_bounds__(256) subset_dp_kernel(const dm_tables* __restr
             while (j <= n && fits_range(t, wi, i, j)) ++j;
             d.jlim[i * p + wi] = (int16_t)j;
         }
-        // ---- chunk_cost (:294-302): default link, edges with src < i only
-        for (int it = threadIdx.x; it < n * n; it += blockDim.x) {
-            int i = it / n, j = it % n + 1;
-            if (j <= i) continue;
-            double fl = col_range(t.flops, t.pre_flops, flops_exact(t), i, j, np_flops(t));
+        // ---- chunk_cost (:294-302): default link, edges with src < i only;
+        //      one thread per (i, wi), the read growing stage by stage in the
+        //      reference's (stage, edge) order
+        for (int it = threadIdx.x; it < n * p; it += blockDim.x) {
+            const int i = it / p, wi = it % p;
             double rd = 0.0;
-            if (include_comm(t)) {
-                for (int s = i; s < j; ++s)
-                    for (int e = t.edge_ptr[s]; e < t.edge_ptr[s + 1]; ++e)
+            for (int j = i + 1; j <= n; ++j) {
+                if (include_comm(t))
+                    for (int e = t.edge_ptr[j - 1]; e < t.edge_ptr[j]; ++e)
                         if (t.edge_src[e] < i) rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
-            }
-            double* row = d.cc + ((size_t)i * n1 + j) * p;
-            for (int wi = 0; wi < p; ++wi) {
-                double compute = fl / t.speed[wi];
-                row[wi] = compute + rd;
+                const double fl = col_range(t.flops, t.pre_flops, flops_exact(t), i, j, np_flops(t));
+                d.cc[((size_t)i * n1 + j) * p + wi] = fl / t.speed[wi] + rd;
             }
         }
         for (int64_t it = threadIdx.x; it < (int64_t)n1 * S; it += blockDim.x) d.back[it] = -1;
@@ -174,6 +172,167 @@ __global__ void __launch_bounds__(256) subset_dp_kernel(const dm_tables* __restr
     }
 }
 
+// ---- small fleets (2^p <= 32 masks): one WARP per scenario, lanes over the
+//      target masks of a level, __syncwarp between levels, every table in the
+//      warp's slice of shared memory.  Same pull-form key and finals as above.
+constexpr int kDpWarps = 4;
+
+// Per-warp shared memory: chunk costs, states, back pointers, break points,
+// then the instance columns the DP reads (staged once, so the table builds
+// run from shared memory instead of dependent global loads).
+__host__ __device__ inline size_t dpw_cols_bytes(int n, int p, int e_max) {
+    const size_t n1 = (size_t)n + 1;
+    return align_up(4 * n1 * 8) + align_up(4 * (size_t)n * 8) + align_up(n1 * 4) + align_up((size_t)e_max * 4) +
+           align_up((size_t)e_max * 8) + align_up(4 * (size_t)p * 8);
+}
+
+__host__ __device__ inline size_t dpw_bytes(int n, int p, int e_max) {
+    const size_t n1 = (size_t)n + 1, S = (size_t)1 << p;
+    return align_up((size_t)n * n1 / 2 * p * 8) + align_up(n1 * S * 8) + align_up(n1 * S * 4) + align_up(n1 * p * 2) +
+           dpw_cols_bytes(n, p, e_max);
+}
+
+// Copy the DP's columns of t into smem at b (warp-cooperative) and return a
+// dm_tables whose pointers refer to the copies.
+__device__ inline dm_tables dpw_stage(const dm_tables& t, unsigned char* b, int lane, int e_max) {
+    const int n = t.n, p = t.p, n1 = n + 1, E = t.n_edges;
+    dm_tables c = t;
+    int64_t* pre = reinterpret_cast<int64_t*>(b); b += align_up(4 * (size_t)n1 * 8);
+    double* col = reinterpret_cast<double*>(b); b += align_up(4 * (size_t)n * 8);
+    int32_t* eptr = reinterpret_cast<int32_t*>(b); b += align_up((size_t)n1 * 4);
+    int32_t* esrc = reinterpret_cast<int32_t*>(b); b += align_up((size_t)e_max * 4);
+    double* em = reinterpret_cast<double*>(b); b += align_up((size_t)e_max * 8);
+    double* peer = reinterpret_cast<double*>(b);
+    for (int i = lane; i < n1; i += 32) {
+        pre[i] = t.pre_flops[i]; pre[n1 + i] = t.pre_gpu[i]; pre[2 * n1 + i] = t.pre_cpu[i];
+        pre[3 * n1 + i] = t.pre_disk[i]; eptr[i] = t.edge_ptr[i];
+    }
+    for (int i = lane; i < n; i += 32) {
+        col[i] = t.flops[i]; col[n + i] = t.gpu[i]; col[2 * n + i] = t.cpu[i]; col[3 * n + i] = t.disk[i];
+    }
+    const bool stage_edges = E <= e_max;
+    if (stage_edges)
+        for (int e = lane; e < E; e += 32) { esrc[e] = t.edge_src[e]; em[e] = t.edge_m[e]; }
+    for (int w = lane; w < p; w += 32) {
+        peer[w] = t.speed[w]; peer[p + w] = t.cap_gpu[w]; peer[2 * p + w] = t.cap_cpu[w]; peer[3 * p + w] = t.cap_disk[w];
+    }
+    c.pre_flops = pre; c.pre_gpu = pre + n1; c.pre_cpu = pre + 2 * n1; c.pre_disk = pre + 3 * n1;
+    c.flops = col; c.gpu = col + n; c.cpu = col + 2 * n; c.disk = col + 3 * n;
+    c.edge_ptr = eptr;
+    if (stage_edges) { c.edge_src = esrc; c.edge_m = em; }
+    c.speed = peer; c.cap_gpu = peer + p; c.cap_cpu = peer + 2 * p; c.cap_disk = peer + 3 * p;
+    return c;
+}
+
+__device__ __forceinline__ int dpw_pair(int i, int j, int n) { return i * n - i * (i - 1) / 2 + (j - i - 1); }
+
+__global__ void __launch_bounds__(32 * kDpWarps) subset_dp_warp_kernel(const dm_tables* __restrict__ tables,
+                                                                       int32_t n_scen, int32_t n_max,
+                                                                       int32_t p_max, int32_t e_max,
+                                                                       int16_t* out_owner, double* out_mk,
+                                                                       int32_t* out_found) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    unsigned char* base = dsm + (size_t)wl * dpw_bytes(n_max, p_max, e_max);
+    for (int sc = blockIdx.x * kDpWarps + wl; sc < n_scen; sc += gridDim.x * kDpWarps) {
+        const dm_tables tg = tables[sc];
+        const int n = tg.n, p = tg.p, S = 1 << p, n1 = n + 1;
+        unsigned char* b = base;
+        double* cc = reinterpret_cast<double*>(b); b += align_up((size_t)n * n1 / 2 * p * 8);
+        double* mk = reinterpret_cast<double*>(b); b += align_up((size_t)n1 * S * 8);
+        int32_t* back = reinterpret_cast<int32_t*>(b); b += align_up((size_t)n1 * S * 4);
+        int16_t* jlim = reinterpret_cast<int16_t*>(b); b += align_up((size_t)n1 * p * 2);
+        __syncwarp();
+        const dm_tables t = dpw_stage(tg, b, lane, e_max);
+        __syncwarp();
+        for (int it = lane; it < n * p; it += 32) {             // _fits break points (:313-315)
+            const int i = it / p, wi = it % p;
+            int j = i + 1;
+            while (j <= n && fits_range(t, wi, i, j)) ++j;
+            jlim[i * p + wi] = (int16_t)j;
+        }
+        for (int i = lane; i < n; i += 32) {                   // chunk_cost (:294-302), lanes over i:
+            double rd = 0.0;                                    // the read grows stage by stage, in the
+            for (int j = i + 1; j <= n; ++j) {                  // reference's (stage, edge) order
+                if (include_comm(t))
+                    for (int e = t.edge_ptr[j - 1]; e < t.edge_ptr[j]; ++e)
+                        if (t.edge_src[e] < i) rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
+                const double fl = col_range(t.flops, t.pre_flops, flops_exact(t), i, j, np_flops(t));
+                double* row = cc + (size_t)dpw_pair(i, j, n) * p;
+                for (int wi = 0; wi < p; ++wi) row[wi] = fl / t.speed[wi] + rd;
+            }
+        }
+        for (int it = lane; it < n1 * S; it += 32) back[it] = -1;
+        __syncwarp();
+        if (lane == 0) { mk[0] = 0.0; back[0] = 0; }
+        __syncwarp();
+        // levels: lane = (target mask M, source-prefix class g); lanes of one M
+        // split the prefixes i (i = g mod G) and combine by shuffles
+        const int G = 32 / S;                                   // lanes per target mask (S <= 32)
+        const int M = lane & (S - 1), g = lane / S;
+        const int pc = __popc(M);
+        for (int j = 1; j <= n; ++j) {
+            double bv = 0.0;
+            int bsec = 0x7fffffff, bsrc = -1;
+            if (pc >= 1 && pc <= j) {
+                for (int i = g; i < j; i += G) {
+                    const double* crow = cc + (size_t)dpw_pair(i, j, n) * p;
+                    for (uint32_t mm = (uint32_t)M; mm; mm &= mm - 1) {
+                        const int wi = __ffs(mm) - 1;
+                        const int src = i * S + (M ^ (1 << wi));
+                        const int32_t bk = back[src];          // all loads first: one round trip
+                        const int jl = jlim[i * p + wi];
+                        const double m0 = mk[src], c = crow[wi];
+                        const double v = c > m0 ? c : m0;      // max(mk, chunk_cost) :316
+                        const int sec = i * 64 + (63 - wi);
+                        if (bk >= 0 && j < jl && (bsrc < 0 || key_less(v, sec, bv, bsec))) {
+                            bv = v; bsec = sec; bsrc = (i << 8) | wi;
+                        }
+                    }
+                }
+            }
+            for (int off = S; off < 32; off <<= 1) {           // combine the G lanes of this M
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int osec = __shfl_xor_sync(0xffffffffu, bsec, off);
+                const int osrc = __shfl_xor_sync(0xffffffffu, bsrc, off);
+                if (osrc >= 0 && (bsrc < 0 || key_less(ov, osec, bv, bsec))) { bv = ov; bsec = osec; bsrc = osrc; }
+            }
+            if (g == 0 && bsrc >= 0) { mk[j * S + M] = bv; back[j * S + M] = bsrc; }
+            __syncwarp();
+        }
+        // finals: smallest (makespan, mask) among states with j == n (:321-325)
+        double bv = 0.0;
+        long long bm = -1;
+        if (lane < S && back[n * S + lane] >= 0) { bv = mk[n * S + lane]; bm = lane; }
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ov = __shfl_down_sync(0xffffffffu, bv, off);
+            const long long om = __shfl_down_sync(0xffffffffu, bm, off);
+            if (om >= 0 && (bm < 0 || ov < bv || (ov == bv && om < bm))) { bv = ov; bm = om; }
+        }
+        int16_t* own = out_owner + (size_t)sc * n_max;
+        for (int i = lane; i < n_max; i += 32) own[i] = -1;
+        __syncwarp();
+        if (lane == 0) {
+            if (bm >= 0) {
+                int j = n;
+                int M = (int)bm;
+                while (j > 0) {
+                    const int32_t bb = back[j * S + M];
+                    const int i = bb >> 8, wi = bb & 0xff;
+                    for (int s2 = i; s2 < j; ++s2) own[s2] = (int16_t)wi;
+                    M &= ~(1 << wi);
+                    j = i;
+                }
+                out_mk[sc] = bv;
+                out_found[sc] = 1;
+            } else {
+                out_mk[sc] = __longlong_as_double(0x7ff0000000000000LL);
+                out_found[sc] = 0;
+            }
+        }
+    }
+}
+
 }  // namespace dm
 
 extern "C" {
@@ -194,6 +353,24 @@ int dm_subset_dp(const dm_tables* tables, int32_t n_scen, int32_t n_max, int32_t
         return dmabi::fail(DM_E_ARG, "dm_subset_dp: bad arguments");
     if (p_max > 24) return dmabi::fail(DM_E_TOO_LARGE, "dm_subset_dp: at most 24 workers");
     if (n_scen == 0) return DM_OK;
+    {   // small fleets: one warp per scenario
+        const int e_max = 4 * n_max;      // staged edge capacity (larger DAGs read edges from global)
+        const size_t per_cta = dm::dpw_bytes(n_max, p_max, e_max) * dm::kDpWarps;
+        const char* dis = std::getenv("DM_DISABLE_DP_WARP");
+        if (p_max <= 5 && per_cta <= 100 * 1024 && !(dis && dis[0] && dis[0] != '0')) {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            int64_t grid = (n_scen + dm::kDpWarps - 1) / dm::kDpWarps;
+            const int per_sm = (int)((220 * 1024) / (per_cta + 1024));
+            if (grid > (int64_t)sms * per_sm * 4) grid = (int64_t)sms * per_sm * 4;
+            cudaFuncSetAttribute(dm::subset_dp_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_cta);
+            dm::subset_dp_warp_kernel<<<(int)grid, 32 * dm::kDpWarps, per_cta, (cudaStream_t)stream>>>(
+                tables, n_scen, n_max, p_max, e_max, out_owner, out_makespan, out_found);
+            DM_CHECK_LAUNCH();
+            return DM_OK;
+        }
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
