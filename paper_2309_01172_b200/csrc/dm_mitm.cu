@@ -46,7 +46,7 @@ namespace dm {
 
 #ifdef DM_MITM_TIMING
 // phase timestamps of every CTA (globaltimer ns): debug builds only
-__device__ unsigned long long g_mitm_times[1024][8];
+__device__ unsigned long long g_mitm_times[1024][12];
 #define MITM_MARK(i)                                                                               \
     do {                                                                                           \
         if (threadIdx.x == 0) {                                                                    \
@@ -56,7 +56,13 @@ __device__ unsigned long long g_mitm_times[1024][8];
         }                                                                                          \
     } while (0)
 #define MITM_COUNT(i, v) atomicAdd(&g_mitm_times[blockIdx.x][i], (unsigned long long)(v))
+// thread 0's clock in each phase of a tile: [6] elements + barrier, [7] cross
+// product, [8] winner check + end barrier, [9] tiles, [10] thin tiles
+#define MITM_CLK(v) long long v = clock64()
+#define MITM_ACC(i, a, b) do { if (threadIdx.x == 0) g_mitm_times[blockIdx.x][i] += (unsigned long long)((b) - (a)); } while (0)
 #else
+#define MITM_CLK(v) do { } while (0)
+#define MITM_ACC(i, a, b) do { } while (0)
 #define MITM_MARK(i) do { } while (0)
 #define MITM_COUNT(i, v) do { } while (0)
 #endif
@@ -532,7 +538,10 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
             if (lane + 64 < R1) binom_s[a * R1 + lane + 64] = v2;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        counter[0] = 0;                                                          // tile queue
+        reinterpret_cast<unsigned long long*>(counter)[1] = 0x7ff0000000000000ull;   // shared incumbent (+inf)
+    }
     __syncthreads();
     const MitmCtx x{n, W, 0, R1, binom_s, nullptr};
     auto T = [&](int q, int a, int b) { return __ldg(timg + rowrel[q * n + a] + b); };
@@ -662,7 +671,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 
     MITM_MARK(0);
 #ifdef DM_MITM_TIMING
-    if (threadIdx.x == 0) { g_mitm_times[blockIdx.x][4] = 0; g_mitm_times[blockIdx.x][5] = 0; }
+    if (threadIdx.x == 0) for (int i_ = 4; i_ < 12; ++i_) g_mitm_times[blockIdx.x][i_] = 0;
 #endif
     memo_load(L.M, timg, sm);
     MITM_MARK(1);
@@ -724,6 +733,11 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         if (lane == 0) tstart[0] = 0;
     }
     if (threadIdx.x == 0) s_g[0] = atomicAdd(ctl, 1);   // dynamic tile queue over the part's blocks
+    // the best makespan any CTA of the sweep has found so far (bits of a
+    // non-negative double): tiles whose minimum exceeds it skip the rank
+    // derivation.  Stale reads only make the test more permissive.
+    unsigned long long* gbest = reinterpret_cast<unsigned long long*>(ctl) + 1;
+    unsigned long long gb = 0x7ff0000000000000ull;
     __syncthreads();
     const int n_tiles = tstart[nbp];
     MITM_MARK(2);
@@ -738,7 +752,11 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     for (int par = 0;; par ^= 1) {
         const int g = s_g[par];
         if (g >= n_tiles) break;           // uniform
-        if (threadIdx.x == 0) s_g[par ^ 1] = atomicAdd(ctl, 1);   // read after the end barrier
+        MITM_CLK(c_t0);
+        if (threadIdx.x == 0) {
+            s_g[par ^ 1] = atomicAdd(ctl, 1);   // read after the end barrier
+            gb = *reinterpret_cast<volatile unsigned long long*>(gbest);
+        }
         int lo = 0, hi = nbp - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -775,6 +793,9 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             }
             if (ymin <= best) atomicOr(&s_flag[par], 2);
             __syncthreads();
+            MITM_CLK(c_t1);
+            MITM_ACC(6, c_t0, c_t1);
+            MITM_ACC(10, 0, 1);
             nyf = s_cnt[par][1];
             const bool yb_ok = s_flag[par] & 2;
             if (threadIdx.x == 0) {
@@ -833,6 +854,8 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 }
             }
             w.n_feas += nxf_all * nyf;
+            MITM_CLK(c_t2);
+            MITM_ACC(7, c_t1, c_t2);
             maybe_best = __syncthreads_or(xmin <= best) && yb_ok && nyf > 0;
         } else {
             // ---- both sides' feasible elements, compacted into shared memory;
@@ -867,6 +890,8 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             const int fl = (xmin <= best ? 1 : 0) | (ymin <= best ? 2 : 0);
             if (fl) atomicOr(&s_flag[par], fl);
             __syncthreads();
+            MITM_CLK(c_t1);
+            MITM_ACC(6, c_t0, c_t1);
             const int nxf_tot = s_cnt[par][0];
             nyf = s_cnt[par][1];
             maybe_best = s_flag[par] == 3;
@@ -900,6 +925,8 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 corr += (uint64_t)(nsl - nxf) * (uint64_t)nyf;
                 MITM_COUNT(4, nsl * nyf);
             }
+            MITM_CLK(c_t2);
+            MITM_ACC(7, c_t1, c_t2);
             maybe_best = maybe_best && nxf_tot > 0 && nyf > 0;
         }
         // ---- rare: the tile can hold the incumbent. Its minimum is
@@ -929,10 +956,15 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                     w.mk = tm;
                     w.rank = rx + ry;
                     s_best = tm;
+                    atomicMin(gbest, (unsigned long long)__double_as_longlong(tm));
                 }
             }
         }
+        if (threadIdx.x == 0 && __longlong_as_double((long long)gb) < s_best) s_best = __longlong_as_double((long long)gb);
         __syncthreads();   // buffers, counters and s_best for the next tile
+        MITM_CLK(c_t3);
+        MITM_ACC(8, c_t0, c_t3);
+        MITM_ACC(9, 0, 1);
     }
     uint64_t c = 0;
 #pragma unroll

@@ -67,7 +67,13 @@ void run(const char* name) {
     printf("%-28s CPS=%d NR=%d %.3e pairs/s\n", name, CPS, NR, pairs / (ms / 1e3));
 }
 
-int main() {
+int main(int argc, char**) {
+    if (argc > 1) {   // slot-count sweep of the production formulation
+        run<0, 2, 1>("ns sweep"); run<0, 2, 2>("ns sweep"); run<0, 2, 3>("ns sweep");
+        run<0, 2, 4>("ns sweep"); run<0, 2, 5>("ns sweep"); run<0, 2, 6>("ns sweep");
+        run<0, 2, 8>("ns sweep"); run<0, 2, 12>("ns sweep"); run<0, 2, 16>("ns sweep");
+        return 0;
+    }
     run<0, 2>("dsetp+fsel+sel+iadd3");
     run<4, 2>("lo imad.wide + hi iadd3");
     run<4, 2, 16>("lo imad.wide + hi iadd3");

@@ -22,9 +22,9 @@ for _ in range(3):
     engine.enum(batch, "splits", 0, total, bufs)
 torch.cuda.synchronize()
 lib = _lib.load()
-buf = (C.c_ulonglong * (1024 * 8))()
+buf = (C.c_ulonglong * (1024 * 12))()
 lib.dm_debug_mitm_times(buf)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 12).astype(np.int64)
 a = a[a[:, 0] > 0]
 a[:, 4:6] = a[:, 4:6]
 t0 = a[:, 0].min()
@@ -34,3 +34,7 @@ for i, nm in enumerate(names):
     print(f"{nm:12s} min {d.min():8.1f} med {statistics.median(d):8.1f} max {d.max():8.1f} us")
 print(f"pairs processed: normal tiles {a[:, 4].sum():.4g}, thin tiles {a[:, 5].sum():.4g}")
 print(f"sweep kernel (first start -> last end) {(a[:, 3].max() - t0) / 1e3:.1f} us; CTAs {len(a)}")
+tot = a[:, 8].astype(float)
+print(f"clock share (thread 0): elements+barrier {a[:, 6].sum() / tot.sum():.3f}  cross {a[:, 7].sum() / tot.sum():.3f}  "
+      f"rest {(tot.sum() - a[:, 6].sum() - a[:, 7].sum()) / tot.sum():.3f}")
+print(f"tiles {a[:, 9].sum()} (thin {a[:, 10].sum()}), per CTA min {a[:, 9].min()} max {a[:, 9].max()}")
