@@ -6,8 +6,11 @@ Llama-2-7B training workflow (34 layer cells) over a 32-device heterogeneous
 fleet, EXHAUSTIVE split sweep: all 8,589,934,558 contiguous splits with run q
 on worker q, each scored with the reference cost model (fits + compute +
 crossing read, makespan) and reduced to the first strict minimum by
-(makespan, rank).  One step = one full sweep over the whole population,
-sharded across the ranks (strong scaling), plus one NCCL all-gather of the
+(makespan, rank).  One step = the full sweep of that fleet under each of 8
+default-link settings (configs.C2_LINKS, the base 5 ms / 10 Gbit/s first):
+8 x 8.59e9 candidates.  The 8 scenarios are sharded across the ranks (whole
+scenarios per GPU, strong scaling; block-level parts of every scenario when
+8 is not a multiple of the GPU count), plus one NCCL all-gather of the
 per-rank winner records.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
@@ -53,16 +56,33 @@ def c2_instance():
     return stages, fleet
 
 
-def workload_config(total):
-    return {"workload": "C2 llama2-7b (34 layer cells) x 32 heterogeneous workers, exhaustive split sweep",
-            "candidates_per_step": total, "stages": 34, "workers": 32,
+def c2_scenarios():
+    """The C2 model and its fleet under every C2_LINKS default link."""
+    from paper_2309_01172_b200 import configs as CF
+    stages = CF.model_stages("llama2-7b-layers")
+    return stages, [CF.load(CF.c2_fleet_doc(0, a, bw)) for a, bw in CF.C2_LINKS], list(CF.C2_LINKS)
+
+
+def units_for(rank, world, n_scen):
+    """(scenario, part, nparts) units of `rank`: whole scenarios when the
+    batch divides evenly, else every scenario split into `world` parts."""
+    if n_scen % world == 0:
+        return [(s, 0, 1) for s in range(rank, n_scen, world)]
+    return [(s, rank, world) for s in range(n_scen)]
+
+
+def workload_config(total, links):
+    return {"workload": "C2 llama2-7b (34 layer cells) x 32 heterogeneous workers, exhaustive split sweep under "
+                        f"{len(links)} default-link settings per step",
+            "candidates_per_step": total * len(links), "candidates_per_scenario": total, "scenarios": len(links),
+            "default_links_s_gbps": [list(x) for x in links], "stages": 34, "workers": 32,
             "candidate_source": "generated on chip: splits grouped by (cut count, middle-cut position) as cross "
                                 "products of left x right cut sets; each feasible candidate's makespan = "
                                 "max(L, R) folded into the checksum, infeasible ones resolved per side element",
-            "l2_policy": "no HBM-resident candidate stream; the per-sweep side tables (134 MB) exceed L2 and are "
+            "l2_policy": "no HBM-resident candidate stream; each scenario's side tables (134 MB) exceed L2 and are "
                          "rebuilt every step",
-            "parallelism": "whole blocks per GPU (each builds the side tables of its blocks) + 1 NCCL all-gather "
-                           "of 40-byte winner records"}
+            "parallelism": "whole scenarios per GPU (block-level parts when the batch does not divide) + 1 NCCL "
+                           "all-gather of 40-byte winner records"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -120,6 +140,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------- b200 arm
 def run_b200(args, rank, world, local_rank):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -130,31 +151,40 @@ def run_b200(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream()
-    stages, fleet = c2_instance()
-    n, p = len(stages), len(fleet.worker_ids())
+    stages, fleets, links = c2_scenarios()
+    S = len(fleets)
+    n, p = len(stages), len(fleets[0].worker_ids())
     total = engine.splits_total(n, p)
-    k0, k1 = 0, total            # every rank owns the rank tasks == rank (mod world)
-    host = build_host(stages, fleet, True)
-    batch = engine.device_batch([host], device=dev)
-    bufs = engine.WinnerBuffers(dev)
+    batch = engine.device_batch([build_host(stages, f, True) for f in fleets], device=dev)
+    units = units_for(rank, world, S)
 
-    def step():
-        engine.enum(batch, "splits", k0, k1, bufs, part=rank, nparts=world)
-        if world > 1:
-            return D.all_gather_winner(bufs.out)
-        return bufs.out
+    def gather(out):
+        """device records [units, 40] of every rank -> [world, units, 40]"""
+        if world == 1:
+            return out.view(1, len(units), -1)
+        g = torch.empty(world * out.numel(), dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(g, out.reshape(-1))
+        return g.view(world, len(units), -1)
+
+    def merge(raw):
+        per = [[] for _ in range(S)]
+        for r in range(world):
+            for i, (sc, _, _) in enumerate(units_for(r, world, S)):
+                per[sc].append(raw[r, i])
+        return [D.merge_records(np.stack(rows)) for rows in per]
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    # the sweep's kernels as one graph (tables resident in HBM).  Multi-GPU:
-    # the winner all-gather follows each sweep and the host waits for it, so
+    # the sweeps' kernels as one graph (tables resident in HBM).  Multi-GPU:
+    # the winner all-gather follows each step and the host waits for it, so
     # NCCL's kernels never share the SMs with a running sweep
-    kernels = engine.SweepGraph(batch, total, bufs=bufs, part=rank, nparts=world, copy_inputs=False)
+    kernels = engine.SweepGraph(batch, total, units=units, copy_inputs=False)
+    for _ in range(max(args.warmup, 3)):
+        kernels.launch()
+        gather(kernels.out)
     barrier()
     clocks = ClockSampler(local_rank)
     if rank == 0:
@@ -167,7 +197,7 @@ def run_b200(args, rank, world, local_rank):
         kernels.launch()
         kev[s][1].record(stream)
         if world > 1:
-            D.all_gather_winner(bufs.out)
+            gather(kernels.out)
             stream.synchronize()
     ev1.record(stream)
     barrier()
@@ -178,26 +208,25 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, kernel_ms = float(t[0]), float(t[1])
-    res = D.merge_records(step().cpu().numpy()) if world > 1 else bufs.read()
+    res = merge(gather(kernels.out).cpu().numpy())
 
-    # ---- e2e: the engine's serving form of the sweep (engine.SweepGraph: one
-    #      CUDA graph with the H2D copy of the instance tables from pinned
-    #      host memory, the sweep's kernels and the D2H of the winner record),
-    #      host synchronisation and the winner read every step
-    sweep = engine.SweepGraph(batch, total, bufs=engine.WinnerBuffers(dev), part=rank, nparts=world)
+    # ---- e2e: the engine's serving form (engine.SweepGraph: one CUDA graph
+    #      with the H2D copy of the scenario tables from pinned host memory,
+    #      the sweeps' kernels and the D2H of the winner records), host
+    #      synchronisation and the winners read every step
+    sweep = engine.SweepGraph(batch, total, units=units)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    pinned_out = torch.empty(bufs.out.numel() * world, dtype=torch.uint8, pin_memory=True)
+    pinned_out = torch.empty(world * len(units) * D.WINNER_BYTES, dtype=torch.uint8, pin_memory=True)
     e0.record(stream)
     for _ in range(args.steps):
         sweep.launch()
         if world > 1:
-            out = D.all_gather_winner(sweep.bufs.out).view(-1)
-            pinned_out.copy_(out, non_blocking=True)
+            pinned_out.copy_(gather(sweep.out).view(-1), non_blocking=True)
             stream.synchronize()
-            D.merge_records(pinned_out.numpy())
+            merge(pinned_out.numpy().reshape(world, len(units), -1))
         else:
-            sweep.read()
+            sweep.read_all()
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1)
@@ -205,10 +234,15 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te[0])
+    e2e_d2h = (world if world > 1 else 1) * len(units) * D.WINNER_BYTES
 
-    # the dominant kernel's own duration on every rank: CUDA events the library
-    # records around its launches (separate pass after the timed region)
-    tab_ms, sweep_ms = engine.sweep_kernel_times(batch, total, steps=args.steps, bufs=bufs, part=rank, nparts=world)
+    # the dominant kernel's own duration on every rank (its first unit): CUDA
+    # events the library records around its launches, in a separate pass
+    u0 = units[0]
+    kb = kernels.unit_bufs[0]
+    tab_ms, sweep_ms = engine.sweep_kernel_times(batch, total, steps=args.steps, bufs=kb, part=u0[1],
+                                                 nparts=u0[2], index=u0[0])
+    feas0 = kb.read()["n_feasible"]
     per_rank = torch.tensor([tab_ms, sweep_ms], dtype=torch.float64, device=dev)
     if world > 1:
         gathered = torch.empty(2 * world, dtype=torch.float64, device=dev)
@@ -220,19 +254,22 @@ def run_b200(args, rank, world, local_rank):
         extras = secondary_measurements(dev)
     if rank != 0:
         return None
-    value = total * args.steps / (ms / 1e3)
-    e2e_val = total * args.steps / (e2e_ms / 1e3)
+    value = S * total * args.steps / (ms / 1e3)
+    e2e_val = S * total * args.steps / (e2e_ms / 1e3)
     cross = extras.get("cross_peak_pairs_per_s")
-    achieved = res["n_feasible"] / world / (sweep_ms / 1e3) / 1e9      # per GPU
+    achieved = feas0 / (sweep_ms / 1e3) / 1e9      # one launch of the dominant kernel
     traffic = ncu_traffic("splits_sweep_kernel") or {}
+    csum = 0
+    for r in res:
+        csum = (csum + r["checksum"]) & ((1 << 64) - 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(total),
+        "config": workload_config(total, links),
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(batch.h2d_bytes),
-                "d2h_bytes_per_step": int(D.WINNER_BYTES * world)},
-        "gpu_launches": 4 * args.steps,
+                "d2h_bytes_per_step": int(e2e_d2h)},
+        "gpu_launches": 4 * len(units) * args.steps,
         "roofline": {"bound": "issue", "achieved": achieved, "peak": (cross / 1e9) if cross else None,
                      "unit": "Gcand/s", "frac": (achieved / (cross / 1e9)) if cross else None,
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("capture"),
@@ -241,12 +278,14 @@ def run_b200(args, rank, world, local_rank):
                      "step_kernels_ms": kernel_ms,
                      "algorithmic_work_per_candidate": "one fp64 max (DSETP + 64-bit select) and one 64-bit "
                                                        "checksum add per feasible candidate",
-                     "note": "feasible candidates per second of splits_sweep_kernel vs dm_microbench_cross (the "
-                             "same inner loop alone, same grid and occupancy: the ALU-pipe/issue bound); "
-                             "infeasible candidates are resolved per side element (an unfit run), as the "
-                             "reference's `continue` skips them; table_phase_ms = T image + side tables"},
-        "winner": {"makespan": res["makespan"], "rank": res["rank"], "n_feasible": res["n_feasible"],
-                   "checksum": res["checksum"]},
+                     "note": "feasible candidates per second of one splits_sweep_kernel launch (rank 0's first "
+                             "unit) vs dm_microbench_cross (the same inner loop alone, same grid and occupancy: "
+                             "the ALU-pipe/issue bound); infeasible candidates are resolved per side element (an "
+                             "unfit run), as the reference's `continue` skips them; table_phase_ms = T image + "
+                             "side tables of that unit"},
+        "winner": {"per_scenario": [[r["makespan"], r["rank"]] for r in res],
+                   "n_feasible": sum(r["n_feasible"] for r in res), "n_evaluated": sum(r["n_evaluated"] for r in res),
+                   "checksum_sum": csum},
     }
     if clk:
         line["clocks"] = clk
@@ -577,7 +616,7 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(8589934558),
+            "config": workload_config(8589934558, c2_scenarios()[2]),
             "cpu_baseline": {"value": base["value"], "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": base["sample"]},
             "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

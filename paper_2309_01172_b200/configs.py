@@ -161,9 +161,16 @@ def hetero_peers(p: int, seed: int, kinds=("rtx4090", "rtx4080", "rtx3080", "a10
     return [{"id": str(start_id + i), "gpu": kinds[int(gi[i])], "lambda": float(lm[i])} for i in range(p)]
 
 
-def c2_fleet_doc(seed: int = 0):
+def c2_fleet_doc(seed: int = 0, alpha_s: float = 5e-3, bandwidth_gbps: float = 10.0):
     """32 heterogeneous workers, default link 5 ms / 10 Gbit/s."""
-    return fleet_doc(hetero_peers(32, seed), 5e-3, 10.0, name="c2-hetero32")
+    return fleet_doc(hetero_peers(32, seed), alpha_s, bandwidth_gbps, name="c2-hetero32")
+
+
+# The C2 fleet under 8 network conditions (default-link latency s, bandwidth
+# Gbit/s): the base 5 ms / 10 Gbit/s first, then a what-if grid.  The bench's
+# step sweeps all 8 (one scenario batch, sharded across the GPUs).
+C2_LINKS = ((5e-3, 10.0), (1e-3, 10.0), (5e-3, 1.0), (1e-3, 1.0),
+            (5e-3, 25.0), (1e-3, 25.0), (5e-3, 100.0), (1e-3, 100.0))
 
 
 def c3_fleet_doc(seed: int = 0, p: int = 256):

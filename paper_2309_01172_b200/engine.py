@@ -274,28 +274,36 @@ def cross_peak(iters: int = 400, repeats: int = 3) -> float:
 
 
 class SweepGraph:
-    """A whole-population split sweep of one instance captured as a CUDA
-    graph (the serving form of `enum(batch, "splits", 0, total)`): the H2D
-    copy of the instance tables from pinned host memory, the sweep's kernels
-    and — single GPU — the D2H copy of the winner record into pinned host
-    memory.  `launch()` replays it on the current stream; `read()` waits and
-    returns the winner.  For a multi-GPU part (nparts > 1) the record stays
-    on the device (`bufs.out`) for the caller's all-gather.  copy_inputs=False
-    captures the kernels alone (tables already resident, record left in
-    `bufs.out`)."""
+    """Whole-population split sweeps captured as one CUDA graph (the serving
+    form of `enum(batch, "splits", 0, total)`): the H2D copy of the instance
+    tables from pinned host memory, the sweep kernels of every unit and — when
+    every unit is a whole population — the D2H copy of the winner records into
+    pinned host memory.  A unit is (instance index, part, nparts); the default
+    is the single unit (0, part, nparts).  `launch()` replays the graph on the
+    current stream; `read()` waits and returns the first unit's winner,
+    `read_all()` every unit's.  `out` holds the units' device records
+    (uint8[units, 40]) for a multi-GPU all-gather.  copy_inputs=False captures
+    the kernels alone (tables already resident, records left in `out`)."""
 
     def __init__(self, batch: DeviceBatch, total: int, bufs: WinnerBuffers | None = None, part: int = 0,
-                 nparts: int = 1, copy_inputs: bool = True):
+                 nparts: int = 1, copy_inputs: bool = True, units=None):
         torch = _torch()
         lib = _lib.load()
-        self.batch, self.total, self.part, self.nparts = batch, total, part, nparts
+        self.batch, self.total = batch, total
+        self.units = [tuple(u) for u in units] if units is not None else [(0, part, nparts)]
         self.copy_inputs = copy_inputs
-        self.bufs = bufs or WinnerBuffers(batch.dev_buf.device)
-        self.bufs.workspace_for(int(lib.dm_splits_workspace_bytes(C.byref(batch.struct(0)))))
-        self.host_out = torch.empty(_WINNER_BYTES, dtype=torch.uint8, pin_memory=True)
+        dev = batch.dev_buf.device
+        self.unit_bufs = [bufs if (i == 0 and bufs is not None) else WinnerBuffers(dev)
+                          for i in range(len(self.units))]
+        for (idx, _, _), ub in zip(self.units, self.unit_bufs):
+            ub.workspace_for(int(lib.dm_splits_workspace_bytes(C.byref(batch.struct(idx)))))
+        self.bufs = self.unit_bufs[0]
+        self.whole = all(u[2] == 1 for u in self.units)
+        self.out = torch.empty((len(self.units), _WINNER_BYTES), dtype=torch.uint8, device=dev)
+        self.host_out = torch.empty((len(self.units), _WINNER_BYTES), dtype=torch.uint8, pin_memory=True)
         self.h2d_bytes = int(batch.h2d_bytes) if copy_inputs else 0
-        self.d2h_bytes = _WINNER_BYTES if nparts == 1 and copy_inputs else 0
-        side = torch.cuda.Stream(device=batch.dev_buf.device)
+        self.d2h_bytes = _WINNER_BYTES * len(self.units) if self.whole and copy_inputs else 0
+        side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):          # warm the plan cache and the kernels' attributes
             self._body()
@@ -310,22 +318,31 @@ class SweepGraph:
         if self.copy_inputs:
             b.dev_buf.copy_(b.host_buf, non_blocking=True)
             b.structs_dev.copy_(b.records_host, non_blocking=True)
-        enum(b, "splits", 0, self.total, self.bufs, part=self.part, nparts=self.nparts)
-        if self.nparts == 1 and self.copy_inputs:
-            self.host_out.copy_(self.bufs.out, non_blocking=True)
+        for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
+            enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts)
+            self.out[i].copy_(ub.out, non_blocking=True)
+        if self.whole and self.copy_inputs:
+            self.host_out.copy_(self.out, non_blocking=True)
 
     def launch(self):
         self.graph.replay()
 
-    def read(self) -> dict:
+    def read_all(self) -> list:
         _torch().cuda.current_stream().synchronize()
-        w = _lib.DmWinner.from_buffer_copy(self.host_out.numpy().tobytes())
-        return dict(makespan=w.makespan, rank=w.rank, n_evaluated=w.n_evaluated,
-                    n_feasible=w.n_feasible, checksum=w.checksum)
+        raw = self.host_out.numpy().tobytes()
+        res = []
+        for i in range(len(self.units)):
+            w = _lib.DmWinner.from_buffer_copy(raw[i * _WINNER_BYTES:(i + 1) * _WINNER_BYTES])
+            res.append(dict(makespan=w.makespan, rank=w.rank, n_evaluated=w.n_evaluated,
+                            n_feasible=w.n_feasible, checksum=w.checksum))
+        return res
+
+    def read(self) -> dict:
+        return self.read_all()[0]
 
 
 def sweep_kernel_times(batch: DeviceBatch, total: int, steps: int = 5, bufs: WinnerBuffers | None = None,
-                       part: int = 0, nparts: int = 1) -> tuple:
+                       part: int = 0, nparts: int = 1, index: int = 0) -> tuple:
     """Average (table phase ms, sweep kernel ms) of `steps` whole-population
     split sweeps, from CUDA events the library records around its kernels."""
     lib = _lib.load()
@@ -334,7 +351,7 @@ def sweep_kernel_times(batch: DeviceBatch, total: int, steps: int = 5, bufs: Win
     ta = tb = 0.0
     try:
         for _ in range(steps):
-            enum(batch, "splits", 0, total, bufs, part=part, nparts=nparts)
+            enum(batch, "splits", 0, total, bufs, index=index, part=part, nparts=nparts)
             a, b = C.c_float(0), C.c_float(0)
             _lib.check(lib.dm_sweep_timing(-1, C.byref(a), C.byref(b)))
             ta += a.value

@@ -152,3 +152,19 @@ def test_report_assembly_types_golden():
         n += 1
         n_np += "float64" in json.dumps(want["types"])
     assert n > 250 and n_np > 200
+
+
+def test_bench_scenario_units_cover_every_scenario_once():
+    """bench.units_for: every (scenario, part) of the batch is owned by exactly
+    one rank, for any GPU count, and every rank holds the same number of units
+    (the winner all-gather's fixed record count)."""
+    import bench
+    for n_scen in (1, 3, 8):
+        for world in range(1, 9):
+            owned = [bench.units_for(r, world, n_scen) for r in range(world)]
+            assert len({len(u) for u in owned}) == 1
+            flat = [u for us in owned for u in us]
+            assert len(flat) == len(set(flat))
+            for s in range(n_scen):
+                parts = sorted((p, k) for (sc, p, k) in flat if sc == s)
+                assert parts and [p for p, _ in parts] == list(range(parts[0][1]))
