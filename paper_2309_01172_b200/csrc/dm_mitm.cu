@@ -93,13 +93,14 @@ __host__ __device__ inline int memo_row(int q, int a, int n) {
     return base + (a - q) * n - ((a - q) * (a + q - 1)) / 2 - (a + 1);
 }
 
-// Shared memory of the sweep: the memo tables, the block plan (mbase[m], per
-// block m and c, size-order position -> block, tile prefix tstart), the
-// compacted X and Y values, reduction space.
+// Shared memory of the sweep: binomials and cum (the rank terms), the block
+// plan (mbase[m], per block m and c, size-order position -> block, tile
+// prefix tstart), the compacted X and Y values, reduction space.  The run
+// costs T stay in the global image (57 KB for n = 34, L1-resident).
 struct MitmLayout {
-    MemoLayout M;
+    MemoLayout M;      // sizes of the T image (rmax, t_elems); its shared offsets are not used
     int n_blocks;
-    size_t off_mbase, off_bm, off_bc, off_pos, off_tstart, off_bx, off_by, off_red, bytes;
+    size_t off_binom, off_cum, off_mbase, off_bm, off_bc, off_pos, off_tstart, off_bx, off_by, off_red, bytes;
 };
 
 __host__ __device__ inline MitmLayout mitm_layout(int n, int p) {
@@ -109,7 +110,10 @@ __host__ __device__ inline MitmLayout mitm_layout(int n, int p) {
     int nb = 0;
     for (int m = 0; m < rmax; ++m) nb += mitm_blocks_of(m, W);
     L.n_blocks = nb;
-    size_t off = L.M.off_tail;
+    size_t off = 0;
+    L.off_binom = off; off += (size_t)n * (rmax + 1) * 8;
+    L.off_cum = off; off += (size_t)(rmax + 2) * 8;
+    off = (off + 15) & ~(size_t)15;
     L.off_mbase = off; off += (size_t)(rmax + 1) * 4;
     L.off_tstart = off; off += (size_t)(nb + 1) * 4;
     L.off_bm = off; off += (size_t)nb;
@@ -162,13 +166,13 @@ struct Side {
 };
 
 struct MitmCtx {
-    int n, W, S, R1;
+    int n, W, R1;
     const int64_t* binom;
-    const int32_t* rowoff;
+    const double* timg;    // the global T image (memo_row layout)
 };
 
 __device__ __forceinline__ double tval(const MitmCtx& x, int q, int a, int b) {
-    return lds_f64((uint32_t)x.rowoff[q * x.S + a] + 8u * (uint32_t)b);
+    return __ldg(x.timg + memo_row(q, a, x.n) + b);
 }
 
 // colex unrank of element idx among the k-subsets of bit positions 0..P-1:
@@ -235,7 +239,7 @@ __device__ __forceinline__ void append_if(bool keep, double v, double* buf, int*
 struct Blk {
     int m, j, c, R;    // R: rounds of kMitmTX X elements per tile (thin blocks)
     int64_t nl, nr, offl, offr;
-    uint32_t rbase;    // shared address of T[j][c][0] (right sides)
+    int32_t rrow;      // image index of T[j][c][0] (right sides)
 };
 
 __device__ __forceinline__ double left_val(const MitmCtx& x, const Blk& B, const double* val, const uint8_t* bnd,
@@ -248,9 +252,9 @@ __device__ __forceinline__ double left_val(const MitmCtx& x, const Blk& B, const
 
 __device__ __forceinline__ double right_val(const MitmCtx& x, const Blk& B, const double* val, const uint8_t* bnd,
                                             int64_t e) {
-    if (B.m == 0) return lds_f64(B.rbase + 8u * (uint32_t)x.n);
+    if (B.m == 0) return __ldg(x.timg + B.rrow + x.n);
     const double sv = val[B.offr + e];
-    const double tv = lds_f64(B.rbase + 8u * (uint32_t)bnd[B.offr + e]);
+    const double tv = __ldg(x.timg + B.rrow + bnd[B.offr + e]);
     return tv > sv ? tv : sv;
 }
 
@@ -276,8 +280,8 @@ __device__ __forceinline__ double side_value(const MitmCtx& x, const Blk& B, boo
 
 // The same from an element's already loaded table value and boundary cut.
 __device__ __forceinline__ double side_finish(const MitmCtx& x, const Blk& B, bool left, double raw, int b) {
-    if (B.m == 0) return left ? -__longlong_as_double(0x7ff0000000000000LL) : lds_f64(B.rbase + 8u * (uint32_t)x.n);
-    const double tv = left ? tval(x, B.j - 1, b, B.c) : lds_f64(B.rbase + 8u * (uint32_t)b);
+    if (B.m == 0) return left ? -__longlong_as_double(0x7ff0000000000000LL) : __ldg(x.timg + B.rrow + x.n);
+    const double tv = left ? tval(x, B.j - 1, b, B.c) : __ldg(x.timg + B.rrow + b);
     return tv > raw ? tv : raw;
 }
 
@@ -543,7 +547,7 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
         reinterpret_cast<unsigned long long*>(counter)[1] = 0x7ff0000000000000ull;   // shared incumbent (+inf)
     }
     __syncthreads();
-    const MitmCtx x{n, W, 0, R1, binom_s, nullptr};
+    const MitmCtx x{n, W, R1, binom_s, nullptr};
     auto T = [&](int q, int a, int b) { return __ldg(timg + rowrel[q * n + a] + b); };
     const double ninf = -__longlong_as_double(0x7ff0000000000000LL);
     const int64_t E = st.start[st.n_tab];
@@ -601,21 +605,9 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
 }
 
 // ------------------------------------------------------------- 3. sweep
-// shared copy of T from the image, row offsets, the -inf row, binomials
-// (Pascal's triangle in warp 0) and cum.
-__device__ inline void memo_load(const MemoLayout& L, const double* __restrict__ timg, unsigned char* sm) {
-    const int n = L.n, rmax = L.rmax, S = L.S, R1 = rmax + 1;
-    double* Tm = reinterpret_cast<double*>(sm);
-    for (int i = threadIdx.x; i < L.t_elems; i += blockDim.x) Tm[i] = timg[i];
-    int32_t* rowoff = reinterpret_cast<int32_t*>(sm + L.off_rowoff);
-    const uint32_t sm_base = (uint32_t)__cvta_generic_to_shared(sm);
-    for (int i = threadIdx.x; i < (rmax + 4) * S; i += blockDim.x) {
-        const int q = i / S, a = i % S;
-        const int32_t v = (q < rmax && a >= q && a < n) ? memo_row(q, a, n) * 8 : (int32_t)L.off_dummy;
-        rowoff[i] = (int32_t)(sm_base + (uint32_t)v);
-    }
-    for (int i = threadIdx.x; i <= n; i += blockDim.x)
-        reinterpret_cast<double*>(sm + L.off_dummy)[i] = -__longlong_as_double(0x7ff0000000000000LL);
+// binomials (Pascal's triangle in warp 0) and cum in shared memory.
+__device__ inline void sweep_prologue(const MitmLayout& L, unsigned char* sm) {
+    const int n = L.M.n, rmax = L.M.rmax, R1 = rmax + 1;
     if (threadIdx.x < 32) {
         int64_t* binom = reinterpret_cast<int64_t*>(sm + L.off_binom);
         const int lane = threadIdx.x;
@@ -656,9 +648,8 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     const int n = t.n;
     const MitmLayout L = mitm_layout(n, t.p);
     const int rmax = L.M.rmax, nb = L.n_blocks;
-    const MitmCtx x{n, n - 1, L.M.S, rmax + 1, reinterpret_cast<const int64_t*>(sm + L.M.off_binom),
-                    reinterpret_cast<const int32_t*>(sm + L.M.off_rowoff)};
-    const int64_t* cum = reinterpret_cast<const int64_t*>(sm + L.M.off_cum);
+    const MitmCtx x{n, n - 1, rmax + 1, reinterpret_cast<const int64_t*>(sm + L.off_binom), timg};
+    const int64_t* cum = reinterpret_cast<const int64_t*>(sm + L.off_cum);
     int32_t* mbase = reinterpret_cast<int32_t*>(sm + L.off_mbase);
     int32_t* tstart = reinterpret_cast<int32_t*>(sm + L.off_tstart);
     uint8_t* bm = sm + L.off_bm;
@@ -673,7 +664,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #ifdef DM_MITM_TIMING
     if (threadIdx.x == 0) for (int i_ = 4; i_ < 12; ++i_) g_mitm_times[blockIdx.x][i_] = 0;
 #endif
-    memo_load(L.M, timg, sm);
+    sweep_prologue(L, sm);
     MITM_MARK(1);
     if (threadIdx.x == 0) {
         int b = 0;
@@ -693,7 +684,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             B.nr = x.binom[(x.W - c) * x.R1 + (m - B.j)];
             B.offl = P.offL[m]; B.offr = P.offR[m];
         }
-        B.rbase = (uint32_t)x.rowoff[B.j * x.S + c];
+        B.rrow = memo_row(B.j, c, x.n);
         const int64_t nY = B.nl >= B.nr ? B.nr : B.nl;
         int64_t R = nY >= kThinY ? 1 : kThinPairs / (kMitmTX * nY);
         B.R = (int)(R < 1 ? 1 : (R > kThinRounds ? kThinRounds : R));
