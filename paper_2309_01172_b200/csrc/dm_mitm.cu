@@ -69,7 +69,7 @@ __device__ unsigned long long g_mitm_times[1024][12];
 
 constexpr int kMitmThreads = 256;
 constexpr int kMitmNR = 8;                           // X elements per thread (register slots)
-constexpr int kMitmNY = 4;                           // Y elements built per thread
+constexpr int kMitmNY = 8;                           // Y elements built per thread
 constexpr int kMitmTX = kMitmThreads * kMitmNR;      // 2048
 constexpr int kMitmTY = kMitmThreads * kMitmNY;      // 1024
 constexpr int kMitmCtasPerSm = 2;
