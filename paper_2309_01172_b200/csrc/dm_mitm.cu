@@ -772,9 +772,9 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             // ---- thin tile: the few feasible Y once in shared memory, then
             //      rounds of kMitmTX X elements straight into registers
             //      (infeasible X slots stay +inf and are counted)
-#pragma unroll
-            for (int u = 0; u < kMitmNY; ++u) {
-                const int e = u * kMitmThreads + threadIdx.x;
+            static_assert(kThinY <= kMitmThreads, "a thin tile's Y fits one element per thread");
+            {
+                const int e = threadIdx.x;
                 double v = inf;
                 if (e < nYr) {
                     v = side_finish(x, B, !xl, B.m ? val[yoff + y0 + e] : 0.0, B.m ? bnd[yoff + y0 + e] : 0);
@@ -852,15 +852,16 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             // ---- both sides' feasible elements, compacted into shared memory;
             //      element raw data (table value, boundary cut) for every slot
             //      first, so all global loads are in flight together
-            double xr[kMitmNR], yr[kMitmNY];
-            int xb[kMitmNR], yb[kMitmNY];
+            constexpr int kYc = kMitmNY < 8 ? kMitmNY : 8;    // Y elements per load batch
+            double xr[kMitmNR], yr[kYc];
+            int xb[kMitmNR], yb[kYc];
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
                 if (e < nXr && B.m) { xr[u] = val[xoff + x0 + e]; xb[u] = bnd[xoff + x0 + e]; }
             }
     #pragma unroll
-            for (int u = 0; u < kMitmNY; ++u) {
+            for (int u = 0; u < kYc; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
                 if (e < nYr && B.m) { yr[u] = val[yoff + y0 + e]; yb[u] = bnd[yoff + y0 + e]; }
             }
@@ -871,12 +872,22 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 if (e < nXr) { v = side_finish(x, B, xl, xr[u], xb[u]); xmin = v < xmin ? v : xmin; }
                 append_if(v != inf, v, bx, &s_cnt[par][0]);
             }
+    #pragma unroll 1
+            for (int h = 0; h < kMitmNY; h += kYc) {
+                if (h > 0) {
     #pragma unroll
-            for (int u = 0; u < kMitmNY; ++u) {
-                const int e = u * kMitmThreads + threadIdx.x;
-                double v = inf;
-                if (e < nYr) { v = side_finish(x, B, !xl, yr[u], yb[u]); ymin = v < ymin ? v : ymin; }
-                append_if(v != inf, v, by, &s_cnt[par][1]);
+                    for (int u = 0; u < kYc; ++u) {
+                        const int e = (h + u) * kMitmThreads + threadIdx.x;
+                        if (e < nYr && B.m) { yr[u] = val[yoff + y0 + e]; yb[u] = bnd[yoff + y0 + e]; }
+                    }
+                }
+    #pragma unroll
+                for (int u = 0; u < kYc; ++u) {
+                    const int e = (h + u) * kMitmThreads + threadIdx.x;
+                    double v = inf;
+                    if (e < nYr) { v = side_finish(x, B, !xl, yr[u], yb[u]); ymin = v < ymin ? v : ymin; }
+                    append_if(v != inf, v, by, &s_cnt[par][1]);
+                }
             }
             const int fl = (xmin <= best ? 1 : 0) | (ymin <= best ? 2 : 0);
             if (fl) atomicOr(&s_flag[par], fl);
