@@ -12,6 +12,7 @@
 //  * argmin kernels: block/warp arg-min over (makespan, rank).
 #include "dm_common.cuh"
 #include "dm_abi_util.cuh"
+#include <cstdio>
 #include <cstdlib>
 
 namespace dm {
@@ -374,6 +375,73 @@ __device__ __forceinline__ unsigned long long boundary_mask_n(int nw, uint32_t w
     }
 }
 
+// Per-launch constants of the stream kernel's candidate loop.
+struct StreamCtx {
+    int n;
+    uint32_t uP, Pm1, n1P8, T_s, C_s, rowidx_s, mask_lo, mask_hi;
+};
+
+// Score this thread's candidates of one resident tile (NW: boundary-mask
+// words).  A run failing _fits only records its table address; the first
+// one's violation code is read after the runs (rare).
+template <bool PAIR, bool SQUARE, int NT, int NW>
+__device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx& X, uint32_t tile_s,
+                                            const unsigned char* tile, int cnt, int64_t c0,
+                                            double* __restrict__ out_mk, uint8_t* __restrict__ out_code,
+                                            int64_t rank_base, bool fuse, Win& win) {
+    const int n = X.n;
+#pragma unroll 1
+    for (int ci = threadIdx.x; ci < cnt; ci += NT) {
+        const uint32_t row_s = tile_s + (uint32_t)ci * n;        // shared address of the row
+        const unsigned long long bm = boundary_mask<NW>(row_s & ~3u, (int)(row_s & 3u) * 8);
+        // ---- runs: b = each boundary in ascending order, then n
+        double mk = 0.0;
+        int a = 0, prev = -1, nruns = 0;
+        uint32_t wmax = 0, seen = 0, rowb = X.T_s, bad = 0;      // rowb: address of T[a][0][0] (square)
+        auto run = [&](int b) {
+            uint32_t w = lds_u8(row_s + a);
+            wmax = max(wmax, w);
+            w = min(w, X.Pm1);
+            seen |= 1u << w;
+            ++nruns;
+            uint32_t addr;
+            if (SQUARE) addr = rowb + 8u * ((uint32_t)b * X.uP + w);
+            else addr = X.T_s + 8u * ((lds_u32(X.rowidx_s + 4u * a) + b) * X.uP + w);
+            const double tv = lds_f64s(addr);
+            double v = fabs(tv);
+            if (PAIR && a > 0) {
+                double al, be;
+                link_of(t, prev, (int)w, al, be);
+                double rd = 0.0;
+                for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
+                    rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
+                v = v + rd;
+            }
+            mk = v > mk ? v : mk;
+            bad = (signbit(tv) && !bad) ? (addr | 0x80000000u) : bad;   // shared addresses < 2^31
+            prev = (int)w; a = b;
+            if (SQUARE) rowb = X.T_s + (uint32_t)b * X.n1P8;
+        };
+        for (uint32_t y = (uint32_t)bm & X.mask_lo; y; y &= y - 1) run(__ffs(y));
+        if (NW > 8)
+            for (uint32_t y = (uint32_t)(bm >> 32) & X.mask_hi; y; y &= y - 1) run(32 + __ffs(y));
+        run(n);
+        int code = bad ? (int)lds_u8(X.C_s + (((bad & 0x7fffffffu) - X.T_s) >> 3)) : DM_V_OK;
+        const bool unknown = wmax >= X.uP;
+        if (!unknown && __popc(seen) != nruns) eval_owner_grouped(t, tile + (size_t)ci * n, mk, code);
+        out_mk[c0 + ci] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
+        out_code[c0 + ci] = unknown ? (uint8_t)0xFF : (uint8_t)code;
+        if (fuse) {                          // fused arg-min (first strict minimum by rank)
+            win.n_eval++;
+            if (!unknown && code == DM_V_OK) {
+                win.n_feas++;
+                win.csum += (uint64_t)__double_as_longlong(mk);
+                if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank_base + c0 + ci; }
+            }
+        }
+    }
+}
+
 template <bool PAIR, bool SQUARE, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t, int64_t n_cand,
                                                                               const uint8_t* __restrict__ owner,
@@ -436,9 +504,11 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
     const uint32_t sm_s = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t T_s = sm_s + (uint32_t)L.off_T, rowidx_s = sm_s + (uint32_t)L.off_rowidx;
     const uint32_t C_s = sm_s + (uint32_t)L.off_code;
-    const uint32_t uP = (uint32_t)P, Pm1 = uP - 1u, n1P8 = 8u * (uint32_t)(n + 1) * uP;
-    const uint32_t stage_mask_lo = n - 1 >= 32 ? 0xffffffffu : ((1u << (n - 1)) - 1u);
-    const uint32_t stage_mask_hi = n - 1 >= 64 ? 0xffffffffu : (n - 1 > 32 ? ((1u << (n - 33)) - 1u) : 0u);
+    StreamCtx X;
+    X.n = n; X.uP = (uint32_t)P; X.Pm1 = X.uP - 1u; X.n1P8 = 8u * (uint32_t)(n + 1) * X.uP;
+    X.T_s = T_s; X.C_s = C_s; X.rowidx_s = rowidx_s;
+    X.mask_lo = n - 1 >= 32 ? 0xffffffffu : ((1u << (n - 1)) - 1u);
+    X.mask_hi = n - 1 >= 64 ? 0xffffffffu : (n - 1 > 32 ? ((1u << (n - 33)) - 1u) : 0u);
     Win win; win_init(win);
     int64_t it_local = 0;
     for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x, ++it_local) {
@@ -454,53 +524,16 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
             __syncthreads();
         }
         const uint32_t tile_s = sm_s + (uint32_t)(tile - sm);
-#pragma unroll 1
-        for (int ci = tid; ci < cnt; ci += NT) {
-            const uint32_t row_s = tile_s + (uint32_t)ci * n;        // shared address of the row
-            const unsigned long long bm = boundary_mask_n(nw, row_s & ~3u, (int)(row_s & 3u) * 8);
-            // ---- runs: b = each boundary in ascending order, then n
-            double mk = 0.0;
-            int code = DM_V_OK, a = 0, prev = -1, nruns = 0;
-            uint32_t wmax = 0, seen = 0, rowb = T_s;                 // rowb: address of T[a][0][0] (square)
-            auto run = [&](int b) {
-                uint32_t w = lds_u8(row_s + a);
-                wmax = max(wmax, w);
-                w = min(w, Pm1);
-                seen |= 1u << w;
-                ++nruns;
-                uint32_t addr;
-                if (SQUARE) addr = rowb + 8u * ((uint32_t)b * uP + w);
-                else addr = T_s + 8u * ((lds_u32(rowidx_s + 4u * a) + b) * uP + w);
-                const double tv = lds_f64s(addr);
-                double v = fabs(tv);
-                if (PAIR && a > 0) {
-                    double al, be;
-                    link_of(t, prev, (int)w, al, be);
-                    double rd = 0.0;
-                    for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
-                        rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
-                    v = v + rd;
-                }
-                mk = v > mk ? v : mk;
-                if (signbit(tv) && code == DM_V_OK) code = lds_u8(C_s + ((addr - T_s) >> 3));
-                prev = (int)w; a = b;
-                if (SQUARE) rowb = T_s + (uint32_t)b * n1P8;
-            };
-            for (uint32_t y = (uint32_t)bm & stage_mask_lo; y; y &= y - 1) run(__ffs(y));
-            for (uint32_t y = (uint32_t)(bm >> 32) & stage_mask_hi; y; y &= y - 1) run(32 + __ffs(y));
-            run(n);
-            const bool unknown = wmax >= uP;
-            if (!unknown && __popc(seen) != nruns) eval_owner_grouped(t, tile + (size_t)ci * n, mk, code);
-            out_mk[c0 + ci] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
-            out_code[c0 + ci] = unknown ? (uint8_t)0xFF : (uint8_t)code;
-            if (partial) {                       // fused arg-min (first strict minimum by rank)
-                win.n_eval++;
-                if (!unknown && code == DM_V_OK) {
-                    win.n_feas++;
-                    win.csum += (uint64_t)__double_as_longlong(mk);
-                    if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank_base + c0 + ci; }
-                }
-            }
+        switch (nw) {     // the boundary-mask width is fixed per launch: one dispatch per tile
+#define DM_STREAM_TILE(W)                                                                              \
+            case W: stream_tile<PAIR, SQUARE, NT, W>(t, X, tile_s, tile, cnt, c0, out_mk, out_code, rank_base, \
+                                                     partial != nullptr, win); break;
+            DM_STREAM_TILE(1) DM_STREAM_TILE(2) DM_STREAM_TILE(3) DM_STREAM_TILE(4) DM_STREAM_TILE(5)
+            DM_STREAM_TILE(6) DM_STREAM_TILE(7) DM_STREAM_TILE(8) DM_STREAM_TILE(9) DM_STREAM_TILE(10)
+            DM_STREAM_TILE(11) DM_STREAM_TILE(12) DM_STREAM_TILE(13) DM_STREAM_TILE(14) DM_STREAM_TILE(15)
+            default: stream_tile<PAIR, SQUARE, NT, 16>(t, X, tile_s, tile, cnt, c0, out_mk, out_code, rank_base,
+                                                       partial != nullptr, win); break;
+#undef DM_STREAM_TILE
         }
         __syncthreads();  // every thread is done with this slot
         if (tid == 0) {
@@ -622,15 +655,27 @@ static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner
     {
         const uint32_t f = t->flags;
         bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
-        // pick a configuration: a square table with 3 CTAs x 256 threads per
-        // SM (<= 85 registers) when the table and a 2-candidate x 3-stage tile
-        // ring fit in a third of the SM, else 2 CTAs with deeper tiles, else the
-        // triangular table with one 512-thread CTA per SM
+        // pick a configuration: a square table with 2 CTAs x 256 threads per
+        // SM and a 4-candidate x 3-stage tile ring when it fits half the SM
+        // (C1: 8.4e10 vs 7.7e10 cand/s for 3 CTAs x 2 candidates), else 3 CTAs
+        // (<= 85 registers) with 2-candidate tiles, else 2 CTAs with other
+        // tile shapes, else the triangular table with one 512-thread CTA per SM
         dm::StreamLayout L{};
         bool found = false;
         int minb = 2;
-        L = dm::stream_layout(t->n, t->P, 3, 2, true, 256);
-        if (L.bytes <= 72 * 1024) { found = true; minb = 3; }
+        L = dm::stream_layout(t->n, t->P, 3, 4, true, 256);
+        if (L.bytes <= 110 * 1024) found = true;
+        if (!found) {
+            L = dm::stream_layout(t->n, t->P, 3, 2, true, 256);
+            if (L.bytes <= 72 * 1024) { found = true; minb = 3; }
+        }
+        if (const char* cfg = std::getenv("DM_MODEA_CFG")) {      // experiments: "minb,cpt,stages" (square)
+            int mb = 0, cp = 0, sg = 0;
+            if (std::sscanf(cfg, "%d,%d,%d", &mb, &cp, &sg) == 3 && (mb == 2 || mb == 3)) {
+                dm::StreamLayout L2 = dm::stream_layout(t->n, t->P, sg, cp, true, 256);
+                if (L2.bytes <= (mb == 3 ? 72 : 110) * 1024) { L = L2; found = true; minb = mb; }
+            }
+        }
         for (int sq = 1; sq >= 0 && !found; --sq) {
             const int nt = sq ? 256 : 512;
             for (int cpt = 4; cpt >= 1 && !found; cpt /= 2)
