@@ -383,11 +383,11 @@ def mode_a_measure(dev, which):
     peak, src = _hbm_peak()
     algo = N * (n * 1 + 9)
     achieved = algo / (ms / 1e3) / 1e9
-    tr = ncu_traffic("eval_owner_stream_kernel") if which == "c1" else None
+    tr = ncu_traffic("eval_owner_stream_kernel", f"r1_prof_modea_{which}*_raw.csv") if which == "c1" else None
     res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                        "traffic": (tr["bytes"] / (1 << 25) * N) if tr else None,
-                       "traffic_note": (f"{tr['capture']}: DRAM read+write of a 2^25-candidate launch, scaled per "
-                                        "candidate to this launch") if tr else None,
+                       "traffic_note": (f"{tr['capture']}: DRAM read+write of a 2^25-candidate launch (same "
+                                        "population), scaled per candidate to this launch") if tr else None,
                        "bytes_per_candidate": n + 9, "peak_source": src}
     inst = oracle.Instance(stages, fleet)
     sample = own[:20000].cpu().numpy().astype("int64")
