@@ -230,6 +230,16 @@ DM_API int dm_enum_splits_ws(const dm_tables* t, int64_t k0, int64_t k1, int32_t
                              dm_winner* out, void* scratch, void* workspace, int64_t workspace_bytes,
                              void* stream);
 
+/* dm_enum_splits_phase — dm_enum_splits_ws in two stream-ordered halves so a
+ * batch of sweeps can overlap one instance's table phase with another's
+ * sweep: phase 1 builds the side tables into `workspace` (required, at least
+ * dm_splits_workspace_bytes), phase 2 sweeps them and writes `out`; phase 3
+ * does both.  Phase 1 then phase 2 on the same workspace equals phase 3.
+ * Instances that take the rank-range kernels do all their work in phase 2. */
+DM_API int dm_enum_splits_phase(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts,
+                                dm_winner* out, void* scratch, void* workspace, int64_t workspace_bytes,
+                                int32_t phase, void* stream);
+
 /*
  * dm_enum_random — counter-RNG random contiguous placements (config C5):
  * candidate k (k0 <= k < k1) is generated from SplitMix64 keyed (seed, k):

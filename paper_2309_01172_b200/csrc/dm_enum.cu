@@ -692,22 +692,27 @@ bool nparts_full_range(const dm_tables* t, int64_t k0, int64_t k1) {
 }
 
 int enum_splits_impl(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts, dm_winner* out,
-                     void* scratch, void* ws, int64_t ws_bytes, void* stream) {
-    if (!t || !out || !scratch || t->n <= 0 || t->p <= 0 || nparts < 1 || part < 0 || part >= nparts)
+                     void* scratch, void* ws, int64_t ws_bytes, void* stream, int phase = 3) {
+    if (!t || !out || !scratch || t->n <= 0 || t->p <= 0 || nparts < 1 || part < 0 || part >= nparts ||
+        phase < 1 || phase > 3)
         return dmabi::fail(DM_E_ARG, "bad arguments");
     cudaStream_t s = (cudaStream_t)stream;
     const bool memo_ok = dm::memo_valid(*t) && !getenv_flag("DM_DISABLE_MEMO");
     if (memo_ok && nparts_full_range(t, k0, k1) && !getenv_flag("DM_DISABLE_MITM")) {
         int n_partials = 0;
         int rc = dm::launch_splits_mitm(*t, part, nparts, (dm_winner*)scratch, enum_grid() / 8, ws, ws_bytes,
-                                        &n_partials, s);
+                                        &n_partials, s, phase);
+        if (rc == DM_E_ARG) return dmabi::fail(DM_E_ARG, "split phases need a workspace of dm_splits_workspace_bytes");
         if (rc != DM_E_TOO_LARGE) {
             if (rc != DM_OK) return rc;
-            dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, n_partials, out);
-            DM_CHECK_LAUNCH();
+            if (phase & 2) {
+                dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, n_partials, out);
+                DM_CHECK_LAUNCH();
+            }
             return DM_OK;
         }
     }
+    if (!(phase & 2)) return DM_OK;     // the rank-range kernels have no table phase
     dm::MemoLayout L = dm::memo_layout(t->n, t->p);
     const size_t memo_bytes = L.off_tail + dm::memo_cut_bytes(L);
     if (memo_ok && t->n <= 64 && memo_bytes <= 110 * 1024) {
@@ -759,6 +764,11 @@ int64_t dm_splits_workspace_bytes(const dm_tables* t) {
 int dm_enum_splits_ws(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts, dm_winner* out,
                       void* scratch, void* workspace, int64_t workspace_bytes, void* stream) {
     return enum_splits_impl(t, k0, k1, part, nparts, out, scratch, workspace, workspace_bytes, stream);
+}
+
+int dm_enum_splits_phase(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts, dm_winner* out,
+                         void* scratch, void* workspace, int64_t workspace_bytes, int32_t phase, void* stream) {
+    return enum_splits_impl(t, k0, k1, part, nparts, out, scratch, workspace, workspace_bytes, stream, phase);
 }
 
 int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,

@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 const int e = threadIdx.x;
                 double v = inf;
                 if (e < nYr) {
-                    v = side_finish(x, B, !xl, B.m ? val[yoff + y0 + e] : 0.0, B.m ? bnd[yoff + y0 + e] : 0);
+                    v = side_finish(x, B, !xl, B.m ? __ldcg(val + yoff + y0 + e) : 0.0, B.m ? __ldcg(bnd + yoff + y0 + e) : 0);
                     ymin = v < ymin ? v : ymin;
                 }
                 append_if(v != inf, v, by, &s_cnt[par][1]);
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
                     for (int u = 0; u < kMitmNR; ++u) {
                         const int e = r0 + u * kMitmThreads + threadIdx.x;
-                        if (e < nXr && B.m) { xr[u] = val[xoff + x0 + e]; xb[u] = bnd[xoff + x0 + e]; }
+                        if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
                     }
                     int f = 0;
 #pragma unroll
@@ -858,12 +858,12 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                if (e < nXr && B.m) { xr[u] = val[xoff + x0 + e]; xb[u] = bnd[xoff + x0 + e]; }
+                if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
             }
     #pragma unroll
             for (int u = 0; u < kYc; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                if (e < nYr && B.m) { yr[u] = val[yoff + y0 + e]; yb[u] = bnd[yoff + y0 + e]; }
+                if (e < nYr && B.m) { yr[u] = __ldcg(val + yoff + y0 + e); yb[u] = __ldcg(bnd + yoff + y0 + e); }
             }
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
@@ -878,7 +878,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     #pragma unroll
                     for (int u = 0; u < kYc; ++u) {
                         const int e = (h + u) * kMitmThreads + threadIdx.x;
-                        if (e < nYr && B.m) { yr[u] = val[yoff + y0 + e]; yb[u] = bnd[yoff + y0 + e]; }
+                        if (e < nYr && B.m) { yr[u] = __ldcg(val + yoff + y0 + e); yb[u] = __ldcg(bnd + yoff + y0 + e); }
                     }
                 }
     #pragma unroll
@@ -1037,7 +1037,7 @@ inline SweepTiming& sweep_timing() {
 }
 
 int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* partial, int sms, void* ws,
-                       int64_t ws_bytes, int* n_partials, cudaStream_t s) {
+                       int64_t ws_bytes, int* n_partials, cudaStream_t s, int phase) {
     if (!memo_valid(t)) return DM_E_TOO_LARGE;
     const PlanEntry& pe = cached_plan(t.n, t.p, part, nparts);
     if (!pe.ok) return DM_E_TOO_LARGE;
@@ -1047,6 +1047,7 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
     const MitmLayout L = mitm_layout(t.n, t.p);
     void* buf = ws;
     const bool own = !ws || ws_bytes < (int64_t)W.bytes;
+    if (own && phase != 3) return DM_E_ARG;     // split phases keep the tables in the caller's workspace
     if (own) DM_CUDA(cudaMallocAsync(&buf, W.bytes, s));
     unsigned char* b8 = static_cast<unsigned char*>(buf);
     int* ctl = reinterpret_cast<int*>(b8);
@@ -1055,17 +1056,15 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
     uint8_t* bnd = b8 + W.off_bnd;
     const int rmax = t.n < t.p ? t.n : t.p;
     SweepTiming& tm = sweep_timing();
-    if (tm.on) {
-        for (auto& e : tm.ev) if (!e) DM_CUDA(cudaEventCreate(&e));
-        DM_CUDA(cudaEventRecord(tm.ev[0], s));
-    }
-    {
+    if (tm.on) for (auto& e : tm.ev) if (!e) DM_CUDA(cudaEventCreate(&e));
+    if (tm.on && (phase & 1)) DM_CUDA(cudaEventRecord(tm.ev[0], s));
+    if (phase & 1) {
         const int64_t work = (int64_t)rmax * t.n * t.n;
         int blocks = (int)((work + 255) / 256);
         memo_image_kernel<<<blocks, 256, 0, s>>>(t, timg);
         DM_CHECK_LAUNCH();
     }
-    {
+    if (phase & 1) {
         const size_t smem = (size_t)t.n * (rmax + 1) * 8 + (size_t)rmax * t.n * 4;
         const int64_t per = (int64_t)256 * kTabPass;
         int64_t blocks = (W.entries + per - 1) / per;
@@ -1075,14 +1074,16 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         else side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl);
         DM_CHECK_LAUNCH();
     }
-    DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
     const int grid = mitm_grid(sms);
-    if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
-    splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial);
-    DM_CHECK_LAUNCH();
-    if (tm.on) {
-        DM_CUDA(cudaEventRecord(tm.ev[2], s));
-        tm.pending = true;
+    if (phase & 2) {
+        DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+        if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
+        splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial);
+        DM_CHECK_LAUNCH();
+        if (tm.on) {
+            DM_CUDA(cudaEventRecord(tm.ev[2], s));
+            tm.pending = true;
+        }
     }
     if (own) DM_CUDA(cudaFreeAsync(buf, s));
     *n_partials = grid;

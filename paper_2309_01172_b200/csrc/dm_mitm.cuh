@@ -21,7 +21,9 @@ int64_t mitm_workspace_bytes(const dm_tables& t);
 // nparts-th tile, so the parts of one population are disjoint and their merged
 // records equal the single sweep.  Returns DM_E_TOO_LARGE when the instance
 // does not fit the kernel (the caller falls back to the rank-range kernels).
+// phase: 1 = T image + side tables, 2 = the sweep kernel, 3 = both (phases
+// 1 and 2 apart need the caller's workspace, which carries the tables).
 int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* partial, int sms, void* ws,
-                       int64_t ws_bytes, int* n_partials, cudaStream_t stream);
+                       int64_t ws_bytes, int* n_partials, cudaStream_t stream, int phase = 3);
 
 }  // namespace dm

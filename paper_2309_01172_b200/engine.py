@@ -146,9 +146,12 @@ def argmin_scores(mk, code, rank_base: int = 0, bufs: WinnerBuffers | None = Non
 
 
 def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | None = None,
-         index: int = 0, online=None, mults=None, seed: int = 0, part: int = 0, nparts: int = 1):
+         index: int = 0, online=None, mults=None, seed: int = 0, part: int = 0, nparts: int = 1,
+         phase: int = 3):
     """Mode B enumeration: 'bruteforce' | 'splits' | 'random'. Returns bufs
-    (call bufs.read() to synchronise and fetch the winner)."""
+    (call bufs.read() to synchronise and fetch the winner).  'splits' takes
+    `phase` (dm_enum_splits_phase): 1 = side tables only, 2 = sweep only,
+    3 = both."""
     lib = _lib.load()
     bufs = bufs or WinnerBuffers(batch.dev_buf.device)
     st = batch.struct(index)
@@ -158,9 +161,9 @@ def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | 
     elif mode == "splits":
         need = int(lib.dm_splits_workspace_bytes(C.byref(st)))
         ws = bufs.workspace_for(need)
-        _lib.check(lib.dm_enum_splits_ws(C.byref(st), k0, k1, part, nparts, bufs.out.data_ptr(),
-                                         bufs.scratch.data_ptr(), ws.data_ptr() if ws is not None else None,
-                                         max(need, 0), s))
+        _lib.check(lib.dm_enum_splits_phase(C.byref(st), k0, k1, part, nparts, bufs.out.data_ptr(),
+                                            bufs.scratch.data_ptr(), ws.data_ptr() if ws is not None else None,
+                                            max(need, 0), phase, s))
     elif mode == "random":
         _lib.check(lib.dm_enum_random(C.byref(st), online.data_ptr(), online.numel(), mults.data_ptr(),
                                       mults.numel(), seed & 0xFFFFFFFFFFFFFFFF, k0, k1, bufs.out.data_ptr(),
@@ -286,13 +289,18 @@ class SweepGraph:
     the kernels alone (tables already resident, records left in `out`)."""
 
     def __init__(self, batch: DeviceBatch, total: int, bufs: WinnerBuffers | None = None, part: int = 0,
-                 nparts: int = 1, copy_inputs: bool = True, units=None):
+                 nparts: int = 1, copy_inputs: bool = True, units=None, overlap: bool = True):
         torch = _torch()
         lib = _lib.load()
         self.batch, self.total = batch, total
         self.units = [tuple(u) for u in units] if units is not None else [(0, part, nparts)]
         self.copy_inputs = copy_inputs
         dev = batch.dev_buf.device
+        # several units: unit i+1's table phase (side stream) overlaps unit
+        # i's sweep (the table kernels are L1/latency bound, the sweep is
+        # ALU bound); every unit has its own workspace
+        self.overlap = overlap and len(self.units) > 1
+        self.side = torch.cuda.Stream(device=dev) if self.overlap else None
         self.unit_bufs = [bufs if (i == 0 and bufs is not None) else WinnerBuffers(dev)
                           for i in range(len(self.units))]
         for (idx, _, _), ub in zip(self.units, self.unit_bufs):
@@ -314,13 +322,30 @@ class SweepGraph:
             self._body()
 
     def _body(self):
+        torch = _torch()
         b = self.batch
         if self.copy_inputs:
             b.dev_buf.copy_(b.host_buf, non_blocking=True)
             b.structs_dev.copy_(b.records_host, non_blocking=True)
-        for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
-            enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts)
-            self.out[i].copy_(ub.out, non_blocking=True)
+        if self.overlap:
+            main = torch.cuda.current_stream()
+            self.side.wait_stream(main)
+            ready = []
+            with torch.cuda.stream(self.side):
+                for (idx, part, nparts), ub in zip(self.units, self.unit_bufs):
+                    enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts, phase=1)
+                    ev = torch.cuda.Event()
+                    ev.record(self.side)
+                    ready.append(ev)
+            for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
+                main.wait_event(ready[i])
+                enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts, phase=2)
+                self.out[i].copy_(ub.out, non_blocking=True)
+            main.wait_stream(self.side)
+        else:
+            for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
+                enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts)
+                self.out[i].copy_(ub.out, non_blocking=True)
         if self.whole and self.copy_inputs:
             self.host_out.copy_(self.out, non_blocking=True)
 

@@ -420,3 +420,28 @@ def test_sweep_graph_matches_enum(engine_ready):
     for _ in range(3):
         g.launch()
         assert g.read() == want
+
+
+def test_sweep_graph_units_overlap_matches_enum(engine_ready):
+    """A SweepGraph over several instances (unit i+1's side tables on a side
+    stream, overlapping unit i's sweep) returns every instance's own record,
+    and dm_enum_splits_phase 1 then 2 equals the one-call sweep."""
+    import torch
+    rng = np.random.default_rng(11)
+    hosts = []
+    for _ in range(3):
+        st, fleet = big_instance(rng, 22, 16, dag=False, links=True, pressure=(0.1, 0.7))
+        hosts.append(build_host(st, fleet))
+    batch = engine.device_batch(hosts)
+    total = engine.splits_total(22, 16)
+    want = [engine.enum(batch, "splits", 0, total, index=i).read() for i in range(3)]
+    g = engine.SweepGraph(batch, total, units=[(0, 0, 1), (1, 0, 1), (2, 0, 1)])
+    assert g.overlap
+    for _ in range(2):
+        g.launch()
+        assert g.read_all() == want
+    bufs = engine.WinnerBuffers(batch.dev_buf.device)
+    engine.enum(batch, "splits", 0, total, bufs, index=1, phase=1)
+    engine.enum(batch, "splits", 0, total, bufs, index=1, phase=2)
+    assert bufs.read() == want[1]
+    torch.cuda.synchronize()
