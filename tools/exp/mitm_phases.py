@@ -38,3 +38,7 @@ tot = a[:, 8].astype(float)
 print(f"clock share (thread 0): elements+barrier {a[:, 6].sum() / tot.sum():.3f}  cross {a[:, 7].sum() / tot.sum():.3f}  "
       f"rest {(tot.sum() - a[:, 6].sum() - a[:, 7].sum()) / tot.sum():.3f}")
 print(f"tiles {a[:, 9].sum()} (thin {a[:, 10].sum()}), per CTA min {a[:, 9].min()} max {a[:, 9].max()}")
+end = np.sort((a[:, 3] - t0) / 1e3)
+print("CTA end times (us) percentiles 0/10/50/90/95/99/100:",
+      [round(float(np.percentile(end, q)), 1) for q in (0, 10, 50, 90, 95, 99, 100)])
+print("last 12 CTAs end:", [round(float(v), 1) for v in end[-12:]])
