@@ -799,14 +799,14 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 // warp-private compaction of each round's feasible X
                 double* wbuf = bx + (threadIdx.x >> 5) * (kMitmNR * 32);
                 const int lane = threadIdx.x & 31;
-                for (int r0 = 0; r0 < nXr; r0 += kMitmTX) {
-                    double xr[kMitmNR];
-                    int xb[kMitmNR];
+                double xr[kMitmNR];
+                int xb[kMitmNR];
 #pragma unroll
-                    for (int u = 0; u < kMitmNR; ++u) {
-                        const int e = r0 + u * kMitmThreads + threadIdx.x;
-                        if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
-                    }
+                for (int u = 0; u < kMitmNR; ++u) {
+                    const int e = u * kMitmThreads + threadIdx.x;
+                    if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
+                }
+                for (int r0 = 0; r0 < nXr; r0 += kMitmTX) {
                     int f = 0;
 #pragma unroll
                     for (int u = 0; u < kMitmNR; ++u) {
@@ -816,6 +816,12 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                         const unsigned bal = __ballot_sync(0xffffffffu, v != inf);
                         if (v != inf) wbuf[f + __popc(bal & ((1u << lane) - 1u))] = v;
                         f += __popc(bal);
+                    }
+                    // the next round's elements are in flight during this round's cross product
+#pragma unroll
+                    for (int u = 0; u < kMitmNR; ++u) {
+                        const int e = r0 + kMitmTX + u * kMitmThreads + threadIdx.x;
+                        if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
                     }
                     __syncwarp();
                     const int nsl = (f + 31) >> 5;
