@@ -910,28 +910,46 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 w.n_feas += (int64_t)nxf_tot * nyf;
             }
             if (nxf_tot > 0 && nyf > 0) {     // uniform
-                const int nsl = (nxf_tot + kMitmThreads - 1) / kMitmThreads;
+                // ---- slot layout: G warp-aligned thread groups, each taking
+                //      every X against 1/G of the Y (fewer padded slots when
+                //      the feasible X do not fill kMitmNR slots per thread);
+                //      cost per thread ~ Y pairs x (slots + 0.5 per-Y overhead)
+                int G = 1, nsl = (nxf_tot + kMitmThreads - 1) / kMitmThreads;
+                int best_cost = nyf * (2 * nsl + 1);
+                for (int g2 = 2; g2 <= 8; g2 <<= 1) {
+                    const int per2 = kMitmThreads / g2, ns2 = (nxf_tot + per2 - 1) / per2;
+                    if (ns2 > kMitmNR) break;
+                    const int yc2 = ((nyf + g2 - 1) / g2 + 1) & ~1;
+                    const int cost = yc2 * (2 * ns2 + 1);
+                    if (cost < best_cost) { best_cost = cost; G = g2; nsl = ns2; }
+                }
+                const int per = kMitmThreads / G, gi = threadIdx.x / per, l = threadIdx.x - gi * per;
+                const int yc = G == 1 ? nyf : (((nyf + G - 1) / G + 1) & ~1);
+                const int ylo = gi * yc < nyf ? gi * yc : nyf;
+                const int nyg = (ylo + yc < nyf ? ylo + yc : nyf) - ylo;
                 double xv[kMitmNR];
                 int nxf = 0;
 #pragma unroll
                 for (int u = 0; u < kMitmNR; ++u) {
-                    const int e = u * kMitmThreads + threadIdx.x;
-                    xv[u] = e < nxf_tot ? bx[e] : inf;
-                    nxf += e < nxf_tot;
+                    const int e = l + u * per;
+                    const bool in = u < nsl && e < nxf_tot;
+                    xv[u] = in ? bx[e] : inf;
+                    nxf += in;
                 }
                 // ---- cross product: one max + checksum add per candidate
+                const double* byg = by + ylo;
                 switch (nsl) {
-                    case 1: mitm_cross<1>(xv, by, nyf, cs); break;
-                    case 2: mitm_cross<2>(xv, by, nyf, cs); break;
-                    case 3: mitm_cross<3>(xv, by, nyf, cs); break;
-                    case 4: mitm_cross<4>(xv, by, nyf, cs); break;
-                    case 5: mitm_cross<5>(xv, by, nyf, cs); break;
-                    case 6: mitm_cross<6>(xv, by, nyf, cs); break;
-                    case 7: mitm_cross<7>(xv, by, nyf, cs); break;
-                    default: mitm_cross<8>(xv, by, nyf, cs); break;
+                    case 1: mitm_cross<1>(xv, byg, nyg, cs); break;
+                    case 2: mitm_cross<2>(xv, byg, nyg, cs); break;
+                    case 3: mitm_cross<3>(xv, byg, nyg, cs); break;
+                    case 4: mitm_cross<4>(xv, byg, nyg, cs); break;
+                    case 5: mitm_cross<5>(xv, byg, nyg, cs); break;
+                    case 6: mitm_cross<6>(xv, byg, nyg, cs); break;
+                    case 7: mitm_cross<7>(xv, byg, nyg, cs); break;
+                    default: mitm_cross<8>(xv, byg, nyg, cs); break;
                 }
-                corr += (uint64_t)(nsl - nxf) * (uint64_t)nyf;
-                MITM_COUNT(4, nsl * nyf);
+                corr += (uint64_t)(nsl - nxf) * (uint64_t)nyg;
+                MITM_COUNT(4, nsl * nyg);
             }
             MITM_CLK(c_t2);
             MITM_ACC(7, c_t1, c_t2);
