@@ -269,7 +269,7 @@ def run_b200(args, rank, world, local_rank):
         "config": workload_config(total, links),
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(batch.h2d_bytes),
                 "d2h_bytes_per_step": int(e2e_d2h)},
-        "gpu_launches": 4 * len(units) * args.steps,
+        "gpu_launches": 5 * len(units) * args.steps,
         "roofline": {"bound": "issue", "achieved": achieved, "peak": (cross / 1e9) if cross else None,
                      "unit": "Gcand/s", "frac": (achieved / (cross / 1e9)) if cross else None,
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("capture"),

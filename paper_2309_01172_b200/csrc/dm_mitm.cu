@@ -143,13 +143,19 @@ struct SideTables {
 // decreasing number of candidates.
 struct SweepParams {
     int64_t offL[kMitmMaxM], offR[kMitmMaxM];
+    int8_t tabL[kMitmMaxM], tabR[kMitmMaxM];   // histogram row of L_k / R(m) (-1: not built by this part)
     int nbp;                          // blocks of this part
     int16_t order[kMitmMaxBlocks];    // the part's blocks, largest tiles first
 };
 
+// Feasibility histogram of the side tables: finite entries per (table,
+// boundary position); the sweep orders its tiles by the feasible pairs this
+// predicts (an upper bound) instead of the raw tile size.
+constexpr int kHistRow = 72;          // boundary positions 0..64
+
 // Global workspace: tile counter, T image, side-table values, boundary bytes.
 struct MitmWorkspace {
-    size_t off_timg, off_val, off_bnd, bytes;
+    size_t off_hist, off_plan, off_timg, off_val, off_bnd, bytes;
     int64_t entries;
 };
 
@@ -476,7 +482,9 @@ inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWo
     }
     st.start[st.n_tab] = (int64_t)e;
     ws.entries = (int64_t)e;
-    ws.off_timg = 256;
+    ws.off_hist = 256;
+    ws.off_plan = ws.off_hist + (((size_t)2 * kMitmMaxM * kHistRow * 4 + 255) & ~(size_t)255);
+    ws.off_timg = ws.off_plan + (((size_t)kMitmMaxBlocks * 2 + (size_t)(kMitmMaxBlocks + 1) * 4 + 255) & ~(size_t)255);
     ws.off_val = ws.off_timg + ((((size_t)L.M.t_elems * 8) + 255) & ~(size_t)255);
     ws.off_bnd = ws.off_val + (((size_t)ws.entries * 8 + 255) & ~(size_t)255);
     ws.bytes = ws.off_bnd + (((size_t)ws.entries + 255) & ~(size_t)255);
@@ -484,15 +492,22 @@ inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWo
         std::stable_sort(mine.begin(), mine.end(), [&](int a, int b) { return blk[a].tile > blk[b].tile; });
         sp->nbp = (int)mine.size();
         for (int i = 0; i < sp->nbp; ++i) sp->order[i] = (int16_t)mine[i];
-        for (int m = 0; m < kMitmMaxM; ++m) { sp->offL[m] = st.offL[m]; sp->offR[m] = st.offR[m]; }
+        for (int m = 0; m < kMitmMaxM; ++m) {
+            sp->offL[m] = st.offL[m]; sp->offR[m] = st.offR[m];
+            sp->tabL[m] = sp->tabR[m] = -1;
+        }
+        for (int i = 0; i < st.n_tab; ++i) (st.kind[i] ? sp->tabR : sp->tabL)[st.km[i]] = (int8_t)i;
     }
     return true;
 }
 
 // ------------------------------------------------------------ 1. T image
-__global__ void __launch_bounds__(256) memo_image_kernel(const dm_tables tp, double* __restrict__ timg) {
+__global__ void __launch_bounds__(256) memo_image_kernel(const dm_tables tp, double* __restrict__ timg,
+                                                         int* __restrict__ hist) {
     const dm_tables t = tp;
     const int n = t.n, rmax = n < t.p ? n : t.p;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * kMitmMaxM * kHistRow; i += gridDim.x * blockDim.x)
+        hist[i] = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)rmax * n * n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int q = (int)(i / ((int64_t)n * n)), a = (int)((i / n) % n), b = (int)(i % n) + 1;
@@ -517,7 +532,7 @@ template <typename Mask>   // uint32_t when every cut position fits 32 bits (n <
 __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, const double* __restrict__ timg,
                                                           const __grid_constant__ SideTables st,
                                                           double* __restrict__ val, uint8_t* __restrict__ bnd,
-                                                          int* __restrict__ counter) {
+                                                          int* __restrict__ counter, int* __restrict__ hist) {
     extern __shared__ __align__(16) int64_t binom_s[];
     const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, R1 = rmax + 1;
     int32_t* rowrel = reinterpret_cast<int32_t*>(binom_s + n * R1);       // memo_row(q, a) for a < n
@@ -563,6 +578,7 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
             ti = lo;
         }
         Mask mk = 0;
+        int key0 = -1, cnt0 = 0;        // histogram bucket of the pass's first entry, its finite count
         for (int u = 0; u < kTabPass; ++u) {
             const int64_t e = e0 + u;
             if (e >= E) break;
@@ -600,8 +616,86 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
             }
             val[e] = v;
             bnd[e] = (uint8_t)prev;
+            const int key = ti * kHistRow + prev;
+            const bool fin = v < __longlong_as_double(0x7ff0000000000000LL);
+            if (key0 < 0) key0 = key;
+            if (key == key0) cnt0 += fin;
+            else if (fin) atomicAdd(hist + key, 1);          // rare: the pass crosses a boundary position
         }
+        // warp-aggregated flush of the first buckets
+        const unsigned act = __activemask();
+        const unsigned grp = __match_any_sync(act, key0);
+        const int sum = __reduce_add_sync(grp, cnt0);
+        if (key0 >= 0 && sum > 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(hist + key0, sum);
     }
+}
+
+// ------------------------------------------------------------ 2b. tile plan
+// One CTA: the part's blocks ordered by the predicted duration of one of
+// their tiles, longest first — feasible pairs bounded by the side tables'
+// finite entries (the histogram by boundary position) plus ~50
+// pair-equivalents per element built; ties keep the host order (largest
+// tiles first).  Writes the order and the inclusive tile prefix.
+constexpr int kPlanThreads = 1024;
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, const __grid_constant__ SweepParams P,
+                                                            const int* __restrict__ hist, int16_t* __restrict__ pos,
+                                                            int32_t* __restrict__ tstart) {
+    __shared__ double key[kMitmMaxBlocks];
+    __shared__ int32_t ntl[kMitmMaxBlocks];
+    __shared__ int32_t cnt[kMitmMaxBlocks];
+    __shared__ int32_t wsum[kPlanThreads / 32];
+    const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, nbp = P.nbp;
+    for (int i = threadIdx.x; i < nbp; i += blockDim.x) {
+        const int b = P.order[i];
+        int m = 0, base = 0;
+        while (m + 1 < rmax && base + mitm_blocks_of(m, W) <= b) { base += mitm_blocks_of(m, W); ++m; }
+        const int j = m == 0 ? 0 : mitm_j(m), c = m == 0 ? 0 : j + (b - base);
+        const int64_t nl = m == 0 ? 1 : binom_sat(c - 1, j - 1), nr = m == 0 ? 1 : binom_sat(W - c, m - j);
+        const int64_t nX = nl >= nr ? nl : nr, nY = nl >= nr ? nr : nl;
+        int64_t R = nY >= kThinY ? 1 : kThinPairs / (kMitmTX * nY);
+        R = R < 1 ? 1 : (R > kThinRounds ? kThinRounds : R);
+        const int64_t txs = (int64_t)kMitmTX * R;
+        const int64_t nt = ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
+        double fl = 1.0, fr = 1.0;
+        if (m > 0 && P.tabL[j - 1] >= 0 && P.tabR[m] >= 0) {
+            const int* hl = hist + P.tabL[j - 1] * kHistRow;
+            const int* hr = hist + P.tabR[m] * kHistRow;
+            int sl = 0, sr = 0;
+            for (int xpos = 0; xpos < c; ++xpos) sl += hl[xpos];
+            for (int xpos = c + 1; xpos <= n; ++xpos) sr += hr[xpos];
+            fl = (double)sl; fr = (double)sr;
+        }
+        const double ex = (double)(nX < txs ? nX : txs), ey = (double)(nY < kMitmTY ? nY : kMitmTY);
+        key[i] = fl * fr / (double)nt + 50.0 * (ex + ey);
+        ntl[i] = (int32_t)nt;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbp; i += blockDim.x) {
+        const double ki = key[i];
+        int r = 0;
+        for (int k2 = 0; k2 < nbp; ++k2) r += key[k2] > ki || (key[k2] == ki && k2 < i);
+        pos[r] = (int16_t)P.order[i];
+        cnt[r] = ntl[i];
+    }
+    __syncthreads();
+    // inclusive prefix of the tile counts in position order
+    const int per = (nbp + kPlanThreads - 1) / kPlanThreads;
+    const int b0 = threadIdx.x * per, b1 = b0 + per < nbp ? b0 + per : nbp;
+    int sum = 0;
+    for (int b = b0; b < b1; ++b) sum += cnt[b];
+    int incl = sum;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int wbase = 0;
+    for (int w2 = 0; w2 < wid; ++w2) wbase += wsum[w2];
+    int run = wbase + incl - sum;
+    for (int b = b0; b < b1; ++b) { run += cnt[b]; tstart[b + 1] = run; }
+    if (threadIdx.x == 0) tstart[0] = 0;
 }
 
 // ------------------------------------------------------------- 3. sweep
@@ -638,7 +732,7 @@ __device__ inline void sweep_prologue(const MitmLayout& L, unsigned char* sm) {
 __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_kernel(
         const dm_tables tp, const __grid_constant__ SweepParams P, int* __restrict__ ctl,
         const double* __restrict__ timg, const double* __restrict__ val, const uint8_t* __restrict__ bnd,
-        dm_winner* partial) {
+        dm_winner* partial, const int16_t* __restrict__ plan_pos, const int32_t* __restrict__ plan_tstart) {
     const dm_tables t = tp;   // register copy (no param-space references)
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ int s_cnt[2][2];       // [tile parity][X, Y] feasible counts
@@ -699,30 +793,10 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         bc[b] = (uint8_t)(m == 0 ? 0 : mitm_j(m) + (b - mbase[m]));
     }
     __syncthreads();
+    // ---- tile order and tile prefix from plan_kernel
     const int nbp = P.nbp;
-    for (int i = threadIdx.x; i < nbp; i += blockDim.x) {
-        const int b = P.order[i];
-        pos_blk[i] = (int16_t)b;
-        const Blk B = block_of(b, bm[b], bc[b]);
-        const int64_t nX = B.nl >= B.nr ? B.nl : B.nr, nY = B.nl >= B.nr ? B.nr : B.nl;
-        const int64_t txs = (int64_t)kMitmTX * B.R;
-        tstart[i + 1] = (int32_t)(((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY));
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x, per = (nbp + 31) / 32;
-        const int b0 = lane * per, b1 = b0 + per < nbp ? b0 + per : nbp;
-        int s = 0;
-        for (int b = b0; b < b1; ++b) s += tstart[b + 1];
-        int incl = s;
-        for (int off = 1; off < 32; off <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += o;
-        }
-        int run = incl - s;
-        for (int b = b0; b < b1; ++b) { run += tstart[b + 1]; tstart[b + 1] = run; }
-        if (lane == 0) tstart[0] = 0;
-    }
+    for (int i = threadIdx.x; i < nbp; i += blockDim.x) pos_blk[i] = plan_pos[i];
+    for (int i = threadIdx.x; i <= nbp; i += blockDim.x) tstart[i] = plan_tstart[i];
     if (threadIdx.x == 0) s_g[0] = atomicAdd(ctl, 1);   // dynamic tile queue over the part's blocks
     // the best makespan any CTA of the sweep has found so far (bits of a
     // non-negative double): tiles whose minimum exceeds it skip the rank
@@ -1075,6 +1149,9 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
     if (own) DM_CUDA(cudaMallocAsync(&buf, W.bytes, s));
     unsigned char* b8 = static_cast<unsigned char*>(buf);
     int* ctl = reinterpret_cast<int*>(b8);
+    int* hist = reinterpret_cast<int*>(b8 + W.off_hist);
+    int16_t* plan_pos = reinterpret_cast<int16_t*>(b8 + W.off_plan);
+    int32_t* plan_tstart = reinterpret_cast<int32_t*>(b8 + W.off_plan + (size_t)kMitmMaxBlocks * 2);
     double* timg = reinterpret_cast<double*>(b8 + W.off_timg);
     double* val = reinterpret_cast<double*>(b8 + W.off_val);
     uint8_t* bnd = b8 + W.off_bnd;
@@ -1085,7 +1162,7 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
     if (phase & 1) {
         const int64_t work = (int64_t)rmax * t.n * t.n;
         int blocks = (int)((work + 255) / 256);
-        memo_image_kernel<<<blocks, 256, 0, s>>>(t, timg);
+        memo_image_kernel<<<blocks, 256, 0, s>>>(t, timg, hist);
         DM_CHECK_LAUNCH();
     }
     if (phase & 1) {
@@ -1094,15 +1171,18 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         int64_t blocks = (W.entries + per - 1) / per;
         if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
         if (blocks < 1) blocks = 1;
-        if (t.n <= 34) side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl);
-        else side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl);
+        if (t.n <= 34) side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist);
+        else side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist);
         DM_CHECK_LAUNCH();
     }
     const int grid = mitm_grid(sms);
     if (phase & 2) {
         DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
         if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
-        splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial);
+        plan_kernel<<<1, kPlanThreads, 0, s>>>(t, sp, hist, plan_pos, plan_tstart);
+        DM_CHECK_LAUNCH();
+        splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial, plan_pos,
+                                                                plan_tstart);
         DM_CHECK_LAUNCH();
         if (tm.on) {
             DM_CUDA(cudaEventRecord(tm.ev[2], s));
