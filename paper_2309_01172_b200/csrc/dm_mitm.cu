@@ -637,20 +637,52 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
 // pair-equivalents per element built; ties keep the host order (largest
 // tiles first).  Writes the order and the inclusive tile prefix.
 constexpr int kPlanThreads = 1024;
+constexpr size_t kPlanSmem = (size_t)kMitmMaxBlocks * (8 + 4 + 2) + (size_t)2 * kMitmMaxM * kHistRow * 4 +
+                             (size_t)64 * (kMitmMaxM + 1) * 8;
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, const __grid_constant__ SweepParams P,
                                                             const int* __restrict__ hist, int16_t* __restrict__ pos,
                                                             int32_t* __restrict__ tstart) {
-    __shared__ double key[kMitmMaxBlocks];
-    __shared__ int32_t ntl[kMitmMaxBlocks];
-    __shared__ int32_t cnt[kMitmMaxBlocks];
+    extern __shared__ __align__(16) unsigned char psm[];   // kPlanSmem bytes
+    double* key = reinterpret_cast<double*>(psm);                                          // [kMitmMaxBlocks]
+    int32_t* ntl = reinterpret_cast<int32_t*>(psm + kMitmMaxBlocks * 8);                   // [kMitmMaxBlocks]
+    int32_t* hp = ntl + kMitmMaxBlocks;              // [2 kMitmMaxM][kHistRow]: per-row inclusive prefix
+    int16_t* sidx = reinterpret_cast<int16_t*>(hp + 2 * kMitmMaxM * kHistRow);            // [kMitmMaxBlocks]
+    int64_t* binom = reinterpret_cast<int64_t*>(sidx + kMitmMaxBlocks);                     // [n][rmax + 1]
     __shared__ int32_t wsum[kPlanThreads / 32];
-    const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, nbp = P.nbp;
-    for (int i = threadIdx.x; i < nbp; i += blockDim.x) {
+    const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, nbp = P.nbp, R1 = rmax + 1;
+    for (int i = threadIdx.x; i < 2 * kMitmMaxM * kHistRow; i += blockDim.x) hp[i] = hist[i];
+    if (threadIdx.x < 32) {                      // Pascal's triangle, exact for n <= 64
+        const int lane = threadIdx.x;
+        int64_t v0 = lane == 0, v1 = 0, v2 = 0;
+        for (int a = 0; a < n; ++a) {
+            if (a > 0) {
+                const int64_t u0 = __shfl_up_sync(0xffffffffu, v0, 1), u1 = __shfl_up_sync(0xffffffffu, v1, 1),
+                              u2 = __shfl_up_sync(0xffffffffu, v2, 1);
+                const int64_t t0 = __shfl_sync(0xffffffffu, v0, 31), t1 = __shfl_sync(0xffffffffu, v1, 31);
+                v2 += lane ? u2 : t1;
+                v1 += lane ? u1 : t0;
+                v0 += lane ? u0 : 0;
+            }
+            if (lane < R1) binom[a * R1 + lane] = v0;
+            if (lane + 32 < R1) binom[a * R1 + lane + 32] = v1;
+            if (lane + 64 < R1) binom[a * R1 + lane + 64] = v2;
+        }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < 2 * kMitmMaxM; r += blockDim.x) {
+        int acc = 0;
+        for (int xpos = 0; xpos < kHistRow; ++xpos) { acc += hp[r * kHistRow + xpos]; hp[r * kHistRow + xpos] = acc; }
+    }
+    __syncthreads();
+    int np2 = 2;
+    while (np2 < nbp) np2 <<= 1;
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        if (i >= nbp) { key[i] = -__longlong_as_double(0x7ff0000000000000LL); sidx[i] = (int16_t)i; continue; }
         const int b = P.order[i];
         int m = 0, base = 0;
         while (m + 1 < rmax && base + mitm_blocks_of(m, W) <= b) { base += mitm_blocks_of(m, W); ++m; }
         const int j = m == 0 ? 0 : mitm_j(m), c = m == 0 ? 0 : j + (b - base);
-        const int64_t nl = m == 0 ? 1 : binom_sat(c - 1, j - 1), nr = m == 0 ? 1 : binom_sat(W - c, m - j);
+        const int64_t nl = m == 0 ? 1 : binom[(c - 1) * R1 + (j - 1)], nr = m == 0 ? 1 : binom[(W - c) * R1 + (m - j)];
         const int64_t nX = nl >= nr ? nl : nr, nY = nl >= nr ? nr : nl;
         int64_t R = nY >= kThinY ? 1 : kThinPairs / (kMitmTX * nY);
         R = R < 1 ? 1 : (R > kThinRounds ? kThinRounds : R);
@@ -658,31 +690,40 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
         const int64_t nt = ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
         double fl = 1.0, fr = 1.0;
         if (m > 0 && P.tabL[j - 1] >= 0 && P.tabR[m] >= 0) {
-            const int* hl = hist + P.tabL[j - 1] * kHistRow;
-            const int* hr = hist + P.tabR[m] * kHistRow;
-            int sl = 0, sr = 0;
-            for (int xpos = 0; xpos < c; ++xpos) sl += hl[xpos];
-            for (int xpos = c + 1; xpos <= n; ++xpos) sr += hr[xpos];
-            fl = (double)sl; fr = (double)sr;
+            const int* hl = hp + P.tabL[j - 1] * kHistRow;
+            const int* hr = hp + P.tabR[m] * kHistRow;
+            fl = (double)hl[c - 1];                              // boundary positions < c
+            fr = (double)(hr[kHistRow - 1] - hr[c]);             // boundary positions > c
         }
         const double ex = (double)(nX < txs ? nX : txs), ey = (double)(nY < kMitmTY ? nY : kMitmTY);
         key[i] = fl * fr / (double)nt + 50.0 * (ex + ey);
+        sidx[i] = (int16_t)i;
         ntl[i] = (int32_t)nt;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nbp; i += blockDim.x) {
-        const double ki = key[i];
-        int r = 0;
-        for (int k2 = 0; k2 < nbp; ++k2) r += key[k2] > ki || (key[k2] == ki && k2 < i);
-        pos[r] = (int16_t)P.order[i];
-        cnt[r] = ntl[i];
-    }
-    __syncthreads();
-    // inclusive prefix of the tile counts in position order
+    // bitonic sort: descending key, ties by ascending host position
+    for (int k = 2; k <= np2; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+                const int ixj = i ^ jj;
+                if (ixj > i) {
+                    const double ka = key[i], kb = key[ixj];
+                    const int ia = sidx[i], ib = sidx[ixj];
+                    const bool b_first = kb > ka || (kb == ka && ib < ia);
+                    const bool a_first = ka > kb || (ka == kb && ia < ib);
+                    if (((i & k) == 0) ? b_first : a_first) {
+                        key[i] = kb; key[ixj] = ka;
+                        sidx[i] = (int16_t)ib; sidx[ixj] = (int16_t)ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // order and inclusive tile prefix in position order
     const int per = (nbp + kPlanThreads - 1) / kPlanThreads;
     const int b0 = threadIdx.x * per, b1 = b0 + per < nbp ? b0 + per : nbp;
     int sum = 0;
-    for (int b = b0; b < b1; ++b) sum += cnt[b];
+    for (int r = b0; r < b1; ++r) { pos[r] = (int16_t)P.order[sidx[r]]; sum += ntl[sidx[r]]; }
     int incl = sum;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int off = 1; off < 32; off <<= 1) {
@@ -694,7 +735,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
     int wbase = 0;
     for (int w2 = 0; w2 < wid; ++w2) wbase += wsum[w2];
     int run = wbase + incl - sum;
-    for (int b = b0; b < b1; ++b) { run += cnt[b]; tstart[b + 1] = run; }
+    for (int r = b0; r < b1; ++r) { run += ntl[sidx[r]]; tstart[r + 1] = run; }
     if (threadIdx.x == 0) tstart[0] = 0;
 }
 
@@ -1179,7 +1220,10 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
     if (phase & 2) {
         DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
         if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
-        plan_kernel<<<1, kPlanThreads, 0, s>>>(t, sp, hist, plan_pos, plan_tstart);
+        // the tile order from the tables' histogram (on the sweep's stream: a
+        // one-CTA kernel queued behind a running sweep would wait for its tail)
+        DM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlanSmem));
+        plan_kernel<<<1, kPlanThreads, kPlanSmem, s>>>(t, sp, hist, plan_pos, plan_tstart);
         DM_CHECK_LAUNCH();
         splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial, plan_pos,
                                                                 plan_tstart);
