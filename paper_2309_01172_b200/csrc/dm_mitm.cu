@@ -59,9 +59,19 @@ __device__ unsigned long long g_mitm_times[1024][12];
 // thread 0's clock in each phase of a tile: [6] elements + barrier, [7] cross
 // product, [8] winner check + end barrier, [9] tiles, [10] thin tiles
 #define MITM_CLK(v) long long v = clock64()
+// per tile: block, clocks of thread 0 from the tile's start to its end barrier, X and Y elements
+__device__ unsigned int g_mitm_tiles[1 << 16][4];
+#define MITM_TILE(g, blk, a, b, nx, ny)                                                                \
+    do {                                                                                           \
+        if (threadIdx.x == 0 && (g) < (1 << 16)) {                                                 \
+            g_mitm_tiles[g][0] = (unsigned)(blk); g_mitm_tiles[g][1] = (unsigned)((b) - (a));       \
+            g_mitm_tiles[g][2] = (unsigned)(nx); g_mitm_tiles[g][3] = (unsigned)(ny);               \
+        }                                                                                          \
+    } while (0)
 #define MITM_ACC(i, a, b) do { if (threadIdx.x == 0) g_mitm_times[blockIdx.x][i] += (unsigned long long)((b) - (a)); } while (0)
 #else
 #define MITM_CLK(v) do { } while (0)
+#define MITM_TILE(g, blk, a, b, nx, ny) do { } while (0)
 #define MITM_ACC(i, a, b) do { } while (0)
 #define MITM_MARK(i) do { } while (0)
 #define MITM_COUNT(i, v) do { } while (0)
@@ -1105,6 +1115,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         __syncthreads();   // buffers, counters and s_best for the next tile
         MITM_CLK(c_t3);
         MITM_ACC(8, c_t0, c_t3);
+        MITM_TILE(g, blk, c_t0, c_t3, nXr, nYr);
         MITM_ACC(9, 0, 1);
     }
     uint64_t c = 0;
@@ -1256,6 +1267,10 @@ extern "C" int dm_sweep_timing(int32_t enable, float* ms_tables, float* ms_sweep
 }
 
 #ifdef DM_MITM_TIMING
+extern "C" __attribute__((visibility("default"))) int dm_debug_mitm_tiles(unsigned int* host) {
+    return (int)cudaMemcpyFromSymbol(host, dm::g_mitm_tiles, sizeof(dm::g_mitm_tiles));
+}
+
 extern "C" __attribute__((visibility("default"))) int dm_debug_mitm_times(unsigned long long* host) {
     return (int)cudaMemcpyFromSymbol(host, dm::g_mitm_times, sizeof(dm::g_mitm_times));
 }
