@@ -6,11 +6,11 @@ Llama-2-7B training workflow (34 layer cells) over a 32-device heterogeneous
 fleet, EXHAUSTIVE split sweep: all 8,589,934,558 contiguous splits with run q
 on worker q, each scored with the reference cost model (fits + compute +
 crossing read, makespan) and reduced to the first strict minimum by
-(makespan, rank).  One step = the full sweep of that fleet under each of 8
+(makespan, rank).  One step = the full sweep of that fleet under each of 16
 default-link settings (configs.C2_LINKS, the base 5 ms / 10 Gbit/s first):
-8 x 8.59e9 candidates.  The 8 scenarios are sharded across the ranks (whole
+16 x 8.59e9 candidates.  The 16 scenarios are sharded across the ranks (whole
 scenarios per GPU, strong scaling; block-level parts of every scenario when
-8 is not a multiple of the GPU count), plus one NCCL all-gather of the
+16 is not a multiple of the GPU count), plus one NCCL all-gather of the
 per-rank winner records.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]

@@ -166,11 +166,11 @@ def c2_fleet_doc(seed: int = 0, alpha_s: float = 5e-3, bandwidth_gbps: float = 1
     return fleet_doc(hetero_peers(32, seed), alpha_s, bandwidth_gbps, name="c2-hetero32")
 
 
-# The C2 fleet under 8 network conditions (default-link latency s, bandwidth
-# Gbit/s): the base 5 ms / 10 Gbit/s first, then a what-if grid.  The bench's
-# step sweeps all 8 (one scenario batch, sharded across the GPUs).
-C2_LINKS = ((5e-3, 10.0), (1e-3, 10.0), (5e-3, 1.0), (1e-3, 1.0),
-            (5e-3, 25.0), (1e-3, 25.0), (5e-3, 100.0), (1e-3, 100.0))
+# The C2 fleet under 16 network conditions (default-link latency s, bandwidth
+# Gbit/s): the base 5 ms / 10 Gbit/s first, then the rest of a what-if grid
+# {5, 2, 1, 0.5} ms x {10, 1, 25, 100} Gbit/s.  The bench's step sweeps all 16
+# (one scenario batch, sharded across the GPUs: 2 per GPU at N = 8).
+C2_LINKS = tuple((a, bw) for a in (5e-3, 2e-3, 1e-3, 5e-4) for bw in (10.0, 1.0, 25.0, 100.0))
 
 
 def c3_fleet_doc(seed: int = 0, p: int = 256):
