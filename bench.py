@@ -258,6 +258,11 @@ def run_b200(args, rank, world, local_rank):
     e2e_val = S * total * args.steps / (e2e_ms / 1e3)
     cross = extras.get("cross_peak_pairs_per_s")
     achieved = feas0 / (sweep_ms / 1e3) / 1e9      # one launch of the dominant kernel
+    # theoretical ALU-pipe bound of the inner loop: 64 integer/select lane-ops
+    # per clock per SM, 3 per candidate pair (FSEL, SEL, half of IADD3 + IADD3.X)
+    alu_peak = None
+    if clk and clk.get("sm_mhz"):
+        alu_peak = torch.cuda.get_device_properties(dev).multi_processor_count * clk["sm_mhz"] * 1e6 * 64 / 3
     traffic = ncu_traffic("splits_sweep_kernel") or {}
     csum = 0
     for r in res:
@@ -273,6 +278,7 @@ def run_b200(args, rank, world, local_rank):
         "roofline": {"bound": "issue", "achieved": achieved, "peak": (cross / 1e9) if cross else None,
                      "unit": "Gcand/s", "frac": (achieved / (cross / 1e9)) if cross else None,
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("capture"),
+                     "alu_peak_pairs_per_s": alu_peak, "frac_of_alu_peak": (achieved * 1e9 / alu_peak) if alu_peak else None,
                      "kernel": "splits_sweep_kernel", "kernel_ms": sweep_ms, "table_phase_ms": tab_ms,
                      "per_rank_table_sweep_ms": per_rank,
                      "step_kernels_ms": kernel_ms,
