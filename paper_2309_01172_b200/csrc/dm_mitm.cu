@@ -13,7 +13,7 @@
 // runs; the winner key (makespan, rank) is the reference's first strict
 // minimum in itertools order.
 //
-// Three launches:
+// Launches per sweep (phase 1: 1-2, phase 2: 3-5; dm_enum_splits_phase):
 //  1. memo_image_kernel: T once into a global image (one entry per thread);
 //  2. side_tables_kernel: the side tables, every entry evaluated directly from
 //     its cut mask at full occupancy (T read through L1).  Left sides: the
@@ -25,9 +25,13 @@
 //     (W, W-1, ...), prefix C(W-c, m-j) for block c; an entry holds SV = max
 //     over the runs starting at one of its cuts and its lowest cut, so
 //     R = max(T[j][c][first], SV).  A side element then costs two loads and a
-//     max in the sweep;
-//  3. splits_sweep_kernel: tiles of the cross products, largest blocks first
-//     from a dynamic queue: TX elements of the larger side (registers, 8 per
+//     max in the sweep.  It also counts the finite entries per (table,
+//     boundary position);
+//  3. plan_kernel (one CTA): the tile order — blocks ranked by the feasible
+//     pairs per tile those counts predict (an upper bound) plus the element
+//     builds, so the longest tiles start first;
+//  4. splits_sweep_kernel: tiles of the cross products from a dynamic queue
+//     in that order: TX elements of the larger side (registers, 8 per
 //     thread, compacted to the feasible ones) x TY elements of the smaller
 //     side (shared memory, compacted).  Each candidate costs one fp64 max and
 //     its checksum add.  The tile's minimum and first rank follow in closed
@@ -35,8 +39,10 @@
 //     with X_x <= tm and Y_y <= tm has makespan exactly tm, so the smallest
 //     rank at tm is min RX + min RY over those elements (ranks are derived
 //     from the elements' cut masks, only for tiles that can hold the
-//     incumbent).  Infeasible pairs (a run that does not fit: T = +inf) are
-//     counted and their +inf contributions removed from the checksum.
+//     incumbent, which the CTAs share through a global atomic min).
+//     Infeasible pairs (a run that does not fit: T = +inf) are counted and
+//     their +inf contributions removed from the checksum;
+//  5. finalize_kernel (dm_enum.cu): the CTAs' partial winners merged.
 #include "dm_common.cuh"
 #include "dm_memo.cuh"
 #include "dm_mitm.cuh"
