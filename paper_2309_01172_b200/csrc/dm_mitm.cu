@@ -307,6 +307,15 @@ __device__ __forceinline__ double side_finish(const MitmCtx& x, const Blk& B, bo
     return tv > raw ? tv : raw;
 }
 
+// The same with the tile's finishing runs staged in shared memory:
+// col[a] = T[j-1][a][c] (left sides), row[b] = T[j][c][b] (right sides).
+__device__ __forceinline__ double side_finish_s(const Blk& B, bool left, double raw, int b, const double* col,
+                                                const double* row, int n) {
+    if (B.m == 0) return left ? -__longlong_as_double(0x7ff0000000000000LL) : row[n];
+    const double tv = left ? col[b] : row[b];
+    return tv > raw ? tv : raw;
+}
+
 __device__ __forceinline__ double block_min_f64(double v, double* red) {
     for (int off = 16; off > 0; off >>= 1) {
         const double o = __shfl_xor_sync(0xffffffffu, v, off);
@@ -862,6 +871,25 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     unsigned long long gb = 0x7ff0000000000000ull;
     __syncthreads();
     const int n_tiles = tstart[nbp];
+    // the finishing runs of a tile, staged one tile ahead by warp 1 into the
+    // other parity's buffers (visible after the tile's end barrier)
+    __shared__ double s_col[2][kMitmMaxM + 1], s_row[2][kMitmMaxM + 2];
+    auto stage = [&](int buf, int gn) {
+        if (gn >= n_tiles) return;
+        int lo = 0, hi = nbp - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (tstart[mid] <= gn) lo = mid; else hi = mid - 1;
+        }
+        const int b = pos_blk[lo], m = bm[b], c = bc[b], j = m == 0 ? 0 : mitm_j(m);
+        const int lane = threadIdx.x & 31;
+        if (m > 0)
+            for (int a = j - 1 + lane; a < c; a += 32) s_col[buf][a] = tval(x, j - 1, a, c);
+        const int rr = memo_row(j, c, n);
+        for (int bb = c + 1 + lane; bb <= n; bb += 32) s_row[buf][bb] = __ldg(timg + rr + bb);
+    };
+    if ((threadIdx.x >> 5) == 1) stage(0, s_g[0]);
+    __syncthreads();
     MITM_MARK(2);
 
     Win w;
@@ -908,13 +936,14 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 const int e = threadIdx.x;
                 double v = inf;
                 if (e < nYr) {
-                    v = side_finish(x, B, !xl, B.m ? __ldcg(val + yoff + y0 + e) : 0.0, B.m ? __ldcg(bnd + yoff + y0 + e) : 0);
+                    v = side_finish_s(B, !xl, B.m ? __ldcg(val + yoff + y0 + e) : 0.0, B.m ? __ldcg(bnd + yoff + y0 + e) : 0, s_col[par], s_row[par], n);
                     ymin = v < ymin ? v : ymin;
                 }
                 append_if(v != inf, v, by, &s_cnt[par][1]);
             }
             if (ymin <= best) atomicOr(&s_flag[par], 2);
             __syncthreads();
+            if ((threadIdx.x >> 5) == 1) stage(par ^ 1, s_g[par ^ 1]);
             MITM_CLK(c_t1);
             MITM_ACC(6, c_t0, c_t1);
             MITM_ACC(10, 0, 1);
@@ -942,7 +971,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
                     for (int u = 0; u < kMitmNR; ++u) {
                         const int e = r0 + u * kMitmThreads + threadIdx.x;
-                        const double v = e < nXr ? side_finish(x, B, xl, xr[u], xb[u]) : inf;
+                        const double v = e < nXr ? side_finish_s(B, xl, xr[u], xb[u], s_col[par], s_row[par], n) : inf;
                         xmin = v < xmin ? v : xmin;
                         const unsigned bal = __ballot_sync(0xffffffffu, v != inf);
                         if (v != inf) wbuf[f + __popc(bal & ((1u << lane) - 1u))] = v;
@@ -1006,7 +1035,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             for (int u = 0; u < kMitmNR; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
                 double v = inf;
-                if (e < nXr) { v = side_finish(x, B, xl, xr[u], xb[u]); xmin = v < xmin ? v : xmin; }
+                if (e < nXr) { v = side_finish_s(B, xl, xr[u], xb[u], s_col[par], s_row[par], n); xmin = v < xmin ? v : xmin; }
                 append_if(v != inf, v, bx, &s_cnt[par][0]);
             }
     #pragma unroll 1
@@ -1022,13 +1051,14 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 for (int u = 0; u < kYc; ++u) {
                     const int e = (h + u) * kMitmThreads + threadIdx.x;
                     double v = inf;
-                    if (e < nYr) { v = side_finish(x, B, !xl, yr[u], yb[u]); ymin = v < ymin ? v : ymin; }
+                    if (e < nYr) { v = side_finish_s(B, !xl, yr[u], yb[u], s_col[par], s_row[par], n); ymin = v < ymin ? v : ymin; }
                     append_if(v != inf, v, by, &s_cnt[par][1]);
                 }
             }
             const int fl = (xmin <= best ? 1 : 0) | (ymin <= best ? 2 : 0);
             if (fl) atomicOr(&s_flag[par], fl);
             __syncthreads();
+            if ((threadIdx.x >> 5) == 1) stage(par ^ 1, s_g[par ^ 1]);
             MITM_CLK(c_t1);
             MITM_ACC(6, c_t0, c_t1);
             const int nxf_tot = s_cnt[par][0];
