@@ -874,6 +874,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     // the finishing runs of a tile, staged one tile ahead by warp 1 into the
     // other parity's buffers (visible after the tile's end barrier)
     __shared__ double s_col[2][kMitmMaxM + 1], s_row[2][kMitmMaxM + 2];
+    __shared__ int s_lo[2];            // the tile's position in the block order
     auto stage = [&](int buf, int gn) {
         if (gn >= n_tiles) return;
         int lo = 0, hi = nbp - 1;
@@ -883,6 +884,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         }
         const int b = pos_blk[lo], m = bm[b], c = bc[b], j = m == 0 ? 0 : mitm_j(m);
         const int lane = threadIdx.x & 31;
+        if (lane == 0) s_lo[buf] = lo;
         if (m > 0)
             for (int a = j - 1 + lane; a < c; a += 32) s_col[buf][a] = tval(x, j - 1, a, c);
         const int rr = memo_row(j, c, n);
@@ -907,11 +909,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             s_g[par ^ 1] = atomicAdd(ctl, 1);   // read after the end barrier
             gb = *reinterpret_cast<volatile unsigned long long*>(gbest);
         }
-        int lo = 0, hi = nbp - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (tstart[mid] <= g) lo = mid; else hi = mid - 1;
-        }
+        const int lo = s_lo[par];          // staged with the tile's finishing runs
         const int blk = pos_blk[lo];
         const Blk B = block_of(blk, bm[blk], bc[blk]);
         const bool xl = B.nl >= B.nr;
