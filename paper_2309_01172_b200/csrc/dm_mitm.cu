@@ -846,8 +846,8 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         }
         B.rrow = memo_row(B.j, c, x.n);
         const int64_t nY = B.nl >= B.nr ? B.nr : B.nl;
-        int64_t R = nY >= kThinY ? 1 : kThinPairs / (kMitmTX * nY);
-        B.R = (int)(R < 1 ? 1 : (R > kThinRounds ? kThinRounds : R));
+        const int R = nY >= kThinY ? 1 : (int)((unsigned)kThinPairs / (unsigned)(kMitmTX * (int)nY));   // 32-bit: nY < kThinY
+        B.R = R < 1 ? 1 : (R > kThinRounds ? kThinRounds : R);
         return B;
     };
     // ---- plan: (m, c) per block; tiles per position of the size order,
