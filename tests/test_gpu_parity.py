@@ -445,3 +445,28 @@ def test_sweep_graph_units_overlap_matches_enum(engine_ready):
     engine.enum(batch, "splits", 0, total, bufs, index=1, phase=2)
     assert bufs.read() == want[1]
     torch.cuda.synchronize()
+
+
+def test_splits_phase_needs_workspace(engine_ready):
+    """dm_enum_splits_phase: the split halves (1, 2) need the caller's
+    workspace (the tables live there between the calls) and fail loudly
+    without one; phase 3 without a workspace allocates its own."""
+    import ctypes as C
+    import torch
+    from paper_2309_01172_b200 import _lib
+    rng = np.random.default_rng(5)
+    st, fleet = big_instance(rng, 16, 8, dag=False, links=False, pressure=(0.1, 0.7))
+    batch = engine.device_batch([build_host(st, fleet)])
+    total = engine.splits_total(16, 8)
+    lib = _lib.load()
+    bufs = engine.WinnerBuffers(batch.dev_buf.device)
+    stt = batch.struct(0)
+    for phase in (1, 2):
+        rc = lib.dm_enum_splits_phase(C.byref(stt), 0, total, 0, 1, bufs.out.data_ptr(), bufs.scratch.data_ptr(),
+                                      None, 0, phase, _lib.stream_ptr())
+        assert rc != 0
+    rc = lib.dm_enum_splits_phase(C.byref(stt), 0, total, 0, 1, bufs.out.data_ptr(), bufs.scratch.data_ptr(),
+                                  None, 0, 3, _lib.stream_ptr())
+    assert rc == 0
+    assert bufs.read() == engine.enum(batch, "splits", 0, total).read()
+    torch.cuda.synchronize()
