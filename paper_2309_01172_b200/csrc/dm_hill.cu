@@ -26,30 +26,74 @@ __device__ __forceinline__ double warp_max(double v) {
 // score() of _hill_climb over contiguous runs bounds[0..r] / peers[0..r)
 // held in shared memory: inf if verify_assignment fails (only capacities can
 // fail for these runs), else max over runs of compute + read.
-__device__ double hill_score(const dm_tables& t, int r, const int32_t* bounds, const int32_t* peers, int lane) {
+// Load of run q (compute + read) and whether it fails _fits.
+__device__ __forceinline__ double run_load(const dm_tables& t, int q, int r, const int32_t* bounds,
+                                           const int32_t* peers, bool& bad) {
+    int a = bounds[q], b = bounds[q + 1], w = peers[q];
+    bad = cap_violation(t, w, a, b) != 0;
+    if (bad) return 0.0;
+    double c, rd;
+    if (chain(t)) {
+        int prev = q > 0 ? peers[q - 1] : -1;
+        run_cost_contig(t, a, b, w, [&](int) { return prev; }, c, rd);
+    } else {
+        BoundsOwner own{bounds, peers, r};
+        run_cost_contig(t, a, b, w, own, c, rd);
+    }
+    return c + rd;
+}
+
+// score() over all runs; when lr/bd are given, every run's load and fit
+// flag are kept there for the incremental scores below.
+__device__ double hill_score(const dm_tables& t, int r, const int32_t* bounds, const int32_t* peers, int lane,
+                             double* lr = nullptr, uint8_t* bd = nullptr) {
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
     bool bad = false;
     double best = 0.0;
     for (int q = lane; q < r; q += 32) {
-        int a = bounds[q], b = bounds[q + 1], w = peers[q];
-        if (cap_violation(t, w, a, b)) { bad = true; continue; }
-        double c, rd;
-        if (chain(t)) {
-            int prev = q > 0 ? peers[q - 1] : -1;
-            run_cost_contig(t, a, b, w, [&](int) { return prev; }, c, rd);
-        } else {
-            BoundsOwner own{bounds, peers, r};
-            run_cost_contig(t, a, b, w, own, c, rd);
-        }
-        double load = c + rd;
+        bool b;
+        const double load = run_load(t, q, r, bounds, peers, b);
+        if (lr) { lr[q] = load; bd[q] = b; }
+        if (b) { bad = true; continue; }
         best = load > best ? load : best;
+    }
+    if (lr) __syncwarp();
+    if (__any_sync(0xffffffffu, bad)) return inf;
+    return warp_max(best);
+}
+
+// score() after moving boundary a+1 when only runs a and a+1 change (chain
+// stages, or links that do not depend on which run owns a source): those
+// two recomputed by lanes 0 and 1, the rest read from lr/bd — the same max
+// as hill_score (max is exact).  nv/nb: the two new loads / flags.
+__device__ double hill_score_move(const dm_tables& t, int r, int a, const int32_t* bounds, const int32_t* peers,
+                                  int lane, const double* lr, const uint8_t* bd, double& nv, bool& nb) {
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    bool bad = false;
+    double best = 0.0;
+    nv = 0.0;
+    nb = false;
+    if (lane < 2) {
+        nv = run_load(t, a + lane, r, bounds, peers, nb);
+        if (nb) bad = true;
+        else best = nv;
+    }
+    for (int q = lane; q < r; q += 32) {
+        if (q == a || q == a + 1) continue;
+        if (bd[q]) { bad = true; continue; }
+        best = lr[q] > best ? lr[q] : best;
     }
     if (__any_sync(0xffffffffu, bad)) return inf;
     return warp_max(best);
 }
 
+// Per-warp shared memory of prop_hill_kernel.
+__host__ __device__ inline size_t hill_warp_bytes(int n_max) {
+    return ((size_t)(2 * n_max + 1) * 8 + (size_t)2 * (n_max + 2) * 4 + (size_t)(n_max + 1) + 15) & ~(size_t)15;
+}
+
 // _proportional_runs on lane 0; returns r and fills bounds/peers.
-__device__ int proportional(const dm_tables& t, int32_t* bounds, int32_t* peers) {
+__device__ int proportional(const dm_tables& t, int32_t* bounds, int32_t* peers, const double* fls) {
     const int n = t.n, p = t.p;
     PySum ts;
     for (int w = 0; w < p; ++w) ts.add(t.speed[w], !(t.peer_np && t.peer_np[w]));
@@ -57,7 +101,7 @@ __device__ int proportional(const dm_tables& t, int32_t* bounds, int32_t* peers)
     double total_flops = col_range(t.flops, t.pre_flops, flops_exact(t), 0, n, np_flops(t));  // :333
     if (total_flops == 0.0) total_flops = 1.0;
     int start = 0, nr = 0;
-    double acc = 0.0, pf = t.flops[0];   // pf = prefix[end-1] (itertools.accumulate :334)
+    double acc = 0.0, pf = fls[0];       // pf = prefix[end-1] (itertools.accumulate :334), flops staged in smem
     int pf_at = 0;
     bounds[0] = 0;
     for (int wi = 0; wi < p; ++wi) {                                     // :337
@@ -69,7 +113,7 @@ __device__ int proportional(const dm_tables& t, int32_t* bounds, int32_t* peers)
             end = start + 1;
             while (true) {                                               // :345-346
                 if (end >= n) break;
-                while (pf_at < end - 1) { ++pf_at; pf = pf + t.flops[pf_at]; }
+                while (pf_at < end - 1) { ++pf_at; pf = pf + fls[pf_at]; }
                 if (!(pf < acc)) break;
                 ++end;
             }
@@ -88,16 +132,22 @@ __device__ int proportional(const dm_tables& t, int32_t* bounds, int32_t* peers)
 __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
         const dm_tables* __restrict__ tables, int32_t n_scen, int32_t n_max, const int16_t* __restrict__ init_owner,
         const uint8_t* __restrict__ do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves) {
-    extern __shared__ int32_t sh[];
+    extern __shared__ __align__(16) unsigned char shb[];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    int32_t* bounds = sh + (size_t)wl * 2 * (n_max + 2);
-    int32_t* peers = bounds + (n_max + 2);
+    unsigned char* mine = shb + (size_t)wl * hill_warp_bytes(n_max);
+    double* fls = reinterpret_cast<double*>(mine);                   // [n_max] the scenario's stage flops
+    double* lr = fls + n_max;                                         // [n_max + 1] run loads
+    int32_t* bounds = reinterpret_cast<int32_t*>(lr + n_max + 1);     // [n_max + 2]
+    int32_t* peers = bounds + (n_max + 2);                            // [n_max + 2]
+    uint8_t* bd = reinterpret_cast<uint8_t*>(peers + (n_max + 2));    // [n_max + 1] run fails _fits
     const int gw = blockIdx.x * kWarpsPerCta + wl, nw = gridDim.x * kWarpsPerCta;
     for (int sc = gw; sc < n_scen; sc += nw) {
         const dm_tables t = tables[sc];
         const int n = t.n;
         __syncwarp();
         int r = 0;
+        if (!init_owner) for (int i = lane; i < n; i += 32) fls[i] = t.flops[i];
+        __syncwarp();
         if (lane == 0) {
             if (init_owner) {
                 const int16_t* o = init_owner + (size_t)sc * n_max;
@@ -105,12 +155,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
                 for (int i = 1; i < n; ++i) if (o[i] != o[i - 1]) { bounds[++r] = i; peers[r] = o[i]; }
                 bounds[++r] = n;
             } else {
-                r = proportional(t, bounds, peers);
+                r = proportional(t, bounds, peers, fls);
             }
         }
         r = __shfl_sync(0xffffffffu, r, 0);
         __syncwarp();
-        double cur = hill_score(t, r, bounds, peers, lane);               // :365
+        // only the two runs at a moved boundary change unless reads depend on
+        // which run owns a source (pair links on DAG stages)
+        const bool incr = chain(t) || !include_comm(t) || !pair_links(t);
+        double cur = incr ? hill_score(t, r, bounds, peers, lane, lr, bd)
+                          : hill_score(t, r, bounds, peers, lane);        // :365
         int moves = 0;
         if (!do_hill || do_hill[sc]) {
             for (int round = 0; round < 200; ++round) {                   // :366
@@ -126,9 +180,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
                         __syncwarp();
                         if (lane == 0) bounds[a + 1] = nb;
                         __syncwarp();
-                        double cs = hill_score(t, r, bounds, peers, lane);
-                        if (cs < cur - 1e-15) { cur = cs; improved = true; ++moves; }  // :383-385
-                        else {
+                        double nv = 0.0;
+                        bool nbad = false;
+                        double cs = incr ? hill_score_move(t, r, a, bounds, peers, lane, lr, bd, nv, nbad)
+                                         : hill_score(t, r, bounds, peers, lane);
+                        if (cs < cur - 1e-15) {                           // :383-385
+                            cur = cs; improved = true; ++moves;
+                            if (incr && lane < 2) { lr[a + lane] = nv; bd[a + lane] = nbad; }
+                            __syncwarp();
+                        } else {
                             __syncwarp();
                             if (lane == 0) bounds[a + 1] = old;
                             __syncwarp();
@@ -239,7 +299,7 @@ int dm_prop_hill(const dm_tables* tables, int32_t n_scen, int32_t n_max, const i
                  const uint8_t* do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves, void* stream) {
     if (!tables || n_scen < 0 || n_max <= 0 || !out_owner || !out_score) return dmabi::fail(DM_E_ARG, "dm_prop_hill: bad arguments");
     if (n_scen == 0) return DM_OK;
-    size_t smem = (size_t)dm::kWarpsPerCta * 2 * (n_max + 2) * sizeof(int32_t);
+    size_t smem = (size_t)dm::kWarpsPerCta * dm::hill_warp_bytes(n_max);
     if (smem > 200 * 1024) return dmabi::fail(DM_E_TOO_LARGE, "dm_prop_hill: too many stages");
     cudaFuncSetAttribute(dm::prop_hill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dm::prop_hill_kernel<<<hill_grid(n_scen), 32 * dm::kWarpsPerCta, smem, (cudaStream_t)stream>>>(
