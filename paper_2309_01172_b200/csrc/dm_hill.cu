@@ -2,10 +2,14 @@
 // pipeline epilogue.  One warp per scenario:
 //   * _proportional_runs (scheduling.py:328-351) runs on lane 0 (O(n + p),
 //     order-sensitive sums restated exactly);
-//   * _hill_climb (:354-388) keeps the reference's sequential first-improvement
-//     walk (uniform control flow across the warp) and parallelises each
-//     score() (:357-362) over runs: lanes cost runs, a warp max-reduce
-//     combines them;
+//   * _hill_climb (:354-388): the reference takes the first improving move
+//     (a, dir) in order, and until one improves every move is scored from the
+//     same state — so when a move changes only the two runs at its boundary
+//     (chain stages, no comm, or no pair links) the lanes score 32 moves at
+//     once (the two new run loads + prefix / suffix maxima of the others),
+//     apply the first improving one and resume after it; otherwise each
+//     score() (:357-362) is parallelised over runs (lanes cost runs, a warp
+//     max-reduce combines them);
 //   * the epilogue scores the final runs (_evaluate :210-232) and applies
 //     Eq. 3 / Eq. 4 (pipeline.py:41-62).
 #include "dm_common.cuh"
@@ -62,34 +66,21 @@ __device__ double hill_score(const dm_tables& t, int r, const int32_t* bounds, c
     return warp_max(best);
 }
 
-// score() after moving boundary a+1 when only runs a and a+1 change (chain
-// stages, or links that do not depend on which run owns a source): those
-// two recomputed by lanes 0 and 1, the rest read from lr/bd — the same max
-// as hill_score (max is exact).  nv/nb: the two new loads / flags.
-__device__ double hill_score_move(const dm_tables& t, int r, int a, const int32_t* bounds, const int32_t* peers,
-                                  int lane, const double* lr, const uint8_t* bd, double& nv, bool& nb) {
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
-    bool bad = false;
-    double best = 0.0;
-    nv = 0.0;
-    nb = false;
-    if (lane < 2) {
-        nv = run_load(t, a + lane, r, bounds, peers, nb);
-        if (nb) bad = true;
-        else best = nv;
-    }
-    for (int q = lane; q < r; q += 32) {
-        if (q == a || q == a + 1) continue;
-        if (bd[q]) { bad = true; continue; }
-        best = lr[q] > best ? lr[q] : best;
-    }
-    if (__any_sync(0xffffffffu, bad)) return inf;
-    return warp_max(best);
+// Load of the run [a, b) on worker w whose predecessor run is on prev, when
+// reads do not depend on which run owns a source: chain stages, no comm, or
+// no pair links (every source outside the run is on another peer).
+__device__ __forceinline__ double run_load_ab(const dm_tables& t, int a, int b, int w, int prev, bool& bad) {
+    bad = cap_violation(t, w, a, b) != 0;
+    if (bad) return 0.0;
+    double c, rd;
+    run_cost_contig(t, a, b, w, [&](int) { return prev; }, c, rd);
+    return c + rd;
 }
 
-// Per-warp shared memory of prop_hill_kernel.
+// Per-warp shared memory of prop_hill_kernel: stage flops, run loads and
+// their prefix / suffix maxima, bounds/peers, run fit flags.
 __host__ __device__ inline size_t hill_warp_bytes(int n_max) {
-    return ((size_t)(2 * n_max + 1) * 8 + (size_t)2 * (n_max + 2) * 4 + (size_t)(n_max + 1) + 15) & ~(size_t)15;
+    return ((size_t)(4 * n_max + 3) * 8 + (size_t)2 * (n_max + 2) * 4 + (size_t)(n_max + 1) + 15) & ~(size_t)15;
 }
 
 // _proportional_runs on lane 0; returns r and fills bounds/peers.
@@ -137,7 +128,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
     unsigned char* mine = shb + (size_t)wl * hill_warp_bytes(n_max);
     double* fls = reinterpret_cast<double*>(mine);                   // [n_max] the scenario's stage flops
     double* lr = fls + n_max;                                         // [n_max + 1] run loads
-    int32_t* bounds = reinterpret_cast<int32_t*>(lr + n_max + 1);     // [n_max + 2]
+    double* pm = lr + n_max + 1;                                      // [n_max + 1] prefix max of the loads
+    double* sm = pm + n_max + 1;                                      // [n_max + 1] suffix max
+    int32_t* bounds = reinterpret_cast<int32_t*>(sm + n_max + 1);     // [n_max + 2]
     int32_t* peers = bounds + (n_max + 2);                            // [n_max + 2]
     uint8_t* bd = reinterpret_cast<uint8_t*>(peers + (n_max + 2));    // [n_max + 1] run fails _fits
     const int gw = blockIdx.x * kWarpsPerCta + wl, nw = gridDim.x * kWarpsPerCta;
@@ -166,7 +159,78 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
         double cur = incr ? hill_score(t, r, bounds, peers, lane, lr, bd)
                           : hill_score(t, r, bounds, peers, lane);        // :365
         int moves = 0;
-        if (!do_hill || do_hill[sc]) {
+        if ((!do_hill || do_hill[sc]) && incr) {
+            // The reference walks moves (a, dir) in order and takes the first
+            // that improves (:366-387); until one does, every move is scored
+            // from the same state, so the lanes score 32 moves at a time:
+            // score = max(0, loads before a, loads after a+1, the two new
+            // loads) from prefix / suffix maxima (+inf marks a run failing
+            // _fits), the first improving move in order is applied and the
+            // walk resumes after it from the new state.
+            const double inf = __longlong_as_double(0x7ff0000000000000LL);
+            const int Lend = 2 * (r - 1);
+            int round = 0, L0 = 0;
+            bool improved = false;
+            while (true) {
+                if (lane == 0) {
+                    double m = 0.0;
+                    for (int q = 0; q < r; ++q) { const double v = bd[q] ? inf : lr[q]; m = v > m ? v : m; pm[q] = m; }
+                    m = 0.0;
+                    for (int q = r - 1; q >= 0; --q) { const double v = bd[q] ? inf : lr[q]; m = v > m ? v : m; sm[q] = m; }
+                }
+                __syncwarp();
+                int found = -1, fnb = 0;
+                double fcs = 0.0, fva = 0.0, fvb = 0.0;
+                bool fba = false, fbb = false;
+                for (int base = L0; base < Lend && found < 0; base += 32) {
+                    const int L = base + lane;
+                    bool imp = false, ba = false, bb = false;
+                    double cs = inf, va = 0.0, vb = 0.0;
+                    int nb = 0;
+                    if (L < Lend) {
+                        const int a = L >> 1, dir = L & 1;
+                        const int la = bounds[a + 1] - bounds[a], lb = bounds[a + 2] - bounds[a + 1];
+                        if ((dir == 0 && la > 1) || (dir == 1 && lb > 1)) {                      // :373-376
+                            nb = dir == 0 ? bounds[a + 1] - 1 : bounds[a + 1] + 1;
+                            va = run_load_ab(t, bounds[a], nb, peers[a], a > 0 ? peers[a - 1] : -1, ba);
+                            vb = run_load_ab(t, nb, bounds[a + 2], peers[a + 1], peers[a], bb);
+                            double sc2 = 0.0;
+                            if (a > 0) sc2 = pm[a - 1] > sc2 ? pm[a - 1] : sc2;
+                            if (a + 2 < r) sc2 = sm[a + 2] > sc2 ? sm[a + 2] : sc2;
+                            const double xa = ba ? inf : va, xb = bb ? inf : vb;
+                            sc2 = xa > sc2 ? xa : sc2;
+                            sc2 = xb > sc2 ? xb : sc2;
+                            cs = sc2;
+                            imp = cs < cur - 1e-15;                                              // :383
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, imp);
+                    if (bal) {
+                        const int src = __ffs(bal) - 1;
+                        found = base + src;
+                        fcs = __shfl_sync(0xffffffffu, cs, src);
+                        fva = __shfl_sync(0xffffffffu, va, src);
+                        fvb = __shfl_sync(0xffffffffu, vb, src);
+                        fba = __shfl_sync(0xffffffffu, (int)ba, src);
+                        fbb = __shfl_sync(0xffffffffu, (int)bb, src);
+                        fnb = __shfl_sync(0xffffffffu, nb, src);
+                    }
+                }
+                if (found >= 0) {                                                                // :384-385
+                    const int a = found >> 1;
+                    __syncwarp();
+                    if (lane == 0) { bounds[a + 1] = fnb; lr[a] = fva; lr[a + 1] = fvb; bd[a] = fba; bd[a + 1] = fbb; }
+                    __syncwarp();
+                    cur = fcs; improved = true; ++moves;
+                    L0 = found + 1;
+                    continue;
+                }
+                ++round;                                                                         // :386-387
+                if (!improved || round >= 200) break;
+                improved = false;
+                L0 = 0;
+            }
+        } else if (!do_hill || do_hill[sc]) {
             for (int round = 0; round < 200; ++round) {                   // :366
                 bool improved = false;
                 for (int a = 0; a + 1 < r; ++a) {                         // :368-369
@@ -180,15 +244,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
                         __syncwarp();
                         if (lane == 0) bounds[a + 1] = nb;
                         __syncwarp();
-                        double nv = 0.0;
-                        bool nbad = false;
-                        double cs = incr ? hill_score_move(t, r, a, bounds, peers, lane, lr, bd, nv, nbad)
-                                         : hill_score(t, r, bounds, peers, lane);
-                        if (cs < cur - 1e-15) {                           // :383-385
-                            cur = cs; improved = true; ++moves;
-                            if (incr && lane < 2) { lr[a + lane] = nv; bd[a + lane] = nbad; }
-                            __syncwarp();
-                        } else {
+                        double cs = hill_score(t, r, bounds, peers, lane);
+                        if (cs < cur - 1e-15) { cur = cs; improved = true; ++moves; }  // :383-385
+                        else {
                             __syncwarp();
                             if (lane == 0) bounds[a + 1] = old;
                             __syncwarp();
