@@ -120,6 +120,64 @@ __device__ int proportional(const dm_tables& t, int32_t* bounds, int32_t* peers,
     return nr;
 }
 
+// The same, warp-cooperative, when the stage flops are exact integers (then
+// prefix[k] = pre_flops[k+1] exactly, whatever the summation order): the
+// boundary of worker wi is max(start + 1, e*) clamped as at :348, where
+// e* = min{end : end == n or prefix[end-1] >= acc_wi} — a binary search per
+// worker on the lanes; acc (:343) and the clamps stay sequential on lane 0.
+// acc: scratch of n_max + 1 doubles.  Returns r on every lane.
+__device__ int proportional_warp(const dm_tables& t, int32_t* bounds, int32_t* peers, double* acc, int lane) {
+    const int n = t.n, p = t.p;
+    const int nw = (p - 1 < n ? p - 1 : n);      // workers that can need a search (each run takes >= 1 stage)
+    double total_speed = 0.0, total_flops = 0.0;
+    if (lane == 0) {
+        PySum ts;
+        for (int w = 0; w < p; ++w) ts.add(t.speed[w], !(t.peer_np && t.peer_np[w]));
+        total_speed = ts.value();                                        // :332
+        total_flops = (double)(t.pre_flops[n] - t.pre_flops[0]);         // :333
+        if (total_flops == 0.0) total_flops = 1.0;
+    }
+    total_speed = __shfl_sync(0xffffffffu, total_speed, 0);
+    total_flops = __shfl_sync(0xffffffffu, total_flops, 0);
+    for (int w = lane; w < nw; w += 32) acc[w] = (total_flops * t.speed[w]) / total_speed;
+    __syncwarp();
+    if (lane == 0) {
+        double a = 0.0;
+        for (int w = 0; w < nw; ++w) { a = a + acc[w]; acc[w] = a; }    // :343, in order
+    }
+    __syncwarp();
+    for (int w = lane; w < nw; w += 32) {
+        const double aw = acc[w];
+        int lo = 1, hi = n;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((double)t.pre_flops[mid] >= aw) hi = mid; else lo = mid + 1;
+        }
+        bounds[w + 1] = lo;                                              // e*, overwritten in order below
+    }
+    __syncwarp();
+    int nr = 0;
+    if (lane == 0) {
+        int start = 0;
+        bounds[0] = 0;
+        for (int wi = 0; wi < p; ++wi) {                                 // :337
+            if (start >= n) break;
+            int end;
+            if (wi == p - 1) end = n;
+            else {
+                end = bounds[wi + 1] > start + 1 ? bounds[wi + 1] : start + 1;   // :344-346
+                const int lim = n - (p - wi - 1);
+                end = end < lim ? end : lim;
+                end = end > start + 1 ? end : start + 1;                 // :348
+            }
+            peers[nr] = wi;
+            bounds[++nr] = end;
+            start = end;
+        }
+    }
+    return __shfl_sync(0xffffffffu, nr, 0);
+}
+
 __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
         const dm_tables* __restrict__ tables, int32_t n_scen, int32_t n_max, const int16_t* __restrict__ init_owner,
         const uint8_t* __restrict__ do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves) {
@@ -139,9 +197,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
         const int n = t.n;
         __syncwarp();
         int r = 0;
-        if (!init_owner) for (int i = lane; i < n; i += 32) fls[i] = t.flops[i];
+        const bool pwarp = !init_owner && flops_exact(t);
+        if (!init_owner && !pwarp) for (int i = lane; i < n; i += 32) fls[i] = t.flops[i];
         __syncwarp();
-        if (lane == 0) {
+        if (pwarp) r = proportional_warp(t, bounds, peers, pm, lane);
+        else if (lane == 0) {
             if (init_owner) {
                 const int16_t* o = init_owner + (size_t)sc * n_max;
                 bounds[0] = 0; peers[0] = o[0];
@@ -172,11 +232,31 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
             int round = 0, L0 = 0;
             bool improved = false;
             while (true) {
-                if (lane == 0) {
-                    double m = 0.0;
-                    for (int q = 0; q < r; ++q) { const double v = bd[q] ? inf : lr[q]; m = v > m ? v : m; pm[q] = m; }
-                    m = 0.0;
-                    for (int q = r - 1; q >= 0; --q) { const double v = bd[q] ? inf : lr[q]; m = v > m ? v : m; sm[q] = m; }
+                {   // warp max-scans, 32 runs at a time (max is exact in any order)
+                    double carry = 0.0;
+                    for (int base = 0; base < r; base += 32) {
+                        const int q = base + lane;
+                        double v = q < r ? (bd[q] ? inf : lr[q]) : 0.0;
+                        for (int off = 1; off < 32; off <<= 1) {
+                            const double o = __shfl_up_sync(0xffffffffu, v, off);
+                            if (lane >= off) v = o > v ? o : v;
+                        }
+                        v = carry > v ? carry : v;
+                        if (q < r) pm[q] = v;
+                        carry = __shfl_sync(0xffffffffu, v, 31);
+                    }
+                    carry = 0.0;
+                    for (int top = r - 1; top >= 0; top -= 32) {
+                        const int q = top - lane;
+                        double v = q >= 0 ? (bd[q] ? inf : lr[q]) : 0.0;
+                        for (int off = 1; off < 32; off <<= 1) {
+                            const double o = __shfl_up_sync(0xffffffffu, v, off);
+                            if (lane >= off) v = o > v ? o : v;
+                        }
+                        v = carry > v ? carry : v;
+                        if (q >= 0) sm[q] = v;
+                        carry = __shfl_sync(0xffffffffu, v, 31);
+                    }
                 }
                 __syncwarp();
                 int found = -1, fnb = 0;
@@ -258,8 +338,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
         }
         __syncwarp();
         int16_t* o = out_owner + (size_t)sc * n_max;
-        for (int q = 0; q < r; ++q)
-            for (int i = bounds[q] + lane; i < bounds[q + 1]; i += 32) o[i] = (int16_t)peers[q];
+        for (int i = lane; i < n; i += 32) {          // each stage's run by binary search over the bounds
+            int lo = 0, hi = r - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (bounds[mid] <= i) lo = mid; else hi = mid - 1;
+            }
+            o[i] = (int16_t)peers[lo];
+        }
         for (int i = n + lane; i < n_max; i += 32) o[i] = -1;
         if (lane == 0) { out_score[sc] = cur; if (out_moves) out_moves[sc] = moves; }
     }
