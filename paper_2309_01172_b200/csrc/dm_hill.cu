@@ -366,13 +366,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) epilogue_kernel(
         const int n = t.n;
         const int16_t* o = owner + (size_t)sc * n_max;
         __syncwarp();
-        int r = 0;
-        if (lane == 0) {
-            bounds[0] = 0; peers[0] = o[0];
-            for (int i = 1; i < n; ++i) if (o[i] != o[i - 1]) { bounds[++r] = i; peers[r] = o[i]; }
-            bounds[++r] = n;
+        int r = 0;                                     // runs from the owner row, 32 stages at a time
+        for (int base = 0; base < n; base += 32) {
+            const int i = base + lane;
+            const int oi = i < n ? o[i] : -1;
+            const bool start = i < n && (i == 0 || oi != o[i - 1]);
+            const unsigned bal = __ballot_sync(0xffffffffu, start);
+            if (start) {
+                const int k = r + __popc(bal & ((1u << lane) - 1u));
+                bounds[k] = i;
+                peers[k] = oi;
+            }
+            r += __popc(bal);
         }
-        r = __shfl_sync(0xffffffffu, r, 0);
+        if (lane == 0) bounds[r] = n;
         __syncwarp();
         int first_bad = 0x7fffffff, bad_code = 0;
         double mk = 0.0, bn = 0.0;
