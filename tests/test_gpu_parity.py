@@ -470,3 +470,20 @@ def test_splits_phase_needs_workspace(engine_ready):
     assert rc == 0
     assert bufs.read() == engine.enum(batch, "splits", 0, total).read()
     torch.cuda.synchronize()
+
+
+def test_sweep_graph_part_units_merge(engine_ready):
+    """A SweepGraph of block-level parts of one instance (the bench's units
+    when the scenario batch does not divide the GPUs): the parts' records
+    merge to the whole sweep's."""
+    import torch
+    from paper_2309_01172_b200 import dist as D
+    rng = np.random.default_rng(13)
+    st, fleet = big_instance(rng, 24, 14, dag=False, links=True, pressure=(0.1, 0.7))
+    batch = engine.device_batch([build_host(st, fleet)])
+    total = engine.splits_total(24, 14)
+    want = engine.enum(batch, "splits", 0, total).read()
+    g = engine.SweepGraph(batch, total, units=[(0, 0, 3), (0, 1, 3), (0, 2, 3)], copy_inputs=False)
+    g.launch()
+    torch.cuda.synchronize()
+    assert D.merge_records(g.out.cpu().numpy()) == want
