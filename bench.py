@@ -264,6 +264,7 @@ def run_b200(args, rank, world, local_rank):
     if clk and clk.get("sm_mhz"):
         alu_peak = torch.cuda.get_device_properties(dev).multi_processor_count * clk["sm_mhz"] * 1e6 * 64 / 3
     traffic = ncu_traffic("splits_sweep_kernel") or {}
+    hbm_peak = _hbm_peak()[0]
     csum = 0
     for r in res:
         csum = (csum + r["checksum"]) & ((1 << 64) - 1)
@@ -279,6 +280,10 @@ def run_b200(args, rank, world, local_rank):
                      "unit": "Gcand/s", "frac": (achieved / (cross / 1e9)) if cross else None,
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("capture"),
                      "alu_peak_pairs_per_s": alu_peak, "frac_of_alu_peak": (achieved * 1e9 / alu_peak) if alu_peak else None,
+                     "hbm_view": ({"achieved_gbs": traffic["bytes"] / (sweep_ms / 1e3) / 1e9, "peak_gbs": hbm_peak,
+                                   "frac": traffic["bytes"] / (sweep_ms / 1e3) / 1e9 / hbm_peak,
+                                   "note": "ncu DRAM bytes of one sweep / the kernel's duration: not memory bound"}
+                                  if traffic.get("bytes") and hbm_peak else None),
                      "kernel": "splits_sweep_kernel", "kernel_ms": sweep_ms, "table_phase_ms": tab_ms,
                      "per_rank_table_sweep_ms": per_rank,
                      "step_kernels_ms": kernel_ms,
