@@ -662,20 +662,27 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
 // pair-equivalents per element built; ties keep the host order (largest
 // tiles first).  Writes the order and the inclusive tile prefix.
 constexpr int kPlanThreads = 1024;
-constexpr size_t kPlanSmem = (size_t)kMitmMaxBlocks * (8 + 4 + 2) + (size_t)2 * kMitmMaxM * kHistRow * 4 +
-                             (size_t)64 * (kMitmMaxM + 1) * 8;
+// Shared memory of plan_kernel sized to the sweep (so it fits the carveout
+// the table and sweep kernels use): keys, tile counts and sort indices for
+// np2 >= nbp blocks, the histogram rows of the hrows tables, Pascal's triangle.
+__host__ __device__ inline size_t plan_smem(int np2, int hrows, int n, int rmax) {
+    return (size_t)np2 * 8 + (size_t)np2 * 4 + (size_t)hrows * kHistRow * 4 + (size_t)n * (rmax + 1) * 8 +
+           (((size_t)np2 * 2 + 15) & ~(size_t)15);
+}
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, const __grid_constant__ SweepParams P,
-                                                            const int* __restrict__ hist, int16_t* __restrict__ pos,
-                                                            int32_t* __restrict__ tstart) {
-    extern __shared__ __align__(16) unsigned char psm[];   // kPlanSmem bytes
-    double* key = reinterpret_cast<double*>(psm);                                          // [kMitmMaxBlocks]
-    int32_t* ntl = reinterpret_cast<int32_t*>(psm + kMitmMaxBlocks * 8);                   // [kMitmMaxBlocks]
-    int32_t* hp = ntl + kMitmMaxBlocks;              // [2 kMitmMaxM][kHistRow]: per-row inclusive prefix
-    int16_t* sidx = reinterpret_cast<int16_t*>(hp + 2 * kMitmMaxM * kHistRow);            // [kMitmMaxBlocks]
-    int64_t* binom = reinterpret_cast<int64_t*>(sidx + kMitmMaxBlocks);                     // [n][rmax + 1]
-    __shared__ int32_t wsum[kPlanThreads / 32];
+                                                            const int* __restrict__ hist, int hrows,
+                                                            int16_t* __restrict__ pos, int32_t* __restrict__ tstart) {
+    extern __shared__ __align__(16) unsigned char psm[];   // plan_smem bytes
     const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, nbp = P.nbp, R1 = rmax + 1;
-    for (int i = threadIdx.x; i < 2 * kMitmMaxM * kHistRow; i += blockDim.x) hp[i] = hist[i];
+    int np2 = 2;
+    while (np2 < nbp) np2 <<= 1;
+    double* key = reinterpret_cast<double*>(psm);                                          // [np2]
+    int64_t* binom = reinterpret_cast<int64_t*>(key + np2);                                // [n][rmax + 1]
+    int32_t* ntl = reinterpret_cast<int32_t*>(binom + n * R1);                             // [np2]
+    int32_t* hp = ntl + np2;                         // [hrows][kHistRow]: per-row inclusive prefix
+    int16_t* sidx = reinterpret_cast<int16_t*>(hp + hrows * kHistRow);                    // [np2]
+    __shared__ int32_t wsum[kPlanThreads / 32];
+    for (int i = threadIdx.x; i < hrows * kHistRow; i += blockDim.x) hp[i] = hist[i];
     if (threadIdx.x < 32) {                      // Pascal's triangle, exact for n <= 64
         const int lane = threadIdx.x;
         int64_t v0 = lane == 0, v1 = 0, v2 = 0;
@@ -694,13 +701,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
         }
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < 2 * kMitmMaxM; r += blockDim.x) {
+    for (int r = threadIdx.x; r < hrows; r += blockDim.x) {
         int acc = 0;
         for (int xpos = 0; xpos < kHistRow; ++xpos) { acc += hp[r * kHistRow + xpos]; hp[r * kHistRow + xpos] = acc; }
     }
     __syncthreads();
-    int np2 = 2;
-    while (np2 < nbp) np2 <<= 1;
     for (int i = threadIdx.x; i < np2; i += blockDim.x) {
         if (i >= nbp) { key[i] = -__longlong_as_double(0x7ff0000000000000LL); sidx[i] = (int16_t)i; continue; }
         const int b = P.order[i];
@@ -1267,8 +1272,11 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
         // the tile order from the tables' histogram (on the sweep's stream: a
         // one-CTA kernel queued behind a running sweep would wait for its tail)
-        DM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlanSmem));
-        plan_kernel<<<1, kPlanThreads, kPlanSmem, s>>>(t, sp, hist, plan_pos, plan_tstart);
+        int np2 = 2;
+        while (np2 < sp.nbp) np2 <<= 1;
+        const size_t psmem = plan_smem(np2, st.n_tab, t.n, rmax);
+        DM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+        plan_kernel<<<1, kPlanThreads, psmem, s>>>(t, sp, hist, st.n_tab, plan_pos, plan_tstart);
         DM_CHECK_LAUNCH();
         splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial, plan_pos,
                                                                 plan_tstart);
