@@ -623,7 +623,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return None
     threads = os.cpu_count() or 1
-    base = cpu_baseline(threads=threads, seconds=max(2.0, 20.0 / max(args.steps, 1)))
+    base = cpu_baseline(threads=threads, seconds=10.0)   # one ~10 s sample on every host core
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
