@@ -308,6 +308,8 @@ class SweepGraph:
         self.bufs = self.unit_bufs[0]
         self.whole = all(u[2] == 1 for u in self.units)
         self.out = torch.empty((len(self.units), _WINNER_BYTES), dtype=torch.uint8, device=dev)
+        for i, ub in enumerate(self.unit_bufs):      # each unit's record lands in its row directly
+            ub.out = self.out[i]
         self.host_out = torch.empty((len(self.units), _WINNER_BYTES), dtype=torch.uint8, pin_memory=True)
         self.h2d_bytes = int(batch.h2d_bytes) if copy_inputs else 0
         self.d2h_bytes = _WINNER_BYTES * len(self.units) if self.whole and copy_inputs else 0
@@ -340,12 +342,10 @@ class SweepGraph:
             for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
                 main.wait_event(ready[i])
                 enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts, phase=2)
-                self.out[i].copy_(ub.out, non_blocking=True)
             main.wait_stream(self.side)
         else:
             for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
                 enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts)
-                self.out[i].copy_(ub.out, non_blocking=True)
         if self.whole and self.copy_inputs:
             self.host_out.copy_(self.out, non_blocking=True)
 
