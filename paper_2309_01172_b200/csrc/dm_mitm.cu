@@ -732,6 +732,34 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
     }
     __syncthreads();
     // bitonic sort: descending key, ties by ascending host position
+    if (np2 <= kPlanThreads) {
+        // one element per thread: strides below 32 exchange through
+        // shuffles, wider strides through shared memory
+        const int tI = threadIdx.x;
+        double kv = tI < np2 ? key[tI] : 0.0;
+        int iv = tI < np2 ? sidx[tI] : tI;
+        for (int k = 2; k <= np2; k <<= 1)
+            for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                double pk;
+                int pi;
+                if (jj >= 32) {
+                    __syncthreads();
+                    if (tI < np2) { key[tI] = kv; sidx[tI] = (int16_t)iv; }
+                    __syncthreads();
+                    pk = tI < np2 ? key[tI ^ jj] : kv;
+                    pi = tI < np2 ? sidx[tI ^ jj] : iv;
+                } else {
+                    pk = __shfl_xor_sync(0xffffffffu, kv, jj);
+                    pi = __shfl_xor_sync(0xffffffffu, iv, jj);
+                }
+                const bool p_first = pk > kv || (pk == kv && pi < iv);
+                const bool up = (tI & k) == 0, lower = (tI & jj) == 0;
+                if (tI < np2 && (lower == up ? p_first : !p_first)) { kv = pk; iv = pi; }
+            }
+        __syncthreads();
+        if (tI < np2) { key[tI] = kv; sidx[tI] = (int16_t)iv; }
+        __syncthreads();
+    } else
     for (int k = 2; k <= np2; k <<= 1)
         for (int jj = k >> 1; jj > 0; jj >>= 1) {
             for (int i = threadIdx.x; i < np2; i += blockDim.x) {
