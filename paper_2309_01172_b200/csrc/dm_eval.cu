@@ -362,19 +362,6 @@ __device__ __forceinline__ unsigned long long boundary_mask(uint32_t waddr, int 
     return (((unsigned long long)m1 << 32) | m0) >> 1;
 }
 
-__device__ __forceinline__ unsigned long long boundary_mask_n(int nw, uint32_t waddr, int sh) {
-    switch (nw) {
-        case 1: return boundary_mask<1>(waddr, sh);   case 2: return boundary_mask<2>(waddr, sh);
-        case 3: return boundary_mask<3>(waddr, sh);   case 4: return boundary_mask<4>(waddr, sh);
-        case 5: return boundary_mask<5>(waddr, sh);   case 6: return boundary_mask<6>(waddr, sh);
-        case 7: return boundary_mask<7>(waddr, sh);   case 8: return boundary_mask<8>(waddr, sh);
-        case 9: return boundary_mask<9>(waddr, sh);   case 10: return boundary_mask<10>(waddr, sh);
-        case 11: return boundary_mask<11>(waddr, sh); case 12: return boundary_mask<12>(waddr, sh);
-        case 13: return boundary_mask<13>(waddr, sh); case 14: return boundary_mask<14>(waddr, sh);
-        case 15: return boundary_mask<15>(waddr, sh); default: return boundary_mask<16>(waddr, sh);
-    }
-}
-
 // Per-launch constants of the stream kernel's candidate loop.
 struct StreamCtx {
     int n;

@@ -300,14 +300,8 @@ __device__ __forceinline__ double side_value(const MitmCtx& x, const Blk& B, boo
     return left ? left_val(x, B, val, bnd, e) : right_val(x, B, val, bnd, e);
 }
 
-// The same from an element's already loaded table value and boundary cut.
-__device__ __forceinline__ double side_finish(const MitmCtx& x, const Blk& B, bool left, double raw, int b) {
-    if (B.m == 0) return left ? -__longlong_as_double(0x7ff0000000000000LL) : __ldg(x.timg + B.rrow + x.n);
-    const double tv = left ? tval(x, B.j - 1, b, B.c) : __ldg(x.timg + B.rrow + b);
-    return tv > raw ? tv : raw;
-}
-
-// The same with the tile's finishing runs staged in shared memory:
+// A side element finished from its loaded table value and boundary cut, the
+// tile's finishing runs staged in shared memory:
 // col[a] = T[j-1][a][c] (left sides), row[b] = T[j][c][b] (right sides).
 __device__ __forceinline__ double side_finish_s(const Blk& B, bool left, double raw, int b, const double* col,
                                                 const double* row, int n) {
