@@ -1099,14 +1099,14 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 // ---- slot layout: G warp-aligned thread groups, each taking
                 //      every X against 1/G of the Y (fewer padded slots when
                 //      the feasible X do not fill kMitmNR slots per thread);
-                //      cost per thread ~ Y pairs x (slots + 0.5 per-Y overhead)
+                //      cost per thread ~ Y pairs x (slots + 1 per-Y overhead)
                 int G = 1, nsl = (nxf_tot + kMitmThreads - 1) / kMitmThreads;
-                int best_cost = nyf * (2 * nsl + 1);
+                int best_cost = nyf * (nsl + 1);
                 for (int g2 = 2; g2 <= 8; g2 <<= 1) {
                     const int per2 = kMitmThreads / g2, ns2 = (nxf_tot + per2 - 1) / per2;
                     if (ns2 > kMitmNR) break;
                     const int yc2 = ((nyf + g2 - 1) / g2 + 1) & ~1;
-                    const int cost = yc2 * (2 * ns2 + 1);
+                    const int cost = yc2 * (ns2 + 1);
                     if (cost < best_cost) { best_cost = cost; G = g2; nsl = ns2; }
                 }
                 const int per = kMitmThreads / G, gi = threadIdx.x / per, l = threadIdx.x - gi * per;
