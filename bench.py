@@ -562,12 +562,15 @@ def api_latency_measure(dev):
     for _ in range(3):
         S.schedule(stages, fleet)
     torch.cuda.synchronize()
-    t0 = _t.perf_counter()
+    times = []
     for _ in range(20):
+        t0 = _t.perf_counter()
         rep = S.schedule(stages, fleet)
-    el = (_t.perf_counter() - t0) / 20
+        times.append((_t.perf_counter() - t0) * 1e3)
     return {"config": "C1 gpt2-small x 4 mixed GPUs (10 Gbit/s, 1 ms): schedule() through the public API",
-            "ms_per_call": el * 1e3, "runs": [list(r[1][:1]) + [r[1][-1], r[0]] for r in rep.runs],
+            "ms_per_call": statistics.median(times), "ms_min": min(times), "ms_max": max(times),
+            "ms_mean": statistics.mean(times), "calls": len(times),
+            "runs": [list(r[1][:1]) + [r[1][-1], r[0]] for r in rep.runs],
             "makespan": rep.makespan, "trace": list(rep.trace)}
 
 
