@@ -495,18 +495,21 @@ def random_measure(dev, which):
     host = build_host(stages, fleet, True)
     batch = engine.device_batch([host], device=dev)
     online = np.array([host.index_of[i] for i in online_ids], np.int32)
-    mults = np.array(R.coprime_multipliers(len(online), 1234), np.int32)
-    on_d, mu_d = torch.from_numpy(online).to(dev), torch.from_numpy(mults).to(dev)
+    on_d = torch.from_numpy(online).to(dev)
     bufs = engine.WinnerBuffers(dev)
     seed = 20260
-    ms = _time_ms(lambda: engine.enum(batch, "random", 0, N, bufs, online=on_d, mults=mu_d, seed=seed), steps=3)
+    ms = _time_ms(lambda: engine.enum(batch, "random", 0, N, bufs, online=on_d, seed=seed), steps=3)
     win = bufs.read()
     inst = oracle.Instance(stages, fleet)
     t0 = _t.perf_counter()
-    ref = inst.enum_random(online, mults, seed, 0, 2000)
-    cpu = 2000 / (_t.perf_counter() - t0)
-    got = engine.enum(batch, "random", 0, 2000, online=on_d, mults=mu_d, seed=seed).read()
+    ref = inst.enum_random(online, seed, 0, 20000)
+    cpu = 20000 / (_t.perf_counter() - t0)
+    got = engine.enum(batch, "random", 0, 20000, online=on_d, seed=seed).read()
     return {"config": desc, "candidates": N, "ms": ms, "value": N / (ms / 1e3), "unit": UNIT,
+            "candidate_distribution": "r ~ U{1..min(n, online)}, uniform (r-1)-subset of the cut positions "
+                                      "(selection sampling), r distinct online peers (keyed Feistel permutation); "
+                                      "paper_2309_01172_b200/rng.py",
+            "feasible_frac": win["n_feasible"] / N,
             "winner": {"makespan": win["makespan"], "rank": win["rank"], "n_feasible": win["n_feasible"],
                        "checksum": win["checksum"]},
             "oracle_prefix_check": got == ref, "cpu_baseline_1core": cpu}

@@ -241,19 +241,20 @@ DM_API int dm_enum_splits_phase(const dm_tables* t, int64_t k0, int64_t k1, int3
                                 int32_t phase, void* stream);
 
 /*
- * dm_enum_random — counter-RNG random contiguous placements (config C5):
- * candidate k (k0 <= k < k1) is generated from SplitMix64 keyed (seed, k):
- * each cut position 1..n-1 is present with probability 1/2, and the r runs go
- * to r distinct peers online[(a*q + b) mod n_online], q = 0..r-1, with
- * a = mults[h % n_mults] (every mult coprime to n_online) and b drawn from
- * the same stream.  Requires chain-structured stages (DM_F_CHAIN) when
- * include_comm is set, and n <= n_online.
- * See paper_2309_01172_b200/rng.py for the exact recipe (shared with the oracle).
+ * dm_enum_random — random contiguous placements scored on chip (configs C3,
+ * C5; replaces scoring a sampled candidate list with evaluate_runs,
+ * scheduling.py:235-239, and keeps brute_force_schedule's arg-min rule :271):
+ * candidate k (k0 <= k < k1) of the stream keyed by `seed` draws
+ * r ~ U{1..min(n, n_online)}, a uniform (r-1)-subset of the cut positions
+ * 1..n-1 (selection sampling) and r distinct online peers (a keyed Feistel
+ * permutation of online[0..n_online)); runs failing _fits make the candidate
+ * infeasible, the winner is the first strict minimum by k.  Recipe:
+ * paper_2309_01172_b200/rng.py (shared bit for bit with the oracle).
+ * Requires chain-structured stages (DM_F_CHAIN) when include_comm is set and
+ * n <= 257.  `scratch` >= dm_enum_scratch_bytes().
  */
-DM_API int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,
-                   const int32_t* mults, int32_t n_mults, uint64_t seed,
-                   int64_t k0, int64_t k1, dm_winner* out,
-                   void* scratch, void* stream);
+DM_API int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online, uint64_t seed,
+                          int64_t k0, int64_t k1, dm_winner* out, void* scratch, void* stream);
 
 /* dm_materialize — write candidates [k0, k0+count) of the brute-force
  * (mode 0) or identity-split (mode 1) order as owner vectors (uint8/uint16

@@ -384,9 +384,19 @@ EXPORT void or_enum(const dm_tables* t, int mode, int64_t k0, int64_t k1, dm_win
         if (k1 <= base) break;
         if (k0 >= base + blk) { base += blk; continue; }
         int64_t lo = k0 > base ? k0 - base : 0, hi = (k1 < base + blk ? k1 : base + blk) - base;
+        int64_t have_c = -1;
         for (int64_t kk = lo; kk < hi; ++kk) {
             int64_t c = kk / np, pi = kk % np;
-            unrank_comb(n, r - 1, c, cuts);
+            if (have_c < 0) unrank_comb(n, r - 1, c, cuts);
+            else if (c != have_c) {
+                /* itertools.combinations successor: bump the rightmost cut
+                 * that can move, reset the ones after it */
+                int m = r - 1, i = m - 1;
+                while (i >= 0 && cuts[i] == n - 1 - (m - 1 - i)) --i;
+                cuts[i]++;
+                for (int j = i + 1; j < m; ++j) cuts[j] = cuts[j - 1] + 1;
+            }
+            have_c = c;
             bounds[0] = 0;
             for (int q = 0; q < r - 1; ++q) bounds[q + 1] = cuts[q];
             bounds[r] = n;
@@ -424,52 +434,84 @@ EXPORT int or_unrank(const dm_tables* t, int mode, int64_t k, int32_t* bounds, i
 
 /* ---------------------------------------------------- random placements */
 
+/* Candidate k of the random-placement stream (configs C3/C5; the recipe is
+ * documented in paper_2309_01172_b200/rng.py and restated in
+ * csrc/dm_random.cu): xoshiro128** seeded from (seed, k), r ~ U{1..rmax},
+ * Knuth's selection sampling for the r-1 cut positions, a keyed 4-round
+ * Feistel permutation (cycle walking) of the online peers. */
 static inline uint64_t fmix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
     return z ^ (z >> 31);
 }
-/* word j of candidate k (paper_2309_01172_b200/rng.py) */
-static inline uint64_t rng_word(uint64_t key, int64_t k, int j) {
-    return fmix64(key + fmix64((uint64_t)k * 8ULL + (uint64_t)j + 1ULL));
+static inline uint32_t rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+typedef struct { uint32_t s[4]; } xo128;
+static void xo_seed(xo128* g, uint64_t key, int64_t k) {
+    uint64_t za = fmix64(key + 2ULL * (uint64_t)k + 1ULL), zb = fmix64(key + 2ULL * (uint64_t)k + 2ULL);
+    g->s[0] = (uint32_t)za; g->s[1] = (uint32_t)(za >> 32); g->s[2] = (uint32_t)zb; g->s[3] = (uint32_t)(zb >> 32);
+    if (!(g->s[0] | g->s[1] | g->s[2] | g->s[3])) g->s[0] = 1;
+}
+static inline uint32_t xo_next(xo128* g) {
+    uint32_t* s = g->s;
+    uint32_t res = rotl32(s[1] * 5u, 7) * 9u, t = s[1] << 9;
+    s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t; s[3] = rotl32(s[3], 11);
+    return res;
+}
+static inline uint32_t mulhi32(uint32_t u, uint32_t m) { return (uint32_t)(((uint64_t)u * m) >> 32); }
+static int feistel_h(int32_t n_online) {
+    int bits = 0; uint32_t v = (uint32_t)(n_online > 1 ? n_online - 1 : 1);
+    while (v) { ++bits; v >>= 1; }
+    int h = (bits + 1) / 2;
+    return h < 1 ? 1 : h;
+}
+static int32_t feistel_perm(int32_t q, int32_t n_online, const uint32_t kr[4]) {
+    int h = feistel_h(n_online);
+    uint32_t mask = (1u << h) - 1u, x = (uint32_t)q;
+    do {
+        uint32_t L = x >> h, R = x & mask;
+        for (int i = 0; i < 4; ++i) { uint32_t nl = R; R = L ^ (((R ^ kr[i]) * 0x9E3779B1u) >> (32 - h)); L = nl; }
+        x = (L << h) | R;
+    } while (x >= (uint32_t)n_online);
+    return (int32_t)x;
 }
 
-EXPORT int or_random_candidate(int n, int32_t n_online, const int32_t* online,
-                               const int32_t* mults, int32_t n_mults,
-                               uint64_t seed, int64_t k, int32_t* bounds, int32_t* peers) {
+/* bounds[0..r], run q -> online index peer_idx[q]; returns r */
+EXPORT int or_random_candidate(int n, int32_t n_online, uint64_t seed, int64_t k,
+                               int32_t* bounds, int32_t* peer_idx) {
     uint64_t key = fmix64(seed + 0x9E3779B97F4A7C15ULL);
-    int r = 0;
-    bounds[r++] = 0;
-    for (int pos = 1; pos < n; ++pos) {
-        int j = (pos - 1) >> 6, b = (pos - 1) & 63;
-        uint64_t wd = rng_word(key, k, j);
-        if ((wd >> b) & 1ULL) bounds[r++] = pos;
-    }
-    bounds[r] = n;
-    uint64_t h4 = rng_word(key, k, 6), h5 = rng_word(key, k, 7);
-    int64_t a = mults[h4 % (uint64_t)n_mults], b0 = (int64_t)(h5 % (uint64_t)n_online);
-    for (int q = 0; q < r; ++q) peers[q] = online[(b0 + a * q) % n_online];
+    xo128 g; xo_seed(&g, key, k);
+    uint32_t rmax = (uint32_t)(n < n_online ? n : n_online);
+    int r = 1 + (int)mulhi32(xo_next(&g), rmax), need = r - 1, nb = 0;
+    bounds[nb++] = 0;
+    for (int pos = 1; pos < n && need > 0; ++pos)
+        if (mulhi32(xo_next(&g), (uint32_t)(n - pos)) < (uint32_t)need) { bounds[nb++] = pos; --need; }
+    bounds[nb] = n;
+    uint32_t kr[4];
+    for (int i = 0; i < 4; ++i) kr[i] = xo_next(&g);
+    for (int q = 0; q < r; ++q) peer_idx[q] = feistel_perm(q, n_online, kr);
     return r;
 }
 
-EXPORT void or_enum_random(const dm_tables* t, int32_t n_online, const int32_t* online,
-                           const int32_t* mults, int32_t n_mults, uint64_t seed,
+EXPORT void or_enum_random(const dm_tables* t, int32_t n_online, const int32_t* online, uint64_t seed,
                            int64_t k0, int64_t k1, dm_winner* out) {
     int n = t->n;
-    int32_t bounds[1100], peers[1100];
+    int32_t* bounds = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 2));
+    int32_t* pidx = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    int32_t* peers = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
     int32_t* peer_of = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
     int32_t* idxbuf = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
     uint8_t* inside = (uint8_t*)calloc((size_t)n, 1);
     or_win w = {INFINITY, -1, 0, 0, 0};
     for (int64_t k = k0; k < k1; ++k) {
-        int r = or_random_candidate(n, n_online, online, mults, n_mults, seed, k, bounds, peers);
+        int r = or_random_candidate(n, n_online, seed, k, bounds, pidx);
+        for (int q = 0; q < r; ++q) peers[q] = online[pidx[q]];
         double mk;
         w.n_eval++;
         if (score_contiguous(t, r, bounds, peers, peer_of, idxbuf, inside, &mk)) win_update(&w, mk, k);
     }
     out->makespan = w.mk; out->rank = w.rank; out->n_evaluated = w.n_eval;
     out->n_feasible = w.n_feas; out->checksum = w.csum;
-    free(peer_of); free(idxbuf); free(inside);
+    free(bounds); free(pidx); free(peers); free(peer_of); free(idxbuf); free(inside);
 }
 
 /* ------------------------------------------------------------ _subset_dp */

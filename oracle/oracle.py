@@ -73,9 +73,9 @@ def lib():
         L.or_unrank.restype = C.c_int
         L.or_unrank.argtypes = [_P, C.c_int, C.c_int64, _P, _P]
         L.or_random_candidate.restype = C.c_int
-        L.or_random_candidate.argtypes = [C.c_int, C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_int64, _P, _P]
+        L.or_random_candidate.argtypes = [C.c_int, C.c_int32, C.c_uint64, C.c_int64, _P, _P]
         L.or_enum_random.restype = None
-        L.or_enum_random.argtypes = [_P, C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, _P]
+        L.or_enum_random.argtypes = [_P, C.c_int32, _P, C.c_uint64, C.c_int64, C.c_int64, _P]
         L.or_subset_dp.restype = C.c_int
         L.or_subset_dp.argtypes = [_P, _P, _P]
         L.or_proportional.restype = C.c_int
@@ -247,13 +247,18 @@ class Instance:
         r = lib().or_unrank(C.byref(self.t), {"bruteforce": 0, "splits": 1}[mode], k, _ptr(b), _ptr(p))
         return b[: r + 1].tolist(), p[:r].tolist()
 
-    def enum_random(self, online, mults, seed, k0, k1):
+    def enum_random(self, online, seed, k0, k1):
         on = np.ascontiguousarray(online, np.int32)
-        mu = np.ascontiguousarray(mults, np.int32)
         w = Winner()
-        lib().or_enum_random(C.byref(self.t), on.size, _ptr(on), _ptr(mu), mu.size, seed, k0, k1, C.byref(w))
+        lib().or_enum_random(C.byref(self.t), on.size, _ptr(on), seed & 0xFFFFFFFFFFFFFFFF, k0, k1, C.byref(w))
         return dict(makespan=w.makespan, rank=w.rank, n_evaluated=w.n_evaluated, n_feasible=w.n_feasible,
                     checksum=w.checksum)
+
+    def random_candidate(self, n_online, seed, k):
+        b = np.zeros(self.n + 2, np.int32)
+        q = np.zeros(self.n + 1, np.int32)
+        r = lib().or_random_candidate(self.n, n_online, seed & 0xFFFFFFFFFFFFFFFF, k, _ptr(b), _ptr(q))
+        return b[: r + 1].tolist(), q[:r].tolist()
 
     def subset_dp(self):
         own = np.full(self.n, -1, np.int32)

@@ -16,9 +16,9 @@ include/dagmesh_b200.h); there is no CPU fallback.
 
 from __future__ import annotations
 
-from . import _lib, engine, model, opcost, pipeline, scheduling, tensorize
+from . import _lib, engine, opcost, pipeline, refapi, scheduling, tensorize
 from ._lib import EngineError, EngineUnavailable
-from .model import (GPU_TABLE, DagmeshError, Fleet, FleetError, Link, Peer, PeerLoad, Role,
+from .refapi import (GPU_TABLE, DagmeshError, Fleet, FleetError, Link, Peer, PeerLoad, Role,
                     ScheduleReport, SchedulingError, Stage, ZERO_LINK, bandwidth_to_beta, comm_time,
                     effective_speed, format_stage_run, load_fleet, parse_fleet, peer_sort_key)
 from .pipeline import (StageProfile, SweepResult, SweepRow, asymptotic_throughput, bottleneck, fp_latency,
@@ -88,9 +88,9 @@ def install(dagmesh_module=None):
     def uninstall():
         for (mod, name), fn in saved.items():
             setattr(mod, name, fn)
-        scheduling.T.ScheduleReport = model.ScheduleReport
-        scheduling.T.PeerLoad = model.PeerLoad
-        scheduling.T.SchedulingError = model.SchedulingError
-        scheduling.T.FleetError = model.FleetError
+        scheduling.T.ScheduleReport = refapi.ScheduleReport
+        scheduling.T.PeerLoad = refapi.PeerLoad
+        scheduling.T.SchedulingError = refapi.SchedulingError
+        scheduling.T.FleetError = refapi.FleetError
 
     return uninstall

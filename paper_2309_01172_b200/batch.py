@@ -15,7 +15,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .model import GPU_TABLE
+from .refapi import GPU_TABLE
 from .tensorize import TABLES_DTYPE, HostTables
 
 _KINDS = tuple(GPU_TABLE)
@@ -107,7 +107,7 @@ def c4_batch(n_scen: int, seed: int = 0, device="cuda", vocab: int = 32000, batc
     GPU_TABLE, lambda ~ U[.3, 1], alpha ~ U[0, 10 ms], bandwidth ~ LogU[.1, 10]
     Gbit/s.  Returns (ScenarioBatch, model_keys, per-scenario arrays)."""
     from .configs import C4_HIDDEN, encoder_stages
-    from .model import Fleet, Peer
+    from .refapi import Fleet, Peer
     from .tensorize import build_host
 
     rng = np.random.default_rng(seed)
@@ -133,7 +133,7 @@ def scenario_instance(sb: ScenarioBatch, s: int):
     """Rebuild scenario s as (stages, Fleet) with the mirror types — the exact
     values parse_fleet would produce for the scenario's fleet document."""
     from .configs import C4_HIDDEN, encoder_stages
-    from .model import Fleet, Link, Peer
+    from .refapi import Fleet, Link, Peer
 
     L, h = sb.params["keys"][int(sb.scen_model[s])]
     stages = encoder_stages(C4_HIDDEN[h], L, 32000, 4, 1024)

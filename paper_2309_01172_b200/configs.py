@@ -13,11 +13,12 @@ here (the "tensoriser fast path for build_stages"):
 * one (src = i-1, 4bsh bytes) in-edge per stage after the first
   (build_stages :123-139, message_bytes hardware.py:157-158).
 
-tests/test_configs_reference.py pins every model used here against the
-reference's own parse_job_definition + build_stages.
+tests/test_host_cpu.py::test_closed_form_stages_match_reference_digests pins
+every model used here against the reference's own parse_job_definition +
+build_stages (sha256 digests in tests/golden/stage_digests.json).
 
 Fleets are reference-schema fleet documents (hardware.py:265-354) loaded with
-the mirror parse_fleet.
+the reference's own parse_fleet.
 """
 
 from __future__ import annotations
@@ -27,7 +28,7 @@ import math
 
 import numpy as np
 
-from .model import GPU_TABLE, Stage, parse_fleet
+from .refapi import GPU_TABLE, Stage, parse_fleet
 
 ELEMENT_BYTES = 4
 

@@ -322,78 +322,6 @@ __global__ void __launch_bounds__(kMemoThreads, 2) splits_memo_kernel(dm_tables 
     block_reduce_win_store(w, partial);
 }
 
-// --------------------------------------------------------- random stream
-__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
-}
-__device__ __forceinline__ uint64_t rng_word(uint64_t key, int64_t k, int j) {
-    return fmix64(key + fmix64((uint64_t)k * 8ULL + (uint64_t)j + 1ULL));
-}
-
-// Config C5: candidate k is a random contiguous placement (see
-// paper_2309_01172_b200/rng.py).  Runs are walked on the fly from the cut
-// bits, so no per-candidate arrays are needed for chain-structured stages.
-__global__ void __launch_bounds__(256) enum_random_kernel(dm_tables t, const int32_t* __restrict__ online,
-                                                          int32_t n_online, const int32_t* __restrict__ mults,
-                                                          int32_t n_mults, uint64_t key, int64_t k0, int64_t k1,
-                                                          dm_winner* partial) {
-    Win w; win_init(w);
-    const int n = t.n;
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1; k += stride) {
-        uint64_t h4 = rng_word(key, k, 6), h5 = rng_word(key, k, 7);
-        int64_t am = mults[h4 % (uint64_t)n_mults];
-        int64_t b0 = (int64_t)(h5 % (uint64_t)n_online);
-        // pass 1: _fits for every run (skip candidate on the first failure)
-        bool ok = true;
-        {
-            int a = 0, q = 0;
-            uint64_t wd = rng_word(key, k, 0);
-            for (int pos = 1; pos <= n && ok; ++pos) {
-                bool cut = pos == n;
-                if (!cut) {
-                    int j = (pos - 1) >> 6, bb = (pos - 1) & 63;
-                    if (bb == 0 && j > 0) wd = rng_word(key, k, j);
-                    cut = (wd >> bb) & 1ULL;
-                }
-                if (cut) {
-                    int pe = online[(b0 + am * q) % n_online];
-                    ok = fits_range(t, pe, a, pos);
-                    a = pos; ++q;
-                }
-            }
-        }
-        w.n_eval++;
-        if (!ok) continue;
-        // pass 2: cost (chain stages: the crossing read of run q comes from run q-1)
-        double best = 0.0;
-        {
-            int a = 0, q = 0, prev = -1;
-            uint64_t wd = rng_word(key, k, 0);
-            for (int pos = 1; pos <= n; ++pos) {
-                bool cut = pos == n;
-                if (!cut) {
-                    int j = (pos - 1) >> 6, bb = (pos - 1) & 63;
-                    if (bb == 0 && j > 0) wd = rng_word(key, k, j);
-                    cut = (wd >> bb) & 1ULL;
-                }
-                if (cut) {
-                    int pe = online[(b0 + am * q) % n_online];
-                    double c, rd;
-                    run_cost_contig(t, a, pos, pe, [&](int) { return prev; }, c, rd);
-                    double load = c + rd;
-                    if (q == 0 || load > best) best = load;
-                    prev = pe; a = pos; ++q;
-                }
-            }
-        }
-        win_add(w, best, k);
-    }
-    block_reduce_win_store(w, partial);
-}
-
 // -------------------------------------------------- candidate materialiser
 // Writes candidates [k0, k0 + count) of the brute-force (MODE 0) or
 // identity-split (MODE 1) order as owner vectors (worker index per stage):
@@ -440,181 +368,6 @@ __global__ void __launch_bounds__(256) materialize_kernel(int n, int p, int64_t 
         used.clear(p);
         for (int q = 0; q < r; ++q) { peers[q] = q; if (MODE == 0) used.set(q); }
     }
-}
-
-// ------------------------------------------- random stream, staged fast path
-// Config C3/C5 scale: chain-structured stages with exact (integral) columns.
-// Per CTA the stage prefix sums, the per-boundary uniform read
-// R[a] = naive sum over stage a's in-edges of comm(default, M), and the peer
-// columns (speed, 1/speed, capacities) are staged into shared memory; each
-// thread scores one candidate per iteration in a single pass over its runs
-// (fits and load together — the reference's skip-if-any-run-fails is
-// order-independent).  compute = flops / speed uses Markstein's correction
-// q1 = q0 + (flops - q0*speed) * rcp with rcp = RN(1/speed), which yields the
-// correctly rounded quotient (validated bitwise against div.rn in
-// tests/test_gpu_parity.py and on 2e8 CPU samples).
-struct RandLayout {
-    size_t off_stage, off_peer, off_online, off_mults, bytes;
-};
-
-// Stage record (boundary i): exact prefix sums of flops / gpu / cpu / disk as
-// doubles (integers < 2^53, so differences are exact) and R[i], the uniform
-// read of a run starting at stage i.  Peer record: speed, RN(1/speed), caps.
-struct __align__(16) StageRec { double pf, pg, pc, pd, R, pad; };
-struct __align__(16) PeerRec { double speed, rcp, cg, cc, cd; int32_t pe, pad; };
-
-__host__ __device__ inline RandLayout rand_layout(int n, int P, int n_online, int n_mults) {
-    RandLayout L;
-    size_t off = 0;
-    L.off_stage = off; off += (size_t)(n + 1) * sizeof(StageRec);
-    L.off_peer = off; off += (size_t)n_online * sizeof(PeerRec);   // in online order
-    L.off_online = off;
-    L.off_mults = off; off += ((size_t)n_mults * 4 + 15) & ~(size_t)15;
-    L.bytes = off;
-    return L;
-}
-
-__device__ __forceinline__ double div_markstein(double a, double b, double rcp) {
-    double q0 = __dmul_rn(a, rcp);
-    double rem = __fma_rn(-q0, b, a);
-    return __fma_rn(rem, rcp, q0);
-}
-
-__device__ __forceinline__ void lds_v2(uint32_t a, double& x, double& y) {
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
-}
-__device__ __forceinline__ double lds_d(uint32_t a) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ int lds_i(uint32_t a) {
-    int v;
-    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-
-// Cut positions of candidate k in ascending order, then n, then -1.  The
-// (n-1)-bit cut mask (<= 4 words, n <= 257) is generated up front and
-// consumed as a 4-word shift queue, so no RNG work sits in the run loop.
-struct CutIter {
-    uint64_t cw, w1, w2, w3;
-    int base, n;
-    bool done;
-    __device__ __forceinline__ void init(uint64_t key, int64_t k, int n_) {
-        n = n_; base = 0; done = false;
-        const int nwords = (n - 1 + 63) >> 6;
-        uint64_t w[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (j < nwords) {
-                uint64_t x = rng_word(key, k, j);
-                const int valid = (n - 1) - 64 * j;
-                if (valid < 64) x &= (1ull << valid) - 1ull;
-                w[j] = x;
-            }
-        }
-        cw = w[0]; w1 = w[1]; w2 = w[2]; w3 = w[3];
-    }
-    __device__ __forceinline__ int next() {
-        while (!cw) {
-            if (!(w1 | w2 | w3)) {
-                if (done) return -1;
-                done = true;
-                return n;
-            }
-            cw = w1; w1 = w2; w2 = w3; w3 = 0ull; base += 64;
-        }
-        const int b = base + __ffsll((long long)cw);
-        cw &= cw - 1;
-        return b;
-    }
-};
-
-__global__ void __launch_bounds__(256, 3) enum_random_fast_kernel(dm_tables t, const int32_t* __restrict__ online,
-                                                               int32_t n_online, const int32_t* __restrict__ mults,
-                                                               int32_t n_mults, uint64_t key, int64_t k0, int64_t k1,
-                                                               dm_winner* partial) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    const int n = t.n, P = t.P;
-    const RandLayout L = rand_layout(n, P, n_online, n_mults);
-    StageRec* SR = reinterpret_cast<StageRec*>(sm + L.off_stage);
-    PeerRec* PR = reinterpret_cast<PeerRec*>(sm + L.off_peer);
-    int32_t* mul = reinterpret_cast<int32_t*>(sm + L.off_mults);
-    const bool comm = include_comm(t), pair = pair_links(t);
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) {
-        StageRec r;
-        r.pf = (double)t.pre_flops[i]; r.pg = (double)t.pre_gpu[i];
-        r.pc = (double)t.pre_cpu[i]; r.pd = (double)t.pre_disk[i];
-        double rd = 0.0;
-        if (comm && i < n)
-            for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e)
-                rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
-        r.R = rd; r.pad = 0.0;
-        SR[i] = r;
-    }
-    for (int i = threadIdx.x; i < n_online; i += blockDim.x) {
-        const int w = online[i];
-        PeerRec r;
-        r.speed = t.speed[w]; r.rcp = 1.0 / r.speed;
-        r.cg = t.cap_gpu[w]; r.cc = t.cap_cpu[w]; r.cd = t.cap_disk[w]; r.pe = w; r.pad = 0;
-        PR[i] = r;
-    }
-    for (int i = threadIdx.x; i < n_mults; i += blockDim.x) mul[i] = mults[i];
-    __syncthreads();
-
-    const uint32_t SR_s = (uint32_t)__cvta_generic_to_shared(SR), PR_s = (uint32_t)__cvta_generic_to_shared(PR);
-    Win w; win_init(w);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1; k += stride) {
-        const uint64_t h4 = rng_word(key, k, 6), h5 = rng_word(key, k, 7);
-        const int am = (int)(((int64_t)mul[h4 % (uint64_t)n_mults]) % n_online);
-        int pos = (int)(h5 % (uint64_t)n_online);                   // (b0 + am*q) mod n_online
-        CutIter it;
-        it.init(key, k, n);
-        bool ok = true;
-        double mk = 0.0;
-        int a = 0, prev = -1;
-        // previous boundary record (prefix sums at a, read of a run starting at a)
-        double af, ag, ac, ad, aR;
-        lds_v2(SR_s, af, ag); lds_v2(SR_s + 16, ac, ad); aR = lds_d(SR_s + 32);
-        int b = it.next();
-        while (b >= 0) {
-            // both records of this run are requested before any arithmetic
-            const uint32_t sb = SR_s + (uint32_t)b * (uint32_t)sizeof(StageRec);
-            const uint32_t pb = PR_s + (uint32_t)pos * (uint32_t)sizeof(PeerRec);
-            double bf, bg, bc, bd, bR, sp, rc, cg, cc, cd;
-            lds_v2(sb, bf, bg); lds_v2(sb + 16, bc, bd); bR = lds_d(sb + 32);
-            lds_v2(pb, sp, rc); lds_v2(pb + 16, cg, cc); cd = lds_d(pb + 32);
-            const int pe = pair ? lds_i(pb + 40) : 0;
-            const int bn = it.next();                                  // next boundary, off the critical path
-            pos += am;
-            if (pos >= n_online) pos -= n_online;
-            // _fits (scheduling.py:172-176): exact prefix differences vs capacities
-            ok &= (bg - ag <= cg) & (bc - ac <= cc) & (bd - ad <= cd);
-            // _run_cost: compute (Markstein-corrected quotient) + crossing read
-            const double compute = div_markstein(bf - af, sp, rc);
-            double rd = 0.0;
-            if (comm && a > 0) {
-                if (pair) {
-                    double al, be;
-                    link_of(t, prev, pe, al, be);
-                    for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
-                        rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
-                } else {
-                    rd = aR;
-                }
-            }
-            const double load = compute + rd;
-            mk = load > mk ? load : mk;
-            prev = pe; a = b;
-            af = bf; ag = bg; ac = bc; ad = bd; aR = bR;
-            b = bn;
-        }
-        w.n_eval++;
-        if (ok) win_add(w, mk, k);
-    }
-    block_reduce_win_store(w, partial);
 }
 
 // ------------------------------------------------------------ final merge
@@ -769,38 +522,6 @@ int dm_enum_splits_ws(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, 
 int dm_enum_splits_phase(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts, dm_winner* out,
                          void* scratch, void* workspace, int64_t workspace_bytes, int32_t phase, void* stream) {
     return enum_splits_impl(t, k0, k1, part, nparts, out, scratch, workspace, workspace_bytes, stream, phase);
-}
-
-int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online,
-                   const int32_t* mults, int32_t n_mults, uint64_t seed, int64_t k0, int64_t k1,
-                   dm_winner* out, void* scratch, void* stream) {
-    if (!t || !online || !mults || n_online <= 0 || n_mults <= 0 || !out || !scratch)
-        return dmabi::fail(DM_E_ARG, "bad arguments");
-    if (t->n > n_online) return dmabi::fail(DM_E_ARG, "random placements need n <= online peers");
-    if (t->n > 385) return dmabi::fail(DM_E_TOO_LARGE, "random placements support n <= 385");
-    if (!(t->flags & DM_F_CHAIN) && (t->flags & DM_F_INCLUDE_COMM))
-        return dmabi::fail(DM_E_ARG, "random placements need chain-structured stages");
-    cudaStream_t s = (cudaStream_t)stream;
-    int grid = enum_grid();
-    uint64_t key = dm::fmix64(seed + 0x9E3779B97F4A7C15ULL);
-    dm::RandLayout L = dm::rand_layout(t->n, t->P, n_online, n_mults);
-    const bool exact = (t->flags & DM_F_FLOPS_EXACT) && (t->flags & DM_F_BYTES_EXACT);
-    if (exact && t->n <= 257 && L.bytes <= 200 * 1024 && !getenv_flag("DM_DISABLE_MEMO")) {
-        int per_sm = (int)((220 * 1024) / (L.bytes + 2048));
-        if (per_sm > 3) per_sm = 3;
-        if (per_sm < 1) per_sm = 1;
-        grid = enum_grid() / 8 * per_sm;
-        cudaFuncSetAttribute(dm::enum_random_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
-        dm::enum_random_fast_kernel<<<grid, kThreads, L.bytes, s>>>(*t, online, n_online, mults, n_mults, key, k0,
-                                                                    k1, (dm_winner*)scratch);
-    } else {
-        dm::enum_random_kernel<<<grid, kThreads, 0, s>>>(*t, online, n_online, mults, n_mults, key, k0, k1,
-                                                         (dm_winner*)scratch);
-    }
-    DM_CHECK_LAUNCH();
-    dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, grid, out);
-    DM_CHECK_LAUNCH();
-    return DM_OK;
 }
 
 int dm_materialize(int32_t n, int32_t p, int32_t mode, int64_t k0, int64_t count, void* owner, int32_t owner_bytes,

@@ -303,7 +303,9 @@ __host__ __device__ inline StreamLayout stream_layout(int n, int P, int stages, 
     L.tile_bytes = al16((size_t)nt * cpt * n);
     L.off_tiles = off; off = al16(off + L.tile_bytes * stages + 16);
     L.off_bar = off; off += 8 * stages;
-    L.bytes = al16(off);
+    // + 2 KB: a run on an owner index >= P (rerouted to the general path
+    // afterwards) may address up to 255 entries past the end of T / codes
+    L.bytes = al16(off) + 2048;
     return L;
 }
 
@@ -365,66 +367,96 @@ __device__ __forceinline__ unsigned long long boundary_mask(uint32_t waddr, int 
 // Per-launch constants of the stream kernel's candidate loop.
 struct StreamCtx {
     int n;
-    uint32_t uP, Pm1, n1P8, T_s, C_s, rowidx_s, mask_lo, mask_hi;
+    uint32_t uP, rowstride, T_s, C_s, mask_lo, mask_hi, tri_k, pmask;
+};
+
+// Lean per-candidate arg-min state: n_evaluated is the number of candidates
+// the thread saw (derived at the end), the feasible count fits 32 bits per
+// thread and launch.
+struct StreamWin {
+    double mk;
+    int64_t rank;
+    uint32_t n_feas;
+    uint64_t csum;
 };
 
 // Score this thread's candidates of one resident tile (NW: boundary-mask
-// words).  A run failing _fits only records its table address; the first
-// one's violation code is read after the runs (rare).
+// words).  Runs are visited from the last boundary down (FLO gives the
+// highest set bit in one instruction); per run: the owner byte, its bit in
+// `seen`, the table address, one 8-byte table load, the running maximum of
+// |T| and the running minimum of the addresses of failing runs (T's sign
+// bit) — table addresses grow with the run's first stage, so the minimum is
+// the first failing run in verify order (scheduling.py:184-203), whose
+// violation code is read once after the loop.  A peer seen twice
+// (non-contiguous owner vector) or an owner index >= P (bit outside the
+// fleet) sends the candidate to the grouped general path.
 template <bool PAIR, bool SQUARE, int NT, int NW>
 __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx& X, uint32_t tile_s,
                                             const unsigned char* tile, int cnt, int64_t c0,
                                             double* __restrict__ out_mk, uint8_t* __restrict__ out_code,
-                                            int64_t rank_base, bool fuse, Win& win) {
+                                            int64_t rank_base, bool fuse, StreamWin& win) {
     const int n = X.n;
 #pragma unroll 1
     for (int ci = threadIdx.x; ci < cnt; ci += NT) {
         const uint32_t row_s = tile_s + (uint32_t)ci * n;        // shared address of the row
         const unsigned long long bm = boundary_mask<NW>(row_s & ~3u, (int)(row_s & 3u) * 8);
-        // ---- runs: b = each boundary in ascending order, then n
         double mk = 0.0;
-        int a = 0, prev = -1, nruns = 0;
-        uint32_t wmax = 0, seen = 0, rowb = X.T_s, bad = 0;      // rowb: address of T[a][0][0] (square)
-        auto run = [&](int b) {
-            uint32_t w = lds_u8(row_s + a);
-            wmax = max(wmax, w);
-            w = min(w, X.Pm1);
-            seen |= 1u << w;
-            ++nruns;
-            uint32_t addr;
-            if (SQUARE) addr = rowb + 8u * ((uint32_t)b * X.uP + w);
-            else addr = X.T_s + 8u * ((lds_u32(X.rowidx_s + 4u * a) + b) * X.uP + w);
-            const double tv = lds_f64s(addr);
-            double v = fabs(tv);
-            if (PAIR && a > 0) {
-                double al, be;
-                link_of(t, prev, (int)w, al, be);
-                double rd = 0.0;
-                for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
-                    rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
-                v = v + rd;
+        uint32_t end = (uint32_t)n, seen = 0, bad = 0xffffffffu;
+        int prev_w = -1;
+        auto run = [&](uint32_t b) {                             // run [b, end)
+            const uint32_t w = lds_u8(row_s + b);
+            seen |= 1u << w;                                     // shl clamps: w >= 32 leaves no bit
+            uint32_t idx;
+            if (SQUARE) idx = b * X.rowstride + end * X.uP + w;
+            else idx = ((b * (X.tri_k - b)) >> 1) * X.uP + (end - b - 1) * X.uP + w;
+            const uint32_t addr = X.T_s + 8u * idx;
+            double v = lds_f64s(addr);
+            if (PAIR) {
+                // chain stages: the crossing read of run [b, end) is priced with
+                // the link from the owner of stage b-1 (the next run visited)
+                if (b > 0) {
+                    const int pw = (int)lds_u8(row_s + b - 1);
+                    double al, be;
+                    link_of(t, pw, (int)w, al, be);
+                    double rd = 0.0;
+                    for (int e = t.edge_ptr[b]; e < t.edge_ptr[b + 1]; ++e)
+                        rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
+                    v = copysign(fabs(v) + rd, v);
+                }
             }
-            mk = v > mk ? v : mk;
-            bad = (signbit(tv) && !bad) ? (addr | 0x80000000u) : bad;   // shared addresses < 2^31
-            prev = (int)w; a = b;
-            if (SQUARE) rowb = X.T_s + (uint32_t)b * X.n1P8;
+            mk = fabs(v) > fabs(mk) ? v : mk;                    // sign cleared after the loop
+            const uint32_t s = (uint32_t)(__double2hiint(v) >> 31);
+            bad = min(bad, addr | ~s);
+            end = b;
         };
-        for (uint32_t y = (uint32_t)bm & X.mask_lo; y; y &= y - 1) run(__ffs(y));
         if (NW > 8)
-            for (uint32_t y = (uint32_t)(bm >> 32) & X.mask_hi; y; y &= y - 1) run(32 + __ffs(y));
-        run(n);
-        int code = bad ? (int)lds_u8(X.C_s + (((bad & 0x7fffffffu) - X.T_s) >> 3)) : DM_V_OK;
-        const bool unknown = wmax >= X.uP;
-        if (!unknown && __popc(seen) != nruns) eval_owner_grouped(t, tile + (size_t)ci * n, mk, code);
+            for (uint32_t y = (uint32_t)(bm >> 32) & X.mask_hi; y; ) {
+                const uint32_t k = 31u - __clz(y);
+                y ^= 1u << k;
+                run(33u + k);
+            }
+        for (uint32_t y = (uint32_t)bm & X.mask_lo; y; ) {
+            const uint32_t k = 31u - __clz(y);
+            y ^= 1u << k;
+            run(1u + k);
+        }
+        run(0u);
+        (void)prev_w;
+        mk = fabs(mk);
+        const int nruns = __popcll(bm & (((unsigned long long)X.mask_hi << 32) | X.mask_lo)) + 1;
+        int code = bad != 0xffffffffu ? (int)lds_u8(X.C_s + ((bad - X.T_s) >> 3)) : DM_V_OK;
+        bool unknown = false;
+        if (__popc(seen) != nruns || (seen & X.pmask)) {        // repeated peer or owner >= P
+            const unsigned char* row = tile + (size_t)ci * n;
+            for (int i = 0; i < n; ++i) if (row[i] >= X.uP) { unknown = true; break; }
+            if (!unknown) eval_owner_grouped(t, row, mk, code);
+        }
         out_mk[c0 + ci] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
         out_code[c0 + ci] = unknown ? (uint8_t)0xFF : (uint8_t)code;
-        if (fuse) {                          // fused arg-min (first strict minimum by rank)
-            win.n_eval++;
-            if (!unknown && code == DM_V_OK) {
-                win.n_feas++;
-                win.csum += (uint64_t)__double_as_longlong(mk);
-                if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank_base + c0 + ci; }
-            }
+        if (fuse && !unknown && code == DM_V_OK) {      // fused arg-min (first strict minimum by rank)
+            win.n_feas++;
+            win.csum += (uint64_t)__double_as_longlong(mk);
+            if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank_base + c0 + ci; }
         }
     }
 }
@@ -489,14 +521,17 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
     const int tid = threadIdx.x;
     const int nw = (n + 3) >> 2;
     const uint32_t sm_s = (uint32_t)__cvta_generic_to_shared(sm);
-    const uint32_t T_s = sm_s + (uint32_t)L.off_T, rowidx_s = sm_s + (uint32_t)L.off_rowidx;
+    const uint32_t T_s = sm_s + (uint32_t)L.off_T;
     const uint32_t C_s = sm_s + (uint32_t)L.off_code;
     StreamCtx X;
-    X.n = n; X.uP = (uint32_t)P; X.Pm1 = X.uP - 1u; X.n1P8 = 8u * (uint32_t)(n + 1) * X.uP;
-    X.T_s = T_s; X.C_s = C_s; X.rowidx_s = rowidx_s;
+    X.n = n; X.uP = (uint32_t)P; X.rowstride = (uint32_t)(n + 1) * X.uP;
+    X.T_s = T_s; X.C_s = C_s; X.tri_k = 2u * (uint32_t)n + 1u;
+    X.pmask = P >= 32 ? 0u : ~((1u << P) - 1u);
     X.mask_lo = n - 1 >= 32 ? 0xffffffffu : ((1u << (n - 1)) - 1u);
     X.mask_hi = n - 1 >= 64 ? 0xffffffffu : (n - 1 > 32 ? ((1u << (n - 33)) - 1u) : 0u);
-    Win win; win_init(win);
+    StreamWin win;
+    win.mk = __longlong_as_double(0x7ff0000000000000LL); win.rank = -1; win.n_feas = 0; win.csum = 0;
+    int64_t n_seen = 0;
     int64_t it_local = 0;
     for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x, ++it_local) {
         const int st = (int)(it_local % stages);
@@ -511,6 +546,7 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
             __syncthreads();
         }
         const uint32_t tile_s = sm_s + (uint32_t)(tile - sm);
+        if (tid < cnt) n_seen += (cnt - tid + NT - 1) / NT;
         switch (nw) {     // the boundary-mask width is fixed per launch: one dispatch per tile
 #define DM_STREAM_TILE(W)                                                                              \
             case W: stream_tile<PAIR, SQUARE, NT, W>(t, X, tile_s, tile, cnt, c0, out_mk, out_code, rank_base, \
@@ -531,7 +567,11 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
             }
         }
     }
-    if (partial) block_reduce_win_store(win, partial);
+    if (partial) {
+        Win w;
+        w.mk = win.mk; w.rank = win.rank; w.n_eval = n_seen; w.n_feas = win.n_feas; w.csum = win.csum;
+        block_reduce_win_store(w, partial);
+    }
 }
 
 // ---------------------------------------------------------------- arg-min
@@ -642,53 +682,49 @@ static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner
     {
         const uint32_t f = t->flags;
         bool memo_ok = !(f & DM_F_INCLUDE_COMM) || !(f & DM_F_PAIR_LINKS) || (f & DM_F_CHAIN);
-        // pick a configuration: a square table with 2 CTAs x 256 threads per
-        // SM and a 4-candidate x 3-stage tile ring when it fits half the SM
-        // (C1: 8.4e10 vs 7.7e10 cand/s for 3 CTAs x 2 candidates), else 3 CTAs
-        // (<= 85 registers) with 2-candidate tiles, else 2 CTAs with other
-        // tile shapes, else the triangular table with one 512-thread CTA per SM
+        // pick a configuration (threads, CTAs per SM, candidates per thread
+        // per tile, ring stages, table shape): the square table when it fits
+        // with several CTAs per SM (no row-offset arithmetic per run), else
+        // the triangular table with one large CTA per SM.  DM_MODEA_CFG =
+        // "nt,minb,cpt,stages,square" overrides (experiments).
+        struct Cfg { int nt, minb, cpt, stages, square; };
+        static const Cfg kCfgs[] = {{256, 2, 4, 3, 1}, {256, 4, 2, 2, 1}, {256, 3, 2, 3, 1}, {256, 2, 2, 2, 1},
+                                    {768, 1, 1, 2, 0}, {512, 1, 1, 2, 0}, {512, 1, 1, 1, 0}};
+        const size_t smem_sm = 227 * 1024;
         dm::StreamLayout L{};
+        Cfg cfg{0, 0, 0, 0, 0};
         bool found = false;
-        int minb = 2;
-        L = dm::stream_layout(t->n, t->P, 3, 4, true, 256);
-        if (L.bytes <= 110 * 1024) found = true;
-        if (!found) {
-            L = dm::stream_layout(t->n, t->P, 3, 2, true, 256);
-            if (L.bytes <= 72 * 1024) { found = true; minb = 3; }
+        for (const Cfg& c : kCfgs) {
+            L = dm::stream_layout(t->n, t->P, c.stages, c.cpt, c.square == 1, c.nt);
+            if ((L.bytes + 1024) * c.minb <= smem_sm) { cfg = c; found = true; break; }
         }
-        if (const char* cfg = std::getenv("DM_MODEA_CFG")) {      // experiments: "minb,cpt,stages" (square)
-            int mb = 0, cp = 0, sg = 0;
-            if (std::sscanf(cfg, "%d,%d,%d", &mb, &cp, &sg) == 3 && (mb == 2 || mb == 3)) {
-                dm::StreamLayout L2 = dm::stream_layout(t->n, t->P, sg, cp, true, 256);
-                if (L2.bytes <= (mb == 3 ? 72 : 110) * 1024) { L = L2; found = true; minb = mb; }
+        if (const char* env = std::getenv("DM_MODEA_CFG")) {
+            Cfg c{};
+            if (std::sscanf(env, "%d,%d,%d,%d,%d", &c.nt, &c.minb, &c.cpt, &c.stages, &c.square) == 5) {
+                dm::StreamLayout L2 = dm::stream_layout(t->n, t->P, c.stages, c.cpt, c.square == 1, c.nt);
+                if ((L2.bytes + 1024) * c.minb <= smem_sm) { L = L2; cfg = c; found = true; }
             }
-        }
-        for (int sq = 1; sq >= 0 && !found; --sq) {
-            const int nt = sq ? 256 : 512;
-            for (int cpt = 4; cpt >= 1 && !found; cpt /= 2)
-                for (int stages = 4; stages >= 2 && !found; --stages) {
-                    L = dm::stream_layout(t->n, t->P, stages, cpt, sq == 1, nt);
-                    if (L.bytes <= (sq ? 110 * 1024 : 220 * 1024)) found = true;
-                }
-            minb = sq ? 2 : 1;
         }
         const char* dis = std::getenv("DM_DISABLE_MEMO");
         bool aligned = (((uintptr_t)owner) & 15) == 0;
         if (found && owner_bytes == 1 && memo_ok && aligned && t->n <= 64 && t->P <= 32 &&
             !(dis && dis[0] && dis[0] != '0')) {
-            int per_sm = minb;
             const int tile_cand = L.nt * L.cpt;
             int64_t n_tiles = (n_cand + tile_cand - 1) / tile_cand;
-            int64_t grid = (int64_t)sm_count() * per_sm;
+            int64_t grid = (int64_t)sm_count() * cfg.minb;
             if (grid > n_tiles) grid = n_tiles;
             if (out && grid > 8 * sm_count()) grid = 8 * sm_count();   // partial slots in scratch
             const bool pair = (t->flags & DM_F_INCLUDE_COMM) && (t->flags & DM_F_PAIR_LINKS);
-            auto kern = !L.square ? (pair ? dm::eval_owner_stream_kernel<true, false, 512, 1>
-                                          : dm::eval_owner_stream_kernel<false, false, 512, 1>)
-                      : minb == 3 ? (pair ? dm::eval_owner_stream_kernel<true, true, 256, 3>
-                                          : dm::eval_owner_stream_kernel<false, true, 256, 3>)
-                                  : (pair ? dm::eval_owner_stream_kernel<true, true, 256, 2>
-                                          : dm::eval_owner_stream_kernel<false, true, 256, 2>);
+            using KernT = void (*)(dm_tables, int64_t, const uint8_t*, double*, uint8_t*, int64_t, dm_winner*, int, int);
+            KernT kern = nullptr;
+#define DM_PICK(NT, MB, SQ)                                                                               \
+            if (cfg.nt == NT && cfg.minb == MB && cfg.square == SQ)                                       \
+                kern = pair ? dm::eval_owner_stream_kernel<true, SQ == 1, NT, MB>                         \
+                            : dm::eval_owner_stream_kernel<false, SQ == 1, NT, MB>;
+            DM_PICK(256, 4, 1) DM_PICK(256, 3, 1) DM_PICK(256, 2, 1) DM_PICK(512, 2, 1) DM_PICK(128, 8, 1)
+            DM_PICK(768, 1, 0) DM_PICK(512, 1, 0) DM_PICK(1024, 1, 0) DM_PICK(256, 2, 0)
+#undef DM_PICK
+            if (!kern) return dmabi::fail(DM_E_ARG, "dm_eval_owner: unsupported DM_MODEA_CFG");
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
             kern<<<(int)grid, L.nt, L.bytes, s>>>(*t, n_cand, (const uint8_t*)owner, out_makespan, out_code, rank_base,
                                                   out ? (dm_winner*)scratch : nullptr, L.stages, L.cpt);

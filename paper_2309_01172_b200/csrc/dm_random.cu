@@ -1,0 +1,347 @@
+// dm_random.cu — random contiguous placements scored in-kernel (configs C3,
+// C5): candidate k of a seeded stream is generated on chip (recipe in
+// paper_2309_01172_b200/rng.py, restated by oracle/dm_oracle.c
+// or_random_candidate) and scored with brute_force_schedule's inner body
+// (scheduling.py:264-272): skip the candidate if any run fails _fits
+// (:172-176), else makespan = max over runs of compute + read (_run_cost
+// :156-169); the winner is the first strict minimum by candidate index.
+//
+//  * random_warp_kernel (chain-structured stages with exact integral columns,
+//    n <= 256): each lane generates one candidate — r, its cut positions
+//    (Knuth's selection sampling, written to a per-lane shared-memory row) and
+//    its four Feistel round keys — then the warp scores its 32 candidates one
+//    after another, lane q taking run q (+32, +64, ...): pass A tests _fits
+//    for every run (early exit on the first chunk with a failing run, warp
+//    vote), pass B (feasible candidates only) prices the runs and max-reduces
+//    over the warp.  Stage prefix records and the online peers' records sit in
+//    shared memory.
+//  * random_generic_kernel: one thread per candidate, runs walked as the
+//    cuts are drawn (any column types, chain-structured or no comm).
+#include "dm_common.cuh"
+#include "dm_abi_util.cuh"
+
+#include <cstdlib>
+
+namespace dm {
+
+// ------------------------------------------------------------ generator
+__host__ __device__ __forceinline__ uint64_t rmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint32_t mulhi32(uint32_t u, uint32_t m) { return __umulhi(u, m); }
+
+// xoshiro128** (Blackman & Vigna), seeded from SplitMix64 of (key, k)
+struct Xo128 {
+    uint32_t s0, s1, s2, s3;
+    __device__ __forceinline__ void seed(uint64_t key, int64_t k) {
+        const uint64_t za = rmix64(key + 2ULL * (uint64_t)k + 1ULL), zb = rmix64(key + 2ULL * (uint64_t)k + 2ULL);
+        s0 = (uint32_t)za; s1 = (uint32_t)(za >> 32); s2 = (uint32_t)zb; s3 = (uint32_t)(zb >> 32);
+        if (!(s0 | s1 | s2 | s3)) s0 = 1u;
+    }
+    __device__ __forceinline__ uint32_t next() {
+        const uint32_t res = __funnelshift_l(s1 * 5u, s1 * 5u, 7) * 9u, t = s1 << 9;
+        s2 ^= s0; s3 ^= s1; s1 ^= s2; s0 ^= s3; s2 ^= t;
+        s3 = __funnelshift_l(s3, s3, 11);
+        return res;
+    }
+};
+
+// keyed 4-round balanced Feistel permutation of [0, n_online) (cycle
+// walking); round function = multiply-shift hash of R ^ key (top h bits)
+struct Feistel {
+    uint32_t k0, k1, k2, k3, h, mask, n, sh;
+    __device__ __forceinline__ uint32_t once(uint32_t x) const {
+        uint32_t L = x >> h, R = x & mask, t;
+        t = R; R = L ^ (((R ^ k0) * 0x9E3779B1u) >> sh); L = t;
+        t = R; R = L ^ (((R ^ k1) * 0x9E3779B1u) >> sh); L = t;
+        t = R; R = L ^ (((R ^ k2) * 0x9E3779B1u) >> sh); L = t;
+        t = R; R = L ^ (((R ^ k3) * 0x9E3779B1u) >> sh); L = t;
+        return (L << h) | R;
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t q) const {
+        uint32_t x = once(q);
+        while (x >= n) x = once(x);
+        return x;
+    }
+};
+
+__host__ __device__ inline uint32_t feistel_half_bits(int32_t n_online) {
+    uint32_t v = (uint32_t)(n_online > 1 ? n_online - 1 : 1), bits = 0;
+    while (v) { ++bits; v >>= 1; }
+    uint32_t h = (bits + 1) / 2;
+    return h < 1 ? 1 : h;
+}
+
+// ------------------------------------------------------ warp-cooperative
+constexpr int kRandThreads = 256;
+
+// bytes per lane row of cut positions: n - 1 cuts at most, rounded to words
+// plus one word so consecutive rows start in different banks
+__host__ __device__ inline int cut_row_bytes(int n) { return ((n + 3) & ~3) + 4; }
+
+struct __align__(16) RStage { double pf, pg, pc, pd, R, pad; };     // exact prefix sums at boundary i; read of a run starting at i
+struct __align__(16) RPeer { double speed, cg, cc, cd; };
+
+struct RandLayout {
+    size_t off_stage, off_peer, off_cuts, bytes;
+};
+
+__host__ __device__ inline RandLayout rand_layout(int n, int n_online) {
+    RandLayout L;
+    size_t off = 0;
+    L.off_stage = off; off += (size_t)(n + 1) * sizeof(RStage);
+    L.off_peer = off; off += (size_t)n_online * sizeof(RPeer);
+    L.off_cuts = off; off += (size_t)kRandThreads * cut_row_bytes(n);
+    L.bytes = (off + 15) & ~(size_t)15;
+    return L;
+}
+
+template <bool PAIR>
+__global__ void __launch_bounds__(kRandThreads, 4) random_warp_kernel(dm_tables t, const int32_t* __restrict__ online,
+                                                                      int32_t n_online, uint64_t key, int64_t k0,
+                                                                      int64_t k1, dm_winner* partial) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int n = t.n;
+    const RandLayout L = rand_layout(n, n_online);
+    RStage* SR = reinterpret_cast<RStage*>(sm + L.off_stage);
+    RPeer* PR = reinterpret_cast<RPeer*>(sm + L.off_peer);
+    unsigned char* cuts = sm + L.off_cuts;
+    const bool comm = include_comm(t);
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+        RStage r;
+        r.pf = (double)t.pre_flops[i]; r.pg = (double)t.pre_gpu[i];
+        r.pc = (double)t.pre_cpu[i]; r.pd = (double)t.pre_disk[i];
+        double rd = 0.0;
+        if (comm && i < n)       // uniform link: a run starting at i reads stage i's in-edges
+            for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e)
+                rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
+        r.R = rd; r.pad = 0.0;
+        SR[i] = r;
+    }
+    for (int i = threadIdx.x; i < n_online; i += blockDim.x) {
+        const int w = online[i];
+        RPeer r;
+        r.speed = t.speed[w]; r.cg = t.cap_gpu[w]; r.cc = t.cap_cpu[w]; r.cd = t.cap_disk[w];
+        PR[i] = r;
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int row_bytes = cut_row_bytes(n);
+    unsigned char* myrow = cuts + (size_t)threadIdx.x * row_bytes;
+    const unsigned char* wrows = cuts + (size_t)(warp * 32) * row_bytes;
+    const uint32_t rmax = (uint32_t)(n < n_online ? n : n_online);
+    Feistel F;
+    F.h = feistel_half_bits(n_online); F.mask = (1u << F.h) - 1u; F.n = (uint32_t)n_online; F.sh = 32u - F.h;
+    Win w; win_init(w);
+    const int64_t span = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = k0 + (int64_t)blockIdx.x * blockDim.x; base < k1; base += span) {
+        // ---- generation: one candidate per lane
+        const int64_t k = base + threadIdx.x;
+        int r = 0;
+        uint32_t kr0 = 0, kr1 = 0, kr2 = 0, kr3 = 0;
+        if (k < k1) {
+            Xo128 g;
+            g.seed(key, k);
+            r = 1 + (int)mulhi32(g.next(), rmax);
+            uint32_t need = (uint32_t)(r - 1);
+            unsigned char* dst = myrow;
+            for (int pos = 1; pos < n && need; ++pos) {
+                const uint32_t cut = mulhi32(g.next(), (uint32_t)(n - pos)) < need ? 1u : 0u;
+                *dst = (unsigned char)pos;          // kept only when this position is a cut
+                dst += cut;
+                need -= cut;
+            }
+            kr0 = g.next(); kr1 = g.next(); kr2 = g.next(); kr3 = g.next();
+            w.n_eval++;
+        }
+        __syncwarp();
+        // ---- scoring: the warp walks its 32 candidates
+        for (int c = 0; c < 32; ++c) {
+            const int rc = __shfl_sync(0xffffffffu, r, c);
+            if (!rc) continue;
+            F.k0 = __shfl_sync(0xffffffffu, kr0, c); F.k1 = __shfl_sync(0xffffffffu, kr1, c);
+            F.k2 = __shfl_sync(0xffffffffu, kr2, c); F.k3 = __shfl_sync(0xffffffffu, kr3, c);
+            const unsigned char* row = wrows + (size_t)c * row_bytes;
+            // pass A: _fits of every run, 32 runs per step
+            bool ok = true;
+            int carry = 0;
+            for (int q0 = 0; q0 < rc; q0 += 32) {
+                const int q = q0 + lane;
+                const bool act = q < rc;
+                const int b = act ? (q == rc - 1 ? n : (int)row[q]) : n;
+                int a = __shfl_up_sync(0xffffffffu, b, 1);
+                if (lane == 0) a = carry;
+                carry = __shfl_sync(0xffffffffu, b, 31);
+                bool fit = true;
+                if (act) {
+                    const uint32_t pid = F((uint32_t)q);
+                    const RStage& sa = SR[a];
+                    const RStage& sb = SR[b];
+                    const RPeer& pr = PR[pid];
+                    fit = (sb.pg - sa.pg <= pr.cg) & (sb.pc - sa.pc <= pr.cc) & (sb.pd - sa.pd <= pr.cd);
+                }
+                if (!__all_sync(0xffffffffu, fit)) { ok = false; break; }
+            }
+            if (!ok) continue;
+            // pass B: loads of the runs of a feasible candidate
+            double mx = 0.0;
+            carry = 0;
+            int carry_pe = -1;
+            for (int q0 = 0; q0 < rc; q0 += 32) {
+                const int q = q0 + lane;
+                const bool act = q < rc;
+                const int b = act ? (q == rc - 1 ? n : (int)row[q]) : n;
+                int a = __shfl_up_sync(0xffffffffu, b, 1);
+                if (lane == 0) a = carry;
+                carry = __shfl_sync(0xffffffffu, b, 31);
+                int pe = -1;
+                double load = 0.0;
+                if (act) {
+                    const uint32_t pid = F((uint32_t)q);
+                    const double sp = PR[pid].speed;
+                    pe = PAIR ? __ldg(online + pid) : 0;
+                    load = (SR[b].pf - SR[a].pf) / sp;
+                }
+                int prev = __shfl_up_sync(0xffffffffu, pe, 1);
+                if (lane == 0) prev = carry_pe;
+                carry_pe = __shfl_sync(0xffffffffu, pe, 31);
+                if (act && comm && a > 0) {
+                    double rd;
+                    if (PAIR) {
+                        double al, be;
+                        link_of(t, prev, pe, al, be);
+                        rd = 0.0;
+                        for (int e = t.edge_ptr[a]; e < t.edge_ptr[a + 1]; ++e)
+                            rd = __dadd_rn(rd, comm_time(al, be, t.edge_m[e]));
+                    } else {
+                        rd = SR[a].R;
+                    }
+                    load = load + rd;
+                }
+                mx = load > mx ? load : mx;
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const double o = __shfl_xor_sync(0xffffffffu, mx, off);
+                mx = o > mx ? o : mx;
+            }
+            if (lane == c) {
+                w.n_feas++;
+                w.csum += (uint64_t)__double_as_longlong(mx);
+                if (w.rank < 0 || mx < w.mk) { w.mk = mx; w.rank = k; }
+            }
+        }
+        __syncwarp();
+    }
+    block_reduce_win_store(w, partial);
+}
+
+// --------------------------------------------------------------- generic
+__global__ void __launch_bounds__(256) random_generic_kernel(dm_tables t, const int32_t* __restrict__ online,
+                                                             int32_t n_online, uint64_t key, int64_t k0, int64_t k1,
+                                                             dm_winner* partial) {
+    Win w; win_init(w);
+    const int n = t.n;
+    const uint32_t rmax = (uint32_t)(n < n_online ? n : n_online);
+    Feistel F;
+    F.h = feistel_half_bits(n_online); F.mask = (1u << F.h) - 1u; F.n = (uint32_t)n_online; F.sh = 32u - F.h;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1; k += stride) {
+        Xo128 g;
+        g.seed(key, k);
+        const int r = 1 + (int)mulhi32(g.next(), rmax);
+        // cut positions first (they consume the draws before the round keys)
+        uint32_t need = (uint32_t)(r - 1);
+        uint64_t cm[4] = {0ull, 0ull, 0ull, 0ull};     // cut bitmap, n <= 257
+        for (int pos = 1; pos < n && need; ++pos)
+            if (mulhi32(g.next(), (uint32_t)(n - pos)) < need) { cm[(pos - 1) >> 6] |= 1ull << ((pos - 1) & 63); --need; }
+        F.k0 = g.next(); F.k1 = g.next(); F.k2 = g.next(); F.k3 = g.next();
+        w.n_eval++;
+        bool ok = true;
+        double mk = 0.0;
+        int a = 0, q = 0, prev = -1;
+        for (int b = 1; b <= n && ok; ++b) {
+            if (b < n && !((cm[(b - 1) >> 6] >> ((b - 1) & 63)) & 1ull)) continue;
+            const int pe = online[F((uint32_t)q)];
+            ok = fits_range(t, pe, a, b);
+            double c, rd;
+            run_cost_contig(t, a, b, pe, [&](int) { return prev; }, c, rd);
+            const double load = c + rd;
+            mk = (q == 0 || load > mk) ? load : mk;
+            prev = pe; a = b; ++q;
+        }
+        if (ok) {
+            w.n_feas++;
+            w.csum += (uint64_t)__double_as_longlong(mk);
+            if (w.rank < 0 || mk < w.mk) { w.mk = mk; w.rank = k; }
+        }
+    }
+    block_reduce_win_store(w, partial);
+}
+
+__global__ void random_finalize_kernel(const dm_winner* partial, int n_parts, dm_winner* out) {
+    Win w; win_init(w);
+    for (int i = threadIdx.x; i < n_parts; i += blockDim.x) {
+        Win o;
+        o.mk = partial[i].makespan; o.rank = partial[i].rank; o.n_eval = partial[i].n_evaluated;
+        o.n_feas = partial[i].n_feasible; o.csum = partial[i].checksum;
+        win_merge(w, o);
+    }
+    __shared__ dm_winner tmp[1];
+    block_reduce_win_store(w, tmp);
+    __syncthreads();
+    if (threadIdx.x == 0) *out = tmp[0];
+}
+
+}  // namespace dm
+
+namespace {
+int sm_count_r() {
+    static thread_local int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+}  // namespace
+
+extern "C" {
+
+int dm_enum_random(const dm_tables* t, const int32_t* online, int32_t n_online, uint64_t seed, int64_t k0,
+                   int64_t k1, dm_winner* out, void* scratch, void* stream) {
+    if (!t || !online || n_online <= 0 || !out || !scratch || t->n <= 0 || k0 < 0 || k1 < k0)
+        return dmabi::fail(DM_E_ARG, "dm_enum_random: bad arguments");
+    if (t->n > 257) return dmabi::fail(DM_E_TOO_LARGE, "random placements support n <= 257");
+    if (!(t->flags & DM_F_CHAIN) && (t->flags & DM_F_INCLUDE_COMM))
+        return dmabi::fail(DM_E_ARG, "random placements need chain-structured stages");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t key = dm::rmix64(seed + 0x9E3779B97F4A7C15ULL);
+    const dm::RandLayout L = dm::rand_layout(t->n, n_online);
+    const bool exact = (t->flags & DM_F_FLOPS_EXACT) && (t->flags & DM_F_BYTES_EXACT);
+    const char* dis = std::getenv("DM_DISABLE_MEMO");
+    int grid;
+    if (exact && t->n <= 256 && L.bytes <= 110 * 1024 && !(dis && dis[0] && dis[0] != '0')) {
+        int per_sm = (int)((227 * 1024) / (L.bytes + 1024));
+        per_sm = per_sm > 4 ? 4 : per_sm;
+        grid = sm_count_r() * per_sm;     // partial slots: <= dm_enum_scratch_bytes
+        const bool pair = (t->flags & DM_F_PAIR_LINKS) && (t->flags & DM_F_INCLUDE_COMM);
+        auto kern = pair ? dm::random_warp_kernel<true> : dm::random_warp_kernel<false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
+        kern<<<grid, dm::kRandThreads, L.bytes, s>>>(*t, online, n_online, key, k0, k1, (dm_winner*)scratch);
+    } else {
+        grid = sm_count_r() * 8;
+        dm::random_generic_kernel<<<grid, 256, 0, s>>>(*t, online, n_online, key, k0, k1, (dm_winner*)scratch);
+    }
+    DM_CHECK_LAUNCH();
+    dm::random_finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, grid, out);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+}  // extern "C"

@@ -146,7 +146,7 @@ def argmin_scores(mk, code, rank_base: int = 0, bufs: WinnerBuffers | None = Non
 
 
 def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | None = None,
-         index: int = 0, online=None, mults=None, seed: int = 0, part: int = 0, nparts: int = 1,
+         index: int = 0, online=None, seed: int = 0, part: int = 0, nparts: int = 1,
          phase: int = 3):
     """Mode B enumeration: 'bruteforce' | 'splits' | 'random'. Returns bufs
     (call bufs.read() to synchronise and fetch the winner).  'splits' takes
@@ -165,9 +165,8 @@ def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | 
                                             bufs.scratch.data_ptr(), ws.data_ptr() if ws is not None else None,
                                             max(need, 0), phase, s))
     elif mode == "random":
-        _lib.check(lib.dm_enum_random(C.byref(st), online.data_ptr(), online.numel(), mults.data_ptr(),
-                                      mults.numel(), seed & 0xFFFFFFFFFFFFFFFF, k0, k1, bufs.out.data_ptr(),
-                                      bufs.scratch.data_ptr(), s))
+        _lib.check(lib.dm_enum_random(C.byref(st), online.data_ptr(), online.numel(), seed & 0xFFFFFFFFFFFFFFFF,
+                                      k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
     else:
         raise ValueError(mode)
     return bufs

@@ -22,7 +22,7 @@ from typing import NamedTuple
 import numpy as np
 
 from . import _lib
-from .model import FleetError
+from .refapi import FleetError
 from .tensorize import build_host
 
 ELEMENT_BYTES = 4

@@ -21,7 +21,7 @@ from typing import Sequence
 import numpy as np
 
 from . import engine, scheduling
-from .model import Link, SchedulingError, bandwidth_to_beta
+from .refapi import Link, SchedulingError, bandwidth_to_beta
 from .tensorize import build_host
 
 

@@ -20,8 +20,8 @@ from types import SimpleNamespace
 import numpy as np
 
 from . import _lib, engine
-from . import model as _model
-from .model import peer_sort_key
+from . import refapi as _model
+from .refapi import peer_sort_key
 from .tensorize import build_host
 
 # Result/error classes; install() points these at the reference's own

@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .model import FleetError, effective_speed
+from .refapi import FleetError, effective_speed
 
 _EXACT_LIMIT = 2 ** 53
 _ALIGN = 256

@@ -10,7 +10,7 @@ links that take the proportional + hill-climb path.
 
 import numpy as np
 
-from paper_2309_01172_b200 import model as M
+from paper_2309_01172_b200 import refapi as M
 
 
 def uniform_fleet(speeds, link=M.ZERO_LINK, gpu_gb=64.0, backups=()):

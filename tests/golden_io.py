@@ -3,8 +3,8 @@
 Ints stay ints and floats are written with repr (bit-exact round trip), so
 the column types the reference's own sum()/compare expressions see are
 preserved.  Loaders rebuild instances in any module that provides the
-reference's type names (the reference package itself, or the engine's
-mirror `paper_2309_01172_b200.model`)."""
+reference's type names (the reference package, directly or through
+`paper_2309_01172_b200.refapi`)."""
 
 from __future__ import annotations
 
@@ -97,3 +97,11 @@ def report_matches(got, want) -> list:
     if "types" in want and g["types"] != want["types"]:
         bad.append("types")
     return bad
+
+
+def c4_record(owner, vals) -> bytes:
+    """One C4 scenario in the full-size digest (tests/golden/make_full_size.py):
+    the owner vector as little-endian int16 and six float64 values (makespan,
+    Eq. 3 latency, bottleneck, Eq. 4 pipe time, throughput, violation code)."""
+    import struct
+    return np.asarray(owner, dtype="<i2").tobytes() + struct.pack("<6d", *[float(v) for v in vals])

@@ -9,7 +9,7 @@ import pathlib
 import pytest
 
 from golden_io import load_fleet, load_stages, report_matches, runs_of
-from paper_2309_01172_b200 import model as M
+from paper_2309_01172_b200 import refapi as M
 from paper_2309_01172_b200 import pipeline as P
 from paper_2309_01172_b200 import scheduling as S
 

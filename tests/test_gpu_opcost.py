@@ -6,7 +6,7 @@ import pytest
 
 from golden_io import load_fleet
 from opcost_util import TableGraph, load
-from paper_2309_01172_b200 import model as M
+from paper_2309_01172_b200 import refapi as M
 from paper_2309_01172_b200 import opcost as O
 
 pytestmark = pytest.mark.gpu

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from gen import big_instance, criterion6_instances, random_stages, uniform_fleet
-from paper_2309_01172_b200 import engine, model as M, rng as R, scheduling as S
+from paper_2309_01172_b200 import engine, refapi as M, rng as R, scheduling as S
 from paper_2309_01172_b200.tensorize import build_host
 
 pytestmark = pytest.mark.gpu
@@ -187,16 +187,15 @@ def _random_case(oracle_mod, rng, links):
     host = build_host(st, fleet)
     batch = engine.device_batch([host])
     online = np.sort(rng.choice(256, 200, replace=False)).astype(np.int32)
-    mults = np.array(R.coprime_multipliers(200, 5), np.int32)
     dev = batch.dev_buf.device
-    on_d, mu_d = torch.from_numpy(online).to(dev), torch.from_numpy(mults).to(dev)
-    for seed, k0, k1 in [(1, 0, 30000), (2, 1000, 21000)]:
-        got = engine.enum(batch, "random", k0, k1, online=on_d, mults=mu_d, seed=seed).read()
-        want = inst.enum_random(online, mults, seed, k0, k1)
+    on_d = torch.from_numpy(online).to(dev)
+    for seed, k0, k1 in [(1, 0, 30000), (2, 1000, 21000), (3, 2**33, 2**33 + 5000)]:
+        got = engine.enum(batch, "random", k0, k1, online=on_d, seed=seed).read()
+        want = inst.enum_random(online, seed, k0, k1)
         assert got == want
         if got["rank"] >= 0:
-            b, pe = R.candidate(60, online, mults, seed, got["rank"])
-            runs = tuple((host.peer_ids[pe[q]], tuple(range(b[q], b[q + 1]))) for q in range(len(pe)))
+            b, pe = R.candidate(60, len(online), seed, got["rank"])
+            runs = tuple((host.peer_ids[online[pe[q]]], tuple(range(b[q], b[q + 1]))) for q in range(len(pe)))
             assert S.evaluate_runs(st, fleet, runs).makespan == got["makespan"]
 
 
@@ -487,3 +486,55 @@ def test_sweep_graph_part_units_merge(engine_ready):
     g.launch()
     torch.cuda.synchronize()
     assert D.merge_records(g.out.cpu().numpy()) == want
+
+
+# Every Mode A stream configuration (threads, CTAs/SM, candidates per thread,
+# ring stages, square/triangular table) against the oracle, with contiguous,
+# non-contiguous and out-of-range owners (P <= w < 32 and w >= 32), a ragged
+# last tile and the fused arg-min.
+MODEA_CFGS = ["256,4,2,3,1", "256,3,2,3,1", "256,2,4,3,1", "128,8,2,3,1", "512,2,1,2,1",
+              "768,1,1,2,0", "512,1,1,2,0", "1024,1,1,2,0", "256,2,2,3,0"]
+
+
+@pytest.mark.parametrize("cfg", MODEA_CFGS)
+@pytest.mark.parametrize("shape", [(26, 4), (34, 32), (12, 7), (64, 9)])
+def test_eval_owner_stream_configs(oracle_mod, engine_ready, monkeypatch, cfg, shape):
+    import torch
+    n, p = shape
+    rng = np.random.default_rng(1000 + n * p)
+    st, fleet = big_instance(rng, n, p, dag=False, links=False, pressure=(0.1, 0.6))
+    inst = oracle_mod.Instance(st, fleet)
+    host = build_host(st, fleet)
+    batch = engine.device_batch([host])
+    N = 4099
+    own = np.zeros((N, n), np.int64)
+    for c in range(N):
+        r = int(rng.integers(1, min(n, p) + 1))
+        cuts = sorted(rng.choice(np.arange(1, n), r - 1, replace=False).tolist()) if r > 1 else []
+        b = [0] + cuts + [n]
+        pe = rng.choice(p, r, replace=False)
+        for q in range(r):
+            own[c, b[q]:b[q + 1]] = pe[q]
+        if c % 97 == 5:
+            own[c] = rng.integers(0, p, n)                     # non-contiguous
+    own[11, n // 2] = p + 1                                    # P <= w < 32
+    own[12, n - 1] = 200                                       # w >= 32
+    own[13, 0] = 255
+    monkeypatch.setenv("DM_MODEA_CFG", cfg)
+    o_d = torch.from_numpy(own.astype(np.uint8)).cuda()
+    (mk, code), bufs = engine.eval_owner_argmin(batch, o_d, rank_base=77)
+    win = bufs.read()
+    mk, code = mk.cpu().numpy(), code.cpu().numpy()
+    best, feas, csum = None, 0, 0
+    for c in range(N):
+        m_o, c_o = inst.eval_owner(own[c])
+        assert int(code[c]) == c_o, (cfg, c)
+        assert same(float(mk[c]), m_o), (cfg, c, float(mk[c]).hex(), m_o.hex())
+        if c_o == 0:
+            feas += 1
+            csum = (csum + int(np.float64(m_o).view(np.uint64))) % (1 << 64)
+            if best is None or m_o < best[0]:
+                best = (m_o, 77 + c)
+    assert win["n_evaluated"] == N and win["n_feasible"] == feas and win["checksum"] == csum
+    if best:
+        assert (win["makespan"], win["rank"]) == best

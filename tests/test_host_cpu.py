@@ -14,7 +14,7 @@ import pytest
 
 from paper_2309_01172_b200 import configs as CF
 from paper_2309_01172_b200 import dist as D
-from paper_2309_01172_b200 import engine, model as M, rng as R
+from paper_2309_01172_b200 import engine, refapi as M, rng as R
 from paper_2309_01172_b200.tensorize import build_host
 
 GOLD = pathlib.Path(__file__).resolve().parent / "golden"
@@ -44,19 +44,43 @@ def test_oracle_unrank_matches_python(oracle_mod):
 
 
 def test_rng_python_matches_c(oracle_mod):
-    online = np.arange(0, 900, 3, dtype=np.int32)
-    mults = np.array(R.coprime_multipliers(len(online), 9), np.int32)
-    assert all(math.gcd(int(a), len(online)) == 1 for a in mults)
-    import ctypes as C
+    """rng.py (product-side restatement of the candidate recipe) and the
+    oracle's C restatement draw identical candidates."""
     L = oracle_mod.lib()
     b = np.zeros(300, np.int32)
     pe = np.zeros(300, np.int32)
-    for k in [0, 1, 2, 17, 10**9, 2**40 + 3]:
-        r = L.or_random_candidate(194, len(online), online.ctypes.data, mults.ctypes.data, len(mults), 12345, k,
-                                  b.ctypes.data, pe.ctypes.data)
-        bb, pp = R.candidate(194, online, mults, 12345, k)
-        assert b[: r + 1].tolist() == bb and pe[:r].tolist() == pp
+    for n, n_online in ((194, 922), (162, 256), (5, 3), (1, 1), (40, 1000), (257, 300)):
+        for k in [0, 1, 2, 17, 10**9, 2**40 + 3]:
+            r = L.or_random_candidate(n, n_online, 12345, k, b.ctypes.data, pe.ctypes.data)
+            bb, pp = R.candidate(n, n_online, 12345, k)
+            assert b[: r + 1].tolist() == bb and pe[:r].tolist() == pp
+            assert len(set(pp)) == len(pp) and all(0 <= x < n_online for x in pp)
+            assert 1 <= r <= min(n, n_online) and bb == sorted(set(bb)) and bb[0] == 0 and bb[-1] == n
+
+
+def test_rng_distribution_matches_survey():
+    """r ~ U{1..min(n, n_online)} and, given r, every
+    (r-1)-subset of the cut positions equally likely (chi-square on a small
+    shape), r distinct peers."""
+    from collections import Counter
+    n, n_online, N = 6, 4, 24000
+    by_r, subsets = Counter(), Counter()
+    for k in range(N):
+        bb, pp = R.candidate(n, n_online, 7, k)
+        by_r[len(pp)] += 1
+        subsets[tuple(bb)] += 1
         assert len(set(pp)) == len(pp)
+    assert set(by_r) == {1, 2, 3, 4}
+    assert all(abs(c - N / 4) < 5 * math.sqrt(N / 4) for c in by_r.values())
+    for r in (2, 3, 4):
+        cells = [c for s, c in subsets.items() if len(s) == r + 1]
+        assert len(cells) == math.comb(n - 1, r - 1)
+        exp = by_r[r] / len(cells)
+        chi2 = sum((c - exp) ** 2 / exp for c in cells)
+        assert chi2 < 3 * len(cells) + 20
+    # peers: every online index appears as run 0 about equally often
+    first = Counter(R.candidate(10, 5, 3, k)[1][0] for k in range(5000))
+    assert set(first) == set(range(5)) and max(first.values()) < 1.25 * min(first.values())
 
 
 def test_shard_covers_range():
@@ -127,7 +151,7 @@ def test_report_assembly_types_golden():
 
     from golden_io import load_fleet, load_stages, report_matches, runs_of
     from oracle import oracle as O
-    from paper_2309_01172_b200 import model as M
+    from paper_2309_01172_b200 import refapi as M
     from paper_2309_01172_b200 import scheduling as S
     from paper_2309_01172_b200.tensorize import build_host
 

@@ -7,7 +7,7 @@ import numpy as np
 
 from golden_io import load_fleet
 from opcost_util import load
-from paper_2309_01172_b200 import model as M
+from paper_2309_01172_b200 import refapi as M
 
 
 def _csr(lists):

@@ -8,7 +8,7 @@ import pathlib
 import pytest
 
 from golden_io import load_fleet, load_stages, runs_of
-from paper_2309_01172_b200 import model as M
+from paper_2309_01172_b200 import refapi as M
 
 GOLD = pathlib.Path(__file__).resolve().parent / "golden"
 CASES = json.loads((GOLD / "scheduling_cases.json").read_text())["cases"]

@@ -25,7 +25,7 @@ def _ref_types(dm):
 
 def test_oracle_matches_live_reference(ref, oracle_mod):
     from gen import big_instance, random_stages, uniform_fleet
-    from paper_2309_01172_b200 import model as M
+    from paper_2309_01172_b200 import refapi as M
     rng = np.random.default_rng(20261018)
     RT = _ref_types(ref)
     S, PL = ref.scheduling, ref.pipeline
