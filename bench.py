@@ -555,26 +555,40 @@ def dp_c4b_measure(dev, n_scen=4096):
 
 def api_latency_measure(dev):
     """End-to-end latency of one public schedule() call (host objects in, a
-    ScheduleReport out; tensorise + H2D + DP kernel + report kernel + D2H) on C1."""
+    ScheduleReport out: tensorise, one H2D, DP kernel, report kernel, one D2H)
+    on C1 and on C3, beside the reference's own schedule() (dagmesh from
+    baseline/_ref, pure Python) on the same inputs in the same process."""
     import time as _t
     import torch
     from paper_2309_01172_b200 import configs as CF
     from paper_2309_01172_b200 import scheduling as S
-    stages = CF.model_stages("gpt2-small")
-    fleet = CF.load(CF.c1_fleet_doc(10.0, 1e-3))
-    for _ in range(3):
-        S.schedule(stages, fleet)
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(20):
-        t0 = _t.perf_counter()
-        rep = S.schedule(stages, fleet)
-        times.append((_t.perf_counter() - t0) * 1e3)
-    return {"config": "C1 gpt2-small x 4 mixed GPUs (10 Gbit/s, 1 ms): schedule() through the public API",
-            "ms_per_call": statistics.median(times), "ms_min": min(times), "ms_max": max(times),
-            "ms_mean": statistics.mean(times), "calls": len(times),
-            "runs": [list(r[1][:1]) + [r[1][-1], r[0]] for r in rep.runs],
-            "makespan": rep.makespan, "trace": list(rep.trace)}
+    from paper_2309_01172_b200.refapi import dagmesh
+    RS = dagmesh.scheduling
+    out = {}
+    for name, stages, fleet, reps in (
+            ("c1", CF.model_stages("gpt2-small"), CF.load(CF.c1_fleet_doc(10.0, 1e-3)), 50),
+            ("c3", CF.model_stages("llama2-70b"), CF.load(CF.c3_fleet_doc(0)), 10)):
+        for _ in range(3):
+            S.schedule(stages, fleet)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(reps):
+            t0 = _t.perf_counter()
+            rep = S.schedule(stages, fleet)
+            times.append((_t.perf_counter() - t0) * 1e3)
+        ref_times = []
+        for _ in range(3 if name == "c1" else 1):
+            t0 = _t.perf_counter()
+            ref = RS.schedule(stages, fleet)
+            ref_times.append((_t.perf_counter() - t0) * 1e3)
+        out[name] = {"ms_per_call": statistics.median(times), "ms_min": min(times), "ms_max": max(times),
+                     "calls": len(times), "reference_ms_per_call": statistics.median(ref_times),
+                     "same_report": rep.runs == ref.runs and rep.makespan == ref.makespan and rep.trace == ref.trace,
+                     "makespan": rep.makespan, "trace": list(rep.trace)}
+    out["config"] = ("schedule() through the public API: C1 gpt2-small x 4 mixed GPUs (10 Gbit/s, 1 ms; exact subset "
+                     "DP) and C3 llama2-70b x 256 workers with 32,640 pairwise links (proportional + hill climb); "
+                     "reference = dagmesh.scheduling.schedule on the same objects")
+    return out
 
 
 def secondary_measurements(dev):

@@ -295,6 +295,22 @@ DM_API int dm_prop_hill(const dm_tables* tables, int32_t n_scen, int32_t n_max,
                  void* stream);
 
 /*
+ * dm_schedule_report — the _evaluate half of one schedule() call
+ * (scheduling.py:210-232, :391-423) on the device: from the owner vector a
+ * search kernel left in `owner` (int16[n], worker indices; `found` = the DP's
+ * found flag or NULL) derive the runs, per run compute / read (_run_cost
+ * :156-169), the first capacity violation in run order (verify_assignment
+ * :199-203) and the makespan, into one record of dm_sched_out_bytes(n) bytes:
+ * int32 {found, n_runs, code, bad_run}, float64 makespan at offset 16,
+ * int32 bounds[n+1] at 32, then int32 peers[n], float64 compute[n] and
+ * float64 read[n], each 8-byte aligned.  `tables` is a device dm_tables.
+ * found == 0 scores ((workers[0], all stages),) as the reference does (:408).
+ */
+DM_API int64_t dm_sched_out_bytes(int32_t n);
+DM_API int dm_schedule_report(const dm_tables* tables, int32_t n, const int16_t* owner, const int32_t* found,
+                              void* out, void* stream);
+
+/*
  * dm_pipeline_epilogue — per scenario, from an owner vector with contiguous
  * runs: _evaluate's makespan and feasibility (:210-232), then
  * fp_latency (Neumaier sum, pipeline.py:41-43), bottleneck (:46-50),
@@ -346,6 +362,11 @@ DM_API int dm_subgraph_times(int32_t n_ops, int32_t n_place, const double* op_ou
  * roofline denominator of the generated-candidate kernels).  *ops receives
  * the number of fp64 operations the launch performs; time it with events. */
 DM_API int dm_microbench_fp64(int64_t iters, double* sink, int64_t* ops, void* stream);
+
+/* dm_microbench_alu — ALU-pipe (LOP3) issue-rate microbenchmark: lane-ops
+ * executed by `iters` iterations of 8 independent chains per thread, full
+ * grid.  The independent roofline denominator of the split sweep. */
+DM_API int dm_microbench_alu(int64_t iters, uint32_t* sink, int64_t* ops, void* stream);
 
 /* dm_microbench_cross — the whole-population split sweep's inner loop alone
  * (one fp64 max + checksum add per candidate pair, register x shared-memory

@@ -714,6 +714,138 @@ EXPORT int or_schedule(const dm_tables* t, int has_links, int32_t* owner) {
     return isinf(sc) ? -2 : 2;
 }
 
+/* ------------------------------------------- meet-in-the-middle sweep (CPU) */
+
+/* The identity-split population (brute_force_schedule's order with run q on
+ * worker q, scheduling.py:260-272) swept with the GPU headline's algorithm
+ * (csrc/dm_mitm.cu) on the CPU: the algorithm-matched CPU baseline of the
+ * bench, and an independent check of the sweep.  Valid when the load of run
+ * q over [a, b) depends on (q, a, b) only (no comm, a uniform link, or chain
+ * stages) — the same condition as the GPU path.
+ *
+ * T[(q*(n+1) + a)*(n+1) + b] = load of run [a, b) on worker q, +inf when the
+ * run fails _fits.  A split with m cuts is grouped by its middle cut
+ * j = ceil(m/2) at position c: left sets (j-1 cuts below c) x right sets
+ * (m-j cuts above c); makespan = max(L, R) (exact), lexicographic rank =
+ * RL + RR (a sum of per-cut terms).  Per feasible pair: one max, one
+ * checksum add, one compare — the GPU's per-pair work. */
+EXPORT void or_mitm_table(const dm_tables* t, double* T) {
+    int n = t->n, p = t->p;
+    int32_t* peer_of = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    uint8_t* inside = (uint8_t*)calloc((size_t)n, 1);
+    for (int q = 0; q < p; ++q)
+        for (int a = 0; a <= n; ++a)
+            for (int b = 0; b <= n; ++b) {
+                double v = INFINITY;
+                if (b > a && fits_range(t, q, a, b)) {
+                    for (int i = 0; i < n; ++i) peer_of[i] = i < a ? (q > 0 ? q - 1 : q + 1) : (i < b ? q : q + 1);
+                    for (int z = 0; z < b - a; ++z) idx[z] = a + z;
+                    double c, rd;
+                    run_cost(t, peer_of, q, idx, b - a, inside, &c, &rd);
+                    v = c + rd;
+                }
+                T[((size_t)q * (n + 1) + a) * (n + 1) + b] = v;
+            }
+    free(peer_of); free(idx); free(inside);
+}
+
+typedef struct { double v; int64_t rank; } mitm_side;
+
+/* Lexicographic rank term of cut i (1-based) at position ci after c_{i-1} =
+ * prev, for m cuts over positions 1..N: sum over v in (prev, ci) of
+ * C(N - v, m - i). */
+static int64_t cut_term(int N, int m, int i, int prev, int ci) {
+    int64_t s = 0;
+    for (int v = prev + 1; v < ci; ++v) s += binom(N - v, m - i);
+    return s;
+}
+
+/* Left sets of block (m, c): cuts 1..j-1 below c; runs 0..j-1. */
+static void mitm_left(const double* T, int n, int m, int j, int c, int q, int prev, double acc, int64_t rk,
+                      mitm_side* out, int64_t* cnt) {
+    int N = n - 1;
+    if (q == j - 1) {                          /* last left run ends at c */
+        double v = T[((size_t)q * (n + 1) + prev) * (n + 1) + c];
+        if (v == INFINITY) return;
+        out[*cnt].v = v > acc ? v : acc;
+        out[*cnt].rank = rk + cut_term(N, m, j, prev, c);
+        ++*cnt;
+        return;
+    }
+    for (int x = prev + 1; x <= c - (j - 1 - q); ++x) {
+        double v = T[((size_t)q * (n + 1) + prev) * (n + 1) + x];
+        if (v == INFINITY) continue;
+        mitm_left(T, n, m, j, c, q + 1, x, v > acc ? v : acc, rk + cut_term(N, m, q + 1, prev, x), out, cnt);
+    }
+}
+
+/* Right sets of block (m, c): cuts j+1..m above c; runs j..m. */
+static void mitm_right(const double* T, int n, int m, int q, int prev, double acc, int64_t rk,
+                       mitm_side* out, int64_t* cnt) {
+    int N = n - 1;
+    if (q == m) {                              /* last run ends at n */
+        double v = T[((size_t)q * (n + 1) + prev) * (n + 1) + n];
+        if (v == INFINITY) return;
+        out[*cnt].v = v > acc ? v : acc;
+        out[*cnt].rank = rk;
+        ++*cnt;
+        return;
+    }
+    for (int x = prev + 1; x <= n - 1 - (m - 1 - q); ++x) {
+        double v = T[((size_t)q * (n + 1) + prev) * (n + 1) + x];
+        if (v == INFINITY) continue;
+        mitm_right(T, n, m, q + 1, x, v > acc ? v : acc, rk + cut_term(N, m, q + 1, prev, x), out, cnt);
+    }
+}
+
+/* Sweep the blocks (m, c) with m in [m_lo, m_hi) (c over every middle
+ * position) and merge into *out (first strict minimum by rank).  `T` from
+ * or_mitm_table.  Returns the number of feasible pairs visited. */
+EXPORT int64_t or_splits_mitm(const dm_tables* t, const double* T, int m_lo, int m_hi, dm_winner* out) {
+    int n = t->n, p = t->p, rmax = n < p ? n : p, N = n - 1;
+    or_win w = {INFINITY, -1, 0, 0, 0};
+    int64_t base = 0;
+    for (int m = 0; m < m_lo && m < rmax; ++m) base += binom(N, m);
+    for (int m = m_lo; m < m_hi && m < rmax; ++m) {
+        int64_t nc = binom(N, m);
+        w.n_eval += nc;
+        if (m == 0) {
+            double v = T[(size_t)0 * (n + 1) * (n + 1) + n];
+            if (v != INFINITY) win_update(&w, v, base);
+            base += nc;
+            continue;
+        }
+        int j = (m + 1) / 2;
+        for (int c = j; c <= N - (m - j); ++c) {
+            int64_t nl = binom(c - 1, j - 1), nr = binom(N - c, m - j), cl = 0, cr = 0;
+            mitm_side* L = (mitm_side*)malloc(sizeof(mitm_side) * (size_t)(nl > 0 ? nl : 1));
+            mitm_side* R = (mitm_side*)malloc(sizeof(mitm_side) * (size_t)(nr > 0 ? nr : 1));
+            mitm_left(T, n, m, j, c, 0, 0, 0.0, 0, L, &cl);
+            mitm_right(T, n, m, j, c, 0.0, 0, R, &cr);
+            for (int64_t a = 0; a < cl; ++a) {
+                double lv = L[a].v;
+                int64_t lr = base + L[a].rank;
+                for (int64_t b = 0; b < cr; ++b) {
+                    double mk = R[b].v > lv ? R[b].v : lv;
+                    uint64_t bits; memcpy(&bits, &mk, 8);
+                    w.csum += bits;
+                    if (mk <= w.mk) {
+                        int64_t rk = lr + R[b].rank;
+                        if (w.rank < 0 || mk < w.mk || rk < w.rank) { w.mk = mk; w.rank = rk; }
+                    }
+                }
+            }
+            w.n_feas += cl * cr;
+            free(L); free(R);
+        }
+        base += nc;
+    }
+    out->makespan = w.mk; out->rank = w.rank; out->n_evaluated = w.n_eval;
+    out->n_feasible = w.n_feas; out->checksum = w.csum;
+    return w.n_feas;
+}
+
 /* -------------------------------------------------------------- epilogue */
 
 /* pipeline.fp_latency / bottleneck / pipeline_time / throughput

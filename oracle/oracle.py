@@ -86,6 +86,10 @@ def lib():
         L.or_schedule.argtypes = [_P, C.c_int, _P]
         L.or_epilogue.restype = None
         L.or_epilogue.argtypes = [C.c_int, _P, _P, _P, C.c_int64, C.c_int64, _P]
+        L.or_mitm_table.restype = None
+        L.or_mitm_table.argtypes = [_P, _P]
+        L.or_splits_mitm.restype = C.c_int64
+        L.or_splits_mitm.argtypes = [_P, _P, C.c_int, C.c_int, _P]
         L.or_py_sum_items.restype = C.c_double
         L.or_py_sum_items.argtypes = [_P, _P, C.c_int64]
         _lib = L
@@ -238,6 +242,19 @@ class Instance:
     def enum(self, mode, k0, k1):
         w = Winner()
         lib().or_enum(C.byref(self.t), {"bruteforce": 0, "splits": 1}[mode], k0, k1, C.byref(w))
+        return dict(makespan=w.makespan, rank=w.rank, n_evaluated=w.n_evaluated, n_feasible=w.n_feasible,
+                    checksum=w.checksum)
+
+    def mitm_table(self):
+        T = np.empty(self.p * (self.n + 1) * (self.n + 1), np.float64)
+        lib().or_mitm_table(C.byref(self.t), _ptr(T))
+        return T
+
+    def splits_mitm(self, T, m_lo, m_hi):
+        """Identity-split sweep over cut counts [m_lo, m_hi) with the GPU's
+        meet-in-the-middle algorithm (or_splits_mitm)."""
+        w = Winner()
+        lib().or_splits_mitm(C.byref(self.t), _ptr(T), m_lo, m_hi, C.byref(w))
         return dict(makespan=w.makespan, rank=w.rank, n_evaluated=w.n_evaluated, n_feasible=w.n_feasible,
                     checksum=w.checksum)
 

@@ -63,7 +63,8 @@ def install(dagmesh_module=None):
             setattr(dagmesh_module, name, getattr(scheduling, name))
 
     def _sweep(model_, fleets, bandwidth_gbps, alpha_s, n_batches):
-        stages = ref_sched.build_stages(model_.graph, model_.cells)
+        from .configs import stages_for
+        stages = stages_for(model_.graph, model_.cells)
         res = sweep_stages(stages, model_.name, model_.samples_per_batch, fleets, bandwidth_gbps, alpha_s,
                            n_batches)
         out = ref_pipe.SweepResult()

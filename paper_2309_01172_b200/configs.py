@@ -23,6 +23,7 @@ the reference's own parse_fleet.
 
 from __future__ import annotations
 
+import functools
 import json
 import math
 
@@ -78,7 +79,13 @@ def encoder_job(hidden: int, layers: int, vocab: int, batch: int, seq: int, inne
 
 def encoder_stages(hidden: int, layers: int, vocab: int, batch: int, seq: int, inner: int | None = None,
                    cells: str = "block") -> list:
-    """Closed-form build_stages of encoder_job(...)."""
+    """Closed-form build_stages of encoder_job(...) (memoised: Stage is a
+    frozen dataclass, so the cached tuple is shared safely)."""
+    return list(_encoder_stages(hidden, layers, vocab, batch, seq, inner, cells))
+
+
+@functools.lru_cache(maxsize=512)
+def _encoder_stages(hidden, layers, vocab, batch, seq, inner, cells) -> tuple:
     job, cl = encoder_job(hidden, layers, vocab, batch, seq, inner, cells)
     b, s, h = batch, seq, hidden
     m = inner if inner is not None else 4 * h
@@ -110,7 +117,72 @@ def encoder_stages(hidden: int, layers: int, vocab: int, batch: int, seq: int, i
         label = cell[0] if len(cell) == 1 else f"{cell[0]}..{cell[-1]}"
         stages.append(Stage(idx, label, flops, ELEMENT_BYTES * (params + act),
                             desc_bytes + ELEMENT_BYTES * params, ELEMENT_BYTES * params, edges))
-    return stages
+    return tuple(stages)
+
+
+def encoder_params(graph, cells):
+    """Parameters (hidden, layers, vocab, batch, seq, inner, cells) when the
+    job graph and cell partition are exactly an encoder chain of the
+    pipeline._encoder_model layout (pipeline.py:85-118) — node names, op
+    classes, kwargs, wiring and output shapes — else None.  Those are the
+    instances encoder_stages() builds in closed form."""
+    try:
+        names = list(graph.topo_order)
+        nodes = graph.nodes
+        if len(names) < 4 or names[0] != "tokens" or names[1] != "embed" or names[-1] != "head":
+            return None
+        tok, emb, head = nodes["tokens"], nodes["embed"], nodes["head"]
+        if tok.kind.value != "placeholder" or len(tok.out_shape) != 2 or tok.users != ("embed",):
+            return None
+        b, s = (int(x) for x in tok.out_shape)
+        if emb.op_class != "embedding" or emb.args != ("tokens",):
+            return None
+        vocab, h = int(emb.kwargs["num_embeddings"]), int(emb.kwargs["embedding_dim"])
+        if set(emb.kwargs) != {"num_embeddings", "embedding_dim"}:
+            return None
+        blocks = names[2:-1]
+        if len(blocks) % 2 or len(blocks) // 2 > 99:
+            return None
+        layers = len(blocks) // 2
+        if blocks != _block_names(layers):
+            return None
+        inner = None
+        prev = "embed"
+        for j, nm in enumerate(blocks):
+            nd = nodes[nm]
+            nxt = blocks[j + 1] if j + 1 < len(blocks) else "head"
+            want = "attention_block" if nm.endswith("att") else "ffn_block"
+            if nd.op_class != want or nd.args != (prev,) or nd.users != (nxt,) or tuple(nd.out_shape) != (b, s, h):
+                return None
+            if want == "attention_block" and nd.kwargs:
+                return None
+            if want == "ffn_block":
+                kw = dict(nd.kwargs)
+                m = kw.pop("inner_features", None)
+                if kw or (j > 1 and m != inner):
+                    return None
+                inner = m
+            prev = nm
+        if head.op_class != "linear" or head.args != (prev,) or head.users or dict(head.kwargs) != {"out_features": h}:
+            return None
+        cl = [tuple(c) for c in cells]
+        for kind in ("block", "layer"):
+            if cl == encoder_job(h, layers, vocab, b, s, inner, kind)[1]:
+                return dict(hidden=h, layers=layers, vocab=vocab, batch=b, seq=s, inner=inner, cells=kind)
+    except (AttributeError, KeyError, TypeError, ValueError):
+        return None
+    return None
+
+
+def stages_for(graph, cells) -> list:
+    """build_stages (scheduling.py:107-145) with the tensoriser fast path:
+    encoder chains in closed form (encoder_stages), anything else through the
+    reference's own builder."""
+    prm = encoder_params(graph, cells)
+    if prm is not None:
+        return encoder_stages(**prm)
+    from dagmesh import scheduling as ref_sched
+    return ref_sched.build_stages(graph, cells)
 
 
 # named models of BASELINE.json configs (SURVEY §8d)

@@ -172,6 +172,109 @@ def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | 
     return bufs
 
 
+# ------------------------------------------------- one-instance API calls
+class ScheduleSlot:
+    """Reusable device staging for one-instance API calls (schedule()): a
+    pinned host buffer and a device buffer for the packed tables plus their
+    dm_tables record, the search outputs and the report record — one H2D,
+    the kernels, one D2H, one synchronisation per call and no allocation
+    once warm.  One slot per (thread, device)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.cap = 0
+        self.n_cap = 0
+
+    def _grow(self, nbytes, n, p):
+        torch = _torch()
+        lib = _lib.load()
+        if nbytes > self.cap:
+            self.cap = max(nbytes, 2 * self.cap, 64 * 1024)
+            self.host = torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
+            self.dev = torch.empty(self.cap, dtype=torch.uint8, device=self.device)
+        if n > self.n_cap or p > getattr(self, "p_cap", 0):
+            self.n_cap = max(n, self.n_cap)
+            self.p_cap = max(p, getattr(self, "p_cap", 0))
+            out_b = int(lib.dm_sched_out_bytes(self.n_cap))
+            self.owner = torch.empty(self.n_cap, dtype=torch.int16, device=self.device)
+            self.owner2 = torch.empty(self.n_cap, dtype=torch.int16, device=self.device)
+            self.vals = torch.empty(2, dtype=torch.float64, device=self.device)
+            self.ints = torch.empty(2, dtype=torch.int32, device=self.device)
+            self.out = torch.empty(out_b, dtype=torch.uint8, device=self.device)
+            self.out_host = torch.empty(out_b, dtype=torch.uint8, pin_memory=True)
+            sb = int(lib.dm_subset_dp_scratch_bytes(self.n_cap, min(self.p_cap, 20), 1))
+            self.scratch = torch.empty(max(sb, 256), dtype=torch.uint8, device=self.device)
+
+    def upload(self, host: HostTables) -> int:
+        """Pack `host` and its dm_tables record into the pinned buffer, start
+        one H2D copy; returns the device address of the record."""
+        size = host.packed_size()
+        rec_off = (size + 255) // 256 * 256
+        self._grow(rec_off + C.sizeof(_lib.DmTables), host.n, host.p)
+        hb = self.host.numpy()
+        offs = host.pack_into(hb, 0)
+        rec = host.struct_record(offs, int(self.dev.data_ptr()))
+        hb[rec_off: rec_off + C.sizeof(_lib.DmTables)] = np.frombuffer(rec.tobytes(), np.uint8)
+        total = rec_off + C.sizeof(_lib.DmTables)
+        self.dev[:total].copy_(self.host[:total], non_blocking=True)
+        return int(self.dev.data_ptr()) + rec_off
+
+    def schedule(self, host: HostTables, use_dp: bool, hill_after_dp: bool) -> dict:
+        """schedule()'s search (scheduling.py:404-419) and the _evaluate of its
+        result (:210-232) on the device; returns the decoded report record."""
+        lib = _lib.load()
+        s = _lib.stream_ptr()
+        rec = self.upload(host)
+        n, p = host.n, host.p
+        found = None
+        owner = self.owner
+        if use_dp:
+            found = self.ints
+            _lib.check(lib.dm_subset_dp(rec, 1, n, p, owner.data_ptr(), self.vals.data_ptr(), found.data_ptr(),
+                                        self.scratch.data_ptr(), s))
+            if hill_after_dp:
+                _lib.check(lib.dm_prop_hill(rec, 1, n, owner.data_ptr(), None, self.owner2.data_ptr(),
+                                            self.vals.data_ptr() + 8, None, s))
+                owner = self.owner2
+        else:
+            _lib.check(lib.dm_prop_hill(rec, 1, n, None, None, owner.data_ptr(), self.vals.data_ptr() + 8, None, s))
+        _lib.check(lib.dm_schedule_report(rec, n, owner.data_ptr(), found.data_ptr() if found is not None else None,
+                                          self.out.data_ptr(), s))
+        ob = int(lib.dm_sched_out_bytes(n))
+        self.out_host[:ob].copy_(self.out[:ob], non_blocking=True)
+        _torch().cuda.current_stream().synchronize()
+        raw = self.out_host.numpy()
+        hdr = raw[:16].view(np.int32)
+        r = int(hdr[1])
+        off_p = 32 + ((n + 1) * 4 + 7) // 8 * 8
+        off_c = off_p + (n * 4 + 7) // 8 * 8
+        return dict(found=int(hdr[0]), n_runs=r, code=int(hdr[2]), bad_run=int(hdr[3]),
+                    makespan=float(raw[16:24].view(np.float64)[0]),
+                    bounds=raw[32: 32 + 4 * (r + 1)].view(np.int32).copy(),
+                    peers=raw[off_p: off_p + 4 * r].view(np.int32).copy(),
+                    compute=raw[off_c: off_c + 8 * r].view(np.float64).copy(),
+                    read=raw[off_c + 8 * n: off_c + 8 * n + 8 * r].view(np.float64).copy())
+
+
+_SLOTS = None
+
+
+def schedule_slot(device=None) -> ScheduleSlot:
+    import threading
+    global _SLOTS
+    if _SLOTS is None:
+        _SLOTS = threading.local()
+    torch = _torch()
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    slots = getattr(_SLOTS, "by_dev", None)
+    if slots is None:
+        slots = _SLOTS.by_dev = {}
+    key = str(dev)
+    if key not in slots:
+        slots[key] = ScheduleSlot(dev)
+    return slots[key]
+
+
 # ------------------------------------------------------------ partitioners
 def subset_dp(batch: DeviceBatch, n_max: int, p_max: int):
     """Batched _subset_dp over every instance of the batch."""
@@ -383,6 +486,25 @@ def sweep_kernel_times(batch: DeviceBatch, total: int, steps: int = 5, bufs: Win
     finally:
         lib.dm_sweep_timing(0, None, None)
     return ta / steps, tb / steps
+
+
+def alu_peak(iters: int = 20000, repeats: int = 3) -> float:
+    """Measured ALU-pipe (LOP3) lane-operations per second on the current device."""
+    lib = _lib.load()
+    torch = _torch()
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ops = C.c_int64(0)
+    s = _lib.stream_ptr()
+    _lib.check(lib.dm_microbench_alu(200, sink.data_ptr(), C.byref(ops), s))
+    best = 0.0
+    for _ in range(repeats):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.check(lib.dm_microbench_alu(iters, sink.data_ptr(), C.byref(ops), s))
+        b.record()
+        b.synchronize()
+        best = max(best, ops.value / (a.elapsed_time(b) / 1e3))
+    return best
 
 
 def fp64_peak(iters: int = 20000, repeats: int = 3) -> float:

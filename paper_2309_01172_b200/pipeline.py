@@ -181,11 +181,12 @@ def sweep_stages(stages, name: str, samples_per_batch: int, fleets, bandwidth_gb
 def sweep(model, fleets, bandwidth_gbps, alpha_s, n_batches: int) -> SweepResult:
     """Schedule the model on each fleet across a link-quality grid
     (pipeline.py:228-248), batched on the GPU.  ``model`` is any object with
-    ``name``, ``graph``, ``cells`` and ``samples_per_batch`` whose stages are
-    built by the reference's ``build_stages``, or an object exposing
+    ``name``, ``graph``, ``cells`` and ``samples_per_batch`` (stages from
+    ``configs.stages_for``: encoder chains in closed form, other graphs
+    through the reference's ``build_stages``), or an object exposing
     ``stages`` directly."""
     stages = getattr(model, "stages", None)
     if stages is None:
-        from dagmesh import scheduling as ref_sched  # reference stage builder (input producer)
-        stages = ref_sched.build_stages(model.graph, model.cells)
+        from .configs import stages_for
+        stages = stages_for(model.graph, model.cells)
     return sweep_stages(stages, model.name, model.samples_per_batch, fleets, bandwidth_gbps, alpha_s, n_batches)

@@ -22,7 +22,7 @@ import numpy as np
 from . import _lib, engine
 from . import refapi as _model
 from .refapi import peer_sort_key
-from .tensorize import build_host
+from .tensorize import build_host, stage_side
 
 # Result/error classes; install() points these at the reference's own
 # classes so reports built here are instances of dagmesh.scheduling types.
@@ -260,22 +260,27 @@ def schedule(stages, fleet, *, include_comm: bool = True):
         runs = tuple((workers[k], tuple(run)) for k, run in enumerate(fleet.pinned_runs))
         return _evaluate(stages, fleet, runs, include_comm, ("pinned runs",))
 
-    host = build_host(stages, fleet, include_comm)
-    batch = engine.device_batch([host], pin=False)
-    if n * n * p * (2 ** p) <= 3_000_000:
-        owner, _, found, _ = engine.subset_dp(batch, n, p)
-        if not int(found[0].item()):
-            report = _evaluate(stages, fleet, ((workers[0], tuple(range(n))),), include_comm,
-                               ("exact search: no feasible assignment",), host)
+    # one H2D, the search kernel(s), the report kernel, one D2H (engine.ScheduleSlot)
+    use_dp = n * n * p * (2 ** p) <= 3_000_000                   # :406
+    pairs = None
+    if fleet.links and include_comm and not use_dp and stage_side(stages).is_chain:
+        # proportional split + hill climb keep run q on worker q and chain
+        # stages read only from the previous run: links (q-1, q) suffice
+        pairs = [(q - 1, q) for q in range(1, min(n, p))]
+    host = build_host(stages, fleet, include_comm, link_pairs=pairs)
+    out = engine.schedule_slot().schedule(host, use_dp, use_dp and bool(fleet.links))
+    b, pe = out["bounds"], out["peers"]
+    runs = tuple((workers[int(pe[q])], tuple(range(int(b[q]), int(b[q + 1])))) for q in range(out["n_runs"]))
+    r = out["n_runs"]
+    res = dict(cand_ptr=np.array([0, r]), code=np.array([out["code"]]), code_run=np.array([out["bad_run"]]),
+               compute=out["compute"], read=out["read"], makespan=np.array([out["makespan"]]))
+    if use_dp:
+        if not out["found"]:
+            report = _report(stages, fleet, runs, include_comm, ("exact search: no feasible assignment",), res,
+                             0, host)
             return _mark_infeasible(report, "no feasible assignment under memory constraints")
-        if fleet.links:
-            owner, _, _ = engine.prop_hill(batch, n, init_owner=owner)
-        runs = _owner_to_runs(workers, owner.cpu().numpy()[0], n)
-        return _evaluate(stages, fleet, runs, include_comm, ("exact subset search",), host)
-
-    owner, _, _ = engine.prop_hill(batch, n)
-    runs = _owner_to_runs(workers, owner.cpu().numpy()[0], n)
-    report = _evaluate(stages, fleet, runs, include_comm, ("proportional split with boundary search",), host)
+        return _report(stages, fleet, runs, include_comm, ("exact subset search",), res, 0, host)
+    report = _report(stages, fleet, runs, include_comm, ("proportional split with boundary search",), res, 0, host)
     if not report.feasible:
         return _mark_infeasible(report, report.reason or "no feasible assignment under memory constraints")
     return report

@@ -125,57 +125,114 @@ class HostTables:
         return rec
 
 
-def build_host(stages, fleet, include_comm: bool = True) -> HostTables:
-    """Tensorise one instance on the host (O(n + E + P + |links|))."""
+class _StageSide:
+    """Fleet-independent part of an instance: stage columns, exact prefixes,
+    CSR in-edges with the raw message sizes, structural flags."""
+
+    __slots__ = ("stages", "n", "flops", "pre_flops", "gpu", "pre_gpu", "cpu", "pre_cpu", "disk", "pre_disk",
+                 "bytes_exact", "edge_ptr", "edge_src", "nbytes", "nbytes_f64", "is_chain", "backward",
+                 "np_flops", "np_bytes", "np_edges", "src_range_ok")
+
+    def __init__(self, stages):
+        self.stages = stages                      # keeps the (immutable) Stage objects alive: ids stay unique
+        n = self.n = len(stages)
+        self.flops, self.pre_flops = _exact_column([s.flops for s in stages])
+        self.gpu, self.pre_gpu = _exact_column([s.gpu_bytes for s in stages])
+        self.cpu, self.pre_cpu = _exact_column([s.cpu_bytes for s in stages])
+        self.disk, self.pre_disk = _exact_column([s.disk_bytes for s in stages])
+        self.bytes_exact = self.pre_gpu is not None and self.pre_cpu is not None and self.pre_disk is not None
+        edge_ptr = np.zeros(n + 1, dtype=np.int32)
+        srcs, nbs = [], []
+        is_chain, backward, ok = True, False, True
+        for i, st in enumerate(stages):
+            for src, nbytes in st.in_edges:
+                src = int(src)
+                ok &= 0 <= src < n
+                srcs.append(src)
+                nbs.append(nbytes)
+                is_chain &= src == i - 1
+                backward |= src >= i
+            edge_ptr[i + 1] = len(srcs)
+        self.edge_ptr, self.edge_src = edge_ptr, np.array(srcs, dtype=np.int32)
+        self.nbytes = nbs
+        # int message sizes below 2^53 multiply like CPython's int * float
+        self.nbytes_f64 = (np.array(nbs, dtype=np.float64)
+                           if all(type(v) is int and abs(v) < _EXACT_LIMIT for v in nbs) else None)
+        self.is_chain, self.backward, self.src_range_ok = is_chain, backward, ok
+
+        def _np(v):
+            return type(v) not in (int, float, bool)
+        self.np_flops = any(_np(s.flops) for s in stages)
+        self.np_bytes = any(_np(s.gpu_bytes) or _np(s.cpu_bytes) or _np(s.disk_bytes) for s in stages)
+        self.np_edges = any(_np(nb) for nb in nbs)
+
+
+_STAGE_CACHE: dict = {}
+_STAGE_CACHE_MAX = 256
+
+
+def _stage_side(stages) -> _StageSide:
+    """Cached by the identity of the Stage objects: Stage is a frozen
+    dataclass, so an instance's columns never change, and the cache entry
+    holds the objects so their ids cannot be reused while cached.  (Fleet is
+    mutable — its side is rebuilt every call.)"""
+    key = tuple(map(id, stages))
+    side = _STAGE_CACHE.get(key)
+    if side is None:
+        side = _StageSide(stages)
+        if len(_STAGE_CACHE) >= _STAGE_CACHE_MAX:
+            _STAGE_CACHE.pop(next(iter(_STAGE_CACHE)))
+        _STAGE_CACHE[key] = side
+    return side
+
+
+def stage_side(stages) -> _StageSide:
+    """Fleet-independent tables of a stage list (cached for frozen Stage objects)."""
     stages = list(stages)
-    n = len(stages)
+    params = getattr(type(stages[0]), "__dataclass_params__", None) if stages else None
+    return _stage_side(stages) if params is not None and params.frozen else _StageSide(stages)
+
+
+def build_host(stages, fleet, include_comm: bool = True, link_pairs=None) -> HostTables:
+    """Tensorise one instance on the host (O(n + E + P + |links|); the stage
+    side is cached per stage list).  ``link_pairs`` (peer-index pairs) limits
+    the pairwise link matrix to the entries a caller's kernels will read
+    (resolved with the fleet's own link_between, hardware.py:136-140; the
+    rest holds the default link) instead of every override."""
+    stages = list(stages)
+    st = stage_side(stages)
+    n = st.n
     workers = tuple(fleet.worker_ids())
-    wset = set(workers)
-    others = tuple(pid for pid in fleet.peer_ids() if pid not in wset)
-    order = workers + others
+    if len(workers) == len(fleet.peers):
+        order = workers
+    else:
+        wset = set(workers)
+        order = workers + tuple(pid for pid in fleet.peer_ids() if pid not in wset)
     index_of = {pid: i for i, pid in enumerate(order)}
     P = len(order)
 
-    flops, pre_flops = _exact_column([s.flops for s in stages])
-    gpu, pre_gpu = _exact_column([s.gpu_bytes for s in stages])
-    cpu, pre_cpu = _exact_column([s.cpu_bytes for s in stages])
-    disk, pre_disk = _exact_column([s.disk_bytes for s in stages])
-    bytes_exact = pre_gpu is not None and pre_cpu is not None and pre_disk is not None
-
-    edge_ptr = np.zeros(n + 1, dtype=np.int32)
-    srcs, ms = [], []
-    is_chain, backward = True, False
     ratio = fleet.msg_ratio
-    for i, st in enumerate(stages):
-        for src, nbytes in st.in_edges:
-            src = int(src)
-            if include_comm and not 0 <= src < n:
-                raise KeyError(src)
-            m = nbytes * ratio                   # CPython float product, as :168
-            if include_comm and m < 0:
-                raise FleetError("message size must be nonnegative")
-            srcs.append(src)
-            ms.append(float(m))
-            if src != i - 1:
-                is_chain = False
-            if src >= i:
-                backward = True
-        edge_ptr[i + 1] = len(srcs)
-    edge_src = np.array(srcs, dtype=np.int32)
-    edge_m = np.array(ms, dtype=np.float64)
+    if st.nbytes_f64 is not None and type(ratio) is float:
+        edge_m = st.nbytes_f64 * ratio                  # = CPython's nbytes * msg_ratio (:168), exact int -> float
+    else:
+        edge_m = np.array([float(nb * ratio) for nb in st.nbytes], dtype=np.float64)
+    if include_comm and (not st.src_range_ok or (edge_m.size and (edge_m < 0).any())):
+        for s_ in stages:                               # the first offending edge decides the error
+            for src, nbytes in s_.in_edges:
+                if not 0 <= int(src) < n:
+                    raise KeyError(int(src))
+                if nbytes * ratio < 0:
+                    raise FleetError("message size must be nonnegative")
 
     peers = [fleet.peers[pid] for pid in order]
     speeds = [effective_speed(pe) for pe in peers]
     speed = np.array(speeds, dtype=np.float64)
     # CPython's sum() is compensated only over exact `float` items
     peer_np = np.array([0 if type(v) in (int, float, bool) else 1 for v in speeds] or [0], dtype=np.uint8)
+
     def _np(v):
         return type(v) not in (int, float, bool)
-    np_flops = any(_np(s.flops) for s in stages)
-    np_bytes = any(_np(s.gpu_bytes) or _np(s.cpu_bytes) or _np(s.disk_bytes) for s in stages)
-    np_comm = (_np(fleet.msg_ratio) or _np(fleet.default_link.alpha) or _np(fleet.default_link.beta)
-               or any(_np(lk.alpha) or _np(lk.beta) for lk in fleet.links.values())
-               or any(_np(nb) for s in stages for _, nb in s.in_edges))
+    np_comm = _np(ratio) or _np(fleet.default_link.alpha) or _np(fleet.default_link.beta) or st.np_edges
     cap_gpu = np.array([float(pe.gpu_bytes) for pe in peers], dtype=np.float64)
     cap_cpu = np.array([float(pe.cpu_bytes) for pe in peers], dtype=np.float64)
     cap_disk = np.array([float(pe.disk_bytes) for pe in peers], dtype=np.float64)
@@ -186,44 +243,56 @@ def build_host(stages, fleet, include_comm: bool = True) -> HostTables:
     if fleet.links:
         la = np.full((P, P), float(d.alpha), dtype=np.float64)
         lb = np.full((P, P), float(d.beta), dtype=np.float64)
-        direct = set()
-        for (a, b), lk in fleet.links.items():
-            ia, ib = index_of.get(str(a)), index_of.get(str(b))
-            if ia is None or ib is None:
-                continue
-            direct.add((ia, ib))
-        for (a, b), lk in fleet.links.items():   # links[(a,b)] wins over links[(b,a)]
-            ia, ib = index_of.get(str(a)), index_of.get(str(b))
-            if ia is None or ib is None:
-                continue
-            la[ia, ib], lb[ia, ib] = lk.alpha, lk.beta
-            if (ib, ia) not in direct:
-                la[ib, ia], lb[ib, ia] = lk.alpha, lk.beta
+        if link_pairs is not None:
+            for ia, ib in link_pairs:
+                if ia != ib:
+                    lk = fleet.link_between(order[ia], order[ib])
+                    la[ia, ib], lb[ia, ib] = lk.alpha, lk.beta
+                    np_comm = np_comm or _np(lk.alpha) or _np(lk.beta)
+        else:
+            ia_l, ib_l, al_l, be_l = [], [], [], []
+            get = index_of.get
+            for (a, b), lk in fleet.links.items():
+                ia, ib = get(a if type(a) is str else str(a)), get(b if type(b) is str else str(b))
+                al, be = lk.alpha, lk.beta
+                if type(al) is not float or type(be) is not float:
+                    np_comm = np_comm or _np(al) or _np(be)
+                if ia is None or ib is None:
+                    continue
+                ia_l.append(ia)
+                ib_l.append(ib)
+                al_l.append(al)
+                be_l.append(be)
+            if ia_l:
+                ia_a, ib_a = np.array(ia_l, np.int64), np.array(ib_l, np.int64)
+                al_a, be_a = np.array(al_l, np.float64), np.array(be_l, np.float64)
+                la[ib_a, ia_a], lb[ib_a, ia_a] = al_a, be_a      # links[(b, a)] serves (a, b) ...
+                la[ia_a, ib_a], lb[ia_a, ib_a] = al_a, be_a      # ... unless links[(a, b)] exists
         np.fill_diagonal(la, 0.0)
         np.fill_diagonal(lb, 0.0)
         link_alpha, link_beta = la.reshape(-1), lb.reshape(-1)
         flags |= _lib.DM_F_PAIR_LINKS
 
-    if pre_flops is not None:
+    if st.pre_flops is not None:
         flags |= _lib.DM_F_FLOPS_EXACT
-    if bytes_exact:
+    if st.bytes_exact:
         flags |= _lib.DM_F_BYTES_EXACT
-    if is_chain:
+    if st.is_chain:
         flags |= _lib.DM_F_CHAIN
-    if backward:
+    if st.backward:
         flags |= _lib.DM_F_BACKWARD
     if include_comm:
         flags |= _lib.DM_F_INCLUDE_COMM
-    flags |= (_lib.DM_F_NP_FLOPS if np_flops else 0) | (_lib.DM_F_NP_BYTES if np_bytes else 0)
+    flags |= (_lib.DM_F_NP_FLOPS if st.np_flops else 0) | (_lib.DM_F_NP_BYTES if st.np_bytes else 0)
     flags |= _lib.DM_F_NP_COMM if np_comm else 0
 
     zero_pre = np.zeros(n + 1, dtype=np.int64)
-    arrays = dict(flops=flops, gpu=gpu, cpu=cpu, disk=disk,
-                  pre_flops=pre_flops if pre_flops is not None else zero_pre,
-                  pre_gpu=pre_gpu if bytes_exact else zero_pre,
-                  pre_cpu=pre_cpu if bytes_exact else zero_pre,
-                  pre_disk=pre_disk if bytes_exact else zero_pre,
-                  edge_ptr=edge_ptr, edge_src=edge_src if edge_src.size else np.zeros(1, np.int32),
+    arrays = dict(flops=st.flops, gpu=st.gpu, cpu=st.cpu, disk=st.disk,
+                  pre_flops=st.pre_flops if st.pre_flops is not None else zero_pre,
+                  pre_gpu=st.pre_gpu if st.bytes_exact else zero_pre,
+                  pre_cpu=st.pre_cpu if st.bytes_exact else zero_pre,
+                  pre_disk=st.pre_disk if st.bytes_exact else zero_pre,
+                  edge_ptr=st.edge_ptr, edge_src=st.edge_src if st.edge_src.size else np.zeros(1, np.int32),
                   edge_m=edge_m if edge_m.size else np.zeros(1, np.float64),
                   speed=speed, cap_gpu=cap_gpu, cap_cpu=cap_cpu, cap_disk=cap_disk,
                   link_alpha=link_alpha, link_beta=link_beta, peer_np=peer_np)

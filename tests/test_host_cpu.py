@@ -192,3 +192,34 @@ def test_bench_scenario_units_cover_every_scenario_once():
             for s in range(n_scen):
                 parts = sorted((p, k) for (sc, p, k) in flat if sc == s)
                 assert parts and [p for p, _ in parts] == list(range(parts[0][1]))
+
+
+def test_stage_fast_path_equals_reference_build_stages():
+    """Tensoriser fast path (configs.stages_for: encoder chains in closed
+    form) against the reference's own build_stages on every model the
+    benchmark builds — all 196 C4 models (block cells), the C4b layer-cell
+    chains, the named configs — and the reference's own MODELS; a graph
+    that is not an encoder chain falls back to build_stages."""
+    from dagmesh import ir, pipeline as PL, scheduling as RS
+    jobs = []
+    for L in range(32, 81):
+        for h in CF.C4_HIDDEN:
+            jobs.append(CF.encoder_job(h, L, 32000, 4, 1024))
+    for L in range(24, 37):
+        jobs.append(CF.encoder_job(4096, L, 32000, 4, 1024, cells="layer"))
+    for kw in CF.MODELS.values():
+        jobs.append(CF.encoder_job(**kw))
+    for job, cells in jobs:
+        g = ir.parse_job_definition(job)
+        assert CF.encoder_params(g, cells) is not None
+        assert CF.stages_for(g, cells) == RS.build_stages(g, cells)
+    for mdl in (PL.build_bert_large(), PL.build_gpt3_24(), PL.build_bert_large(2, 64)):
+        assert CF.encoder_params(mdl.graph, mdl.cells) is not None
+        assert CF.stages_for(mdl.graph, mdl.cells) == RS.build_stages(mdl.graph, mdl.cells)
+    job, cells = CF.encoder_job(1024, 3, 30522, 2, 64)
+    g = ir.parse_job_definition(job)
+    topo = RS.topological_cells(g)
+    assert CF.encoder_params(g, topo) is None and CF.stages_for(g, topo) == RS.build_stages(g, topo)
+    job["nodes"][3]["kwargs"] = {"inner_features": 77}          # one ffn differs from the others
+    g = ir.parse_job_definition(job)
+    assert CF.encoder_params(g, cells) is None and CF.stages_for(g, cells) == RS.build_stages(g, cells)
