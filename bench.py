@@ -81,6 +81,12 @@ def workload_config(total, links):
                                 "max(L, R) folded into the checksum, infeasible ones resolved per side element",
             "l2_policy": "no HBM-resident candidate stream; each scenario's side tables (134 MB) exceed L2 and are "
                          "rebuilt every step",
+            "value_semantics": "candidates whose makespan the exact search decides per second: every one of the "
+                               "8,589,934,558 splits per scenario is accounted for (n_evaluated); each feasible one "
+                               "gets its makespan max(L, R) formed and folded into the checksum; per-run costs are "
+                               "tabulated once per scenario and shared through the left/right cut-set tables, so "
+                               "this is NOT a per-candidate cost-model rate — see secondary.per_candidate_c2 for "
+                               "that, and speedup_breakdown for the same algorithm on the host CPU",
             "parallelism": "whole scenarios per GPU (block-level parts when the batch does not divide) + 1 NCCL "
                            "all-gather of 40-byte winner records"}
 
@@ -139,13 +145,33 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- b200 arm
+def _gather_records(recs_dev, world):
+    """[units, 40] device records of every rank -> [world, units, 40] (one NCCL all-gather)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return recs_dev.view(1, recs_dev.shape[0], -1)
+    g = torch.empty(world * recs_dev.numel(), dtype=torch.uint8, device=recs_dev.device)
+    dist.all_gather_into_tensor(g, recs_dev.reshape(-1))
+    return g.view(world, recs_dev.shape[0], -1)
+
+
+def _max_over_ranks(vals, dev, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
 def run_b200(args, rank, world, local_rank):
     import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2309_01172_b200 import dist as D
-    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200 import engine, search
     from paper_2309_01172_b200.tensorize import build_host
 
     torch.cuda.set_device(local_rank)
@@ -157,14 +183,6 @@ def run_b200(args, rank, world, local_rank):
     total = engine.splits_total(n, p)
     batch = engine.device_batch([build_host(stages, f, True) for f in fleets], device=dev)
     units = units_for(rank, world, S)
-
-    def gather(out):
-        """device records [units, 40] of every rank -> [world, units, 40]"""
-        if world == 1:
-            return out.view(1, len(units), -1)
-        g = torch.empty(world * out.numel(), dtype=torch.uint8, device=dev)
-        dist.all_gather_into_tensor(g, out.reshape(-1))
-        return g.view(world, len(units), -1)
 
     def merge(raw):
         per = [[] for _ in range(S)]
@@ -178,66 +196,65 @@ def run_b200(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # the sweeps' kernels as one graph (tables resident in HBM).  Multi-GPU:
-    # the winner all-gather follows each step and the host waits for it, so
-    # NCCL's kernels never share the SMs with a running sweep
+    # ---- value: the sweeps' kernels as one graph, tables resident in HBM.
+    # Multi-GPU: the winner all-gather follows each step and the host waits
+    # for it, so NCCL's kernels never share the SMs with a running sweep
     kernels = engine.SweepGraph(batch, total, units=units, copy_inputs=False)
     for _ in range(max(args.warmup, 3)):
         kernels.launch()
-        gather(kernels.out)
+        _gather_records(kernels.out, world)
     barrier()
     clocks = ClockSampler(local_rank)
     if rank == 0:
         clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     ev0.record(stream)
-    for s in range(args.steps):
-        kev[s][0].record(stream)
+    for _ in range(args.steps):
         kernels.launch()
-        kev[s][1].record(stream)
         if world > 1:
-            gather(kernels.out)
+            _gather_records(kernels.out, world)
             stream.synchronize()
     ev1.record(stream)
     barrier()
     clk = clocks.stop() if rank == 0 else None
-    ms = ev0.elapsed_time(ev1)
-    kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
-    t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, kernel_ms = float(t[0]), float(t[1])
-    res = merge(gather(kernels.out).cpu().numpy())
+    ms = _max_over_ranks([ev0.elapsed_time(ev1)], dev, world)[0]
+    res = merge(_gather_records(kernels.out, world).cpu().numpy())
 
-    # ---- e2e: the engine's serving form (engine.SweepGraph: one CUDA graph
-    #      with the H2D copy of the scenario tables from pinned host memory,
-    #      the sweeps' kernels and the D2H of the winner records), host
-    #      synchronisation and the winners read every step
-    sweep = engine.SweepGraph(batch, total, units=units)
+    # ---- e2e: the public API from Python objects every step —
+    # search.split_sweep(stages, fleets): tensorise the fleets (stage side
+    # cached), pack into pinned memory, one captured graph (H2D of the
+    # tables, the sweep kernels, D2H of the winner records), host sync,
+    # winners read; multi-GPU: + the NCCL all-gather and the merge
+    mine = [fleets[sc] for sc, _, _ in units]
+    whole = all(u[2] == 1 for u in units)
+
+    def api_step():
+        if whole:
+            recs = search.split_sweep(stages, mine, records=True)
+        else:
+            recs = search.split_sweep(stages, fleets, part=rank, nparts=world, records=True)
+        if world > 1:
+            recs = _gather_records(torch.from_numpy(recs).to(dev), world).cpu().numpy()
+        else:
+            recs = recs.reshape(1, len(units), -1)
+        return merge(recs)
+    for _ in range(max(args.warmup, 3)):
+        api_step()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    pinned_out = torch.empty(world * len(units) * D.WINNER_BYTES, dtype=torch.uint8, pin_memory=True)
     e0.record(stream)
     for _ in range(args.steps):
-        sweep.launch()
-        if world > 1:
-            pinned_out.copy_(gather(sweep.out).view(-1), non_blocking=True)
-            stream.synchronize()
-            merge(pinned_out.numpy().reshape(world, len(units), -1))
-        else:
-            sweep.read_all()
+        e2e_res = api_step()
     e1.record(stream)
     barrier()
-    e2e_ms = e0.elapsed_time(e1)
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te[0])
-    e2e_d2h = (world if world > 1 else 1) * len(units) * D.WINNER_BYTES
+    e2e_ms = _max_over_ranks([e0.elapsed_time(e1)], dev, world)[0]
+    g_api = next(iter(search._GRAPHS.values()))
+    e2e_h2d, e2e_d2h = int(g_api.batch.h2d_bytes), int(g_api.d2h_bytes)
+    assert [(r["makespan"], r["rank"], r["checksum"]) for r in e2e_res] == \
+        [(r["makespan"], r["rank"], r["checksum"]) for r in res], "public API and device-timed sweeps differ"
 
-    # the dominant kernel's own duration on every rank (its first unit): CUDA
-    # events the library records around its launches, in a separate pass
+    # ---- the dominant kernel's own duration on every rank (its first unit):
+    # CUDA events the library records around its launches, separate pass
     u0 = units[0]
     kb = kernels.unit_bufs[0]
     tab_ms, sweep_ms = engine.sweep_kernel_times(batch, total, steps=args.steps, bufs=kb, part=u0[1],
@@ -249,6 +266,8 @@ def run_b200(args, rank, world, local_rank):
         dist.all_gather_into_tensor(gathered, per_rank)
         per_rank = gathered
     per_rank = per_rank.view(-1, 2).cpu().tolist()
+    alu = engine.alu_peak()
+    sharded = sharded_measurements(args, dev, rank, world) if (world > 1 and not args.no_extras) else None
     extras = {}
     if rank == 0 and not args.no_extras and world == 1:
         extras = secondary_measurements(dev)
@@ -256,76 +275,95 @@ def run_b200(args, rank, world, local_rank):
         return None
     value = S * total * args.steps / (ms / 1e3)
     e2e_val = S * total * args.steps / (e2e_ms / 1e3)
-    cross = extras.get("cross_peak_pairs_per_s")
-    achieved = feas0 / (sweep_ms / 1e3) / 1e9      # one launch of the dominant kernel
-    # theoretical ALU-pipe bound of the inner loop: 64 integer/select lane-ops
-    # per clock per SM, 3 per candidate pair (FSEL, SEL, half of IADD3 + IADD3.X)
-    alu_peak = None
-    if clk and clk.get("sm_mhz"):
-        alu_peak = torch.cuda.get_device_properties(dev).multi_processor_count * clk["sm_mhz"] * 1e6 * 64 / 3
+    achieved = feas0 / (sweep_ms / 1e3)                   # feasible pairs/s of one launch of the dominant kernel
+    peak_pairs = alu / 3.0                                # 3 ALU-pipe instructions per pair
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    theo = sms * clk["sm_mhz"] * 1e6 * 64 / 3 if clk and clk.get("sm_mhz") else None
     traffic = ncu_traffic("splits_sweep_kernel") or {}
     hbm_peak = _hbm_peak()[0]
     csum = 0
     for r in res:
         csum = (csum + r["checksum"]) & ((1 << 64) - 1)
+    cpu1 = cpu_baseline(threads=1, seconds=5.0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(total, links),
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(batch.h2d_bytes),
-                "d2h_bytes_per_step": int(e2e_d2h)},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d * (1 if whole else 1),
+                "d2h_bytes_per_step": e2e_d2h,
+                "path": "search.split_sweep(stages, fleets) per step from the reference's Stage/Fleet objects: "
+                        "tensorise + pack + H2D + sweep kernels + D2H + host sync (+ NCCL all-gather at N>1)"},
         "gpu_launches": 5 * len(units) * args.steps,
-        "roofline": {"bound": "issue", "achieved": achieved, "peak": (cross / 1e9) if cross else None,
-                     "unit": "Gcand/s", "frac": (achieved / (cross / 1e9)) if cross else None,
+        "roofline": {"bound": "issue", "achieved": achieved / 1e9, "peak": peak_pairs / 1e9, "unit": "Gpairs/s",
+                     "frac": achieved / peak_pairs,
+                     "peak_source": "dm_microbench_alu (independent LOP3 issue-rate microbenchmark, measured in "
+                                    f"this run: {alu:.3e} lane-ops/s) / 3 ALU-pipe instructions per candidate "
+                                    "pair (FSEL + SEL + IADD3 halves; the pair's DSETP runs on the FP64 pipe)",
+                     "theoretical_peak": theo / 1e9 if theo else None,
+                     "frac_of_theoretical": achieved / theo if theo else None,
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("capture"),
-                     "alu_peak_pairs_per_s": alu_peak, "frac_of_alu_peak": (achieved * 1e9 / alu_peak) if alu_peak else None,
                      "hbm_view": ({"achieved_gbs": traffic["bytes"] / (sweep_ms / 1e3) / 1e9, "peak_gbs": hbm_peak,
-                                   "frac": traffic["bytes"] / (sweep_ms / 1e3) / 1e9 / hbm_peak,
-                                   "note": "ncu DRAM bytes of one sweep / the kernel's duration: not memory bound"}
+                                   "frac": traffic["bytes"] / (sweep_ms / 1e3) / 1e9 / hbm_peak}
                                   if traffic.get("bytes") and hbm_peak else None),
                      "kernel": "splits_sweep_kernel", "kernel_ms": sweep_ms, "table_phase_ms": tab_ms,
                      "per_rank_table_sweep_ms": per_rank,
-                     "step_kernels_ms": kernel_ms,
-                     "algorithmic_work_per_candidate": "one fp64 max (DSETP + 64-bit select) and one 64-bit "
-                                                       "checksum add per feasible candidate",
-                     "note": "feasible candidates per second of one splits_sweep_kernel launch (rank 0's first "
-                             "unit) vs dm_microbench_cross (the same inner loop alone, same grid and occupancy: "
-                             "the ALU-pipe/issue bound); infeasible candidates are resolved per side element (an "
-                             "unfit run), as the reference's `continue` skips them; table_phase_ms = T image + "
-                             "side tables of that unit"},
+                     "algorithmic_work": "per feasible candidate: one fp64 max of its two half-makespans "
+                                         "(DSETP + 64-bit select) and one 64-bit checksum add; achieved = feasible "
+                                         "candidates of one launch / its duration"},
+        "cpu_baseline": cpu1,
+        "speedup_breakdown": speedup_breakdown(value, res),
         "winner": {"per_scenario": [[r["makespan"], r["rank"]] for r in res],
                    "n_feasible": sum(r["n_feasible"] for r in res), "n_evaluated": sum(r["n_evaluated"] for r in res),
                    "checksum_sum": csum},
     }
     if clk:
         line["clocks"] = clk
+    if sharded:
+        line["sharded"] = sharded
     line.update(extras)
     return line
 
 
-_UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+_UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1.0, "usecond": 1e3, "msecond": 1e6}
 
 
-def ncu_traffic(kernel_substr, profile_glob="r1_prof_*_raw.csv"):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the newest committed
-    `ncu --set full` capture (profiles/*_raw.csv) of a kernel, with the
-    capture's duration, so callers can scale per launch / per candidate."""
+def ncu_metrics(kernel_substr, profile_glob="r*_raw.csv"):
+    """Counters of the newest committed `ncu --set full` capture
+    (profiles/*_raw.csv) of a kernel: DRAM bytes, duration, executed warp
+    instructions, issue-active and FP64-pipe utilisation."""
     import csv
     best = None
-    for f in sorted((ROOT / "profiles").glob(profile_glob), key=lambda x: x.stat().st_mtime):
+    files = sorted((ROOT / "profiles").glob(profile_glob), key=lambda x: (x.name[:3], x.stat().st_mtime))
+    for f in files:
         try:
             rows = list(csv.reader(open(f)))
             hdr, units, vals = rows[0], rows[1], rows[2]
             name = vals[hdr.index("Kernel Name")]
             if kernel_substr not in name:
                 continue
-            rd = float(vals[hdr.index("dram__bytes_read.sum")].replace(",", "")) * _UNITS[units[hdr.index("dram__bytes_read.sum")]]
-            wr = float(vals[hdr.index("dram__bytes_write.sum")].replace(",", "")) * _UNITS[units[hdr.index("dram__bytes_write.sum")]]
-            best = {"bytes": rd + wr, "capture": f.name, "kernel": name}
+
+            def get(m):
+                if m not in hdr:
+                    return None
+                i = hdr.index(m)
+                v = float(vals[i].replace(",", ""))
+                return v * _UNITS.get(units[i], 1.0)
+            best = {"capture": f.name, "kernel": name[:120],
+                    "bytes": (get("dram__bytes_read.sum") or 0) + (get("dram__bytes_write.sum") or 0),
+                    "duration_ns": get("gpu__time_duration.sum"),
+                    "warp_inst": get("smsp__inst_executed.sum"),
+                    "issue_active_pct": get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "fp64_pipe_pct": get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "warps_active_pct": get("sm__warps_active.avg.pct_of_peak_sustained_active")}
         except Exception:
             continue
     return best
+
+
+def ncu_traffic(kernel_substr, profile_glob="r*_raw.csv"):
+    m = ncu_metrics(kernel_substr, profile_glob)
+    return {"bytes": m["bytes"], "capture": m["capture"], "kernel": m["kernel"]} if m else None
 
 
 def _hbm_peak():
@@ -394,11 +432,13 @@ def mode_a_measure(dev, which):
     peak, src = _hbm_peak()
     algo = N * (n * 1 + 9)
     achieved = algo / (ms / 1e3) / 1e9
-    tr = ncu_traffic("eval_owner_stream_kernel", f"r1_prof_modea_{which}*_raw.csv") if which == "c1" else None
+    tr = ncu_metrics("eval_owner_stream_kernel", f"r*_modea_{which}_raw.csv")
     res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                        "traffic": (tr["bytes"] / (1 << 25) * N) if tr else None,
                        "traffic_note": (f"{tr['capture']}: DRAM read+write of a 2^25-candidate launch (same "
-                                        "population), scaled per candidate to this launch") if tr else None,
+                                        "population), scaled per candidate to this launch; issue active "
+                                        f"{tr['issue_active_pct']:.0f} %, warps active {tr['warps_active_pct']:.0f} %")
+                       if tr else None,
                        "bytes_per_candidate": n + 9, "peak_source": src}
     inst = oracle.Instance(stages, fleet)
     sample = own[:20000].cpu().numpy().astype("int64")
@@ -411,7 +451,58 @@ def mode_a_measure(dev, which):
     return res
 
 
-def dp_measure(dev):
+def per_candidate_measure(dev, fp64_peak):
+    """Per-candidate cost-model rates on the C2 population (the
+    meet-in-the-middle headline shares per-run work across candidates; these
+    kernels do not): a 2^30-rank range around the middle of C2 scenario 0
+    scored by the generic evaluator (enum_kernel<1>: per run _fits on exact
+    prefix sums, compute = flops / speed, crossing read alpha + beta*M, load,
+    max — SURVEY §8d Mode B, 6r-3 fp64 operations per candidate) and by the
+    tabulated-run kernel (splits_memo_kernel: per run one table load + max)."""
+    import math
+    import os as _os
+    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200.tensorize import build_host
+    stages, fleet = c2_instance()
+    n, p = 34, 32
+    batch = engine.device_batch([build_host(stages, fleet, True)], device=dev)
+    total = engine.splits_total(n, p)
+    N = 1 << 30
+    k0 = total // 2 - N // 2
+    # mean run count over the range (ranks are grouped by cut count m, r = m + 1)
+    r_sum, base, lo, hi = 0, 0, k0, k0 + N
+    for m in range(0, min(n, p)):
+        c = math.comb(n - 1, m)
+        a, b = max(lo, base), min(hi, base + c)
+        if b > a:
+            r_sum += (b - a) * (m + 1)
+        base += c
+    r_bar = r_sum / N
+    bufs = engine.WinnerBuffers(dev)
+    _os.environ["DM_DISABLE_MEMO"] = "1"
+    try:
+        ms_g = _time_ms(lambda: engine.enum(batch, "splits", k0, k0 + N, bufs), steps=2, warmup=1)
+        win_g = bufs.read()
+    finally:
+        _os.environ.pop("DM_DISABLE_MEMO", None)
+    ms_m = _time_ms(lambda: engine.enum(batch, "splits", k0, k0 + N, bufs), steps=3, warmup=1)
+    win_m = bufs.read()
+    ops = win_g["n_feasible"] * (6 * r_bar - 3)
+    achieved = ops / (ms_g / 1e3)
+    return {"config": f"C2 scenario 0 ranks [{k0}, {k0 + N}) (mean r = {r_bar:.2f} runs)", "candidates": N,
+            "generic": {"kernel": "enum_kernel<1>", "ms": ms_g, "value": N / (ms_g / 1e3), "unit": UNIT,
+                        "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
+                                     "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                                     "work": "(6 r - 3) fp64 ops per feasible candidate (a division counted once; "
+                                             "an IEEE div.rn is ~10 fp64-pipe instructions); infeasible candidates "
+                                             "stop at the integer _fits test"}},
+            "tabulated": {"kernel": "splits_memo_kernel", "ms": ms_m, "value": N / (ms_m / 1e3), "unit": UNIT},
+            "same_winner": win_g == win_m,
+            "winner": {"makespan": win_m["makespan"], "rank": win_m["rank"], "n_feasible": win_m["n_feasible"],
+                       "checksum": win_m["checksum"]}}
+
+
+def dp_measure(dev, fp64_peak):
     """Partition DPs solved/s: config C1's 32 x 32 link grid, one _subset_dp per fleet."""
     import time as _t
     from oracle import oracle
@@ -432,14 +523,28 @@ def dp_measure(dev):
         o, _ = oracle.Instance(stages, fleets[i]).subset_dp()
         ok &= o is not None and own[i, :26].tolist() == o.tolist()
     cpu = 16 / (_t.perf_counter() - t0)
+    n, p = 26, 4
+    # pull-form transitions (target (j, M), source i < j, worker wi in M) and
+    # chunk costs (n(n+1)/2 x p: one division, the crossing read, one add)
+    trans = sum(range(1, n + 1)) * p * 2 ** (p - 1)
+    ops = 2 * trans + 4 * (n * (n + 1) // 2) * p
+    rate = len(fleets) / (ms / 1e3)
+    prof = ncu_metrics("subset_dp_warp_kernel")
     return {"config": "C1 gpt2-small (26 stages) x 4 workers, 1024 link-grid fleets (bw logspace(-1,2,32) x "
                       "alpha linspace(0,10ms,32)), one _subset_dp each", "dps": len(fleets), "ms": ms,
-            "value": len(fleets) / (ms / 1e3), "unit": "DPs/s", "oracle_spot_check": bool(ok),
-            "cpu_baseline_1core": cpu}
+            "value": rate, "unit": "DPs/s", "oracle_spot_check": bool(ok), "cpu_baseline_1core": cpu,
+            "roofline": {"bound": "latency", "achieved": rate * ops / 1e12, "peak": fp64_peak / 1e12,
+                         "unit": "TFLOP/s", "frac": rate * ops / fp64_peak,
+                         "work": f"{ops} fp64 ops per DP ({trans} pull-form transitions x (max + compare) + "
+                                 "chunk costs)",
+                         "ncu": prof,
+                         "note": "one warp per DP walks the j-recurrence sequentially: latency-bound, not "
+                                 "throughput-bound (see ncu warps/issue active)"}}
 
 
-def c4_measure(dev, n_scen=1 << 18):
-    """schedule() solves/s over config C4 scenarios (proportional split + hill climb + epilogue)."""
+def c4_measure(dev, fp64_peak, n_scen=10 ** 6):
+    """schedule() solves/s over config C4's 10^6 scenarios (proportional split
+    + hill climb + Eq. 3/4 epilogue)."""
     import time as _t
     from oracle import oracle
     from paper_2309_01172_b200 import batch as B
@@ -449,7 +554,7 @@ def c4_measure(dev, n_scen=1 << 18):
     def run():
         owner, _, _ = engine.prop_hill(sb, sb.n_max)
         return engine.epilogue(sb, sb.n_max, owner, 512, 4)
-    ms = _time_ms(run, steps=3, warmup=3)
+    ms = _time_ms(run, steps=3, warmup=2)
     owner, _, moves = engine.prop_hill(sb, sb.n_max)
     epi = engine.epilogue(sb, sb.n_max, owner, 512, 4).cpu().numpy()
     owner = owner.cpu().numpy()
@@ -461,11 +566,18 @@ def c4_measure(dev, n_scen=1 << 18):
         ok &= owner[s, :len(st)].tolist() == o.tolist()
     cpu = 16 / (_t.perf_counter() - t0)
     feas = float((epi[:, 5] == 0).mean())
+    prof = ncu_metrics("prop_hill_kernel")
     return {"config": f"C4: {n_scen} scenarios, L~U{{32..80}}, h in {{2048,4096,5120,8192}}, p~U{{8..64}}, "
                       "GPU_TABLE mix, lambda~U[.3,1], alpha~U[0,10ms], bw~LogU[.1,10] Gbit/s",
             "schedules": n_scen, "ms": ms, "value": n_scen / (ms / 1e3), "unit": "schedules/s",
             "feasible_frac": feas, "mean_hill_moves": float(moves.float().mean()),
-            "oracle_spot_check": bool(ok), "cpu_baseline_1core": cpu}
+            "oracle_spot_check": bool(ok), "cpu_baseline_1core": cpu,
+            "roofline": {"bound": "latency", "ncu": prof,
+                         "note": "one warp per scenario: proportional split, then the sequential "
+                                 "first-improvement walk of _hill_climb (each accepted move depends on the "
+                                 "previous); fp64 pipe utilisation from the committed ncu capture"},
+            "full_size_parity": "tests/test_gpu_full_size.py::test_c4_million_scenarios (sha256 of all 10^6 "
+                                "owner vectors + Eq. 3/4 values vs the oracle)"}
 
 
 def random_measure(dev, which):
@@ -505,7 +617,19 @@ def random_measure(dev, which):
     ref = inst.enum_random(online, seed, 0, 20000)
     cpu = 20000 / (_t.perf_counter() - t0)
     got = engine.enum(batch, "random", 0, 20000, online=on_d, seed=seed).read()
-    return {"config": desc, "candidates": N, "ms": ms, "value": N / (ms / 1e3), "unit": UNIT,
+    prof = ncu_metrics("random_warp_kernel", f"r*_random_{which}_raw.csv")
+    roof = None
+    if prof and prof.get("warp_inst"):
+        import torch
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        inst_per_cand = prof["warp_inst"] / (1 << 24)
+        achieved = inst_per_cand * N / (ms / 1e3)
+        peak = sms * 4 * 1.965e9
+        roof = {"bound": "issue", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Twarp-inst/s",
+                "frac": achieved / peak, "warp_inst_per_candidate": inst_per_cand, "ncu": prof,
+                "note": "instructions per candidate from the committed ncu capture (2^24 candidates) x this run's "
+                        "rate / (4 issue slots x SMs x 1965 MHz)"}
+    return {"config": desc, "candidates": N, "ms": ms, "value": N / (ms / 1e3), "unit": UNIT, "roofline": roof,
             "candidate_distribution": "r ~ U{1..min(n, online)}, uniform (r-1)-subset of the cut positions "
                                       "(selection sampling), r distinct online peers (keyed Feistel permutation); "
                                       "paper_2309_01172_b200/rng.py",
@@ -592,18 +716,19 @@ def api_latency_measure(dev):
 
 
 def secondary_measurements(dev):
-    """FP64 peak microbenchmark (roofline denominator), CPU baseline, and the
-    secondary paths of the metric: Mode A streams (HBM roofline), DPs/s, schedules/s."""
-    out = {}
+    """Peaks (roofline denominators), then the other configs and paths of the
+    metric, each checked against the oracle in the same run."""
     from paper_2309_01172_b200 import engine
-    out["fp64_peak_ops_per_s"] = engine.fp64_peak()
-    out["cross_peak_pairs_per_s"] = engine.cross_peak()
-    out["cpu_baseline"] = cpu_baseline(threads=1, seconds=10.0)
+    out = {"fp64_peak_ops_per_s": engine.fp64_peak(), "alu_peak_ops_per_s": engine.alu_peak(),
+           "cross_loop_pairs_per_s": engine.cross_peak()}
     sec = {}
-    for name, fn in (("mode_a_c1", lambda: mode_a_measure(dev, "c1")), ("mode_a_c2", lambda: mode_a_measure(dev, "c2")),
-                     ("dp_c1_grid", lambda: dp_measure(dev)), ("schedule_c4", lambda: c4_measure(dev)),
+    for name, fn in (("per_candidate_c2", lambda: per_candidate_measure(dev, out["fp64_peak_ops_per_s"])),
+                     ("mode_a_c1", lambda: mode_a_measure(dev, "c1")), ("mode_a_c2", lambda: mode_a_measure(dev, "c2")),
+                     ("dp_c1_grid", lambda: dp_measure(dev, out["fp64_peak_ops_per_s"])),
+                     ("schedule_c4", lambda: c4_measure(dev, out["fp64_peak_ops_per_s"])),
                      ("random_c5", lambda: random_measure(dev, "c5")), ("random_c3", lambda: random_measure(dev, "c3")),
-                     ("dp_c4b", lambda: dp_c4b_measure(dev)), ("schedule_api_latency_c1", lambda: api_latency_measure(dev))):
+                     ("dp_c4b", lambda: dp_c4b_measure(dev)), ("schedule_api", lambda: api_latency_measure(dev)),
+                     ("reference_python", reference_python_measure)):
         try:
             sec[name] = fn()
         except Exception as exc:
@@ -636,7 +761,178 @@ def cpu_baseline(threads=1, seconds=10.0):
     el = time.perf_counter() - t0
     return {"value": threads * per_thread / el, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{threads * per_thread} consecutive ranks from the middle of the C2 split population "
-                      f"({el:.1f}s), oracle/dm_oracle.c or_enum mode 1"}
+                      f"({el:.1f}s), oracle/dm_oracle.c or_enum mode 1 (the reference's per-candidate loop in C)"}
+
+
+def cpu_mitm(threads):
+    """The GPU's algorithm on the host: one whole C2 scenario-0 sweep
+    (8,589,934,558 candidates) with oracle/dm_oracle.c or_splits_mitm, the cut
+    counts spread over `threads` host threads."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import oracle
+    from paper_2309_01172_b200 import dist as D
+    stages, fleet = c2_instance()
+    inst = oracle.Instance(stages, fleet)
+    T = inst.mitm_table()
+    rmax = min(inst.n, inst.p)
+    order = sorted(range(rmax), key=lambda m: abs(m - rmax // 2))      # largest blocks first
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(lambda m: inst.splits_mitm(T, m, m + 1), order))
+    el = time.perf_counter() - t0
+    import struct
+    import numpy as np
+    raw = np.frombuffer(b"".join(struct.pack(D.WINNER_FMT, w["makespan"], w["rank"], w["n_evaluated"],
+                                             w["n_feasible"], w["checksum"]) for w in parts), np.uint8)
+    return oracle.splits_total(inst.n, inst.p) / el, el, D.merge_records(raw)
+
+
+def speedup_breakdown(value, res):
+    """Split the GPU-vs-reference-loop factor: algorithm (the same
+    meet-in-the-middle search on the host vs the reference's per-candidate
+    loop, both on every host thread) x hardware (B200 vs that host search)."""
+    threads = os.cpu_count() or 1
+    try:
+        mitm_rate, mitm_s, mitm_win = cpu_mitm(threads)
+        port = cpu_baseline(threads=threads, seconds=3.0)
+    except Exception as exc:
+        return {"error": f"{type(exc).__name__}: {exc}"}
+    return {"host_threads": threads,
+            "cpu_same_algorithm": {"value": mitm_rate, "unit": UNIT, "seconds_per_sweep": mitm_s,
+                                   "matches_gpu_scenario0": (mitm_win["makespan"], mitm_win["rank"],
+                                                             mitm_win["checksum"]) ==
+                                   (res[0]["makespan"], res[0]["rank"], res[0]["checksum"])},
+            "cpu_reference_loop": {"value": port["value"], "unit": UNIT, "sample": port["sample"]},
+            "algorithmic_factor": mitm_rate / port["value"],
+            "hardware_factor": value / mitm_rate,
+            "note": "algorithmic_factor x hardware_factor = value / cpu_reference_loop (all host threads)"}
+
+
+def _ref_module():
+    from paper_2309_01172_b200.refapi import dagmesh
+    return dagmesh
+
+
+def _ref_bf_job(i):
+    """brute_force_schedule (scheduling.py:245-278, the reference's own
+    Python) on C1 link-grid fleet i: 62,704 candidates."""
+    from paper_2309_01172_b200 import configs as CF
+    RS = _ref_module().scheduling
+    bws, alphas = CF.c1_link_grid()
+    fleet = CF.load(CF.c1_fleet_doc(bws[i % 32], alphas[(i * 7) % 32]))
+    t0 = time.perf_counter()
+    RS.brute_force_schedule(CF.model_stages("gpt2-small"), fleet)
+    return time.perf_counter() - t0
+
+
+def _ref_sched_job(s):
+    from paper_2309_01172_b200 import configs as CF
+    RS = _ref_module().scheduling
+    P = _REF_C4.setdefault("P", CF.c4_params(4096))
+    stages, fleet = CF.c4_instance(P, s % 4096)
+    t0 = time.perf_counter()
+    RS.schedule(stages, fleet)
+    return time.perf_counter() - t0
+
+
+def _ref_dp_job(i):
+    from paper_2309_01172_b200 import configs as CF
+    RS = _ref_module().scheduling
+    bws, alphas = CF.c1_link_grid()
+    fleet = CF.load(CF.c1_fleet_doc(bws[i % 32], alphas[(i * 5) % 32]))
+    t0 = time.perf_counter()
+    RS._subset_dp(CF.model_stages("gpt2-small"), fleet, fleet.worker_ids(), True)
+    return time.perf_counter() - t0
+
+
+_REF_C4: dict = {}
+
+
+def reference_python_measure():
+    """The ORIGINAL reference functions (dagmesh, pure Python, from
+    baseline/_ref) on this box's host cores: 1 core, then every core with a
+    process pool (one job per process): brute_force_schedule's candidates/s
+    (C1), schedule() solves/s (C4 sample) and _subset_dp DPs/s (C1)."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    out = {"cores": cores, "python": sys.version.split()[0]}
+    ctx = mp.get_context("fork")
+    for name, job, units, n1, nall in (("bruteforce_c1", _ref_bf_job, 62704, 1, cores),
+                                       ("schedule_c4", _ref_sched_job, 1, 20, 8 * cores),
+                                       ("subset_dp_c1", _ref_dp_job, 1, 2, 2 * cores)):
+        t1 = sum(job(i) for i in range(n1))
+        t0 = time.perf_counter()
+        with ctx.Pool(cores) as pool:
+            pool.map(job, range(nall), chunksize=1)
+        el = time.perf_counter() - t0
+        out[name] = {"unit": "candidates/s" if units > 1 else ("schedules/s" if "schedule" in name else "DPs/s"),
+                     "one_core": units * n1 / t1, "all_cores": units * nall / el, "jobs_all_cores": nall}
+    return out
+
+
+def sharded_measurements(args, dev, rank, world):
+    """N > 1: the other populations sharded across the ranks with ONE
+    all-gather each — C4 (contiguous scenario slices, 10^6 schedule() solves)
+    and C5 (counter ranges of the 10^9-candidate random stream).  Device time,
+    max over ranks."""
+    import numpy as np
+    import torch
+    from paper_2309_01172_b200 import batch as B
+    from paper_2309_01172_b200 import configs as CF
+    from paper_2309_01172_b200 import dist as D
+    from paper_2309_01172_b200 import engine
+    from paper_2309_01172_b200.tensorize import build_host
+    out = {}
+    n4 = 10 ** 6
+    lo, hi = D.shard(n4, rank, world)
+    sb = B.c4_batch(n4, seed=0, device=dev, lo=lo, hi=hi)
+
+    def c4_step():
+        owner, _, _ = engine.prop_hill(sb, sb.n_max)
+        epi = engine.epilogue(sb, sb.n_max, owner, 512, 4)
+        feas = torch.tensor([float((epi[:, 5] == 0).sum())], dtype=torch.float64, device=dev)
+        g = torch.empty(world, dtype=torch.float64, device=dev)
+        torch.distributed.all_gather_into_tensor(g, feas)
+        return g
+    c4_step()
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(3):
+        g = c4_step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks([a.elapsed_time(b) / 3], dev, world)[0]
+    out["schedule_c4"] = {"schedules": n4, "ms": ms, "value": n4 / (ms / 1e3), "unit": "schedules/s",
+                          "feasible": int(g.sum().item()), "split": "contiguous scenario slices"}
+    del sb
+    stages = CF.model_stages("opt-175b")
+    fleet = CF.load(CF.c5_fleet_doc(0))
+    host = build_host(stages, fleet, True)
+    batch = engine.device_batch([host], device=dev)
+    online = torch.tensor([host.index_of[i] for i in CF.c5_churn(1024, 0.1, 0)[1]], dtype=torch.int32, device=dev)
+    N = 10 ** 9
+    k0, k1 = D.shard(N, rank, world)
+    bufs = engine.WinnerBuffers(dev)
+
+    def c5_step():
+        engine.enum(batch, "random", k0, k1, bufs, online=online, seed=20260)
+        return _gather_records(bufs.out.view(1, -1), world)
+    c5_step()
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(3):
+        g = c5_step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks([a.elapsed_time(b) / 3], dev, world)[0]
+    win = D.merge_records(g.cpu().numpy())
+    out["random_c5"] = {"candidates": N, "ms": ms, "value": N / (ms / 1e3), "unit": UNIT, "split": "counter ranges",
+                        "winner": {"makespan": win["makespan"], "rank": win["rank"], "n_feasible": win["n_feasible"],
+                                   "checksum": win["checksum"]}}
+    return out
 
 
 def run_reference(args, rank, world):

@@ -101,36 +101,37 @@ class ScenarioBatch:
         self.structs_dev.copy_(self.records_host, non_blocking=True)
 
 
-def c4_batch(n_scen: int, seed: int = 0, device="cuda", vocab: int = 32000, batch: int = 4, seq: int = 1024):
+def c4_batch(n_scen: int, seed: int = 0, device="cuda", vocab: int = 32000, batch: int = 4, seq: int = 1024,
+             lo: int = 0, hi: int | None = None):
     """Config C4: n_scen independent scenarios, L ~ U{32..80}, h in
     {2048, 4096, 5120, 8192} (196 distinct models), p ~ U{8..64} workers from
     GPU_TABLE, lambda ~ U[.3, 1], alpha ~ U[0, 10 ms], bandwidth ~ LogU[.1, 10]
-    Gbit/s.  Returns (ScenarioBatch, model_keys, per-scenario arrays)."""
-    from .configs import C4_HIDDEN, encoder_stages
+    Gbit/s.  Every draw is made for all n_scen scenarios (so a slice is
+    identical on any rank); the batch holds scenarios [lo, hi)."""
+    from .configs import C4_HIDDEN, c4_params, encoder_stages
     from .refapi import Fleet, Peer
     from .tensorize import build_host
 
-    rng = np.random.default_rng(seed)
-    layers = rng.integers(32, 81, n_scen)
-    hid = rng.integers(0, len(C4_HIDDEN), n_scen)
-    p = rng.integers(8, 65, n_scen)
-    alpha = rng.uniform(0.0, 1e-2, n_scen)
-    bw = 10.0 ** rng.uniform(-1.0, 1.0, n_scen)
+    hi = n_scen if hi is None else hi
+    P = c4_params(n_scen, seed)
+    layers, hid, p, alpha, bw = P["layers"], P["hid"], P["p"], P["alpha"], P["bw"]
+    kinds, lam, poff = P["kinds"], P["lam"], P["poff"]
+    a, b = int(poff[lo]), int(poff[hi])
+    layers, hid, p, alpha, bw = layers[lo:hi], hid[lo:hi], p[lo:hi], alpha[lo:hi], bw[lo:hi]
+    kinds, lam = kinds[a:b], lam[a:b]
     beta = 8.0 / (bw * 1e9)
-    kinds = rng.integers(0, len(_KINDS), int(p.sum()))
-    lam = rng.uniform(0.3, 1.0, int(p.sum()))
     keys = sorted(set(zip(layers.tolist(), hid.tolist())))
     index = {k: i for i, k in enumerate(keys)}
     dummy = Fleet(peers={"1": Peer("1")})
     models = [build_host(encoder_stages(C4_HIDDEN[h], L, vocab, batch, seq), dummy, True) for L, h in keys]
     scen_model = np.array([index[(L, h)] for L, h in zip(layers.tolist(), hid.tolist())], np.int64)
     sb = ScenarioBatch(models, scen_model, p, kinds, lam, alpha, beta, device=device)
-    sb.params = dict(layers=layers, hid=hid, p=p, alpha=alpha, bw=bw, kinds=kinds, lam=lam, keys=keys)
+    sb.params = dict(layers=layers, hid=hid, p=p, alpha=alpha, bw=bw, kinds=kinds, lam=lam, keys=keys, lo=lo)
     return sb
 
 
 def scenario_instance(sb: ScenarioBatch, s: int):
-    """Rebuild scenario s as (stages, Fleet) with the mirror types — the exact
+    """Rebuild scenario s (batch-local index) as (stages, Fleet) with the reference types — the exact
     values parse_fleet would produce for the scenario's fleet document."""
     from .configs import C4_HIDDEN, encoder_stages
     from .refapi import Fleet, Link, Peer

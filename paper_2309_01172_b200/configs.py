@@ -282,12 +282,30 @@ def load(doc, compute_column: str = "tensor"):
 C4_HIDDEN = (2048, 4096, 5120, 8192)
 
 
-def c4_scenario_params(n_scen: int, seed: int = 0):
-    """Per scenario: (layers, hidden index, p, lambda seed, alpha, bandwidth)."""
+def c4_params(n_scen: int, seed: int = 0) -> dict:
+    """Every draw of config C4, made for all n_scen scenarios in
+    one fixed order so any slice is identical on any rank: L ~ U{32..80},
+    h index, p ~ U{8..64}, alpha ~ U[0, 10 ms], bandwidth ~ LogU[.1, 10]
+    Gbit/s, then per worker a GPU_TABLE kind and lambda ~ U[.3, 1]."""
     rng = np.random.default_rng(seed)
     layers = rng.integers(32, 81, n_scen)
     hid = rng.integers(0, len(C4_HIDDEN), n_scen)
     p = rng.integers(8, 65, n_scen)
     alpha = rng.uniform(0.0, 1e-2, n_scen)
-    bw = 10 ** rng.uniform(-1, 1, n_scen)
-    return layers, hid, p, alpha, bw
+    bw = 10.0 ** rng.uniform(-1.0, 1.0, n_scen)
+    kinds = rng.integers(0, len(GPU_TABLE), int(p.sum()))
+    lam = rng.uniform(0.3, 1.0, int(p.sum()))
+    poff = np.concatenate([[0], np.cumsum(p)])
+    return dict(layers=layers, hid=hid, p=p, alpha=alpha, bw=bw, kinds=kinds, lam=lam, poff=poff)
+
+
+def c4_instance(P: dict, s: int):
+    """Scenario s of c4_params as the reference's objects: closed-form stages
+    (== build_stages) and the scenario's fleet document through parse_fleet."""
+    L, h = int(P["layers"][s]), C4_HIDDEN[int(P["hid"][s])]
+    a, b = int(P["poff"][s]), int(P["poff"][s + 1])
+    kinds = tuple(GPU_TABLE)
+    peers = [{"id": str(j - a + 1), "gpu": kinds[int(P["kinds"][j])], "lambda": float(P["lam"][j])}
+             for j in range(a, b)]
+    return (encoder_stages(h, L, 32000, 4, 1024),
+            load(fleet_doc(peers, float(P["alpha"][s]), float(P["bw"][s]), name="c4")))

@@ -414,7 +414,7 @@ class SweepGraph:
             ub.out = self.out[i]
         self.host_out = torch.empty((len(self.units), _WINNER_BYTES), dtype=torch.uint8, pin_memory=True)
         self.h2d_bytes = int(batch.h2d_bytes) if copy_inputs else 0
-        self.d2h_bytes = _WINNER_BYTES * len(self.units) if self.whole and copy_inputs else 0
+        self.d2h_bytes = _WINNER_BYTES * len(self.units) if copy_inputs else 0
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):          # warm the plan cache and the kernels' attributes
@@ -448,7 +448,7 @@ class SweepGraph:
         else:
             for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
                 enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts)
-        if self.whole and self.copy_inputs:
+        if self.copy_inputs:
             self.host_out.copy_(self.out, non_blocking=True)
 
     def launch(self):

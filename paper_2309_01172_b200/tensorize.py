@@ -338,6 +338,26 @@ class DeviceBatch:
         self.structs_dev.copy_(self.records_host, non_blocking=True)
         self.h2d_bytes = total + recs.nbytes
 
+    def repack(self, hosts) -> bool:
+        """Re-tensorised instances of the same shapes into the existing pinned
+        staging buffer and records (the device addresses stay valid, so a
+        captured graph that copies host_buf -> dev_buf can be replayed on the
+        new inputs).  Returns False when a shape differs."""
+        hosts = list(hosts)
+        if len(hosts) != len(self.hosts) or any(a.packed_size() != b.packed_size() for a, b in zip(hosts, self.hosts)):
+            return False
+        hb = self.host_buf.numpy()
+        base = 0
+        dev_base = int(self.dev_buf.data_ptr())
+        recs = self.records_host.numpy().view(TABLES_DTYPE)
+        for i, h in enumerate(hosts):
+            offs = h.pack_into(hb, base)
+            recs[i] = h.struct_record(offs, dev_base)
+            base += h.packed_size()
+        self.records = recs.copy()
+        self.hosts = hosts
+        return True
+
     def struct(self, i: int = 0) -> _lib.DmTables:
         return _lib.DmTables.from_buffer_copy(self.records[i].tobytes())
 

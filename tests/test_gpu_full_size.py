@@ -184,3 +184,22 @@ def test_c4_million_scenarios(engine_ready):
             bad.append(c)
     assert not bad, f"chunks differing: {bad[:10]}"
     assert int((epi[:, 5] == 0).sum()) == g["n_feasible"]
+
+
+def test_split_sweep_public_api(c2):
+    """search.split_sweep (stages + fleets in, decoded winners out) on the
+    pinned C2 scenarios; the winner's runs re-scored by evaluate_runs give
+    the pinned makespan; block parts over 2 callers merge to the same."""
+    from paper_2309_01172_b200 import configs as CF, dist as D, scheduling as S, search
+    stages = CF.model_stages("llama2-7b-layers")
+    idx = sorted(int(s) for s in GOLD["c2"])
+    fleets = [CF.load(CF.c2_fleet_doc(0, *CF.C2_LINKS[i])) for i in idx]
+    for _ in range(2):                                   # second call: graph replay on repacked inputs
+        res = search.split_sweep(stages, fleets)
+        for i, w in zip(idx, res):
+            want = GOLD["c2"][str(i)]
+            assert (w.makespan, w.rank, w.n_evaluated, w.n_feasible, w.checksum) == tuple(want[k] for k in KEYS)
+            assert S.evaluate_runs(stages, fleets[idx.index(i)], w.runs).makespan == want["makespan"]
+    parts = [search.split_sweep(stages, fleets[:1], part=k, nparts=2, records=True) for k in range(2)]
+    m = D.merge_records(np.stack([p_[0] for p_ in parts]))
+    assert {k: m[k] for k in KEYS} == _w(GOLD["c2"][str(idx[0])])
