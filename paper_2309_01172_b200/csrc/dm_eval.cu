@@ -394,11 +394,17 @@ template <bool PAIR, bool SQUARE, int NT, int NW>
 __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx& X, uint32_t tile_s,
                                             const unsigned char* tile, int cnt, int64_t c0,
                                             double* __restrict__ out_mk, uint8_t* __restrict__ out_code,
-                                            int64_t rank_base, bool fuse, StreamWin& win) {
+                                            int64_t rank_base, bool fuse, StreamWin& win, uint32_t& n_seen) {
     const int n = X.n;
+    // per-tile bases, advanced per candidate (no per-candidate address rebuild)
+    double* omk = out_mk + c0;
+    uint8_t* ocode = out_code + c0;
+    const int64_t rbase = rank_base + c0;
+    uint32_t row_s = tile_s + (uint32_t)threadIdx.x * n;          // shared address of this thread's row
+    const uint32_t row_step = (uint32_t)NT * n;
 #pragma unroll 1
-    for (int ci = threadIdx.x; ci < cnt; ci += NT) {
-        const uint32_t row_s = tile_s + (uint32_t)ci * n;        // shared address of the row
+    for (int ci = threadIdx.x; ci < cnt; ci += NT, row_s += row_step) {
+        ++n_seen;
         const unsigned long long bm = boundary_mask<NW>(row_s & ~3u, (int)(row_s & 3u) * 8);
         double mk = 0.0;
         uint32_t end = (uint32_t)n, seen = 0, bad = 0xffffffffu;
@@ -435,14 +441,56 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
                 y ^= 1u << k;
                 run(33u + k);
             }
-        for (uint32_t y = (uint32_t)bm & X.mask_lo; y; ) {
-            const uint32_t k = 31u - __clz(y);
-            y ^= 1u << k;
-            run(1u + k);
+        if (PAIR) {
+            for (uint32_t y = (uint32_t)bm & X.mask_lo; y; ) {
+                const uint32_t k = 31u - __clz(y);
+                y ^= 1u << k;
+                run(1u + k);
+            }
+        } else {
+            // two runs per step: both owner-byte and table loads in flight
+            // before either is folded into the maximum (ILP for the few warps
+            // a large table leaves resident)
+            auto fetch = [&](uint32_t b, uint32_t e, uint32_t& w, uint32_t& addr, double& v) {
+                w = lds_u8(row_s + b);
+                uint32_t idx;
+                if (SQUARE) idx = b * X.rowstride + e * X.uP + w;
+                else idx = ((b * (X.tri_k - b)) >> 1) * X.uP + (e - b - 1) * X.uP + w;
+                addr = X.T_s + 8u * idx;
+                v = lds_f64s(addr);
+            };
+            auto fold = [&](uint32_t w, uint32_t addr, double v) {
+                seen |= 1u << w;
+                mk = fabs(v) > fabs(mk) ? v : mk;
+                bad = min(bad, addr | ~(uint32_t)(__double2hiint(v) >> 31));
+            };
+            for (uint32_t y = (uint32_t)bm & X.mask_lo; y; ) {
+                const uint32_t k1 = 31u - __clz(y);
+                y ^= 1u << k1;
+                const uint32_t b1 = 1u + k1;
+                uint32_t w1, a1;
+                double v1;
+                if (y) {
+                    const uint32_t k2 = 31u - __clz(y);
+                    y ^= 1u << k2;
+                    const uint32_t b2 = 1u + k2;
+                    uint32_t w2, a2;
+                    double v2;
+                    fetch(b1, end, w1, a1, v1);
+                    fetch(b2, b1, w2, a2, v2);
+                    fold(w1, a1, v1);
+                    fold(w2, a2, v2);
+                    end = b2;
+                } else {
+                    fetch(b1, end, w1, a1, v1);
+                    fold(w1, a1, v1);
+                    end = b1;
+                }
+            }
         }
         run(0u);
         (void)prev_w;
-        mk = fabs(mk);
+        mk = __hiloint2double(__double2hiint(mk) & 0x7fffffff, __double2loint(mk));   // |mk| without the fp64 pipe
         const int nruns = __popcll(bm & (((unsigned long long)X.mask_hi << 32) | X.mask_lo)) + 1;
         int code = bad != 0xffffffffu ? (int)lds_u8(X.C_s + ((bad - X.T_s) >> 3)) : DM_V_OK;
         bool unknown = false;
@@ -451,12 +499,12 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
             for (int i = 0; i < n; ++i) if (row[i] >= X.uP) { unknown = true; break; }
             if (!unknown) eval_owner_grouped(t, row, mk, code);
         }
-        out_mk[c0 + ci] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
-        out_code[c0 + ci] = unknown ? (uint8_t)0xFF : (uint8_t)code;
+        omk[ci] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
+        ocode[ci] = unknown ? (uint8_t)0xFF : (uint8_t)code;
         if (fuse && !unknown && code == DM_V_OK) {      // fused arg-min (first strict minimum by rank)
             win.n_feas++;
             win.csum += (uint64_t)__double_as_longlong(mk);
-            if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank_base + c0 + ci; }
+            if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rbase + ci; }
         }
     }
 }
@@ -531,11 +579,10 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
     X.mask_hi = n - 1 >= 64 ? 0xffffffffu : (n - 1 > 32 ? ((1u << (n - 33)) - 1u) : 0u);
     StreamWin win;
     win.mk = __longlong_as_double(0x7ff0000000000000LL); win.rank = -1; win.n_feas = 0; win.csum = 0;
-    int64_t n_seen = 0;
-    int64_t it_local = 0;
-    for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x, ++it_local) {
-        const int st = (int)(it_local % stages);
-        const uint32_t parity = (uint32_t)((it_local / stages) & 1);
+    uint32_t n_seen = 0;
+    int st = 0;
+    uint32_t parity = 0;
+    for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x) {
         const int64_t c0 = tl * tile_cand;
         const int cnt = (int)((n_cand - c0) < tile_cand ? (n_cand - c0) : tile_cand);
         unsigned char* tile = tiles + st * L.tile_bytes;
@@ -546,16 +593,15 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
             __syncthreads();
         }
         const uint32_t tile_s = sm_s + (uint32_t)(tile - sm);
-        if (tid < cnt) n_seen += (cnt - tid + NT - 1) / NT;
         switch (nw) {     // the boundary-mask width is fixed per launch: one dispatch per tile
 #define DM_STREAM_TILE(W)                                                                              \
             case W: stream_tile<PAIR, SQUARE, NT, W>(t, X, tile_s, tile, cnt, c0, out_mk, out_code, rank_base, \
-                                                     partial != nullptr, win); break;
+                                                     partial != nullptr, win, n_seen); break;
             DM_STREAM_TILE(1) DM_STREAM_TILE(2) DM_STREAM_TILE(3) DM_STREAM_TILE(4) DM_STREAM_TILE(5)
             DM_STREAM_TILE(6) DM_STREAM_TILE(7) DM_STREAM_TILE(8) DM_STREAM_TILE(9) DM_STREAM_TILE(10)
             DM_STREAM_TILE(11) DM_STREAM_TILE(12) DM_STREAM_TILE(13) DM_STREAM_TILE(14) DM_STREAM_TILE(15)
             default: stream_tile<PAIR, SQUARE, NT, 16>(t, X, tile_s, tile, cnt, c0, out_mk, out_code, rank_base,
-                                                       partial != nullptr, win); break;
+                                                       partial != nullptr, win, n_seen); break;
 #undef DM_STREAM_TILE
         }
         __syncthreads();  // every thread is done with this slot
@@ -566,6 +612,7 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
                 tma_load_1d(tile, owner + nt * tile_cand * n, tile_load, &bars[st]);
             }
         }
+        if (++st == stages) { st = 0; parity ^= 1u; }
     }
     if (partial) {
         Win w;
@@ -722,7 +769,7 @@ static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner
                 kern = pair ? dm::eval_owner_stream_kernel<true, SQ == 1, NT, MB>                         \
                             : dm::eval_owner_stream_kernel<false, SQ == 1, NT, MB>;
             DM_PICK(256, 4, 1) DM_PICK(256, 3, 1) DM_PICK(256, 2, 1) DM_PICK(512, 2, 1) DM_PICK(128, 8, 1)
-            DM_PICK(768, 1, 0) DM_PICK(512, 1, 0) DM_PICK(1024, 1, 0) DM_PICK(256, 2, 0)
+            DM_PICK(768, 1, 0) DM_PICK(512, 1, 0) DM_PICK(1024, 1, 0) DM_PICK(256, 2, 0) DM_PICK(256, 3, 0)
 #undef DM_PICK
             if (!kern) return dmabi::fail(DM_E_ARG, "dm_eval_owner: unsupported DM_MODEA_CFG");
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);

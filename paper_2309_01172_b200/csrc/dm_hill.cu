@@ -365,6 +365,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) epilogue_kernel(
         const dm_tables t = tables[sc];
         const int n = t.n;
         const int16_t* o = owner + (size_t)sc * n_max;
+        if (n <= 0 || o[0] < 0 || o[0] >= t.P) {       // no assignment (unscheduled / DP-infeasible row)
+            if (lane == 0) {
+                double* ob = out + (size_t)sc * 6;
+                const double nan = __longlong_as_double(0x7ff8000000000000LL);
+                ob[0] = nan; ob[1] = nan; ob[2] = nan; ob[3] = nan; ob[4] = nan; ob[5] = -1.0;
+            }
+            continue;
+        }
         __syncwarp();
         int r = 0;                                     // runs from the owner row, 32 stages at a time
         for (int base = 0; base < n; base += 32) {

@@ -81,6 +81,13 @@ def _csr(lists):
 def op_costs(table: OpTable, fleet, placements) -> np.ndarray:
     """Per-op (read_s, compute_s, write_s) for each placement (dict op name ->
     peer id, covering every op)."""
+    _, out, _, n = _op_costs_device(table, fleet, placements)
+    return out.cpu().numpy()[: len(placements) * n * 3].reshape(len(placements), n, 3)
+
+
+def _op_costs_device(table: OpTable, fleet, placements):
+    """dm_op_costs launch; returns (input tensors, per-op costs, numpy-type
+    flags, n_ops) on the device (reentrant: no state kept between calls)."""
     import torch
     lib = _lib.load()
     host = build_host([], fleet, True)
@@ -116,16 +123,14 @@ def op_costs(table: OpTable, fleet, placements) -> np.ndarray:
     st = batch.struct(0)
     _lib.check(lib.dm_op_costs(C.byref(ops), C.byref(st), arrs[6].data_ptr(), len(placements), arrs[7].data_ptr(),
                                out.data_ptr(), out_np.data_ptr(), _lib.stream_ptr()))
-    op_costs._last = (arrs, out, out_np, n)
-    return out.cpu().numpy()[: len(placements) * n * 3].reshape(len(placements), n, 3)
+    return arrs, out, out_np, n
 
 
 def subgraph_costs(table: OpTable, fleet, placements, cells) -> np.ndarray:
     """subgraph_time for every cell (list of op names) and placement: [B, n_cells, 3]."""
     import torch
     lib = _lib.load()
-    op_costs(table, fleet, placements)
-    arrs, out, out_np, n = op_costs._last
+    arrs, out, out_np, n = _op_costs_device(table, fleet, placements)
     idx = table.index
     sptr, sidx = _csr([[idx[x] for x in cell] for cell in cells])
     sp, si = torch.from_numpy(sptr).to(out.device), torch.from_numpy(sidx).to(out.device)

@@ -21,7 +21,7 @@ from typing import Sequence
 import numpy as np
 
 from . import engine, scheduling
-from .refapi import Link, SchedulingError, bandwidth_to_beta
+from .refapi import DagmeshError, Link, SchedulingError, bandwidth_to_beta
 from .tensorize import build_host
 
 
@@ -112,26 +112,37 @@ def sweep_stages(stages, name: str, samples_per_batch: int, fleets, bandwidth_gb
     """Batched sweep over pre-built stages (pipeline.py:228-248 semantics)."""
     stages = list(stages)
     n = len(stages)
-    points = []
+    # the reference walks the grid in order and raises at the first point that
+    # fails (bandwidth_to_beta / Link, schedule()'s input checks, then
+    # pipeline_time's n_batches check on the first feasible point,
+    # pipeline.py:235-245): errors are recorded per point and raised in that
+    # order while the rows are emitted
+    points, pending = [], None
     for fleet, bw, alpha in itertools.product(fleets, bandwidth_gbps, alpha_s):
-        tuned = fleet.with_default_link(Link(alpha=alpha, beta=bandwidth_to_beta(bw)))
+        try:
+            tuned = fleet.with_default_link(Link(alpha=alpha, beta=bandwidth_to_beta(bw)))
+            workers = tuned.worker_ids()
+            scheduling._check_inputs(stages, workers)
+            if tuned.pinned_runs is not None and len(tuned.pinned_runs) > len(workers):
+                raise scheduling.T.SchedulingError(f"{len(tuned.pinned_runs)} pinned runs but only "
+                                                   f"{len(workers)} workers")
+        except DagmeshError as exc:
+            pending = exc
+            break
         points.append((fleet, bw, alpha, tuned))
     result = SweepResult()
     if not points:
+        if pending is not None:
+            raise pending
         return result
-    if n_batches < 1:
-        raise SchedulingError(f"need at least one batch, got {n_batches}")
     hosts = []
     kinds = []  # 'pin' | 'dp' | 'hill' | 'eval'
     owner0 = np.full((len(points), n), -1, dtype=np.int16)
     for s, (_, _, _, tuned) in enumerate(points):
         workers = tuned.worker_ids()
-        scheduling._check_inputs(stages, workers)
         p = len(workers)
         hosts.append(build_host(stages, tuned, True))
         if tuned.pinned_runs is not None:
-            if len(tuned.pinned_runs) > p:
-                raise scheduling.T.SchedulingError(f"{len(tuned.pinned_runs)} pinned runs but only {p} workers")
             own = _contiguous_pins(tuned.pinned_runs, n)
             if own is None:
                 kinds.append("eval")
@@ -159,7 +170,7 @@ def sweep_stages(stages, name: str, samples_per_batch: int, fleets, bandwidth_gb
         sub = engine.device_batch([hosts[s] for s in hill_idx])
         own_h, _, _ = engine.prop_hill(sub, n)
         owner[hill_idx] = own_h
-    out = engine.epilogue(batch, n, owner, n_batches, samples_per_batch).cpu().numpy()
+    out = engine.epilogue(batch, n, owner, max(n_batches, 1), samples_per_batch).cpu().numpy()
     for s, (fleet, bw, alpha, tuned) in enumerate(points):
         kind = kinds[s]
         if kind == "eval" or (kind == "dp" and not dp_ok[s]) or int(out[s, 5]) != 0:
@@ -173,8 +184,12 @@ def sweep_stages(stages, name: str, samples_per_batch: int, fleets, bandwidth_gb
                                         pipeline_time(prof, n_batches),
                                         throughput(prof, n_batches, samples_per_batch)))
             continue
+        if n_batches < 1:                               # pipeline_time on the first feasible point (:53-55)
+            raise SchedulingError(f"need at least one batch, got {n_batches}")
         result.rows.append(SweepRow(name, fleet.name, bw, alpha * 1e3, n_batches, float(out[s, 1]),
                                     float(out[s, 3]), float(out[s, 4])))
+    if pending is not None:
+        raise pending
     return result
 
 
