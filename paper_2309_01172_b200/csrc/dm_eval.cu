@@ -396,14 +396,14 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
                                             double* __restrict__ out_mk, uint8_t* __restrict__ out_code,
                                             int64_t rank_base, bool fuse, StreamWin& win, uint32_t& n_seen) {
     const int n = X.n;
-    // per-tile bases, advanced per candidate (no per-candidate address rebuild)
-    double* omk = out_mk + c0;
-    uint8_t* ocode = out_code + c0;
-    const int64_t rbase = rank_base + c0;
+    // per-thread bases, advanced per candidate (no per-candidate address rebuild)
+    double* omk = out_mk + c0 + threadIdx.x;
+    uint8_t* ocode = out_code + c0 + threadIdx.x;
+    int64_t rank = rank_base + c0 + threadIdx.x;
     uint32_t row_s = tile_s + (uint32_t)threadIdx.x * n;          // shared address of this thread's row
     const uint32_t row_step = (uint32_t)NT * n;
 #pragma unroll 1
-    for (int ci = threadIdx.x; ci < cnt; ci += NT, row_s += row_step) {
+    for (int ci = threadIdx.x; ci < cnt; ci += NT, row_s += row_step, omk += NT, ocode += NT, rank += NT) {
         ++n_seen;
         const unsigned long long bm = boundary_mask<NW>(row_s & ~3u, (int)(row_s & 3u) * 8);
         double mk = 0.0;
@@ -499,12 +499,12 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
             for (int i = 0; i < n; ++i) if (row[i] >= X.uP) { unknown = true; break; }
             if (!unknown) eval_owner_grouped(t, row, mk, code);
         }
-        omk[ci] = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
-        ocode[ci] = unknown ? (uint8_t)0xFF : (uint8_t)code;
+        *omk = unknown ? __longlong_as_double(0x7ff8000000000000LL) : mk;
+        *ocode = unknown ? (uint8_t)0xFF : (uint8_t)code;
         if (fuse && !unknown && code == DM_V_OK) {      // fused arg-min (first strict minimum by rank)
             win.n_feas++;
             win.csum += (uint64_t)__double_as_longlong(mk);
-            if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rbase + ci; }
+            if (win.rank < 0 || mk < win.mk) { win.mk = mk; win.rank = rank; }
         }
     }
 }

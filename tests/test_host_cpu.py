@@ -223,3 +223,36 @@ def test_stage_fast_path_equals_reference_build_stages():
     job["nodes"][3]["kwargs"] = {"inner_features": 77}          # one ffn differs from the others
     g = ir.parse_job_definition(job)
     assert CF.encoder_params(g, cells) is None and CF.stages_for(g, cells) == RS.build_stages(g, cells)
+
+
+def test_tensoriser_link_matrix_and_stage_cache():
+    """Vectorised link matrix == the fleet's own link_between for every pair
+    (asymmetric overrides, both orders present, unknown ids skipped); the
+    lazy form (link_pairs) matches on the requested pairs; the stage side is
+    shared between fleets while fleet columns follow each fleet."""
+    import itertools
+    from paper_2309_01172_b200 import tensorize as TZ
+    doc = {"name": "t", "peers": [{"id": str(i), "gpu": g} for i, g in
+                                  enumerate(["h100", "rtx3080", "a100", "rtx4090", "rtx4080"], 1)],
+           "links": {"default_alpha_s": 0.002, "bandwidth_gbps": 3.0,
+                     "overrides": [{"src": "1", "dst": "2", "alpha_s": 0.5, "bandwidth_gbps": 1.0},
+                                   {"src": "2", "dst": "1", "alpha_s": 0.25, "bandwidth_gbps": 2.0},
+                                   {"src": "3", "dst": "5", "alpha_s": 0.125, "bandwidth_gbps": 4.0}]},
+           "backup_pool": ["4"]}
+    fl = M.parse_fleet(json.dumps(doc))
+    st = CF.model_stages("gpt2-small")
+    h = build_host(st, fl)
+    P = h.P
+    la, lb = h.arrays["link_alpha"].reshape(P, P), h.arrays["link_beta"].reshape(P, P)
+    for i, j in itertools.product(range(P), range(P)):
+        lk = fl.link_between(h.peer_ids[i], h.peer_ids[j])
+        assert (la[i, j], lb[i, j]) == ((0.0, 0.0) if i == j else (lk.alpha, lk.beta))
+    pairs = [(0, 1), (1, 0), (2, 3)]
+    hl = build_host(st, fl, link_pairs=pairs)
+    lla = hl.arrays["link_alpha"].reshape(P, P)
+    assert all(lla[i, j] == la[i, j] for i, j in pairs)
+    fl2 = M.parse_fleet(json.dumps({**doc, "links": {"default_alpha_s": 0.001}}))
+    h2 = build_host(st, fl2)
+    assert h2.arrays["pre_flops"] is h.arrays["pre_flops"]              # cached stage side
+    assert h2.def_alpha == 0.001 and "link_alpha" not in dict(h2.segments())
+    assert TZ.stage_side(st) is TZ.stage_side(list(st))
