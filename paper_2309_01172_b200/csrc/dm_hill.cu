@@ -77,10 +77,36 @@ __device__ __forceinline__ double run_load_ab(const dm_tables& t, int a, int b, 
     return c + rd;
 }
 
+// Staged scenario tables for the fast path (exact integral columns, chain
+// stages or a uniform link, <= kHillPeers workers): per boundary i the exact
+// prefix sums as doubles and R[i], the read of a run starting at i (stage i's
+// in-edges priced with the default link, summed like run_cost_contig); per
+// worker speed and capacities.  Every run load in the hill climb then costs
+// shared-memory reads instead of dependent global loads.
+constexpr int kHillPeers = 64;
+struct HillStage { double pf, pg, pc, pd, R; };
+struct HillPeer { double speed, cg, cc, cd; };
+
 // Per-warp shared memory of prop_hill_kernel: stage flops, run loads and
-// their prefix / suffix maxima, bounds/peers, run fit flags.
-__host__ __device__ inline size_t hill_warp_bytes(int n_max) {
+// their prefix / suffix maxima, bounds/peers, run fit flags, staged tables.
+__host__ __device__ inline size_t hill_core_bytes(int n_max) {
     return ((size_t)(4 * n_max + 3) * 8 + (size_t)2 * (n_max + 2) * 4 + (size_t)(n_max + 1) + 15) & ~(size_t)15;
+}
+__host__ __device__ inline size_t hill_warp_bytes(int n_max) {
+    return hill_core_bytes(n_max) + (size_t)(n_max + 1) * sizeof(HillStage) + (size_t)kHillPeers * sizeof(HillPeer);
+}
+
+// run load on the staged tables (fast path); read of the run = R[a] when it
+// has a predecessor run (chain stages: the previous run is on another worker)
+__device__ __forceinline__ double run_load_staged(const HillStage* hs, const HillPeer* hp, int a, int b, int w,
+                                                  bool comm, bool& bad) {
+    const HillStage& A = hs[a];
+    const HillStage& B = hs[b];
+    const HillPeer& P = hp[w];
+    bad = !((B.pg - A.pg <= P.cg) & (B.pc - A.pc <= P.cc) & (B.pd - A.pd <= P.cd));
+    const double c = (B.pf - A.pf) / P.speed;
+    const double rd = (comm && a > 0) ? A.R : 0.0;
+    return c + rd;
 }
 
 // _proportional_runs on lane 0; returns r and fills bounds/peers.
@@ -178,12 +204,14 @@ __device__ int proportional_warp(const dm_tables& t, int32_t* bounds, int32_t* p
     return __shfl_sync(0xffffffffu, nr, 0);
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
+__global__ void __maxnreg__(168) prop_hill_kernel(
         const dm_tables* __restrict__ tables, int32_t n_scen, int32_t n_max, const int16_t* __restrict__ init_owner,
         const uint8_t* __restrict__ do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves) {
     extern __shared__ __align__(16) unsigned char shb[];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     unsigned char* mine = shb + (size_t)wl * hill_warp_bytes(n_max);
+    HillStage* hs = reinterpret_cast<HillStage*>(mine + hill_core_bytes(n_max));
+    HillPeer* hp = reinterpret_cast<HillPeer*>(hs + n_max + 1);
     double* fls = reinterpret_cast<double*>(mine);                   // [n_max] the scenario's stage flops
     double* lr = fls + n_max;                                         // [n_max + 1] run loads
     double* pm = lr + n_max + 1;                                      // [n_max + 1] prefix max of the loads
@@ -196,6 +224,27 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
         const dm_tables t = tables[sc];
         const int n = t.n;
         __syncwarp();
+        const bool comm = include_comm(t);
+        const bool fast = flops_exact(t) && bytes_exact(t) && chain(t) && !(comm && pair_links(t)) &&
+                          t.p <= kHillPeers && !np_comm(t);
+        if (fast) {                                   // stage the scenario's tables for the hill climb
+            for (int i = lane; i <= n; i += 32) {
+                HillStage h;
+                h.pf = (double)t.pre_flops[i]; h.pg = (double)t.pre_gpu[i];
+                h.pc = (double)t.pre_cpu[i]; h.pd = (double)t.pre_disk[i];
+                double rd = 0.0;
+                if (comm && i < n)
+                    for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e)
+                        rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
+                h.R = rd;
+                hs[i] = h;
+            }
+            for (int w = lane; w < t.p; w += 32) {
+                HillPeer h;
+                h.speed = t.speed[w]; h.cg = t.cap_gpu[w]; h.cc = t.cap_cpu[w]; h.cd = t.cap_disk[w];
+                hp[w] = h;
+            }
+        }
         int r = 0;
         const bool pwarp = !init_owner && flops_exact(t);
         if (!init_owner && !pwarp) for (int i = lane; i < n; i += 32) fls[i] = t.flops[i];
@@ -216,8 +265,23 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
         // only the two runs at a moved boundary change unless reads depend on
         // which run owns a source (pair links on DAG stages)
         const bool incr = chain(t) || !include_comm(t) || !pair_links(t);
-        double cur = incr ? hill_score(t, r, bounds, peers, lane, lr, bd)
-                          : hill_score(t, r, bounds, peers, lane);        // :365
+        double cur;
+        if (fast) {                                                        // :365 on the staged tables
+            const double inf = __longlong_as_double(0x7ff0000000000000LL);
+            bool anybad = false;
+            double best = 0.0;
+            for (int q = lane; q < r; q += 32) {
+                bool b_;
+                const double load = run_load_staged(hs, hp, bounds[q], bounds[q + 1], peers[q], comm, b_);
+                lr[q] = load; bd[q] = b_;
+                anybad |= b_;
+                if (!b_) best = load > best ? load : best;
+            }
+            __syncwarp();
+            cur = __any_sync(0xffffffffu, anybad) ? inf : warp_max(best);
+        } else {
+            cur = incr ? hill_score(t, r, bounds, peers, lane, lr, bd) : hill_score(t, r, bounds, peers, lane);
+        }
         int moves = 0;
         if ((!do_hill || do_hill[sc]) && incr) {
             // The reference walks moves (a, dir) in order and takes the first
@@ -272,8 +336,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) prop_hill_kernel(
                         const int la = bounds[a + 1] - bounds[a], lb = bounds[a + 2] - bounds[a + 1];
                         if ((dir == 0 && la > 1) || (dir == 1 && lb > 1)) {                      // :373-376
                             nb = dir == 0 ? bounds[a + 1] - 1 : bounds[a + 1] + 1;
-                            va = run_load_ab(t, bounds[a], nb, peers[a], a > 0 ? peers[a - 1] : -1, ba);
-                            vb = run_load_ab(t, nb, bounds[a + 2], peers[a + 1], peers[a], bb);
+                            if (fast) {
+                                va = run_load_staged(hs, hp, bounds[a], nb, peers[a], comm, ba);
+                                vb = run_load_staged(hs, hp, nb, bounds[a + 2], peers[a + 1], comm, bb);
+                            } else {
+                                va = run_load_ab(t, bounds[a], nb, peers[a], a > 0 ? peers[a - 1] : -1, ba);
+                                vb = run_load_ab(t, nb, bounds[a + 2], peers[a + 1], peers[a], bb);
+                            }
                             double sc2 = 0.0;
                             if (a > 0) sc2 = pm[a - 1] > sc2 ? pm[a - 1] : sc2;
                             if (a + 2 < r) sc2 = sm[a + 2] > sc2 ? sm[a + 2] : sc2;
