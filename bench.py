@@ -552,11 +552,10 @@ def c4_measure(dev, fp64_peak, n_scen=10 ** 6):
     sb = B.c4_batch(n_scen, seed=0, device=dev)
 
     def run():
-        owner, _, _ = engine.prop_hill(sb, sb.n_max)
-        return engine.epilogue(sb, sb.n_max, owner, 512, 4)
+        return engine.prop_hill_epilogue(sb, sb.n_max, 512, 4)
     ms = _time_ms(run, steps=3, warmup=2)
-    owner, _, moves = engine.prop_hill(sb, sb.n_max)
-    epi = engine.epilogue(sb, sb.n_max, owner, 512, 4).cpu().numpy()
+    owner, _, moves, epi = engine.prop_hill_epilogue(sb, sb.n_max, 512, 4)
+    epi = epi.cpu().numpy()
     owner = owner.cpu().numpy()
     ok = True
     t0 = _t.perf_counter()
@@ -888,8 +887,7 @@ def sharded_measurements(args, dev, rank, world):
     sb = B.c4_batch(n4, seed=0, device=dev, lo=lo, hi=hi)
 
     def c4_step():
-        owner, _, _ = engine.prop_hill(sb, sb.n_max)
-        epi = engine.epilogue(sb, sb.n_max, owner, 512, 4)
+        _, _, _, epi = engine.prop_hill_epilogue(sb, sb.n_max, 512, 4)
         feas = torch.tensor([float((epi[:, 5] == 0).sum())], dtype=torch.float64, device=dev)
         g = torch.empty(world, dtype=torch.float64, device=dev)
         torch.distributed.all_gather_into_tensor(g, feas)

@@ -311,6 +311,16 @@ DM_API int dm_schedule_report(const dm_tables* tables, int32_t n, const int16_t*
                               void* out, void* stream);
 
 /*
+ * dm_prop_hill_epilogue — dm_prop_hill followed, in the same kernel, by the
+ * dm_pipeline_epilogue values of each scenario's final runs (out[s*6 + ...]
+ * as below): batched schedule() + Eq. 3/4 in one launch.
+ */
+DM_API int dm_prop_hill_epilogue(const dm_tables* tables, int32_t n_scen, int32_t n_max,
+                                 const int16_t* init_owner, const uint8_t* do_hill,
+                                 int16_t* out_owner, double* out_score, int32_t* out_moves,
+                                 int64_t n_batches, int64_t samples_per_batch, double* out, void* stream);
+
+/*
  * dm_pipeline_epilogue — per scenario, from an owner vector with contiguous
  * runs: _evaluate's makespan and feasibility (:210-232), then
  * fp_latency (Neumaier sum, pipeline.py:41-43), bottleneck (:46-50),

@@ -85,6 +85,7 @@ _SIGS = {
     "dm_subset_dp_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "dm_subset_dp": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P]),
     "dm_prop_hill": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
+    "dm_prop_hill_epilogue": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, C.c_int64, C.c_int64, _P, _P]),
     "dm_pipeline_epilogue": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int64, C.c_int64, _P, _P]),
     "dm_microbench_fp64": (C.c_int, [C.c_int64, _P, _P, _P]),
     "dm_microbench_cross": (C.c_int, [C.c_int64, _P, _P, _P]),

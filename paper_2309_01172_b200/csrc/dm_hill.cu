@@ -204,9 +204,75 @@ __device__ int proportional_warp(const dm_tables& t, int32_t* bounds, int32_t* p
     return __shfl_sync(0xffffffffu, nr, 0);
 }
 
+// _evaluate + Eq. 3/4 (scheduling.py:210-232, pipeline.py:41-62) over runs
+// bounds[0..r] / peers[0..r) in shared memory, one warp; `loads` is r
+// doubles of scratch.  hs/hp (optional): the scenario's staged tables (the
+// hill climb's fast path) — then run costs come from shared memory.
+__device__ void epilogue_runs(const dm_tables& t, int r, const int32_t* bounds, const int32_t* peers, double* loads,
+                              int lane, int64_t n_batches, int64_t spb, double* ob, const HillStage* hs,
+                              const HillPeer* hp) {
+    int first_bad = 0x7fffffff, bad_code = 0;
+    double mk = 0.0, bn = 0.0;
+    for (int q = lane; q < r; q += 32) {
+        int a = bounds[q], b = bounds[q + 1], w = peers[q];
+        double c, rd;
+        int v;
+        if (hs) {
+            const HillStage& A = hs[a];
+            const HillStage& B = hs[b];
+            const HillPeer& P = hp[w];
+            v = (B.pg - A.pg > P.cg) ? DM_V_GPU : (B.pc - A.pc > P.cc) ? DM_V_CPU : (B.pd - A.pd > P.cd) ? DM_V_DISK : 0;
+            c = (B.pf - A.pf) / P.speed;
+            rd = (include_comm(t) && a > 0) ? A.R : 0.0;
+        } else {
+            v = cap_violation(t, w, a, b);
+            int prev = q > 0 ? peers[q - 1] : -1;
+            if (chain(t)) run_cost_contig(t, a, b, w, [&](int) { return prev; }, c, rd);
+            else { BoundsOwner own{bounds, peers, r}; run_cost_contig(t, a, b, w, own, c, rd); }
+        }
+        if (v && q < first_bad) { first_bad = q; bad_code = v; }
+        double load = c + rd;
+        // Python type of p.compute_s + p.read_s: numpy when the speed, the
+        // FLOPs or (for a run with a crossing read) the link values are
+        // (sum() over them then turns naive, see PySum)
+        bool np_load = (t.peer_np && t.peer_np[w]) || np_flops(t);
+        if (np_comm(t) && include_comm(t)) {
+            if (chain(t)) np_load |= a > 0 && t.edge_ptr[a + 1] > t.edge_ptr[a];
+            else for (int i = a; i < b && !np_load; ++i)
+                for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e)
+                    if (t.edge_src[e] < a || t.edge_src[e] >= b) { np_load = true; break; }
+        }
+        loads[q] = np_load ? -load : load;    // loads are >= 0 (or NaN): the sign bit flags a numpy item
+        mk = load > mk ? load : mk;
+        double m = c >= rd ? c : rd;          // max(p.compute_s, p.read_s) pipeline.py:50
+        bn = m > bn ? m : bn;
+    }
+    mk = warp_max(mk);
+    bn = warp_max(bn);
+    for (int off = 16; off > 0; off >>= 1) {
+        int of = __shfl_xor_sync(0xffffffffu, first_bad, off);
+        int oc = __shfl_xor_sync(0xffffffffu, bad_code, off);
+        if (of < first_bad) { first_bad = of; bad_code = oc; }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        PySum lat;                                 // fp_latency, builtin sum :43
+        for (int q = 0; q < r; ++q) {
+            const double v = loads[q];
+            lat.add(fabs(v), !signbit(v));
+        }
+        double latency = lat.value();
+        double fill = (double)(n_batches - 1) * bn;   // (n_b - 1) * bottleneck :56
+        double pipe = latency + fill;
+        double thr = (double)(n_batches * spb) / pipe; // :62
+        ob[0] = mk; ob[1] = latency; ob[2] = bn; ob[3] = pipe; ob[4] = thr; ob[5] = (double)bad_code;
+    }
+}
+
 __global__ void __maxnreg__(168) prop_hill_kernel(
         const dm_tables* __restrict__ tables, int32_t n_scen, int32_t n_max, const int16_t* __restrict__ init_owner,
-        const uint8_t* __restrict__ do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves) {
+        const uint8_t* __restrict__ do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves,
+        double* epi_out, int64_t n_batches, int64_t spb) {
     extern __shared__ __align__(16) unsigned char shb[];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     unsigned char* mine = shb + (size_t)wl * hill_warp_bytes(n_max);
@@ -417,6 +483,9 @@ __global__ void __maxnreg__(168) prop_hill_kernel(
         }
         for (int i = n + lane; i < n_max; i += 32) o[i] = -1;
         if (lane == 0) { out_score[sc] = cur; if (out_moves) out_moves[sc] = moves; }
+        if (epi_out)                                  // fused epilogue on the final runs (pm is free scratch now)
+            epilogue_runs(t, r, bounds, peers, pm, lane, n_batches, spb, epi_out + (size_t)sc * 6,
+                          fast ? hs : nullptr, hp);
     }
 }
 
@@ -458,53 +527,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) epilogue_kernel(
         }
         if (lane == 0) bounds[r] = n;
         __syncwarp();
-        int first_bad = 0x7fffffff, bad_code = 0;
-        double mk = 0.0, bn = 0.0;
-        for (int q = lane; q < r; q += 32) {
-            int a = bounds[q], b = bounds[q + 1], w = peers[q];
-            int v = cap_violation(t, w, a, b);
-            if (v && q < first_bad) { first_bad = q; bad_code = v; }
-            double c, rd;
-            int prev = q > 0 ? peers[q - 1] : -1;
-            if (chain(t)) run_cost_contig(t, a, b, w, [&](int) { return prev; }, c, rd);
-            else { BoundsOwner own{bounds, peers, r}; run_cost_contig(t, a, b, w, own, c, rd); }
-            double load = c + rd;
-            // Python type of p.compute_s + p.read_s: numpy when the speed, the
-            // FLOPs or (for a run with a crossing read) the link values are
-            // (sum() over them then turns naive, see PySum)
-            bool np_load = (t.peer_np && t.peer_np[w]) || np_flops(t);
-            if (np_comm(t) && include_comm(t)) {
-                if (chain(t)) np_load |= a > 0 && t.edge_ptr[a + 1] > t.edge_ptr[a];
-                else for (int i = a; i < b && !np_load; ++i)
-                    for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e)
-                        if (t.edge_src[e] < a || t.edge_src[e] >= b) { np_load = true; break; }
-            }
-            loads[q] = np_load ? -load : load;    // loads are >= 0 (or NaN): the sign bit flags a numpy item
-            mk = load > mk ? load : mk;
-            double m = c >= rd ? c : rd;          // max(p.compute_s, p.read_s) pipeline.py:50
-            bn = m > bn ? m : bn;
-        }
-        mk = warp_max(mk);
-        bn = warp_max(bn);
-        for (int off = 16; off > 0; off >>= 1) {
-            int of = __shfl_xor_sync(0xffffffffu, first_bad, off);
-            int oc = __shfl_xor_sync(0xffffffffu, bad_code, off);
-            if (of < first_bad) { first_bad = of; bad_code = oc; }
-        }
-        __syncwarp();
-        if (lane == 0) {
-            PySum lat;                                 // fp_latency, builtin sum :43
-            for (int q = 0; q < r; ++q) {
-                const double v = loads[q];
-                lat.add(fabs(v), !signbit(v));
-            }
-            double latency = lat.value();
-            double fill = (double)(n_batches - 1) * bn;   // (n_b - 1) * bottleneck :56
-            double pipe = latency + fill;
-            double thr = (double)(n_batches * spb) / pipe; // :62
-            double* ob = out + (size_t)sc * 6;
-            ob[0] = mk; ob[1] = latency; ob[2] = bn; ob[3] = pipe; ob[4] = thr; ob[5] = (double)bad_code;
-        }
+        epilogue_runs(t, r, bounds, peers, loads, lane, n_batches, spb, out + (size_t)sc * 6, nullptr, nullptr);
     }
 }
 
@@ -531,7 +554,23 @@ int dm_prop_hill(const dm_tables* tables, int32_t n_scen, int32_t n_max, const i
     if (smem > 200 * 1024) return dmabi::fail(DM_E_TOO_LARGE, "dm_prop_hill: too many stages");
     cudaFuncSetAttribute(dm::prop_hill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dm::prop_hill_kernel<<<hill_grid(n_scen), 32 * dm::kWarpsPerCta, smem, (cudaStream_t)stream>>>(
-        tables, n_scen, n_max, init_owner, do_hill, out_owner, out_score, out_moves);
+        tables, n_scen, n_max, init_owner, do_hill, out_owner, out_score, out_moves, nullptr, 1, 1);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
+int dm_prop_hill_epilogue(const dm_tables* tables, int32_t n_scen, int32_t n_max, const int16_t* init_owner,
+                          const uint8_t* do_hill, int16_t* out_owner, double* out_score, int32_t* out_moves,
+                          int64_t n_batches, int64_t samples_per_batch, double* out, void* stream) {
+    if (!tables || n_scen < 0 || n_max <= 0 || !out_owner || !out_score || !out)
+        return dmabi::fail(DM_E_ARG, "dm_prop_hill_epilogue: bad arguments");
+    if (n_scen == 0) return DM_OK;
+    size_t smem = (size_t)dm::kWarpsPerCta * dm::hill_warp_bytes(n_max);
+    if (smem > 200 * 1024) return dmabi::fail(DM_E_TOO_LARGE, "dm_prop_hill_epilogue: too many stages");
+    cudaFuncSetAttribute(dm::prop_hill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dm::prop_hill_kernel<<<hill_grid(n_scen), 32 * dm::kWarpsPerCta, smem, (cudaStream_t)stream>>>(
+        tables, n_scen, n_max, init_owner, do_hill, out_owner, out_score, out_moves, out, n_batches,
+        samples_per_batch);
     DM_CHECK_LAUNCH();
     return DM_OK;
 }

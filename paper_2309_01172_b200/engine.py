@@ -307,6 +307,24 @@ def prop_hill(batch: DeviceBatch, n_max: int, init_owner=None, do_hill=None):
     return owner, score, moves
 
 
+def prop_hill_epilogue(batch: DeviceBatch, n_max: int, n_batches: int, samples_per_batch: int, init_owner=None,
+                       do_hill=None):
+    """Batched schedule() (proportional split + hill climb) and the Eq. 3/4
+    epilogue of the final runs in one launch: (owner, score, moves, out[ns, 6])."""
+    lib = _lib.load()
+    torch = _torch()
+    dev = batch.dev_buf.device
+    ns = len(batch.hosts)
+    owner = torch.empty((ns, n_max), dtype=torch.int16, device=dev)
+    score = torch.empty(ns, dtype=torch.float64, device=dev)
+    moves = torch.empty(ns, dtype=torch.int32, device=dev)
+    out = torch.empty((ns, 6), dtype=torch.float64, device=dev)
+    _lib.check(lib.dm_prop_hill_epilogue(batch.struct_ptr(), ns, n_max, _lib.ptr(init_owner), _lib.ptr(do_hill),
+                                         owner.data_ptr(), score.data_ptr(), moves.data_ptr(), int(n_batches),
+                                         int(samples_per_batch), out.data_ptr(), _lib.stream_ptr()))
+    return owner, score, moves, out
+
+
 def epilogue(batch: DeviceBatch, n_max: int, owner, n_batches: int, samples_per_batch: int):
     lib = _lib.load()
     torch = _torch()

@@ -171,8 +171,9 @@ def test_c4_million_scenarios(engine_ready):
     from paper_2309_01172_b200 import batch as B, engine
     g = GOLD["c4"]
     sb = B.c4_batch(g["scenarios"], seed=0)
-    owner, _, _ = engine.prop_hill(sb, sb.n_max)
+    owner, _, _, epi_f = engine.prop_hill_epilogue(sb, sb.n_max, g["n_batches"], g["samples_per_batch"])
     epi = engine.epilogue(sb, sb.n_max, owner, g["n_batches"], g["samples_per_batch"]).cpu().numpy()
+    assert np.array_equal(epi_f.cpu().numpy().view(np.uint64), epi.view(np.uint64))   # fused == separate
     owner = owner.cpu().numpy()
     ns = sb.records["n"]
     bad = []
