@@ -179,6 +179,92 @@ __global__ void __launch_bounds__(256) enum_kernel(dm_tables t, int64_t k0, int6
     block_reduce_win_store(w, partial);
 }
 
+// ------------------------------------------- direct identity-split scoring
+// Per-candidate cost model for the identity-order population (run q on
+// worker q) with exact integral columns and chain stages or a uniform link —
+// the generic evaluator's work (brute_force_schedule's inner body,
+// scheduling.py:266-270) with the tables staged in shared memory: per run the
+// exact prefix differences at its two boundaries, three capacity compares,
+// compute = flops / speed and the crossing read.  The quotient uses
+// Markstein's correction q1 = q0 + (a - q0*b)*y with y = RN(1/b), q0 = RN(a*y)
+// — within one ulp before the correction, so the result is the correctly
+// rounded a / b (the parity tests compare it with div.rn bit for bit).
+struct __align__(8) DStage { double pf, pg, pc, pd, R; };
+struct __align__(8) DPeer { double speed, rcp, cg, cc, cd; };
+
+__device__ __forceinline__ double div_markstein(double a, double b, double y) {
+    const double q0 = __dmul_rn(a, y);
+    const double rem = __fma_rn(-q0, b, a);
+    return __fma_rn(rem, y, q0);
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(256) splits_direct_kernel(dm_tables t, int64_t k0, int64_t k1, int part, int nparts,
+                                                            int64_t per_thread, dm_winner* partial) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int n = t.n, p = t.p, rmax = n < p ? n : p;
+    DStage* S = reinterpret_cast<DStage*>(dsm);
+    DPeer* Pr = reinterpret_cast<DPeer*>(S + n + 1);
+    const bool comm = include_comm(t);
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+        DStage d;
+        d.pf = (double)t.pre_flops[i]; d.pg = (double)t.pre_gpu[i];
+        d.pc = (double)t.pre_cpu[i]; d.pd = (double)t.pre_disk[i];
+        double rd = 0.0;
+        if (comm && i < n)                       // run starting at i reads stage i's in-edges (default link)
+            for (int e = t.edge_ptr[i]; e < t.edge_ptr[i + 1]; ++e)
+                rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
+        d.R = rd;
+        S[i] = d;
+    }
+    for (int w = threadIdx.x; w < rmax; w += blockDim.x) {
+        DPeer d;
+        d.speed = t.speed[w]; d.rcp = 1.0 / d.speed;
+        d.cg = t.cap_gpu[w]; d.cc = t.cap_cpu[w]; d.cd = t.cap_disk[w];
+        Pr[w] = d;
+    }
+    __syncthreads();
+    Win w; win_init(w);
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t kb = k0 + (tid * nparts + part) * per_thread;
+    int64_t ke = kb + per_thread < k1 ? kb + per_thread : k1;
+    if (kb < ke) {
+        int32_t cuts[RMAX + 1];
+        int r = 1;
+        int64_t off = kb;
+        for (; r <= rmax; ++r) {
+            int64_t nc = binom_sat(n - 1, r - 1);
+            if (off < nc) break;
+            off -= nc;
+        }
+        unrank_comb(n, r - 1, off, cuts);
+        for (int64_t k = kb; k < ke; ++k) {
+            // one pass over the runs: fits (all must hold) and the max load
+            bool ok = true;
+            double mk = 0.0;
+            int a = 0;
+            DStage A = S[0];
+            for (int q = 0; q < r; ++q) {
+                const int b = q + 1 < r ? cuts[q] : n;
+                const DStage B = S[b];
+                const DPeer P = Pr[q];
+                ok &= (B.pg - A.pg <= P.cg) & (B.pc - A.pc <= P.cc) & (B.pd - A.pd <= P.cd);
+                double load = div_markstein(B.pf - A.pf, P.speed, P.rcp);
+                if (comm && a > 0) load = load + A.R;
+                mk = load > mk ? load : mk;
+                a = b; A = B;
+            }
+            w.n_eval++;
+            if (ok) win_add(w, mk, k);
+            if (next_comb(n, r - 1, cuts)) continue;
+            ++r;
+            if (r > rmax) break;
+            for (int q = 0; q < r - 1; ++q) cuts[q] = q + 1;
+        }
+    }
+    block_reduce_win_store(w, partial);
+}
+
 // ------------------------------------------------ memoised identity splits
 // Rank-range form (any [k0, k1)): every candidate is scored from scratch as
 // the max over its r runs of the memo table T (dm_memo.cuh).
@@ -413,6 +499,19 @@ int enum_grid() {
 template <int MODE>
 int launch_enum(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts, dm_winner* out, void* scratch,
                 cudaStream_t s) {
+    {   // ranks beyond the population do not exist: clamp [k0, k1) to it
+        const int rmax_ = t->n < t->p ? t->n : t->p;
+        unsigned __int128 tot = 0;
+        for (int r = 1; r <= rmax_; ++r) {
+            unsigned __int128 nc = 1, np = 1;
+            for (int i = 1; i <= r - 1; ++i) nc = nc * (unsigned __int128)(t->n - r + i) / (unsigned __int128)i;
+            if (MODE == 0) for (int i = 0; i < r; ++i) np *= (unsigned __int128)(t->p - i);
+            tot += nc * np;
+            if (tot > (unsigned __int128)INT64_MAX) break;
+        }
+        if (tot < (unsigned __int128)INT64_MAX && (unsigned __int128)k1 > tot) k1 = (int64_t)tot;
+        if (k0 > k1) k0 = k1;
+    }
     int grid = enum_grid();
     dm_winner* partial = (dm_winner*)scratch;
     int64_t total_threads = (int64_t)grid * kThreads * nparts;
@@ -420,6 +519,20 @@ int launch_enum(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts
     int64_t per = (span + total_threads - 1) / total_threads;
     if (per < 1) per = 1;
     int rmax = t->n < t->p ? t->n : t->p;
+    const uint32_t f = t->flags;
+    const bool direct = MODE == 1 && (f & DM_F_FLOPS_EXACT) && (f & DM_F_BYTES_EXACT) &&
+                        (!(f & DM_F_INCLUDE_COMM) || ((f & DM_F_CHAIN) && !(f & DM_F_PAIR_LINKS))) &&
+                        !getenv_flag("DM_DISABLE_DIRECT");
+    if (direct && rmax <= 64) {
+        const size_t smem = (size_t)(t->n + 1) * sizeof(dm::DStage) + (size_t)rmax * sizeof(dm::DPeer);
+        if (smem <= 48 * 1024) {
+            dm::splits_direct_kernel<64><<<grid, kThreads, smem, s>>>(*t, k0, k1, part, nparts, per, partial);
+            DM_CHECK_LAUNCH();
+            dm::finalize_kernel<<<1, 1024, 0, s>>>(partial, grid, out);
+            DM_CHECK_LAUNCH();
+            return DM_OK;
+        }
+    }
     if (rmax <= 16) dm::enum_kernel<MODE, 16><<<grid, kThreads, 0, s>>>(*t, k0, k1, part, nparts, per, partial);
     else if (rmax <= 64) dm::enum_kernel<MODE, 64><<<grid, kThreads, 0, s>>>(*t, k0, k1, part, nparts, per, partial);
     else if (rmax <= 256) dm::enum_kernel<MODE, 256><<<grid, kThreads, 0, s>>>(*t, k0, k1, part, nparts, per, partial);

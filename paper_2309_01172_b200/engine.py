@@ -156,6 +156,10 @@ def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | 
     bufs = bufs or WinnerBuffers(batch.dev_buf.device)
     st = batch.struct(index)
     s = _lib.stream_ptr()
+    if mode in ("bruteforce", "splits"):              # ranks beyond the population do not exist
+        total = (bruteforce_total if mode == "bruteforce" else splits_total)(st.n, st.p)
+        k1 = min(k1, total)
+        k0 = min(k0, k1)
     if mode == "bruteforce":
         _lib.check(lib.dm_enum_bruteforce(C.byref(st), k0, k1, bufs.out.data_ptr(), bufs.scratch.data_ptr(), s))
     elif mode == "splits":
