@@ -333,6 +333,152 @@ __global__ void __launch_bounds__(32 * kDpWarps) subset_dp_warp_kernel(const dm_
     }
 }
 
+// ---- small fleets, latency form: one CTA of kDpCtaWarps warps per scenario
+//      (the same tables and pull-form key as subset_dp_warp_kernel), so a
+//      batch that does not fill the GPU (the C1 link grid: 1024 DPs) finishes
+//      each DP with 4x the lanes: chunk costs and _fits break points one
+//      (i, worker) pair per thread, each warp reducing a quarter of the target
+//      masks of a level, one __syncthreads between levels.
+constexpr int kDpCtaWarps = 4;
+
+__global__ void __launch_bounds__(32 * kDpCtaWarps) subset_dp_cta_kernel(const dm_tables* __restrict__ tables,
+                                                                         int32_t n_scen, int32_t n_max,
+                                                                         int32_t p_max, int32_t e_max,
+                                                                         int16_t* out_owner, double* out_mk,
+                                                                         int32_t* out_found) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, T = blockDim.x;
+    for (int sc = blockIdx.x; sc < n_scen; sc += gridDim.x) {
+        __syncthreads();
+        const dm_tables tg = tables[sc];
+        const int n = tg.n, p = tg.p, S = 1 << p, n1 = n + 1, E = tg.n_edges;
+        unsigned char* b = dsm;
+        double* cc = reinterpret_cast<double*>(b); b += align_up((size_t)n * n1 / 2 * p * 8);
+        double* mk = reinterpret_cast<double*>(b); b += align_up((size_t)n1 * S * 8);
+        int32_t* back = reinterpret_cast<int32_t*>(b); b += align_up((size_t)n1 * S * 4);
+        int16_t* jlim = reinterpret_cast<int16_t*>(b); b += align_up((size_t)n1 * p * 2);
+        // stage the columns (as dpw_stage, CTA-wide)
+        dm_tables t = tg;
+        {
+            int64_t* pre = reinterpret_cast<int64_t*>(b); b += align_up(4 * (size_t)n1 * 8);
+            double* col = reinterpret_cast<double*>(b); b += align_up(4 * (size_t)n * 8);
+            int32_t* eptr = reinterpret_cast<int32_t*>(b); b += align_up((size_t)n1 * 4);
+            int32_t* esrc = reinterpret_cast<int32_t*>(b); b += align_up((size_t)e_max * 4);
+            double* em = reinterpret_cast<double*>(b); b += align_up((size_t)e_max * 8);
+            double* peer = reinterpret_cast<double*>(b);
+            for (int i = tid; i < n1; i += T) {
+                pre[i] = tg.pre_flops[i]; pre[n1 + i] = tg.pre_gpu[i]; pre[2 * n1 + i] = tg.pre_cpu[i];
+                pre[3 * n1 + i] = tg.pre_disk[i]; eptr[i] = tg.edge_ptr[i];
+            }
+            for (int i = tid; i < n; i += T) {
+                col[i] = tg.flops[i]; col[n + i] = tg.gpu[i]; col[2 * n + i] = tg.cpu[i]; col[3 * n + i] = tg.disk[i];
+            }
+            const bool stage_edges = E <= e_max;
+            if (stage_edges)
+                for (int e = tid; e < E; e += T) { esrc[e] = tg.edge_src[e]; em[e] = tg.edge_m[e]; }
+            for (int w = tid; w < p; w += T) {
+                peer[w] = tg.speed[w]; peer[p + w] = tg.cap_gpu[w]; peer[2 * p + w] = tg.cap_cpu[w];
+                peer[3 * p + w] = tg.cap_disk[w];
+            }
+            t.pre_flops = pre; t.pre_gpu = pre + n1; t.pre_cpu = pre + 2 * n1; t.pre_disk = pre + 3 * n1;
+            t.flops = col; t.gpu = col + n; t.cpu = col + 2 * n; t.disk = col + 3 * n;
+            t.edge_ptr = eptr;
+            if (stage_edges) { t.edge_src = esrc; t.edge_m = em; }
+            t.speed = peer; t.cap_gpu = peer + p; t.cap_cpu = peer + 2 * p; t.cap_disk = peer + 3 * p;
+        }
+        __syncthreads();
+        for (int it = tid; it < n * p; it += T) {              // _fits break points (:313-315)
+            const int i = it / p, wi = it % p;
+            int j = i + 1;
+            while (j <= n && fits_range(t, wi, i, j)) ++j;
+            jlim[i * p + wi] = (int16_t)j;
+        }
+        for (int it = tid; it < n * p; it += T) {              // chunk_cost (:294-302) per (i, worker)
+            const int i = it / p, wi = it % p;
+            const double speed = t.speed[wi];
+            double rd = 0.0;                                    // the read grows stage by stage, in the
+            for (int j = i + 1; j <= n; ++j) {                  // reference's (stage, edge) order
+                if (include_comm(t))
+                    for (int e = t.edge_ptr[j - 1]; e < t.edge_ptr[j]; ++e)
+                        if (t.edge_src[e] < i) rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
+                const double fl = col_range(t.flops, t.pre_flops, flops_exact(t), i, j, np_flops(t));
+                cc[(size_t)dpw_pair(i, j, n) * p + wi] = fl / speed + rd;
+            }
+        }
+        for (int it = tid; it < n1 * S; it += T) back[it] = -1;
+        __syncthreads();
+        if (tid == 0) { mk[0] = 0.0; back[0] = 0; }
+        __syncthreads();
+        // levels: warp w owns masks w*MPW .. w*MPW + MPW - 1, G lanes per mask
+        const int W = T >> 5;
+        const int MPW = S >= W ? S / W : 1;
+        const int G = 32 / MPW;
+        const int M = wid * MPW + lane / G, g = lane % G;
+        const bool mvalid = M < S;
+        const int pc = mvalid ? __popc(M) : 0;
+        for (int j = 1; j <= n; ++j) {
+            double bv = 0.0;
+            int bsec = 0x7fffffff, bsrc = -1;
+            if (mvalid && pc >= 1 && pc <= j) {
+                for (int i = g; i < j; i += G) {
+                    const double* crow = cc + (size_t)dpw_pair(i, j, n) * p;
+                    for (uint32_t mm = (uint32_t)M; mm; mm &= mm - 1) {
+                        const int wi = __ffs(mm) - 1;
+                        const int src = i * S + (M ^ (1 << wi));
+                        const int32_t bk = back[src];
+                        const int jl = jlim[i * p + wi];
+                        const double m0 = mk[src], c = crow[wi];
+                        const double v = c > m0 ? c : m0;      // max(mk, chunk_cost) :316
+                        const int sec = i * 64 + (63 - wi);
+                        if (bk >= 0 && j < jl && (bsrc < 0 || key_less(v, sec, bv, bsec))) {
+                            bv = v; bsec = sec; bsrc = (i << 8) | wi;
+                        }
+                    }
+                }
+            }
+            for (int off = 1; off < G; off <<= 1) {             // combine the G lanes of this mask
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int osec = __shfl_xor_sync(0xffffffffu, bsec, off);
+                const int osrc = __shfl_xor_sync(0xffffffffu, bsrc, off);
+                if (osrc >= 0 && (bsrc < 0 || key_less(ov, osec, bv, bsec))) { bv = ov; bsec = osec; bsrc = osrc; }
+            }
+            if (mvalid && g == 0 && bsrc >= 0) { mk[j * S + M] = bv; back[j * S + M] = bsrc; }
+            __syncthreads();
+        }
+        if (wid == 0) {                                      // finals (:321-325), traceback
+            double bv = 0.0;
+            long long bm = -1;
+            if (lane < S && back[n * S + lane] >= 0) { bv = mk[n * S + lane]; bm = lane; }
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_down_sync(0xffffffffu, bv, off);
+                const long long om = __shfl_down_sync(0xffffffffu, bm, off);
+                if (om >= 0 && (bm < 0 || ov < bv || (ov == bv && om < bm))) { bv = ov; bm = om; }
+            }
+            int16_t* own = out_owner + (size_t)sc * n_max;
+            for (int i = lane; i < n_max; i += 32) own[i] = -1;
+            __syncwarp();
+            if (lane == 0) {
+                if (bm >= 0) {
+                    int j = n;
+                    int Mm = (int)bm;
+                    while (j > 0) {
+                        const int32_t bb = back[j * S + Mm];
+                        const int i = bb >> 8, wi = bb & 0xff;
+                        for (int s2 = i; s2 < j; ++s2) own[s2] = (int16_t)wi;
+                        Mm &= ~(1 << wi);
+                        j = i;
+                    }
+                    out_mk[sc] = bv;
+                    out_found[sc] = 1;
+                } else {
+                    out_mk[sc] = __longlong_as_double(0x7ff0000000000000LL);
+                    out_found[sc] = 0;
+                }
+            }
+        }
+    }
+}
+
 }  // namespace dm
 
 extern "C" {
@@ -361,6 +507,22 @@ int dm_subset_dp(const dm_tables* tables, int32_t n_scen, int32_t n_max, int32_t
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+
+            // a batch too small to fill the GPU with one warp per DP (the C1
+            // link grid) runs one 4-warp CTA per DP: shorter per-DP latency
+            const size_t per_dp = dm::dpw_bytes(n_max, p_max, e_max);
+            const char* cta = std::getenv("DM_DP_CTA");
+            const bool use_cta = cta ? cta[0] == '1' : (int64_t)n_scen * dm::kDpCtaWarps <= (int64_t)sms * 32;
+            if (use_cta) {
+                const int per_sm_c = (int)((220 * 1024) / (per_dp + 1024));
+                int64_t gridc = n_scen;
+                if (gridc > (int64_t)sms * per_sm_c) gridc = (int64_t)sms * per_sm_c;
+                cudaFuncSetAttribute(dm::subset_dp_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_dp);
+                dm::subset_dp_cta_kernel<<<(int)gridc, 32 * dm::kDpCtaWarps, per_dp, (cudaStream_t)stream>>>(
+                    tables, n_scen, n_max, p_max, e_max, out_owner, out_makespan, out_found);
+                DM_CHECK_LAUNCH();
+                return DM_OK;
+            }
             int64_t grid = (n_scen + dm::kDpWarps - 1) / dm::kDpWarps;
             const int per_sm = (int)((220 * 1024) / (per_cta + 1024));
             if (grid > (int64_t)sms * per_sm * 4) grid = (int64_t)sms * per_sm * 4;
