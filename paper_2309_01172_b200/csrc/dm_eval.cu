@@ -14,6 +14,7 @@
 #include "dm_abi_util.cuh"
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 namespace dm {
 
@@ -580,39 +581,43 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
     StreamWin win;
     win.mk = __longlong_as_double(0x7ff0000000000000LL); win.rank = -1; win.n_feas = 0; win.csum = 0;
     uint32_t n_seen = 0;
-    int st = 0;
-    uint32_t parity = 0;
-    for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x) {
-        const int64_t c0 = tl * tile_cand;
-        const int cnt = (int)((n_cand - c0) < tile_cand ? (n_cand - c0) : tile_cand);
-        unsigned char* tile = tiles + st * L.tile_bytes;
-        if (tl < full_tiles) {
-            mbar_wait(&bars[st], parity);
-        } else {  // ragged last tile: plain loads
-            for (int b = tid; b < cnt * n; b += blockDim.x) tile[b] = owner[c0 * n + b];
-            __syncthreads();
-        }
-        const uint32_t tile_s = sm_s + (uint32_t)(tile - sm);
-        switch (nw) {     // the boundary-mask width is fixed per launch: one dispatch per tile
-#define DM_STREAM_TILE(W)                                                                              \
-            case W: stream_tile<PAIR, SQUARE, NT, W>(t, X, tile_s, tile, cnt, c0, out_mk, out_code, rank_base, \
-                                                     partial != nullptr, win, n_seen); break;
-            DM_STREAM_TILE(1) DM_STREAM_TILE(2) DM_STREAM_TILE(3) DM_STREAM_TILE(4) DM_STREAM_TILE(5)
-            DM_STREAM_TILE(6) DM_STREAM_TILE(7) DM_STREAM_TILE(8) DM_STREAM_TILE(9) DM_STREAM_TILE(10)
-            DM_STREAM_TILE(11) DM_STREAM_TILE(12) DM_STREAM_TILE(13) DM_STREAM_TILE(14) DM_STREAM_TILE(15)
-            default: stream_tile<PAIR, SQUARE, NT, 16>(t, X, tile_s, tile, cnt, c0, out_mk, out_code, rank_base,
-                                                       partial != nullptr, win, n_seen); break;
-#undef DM_STREAM_TILE
-        }
-        __syncthreads();  // every thread is done with this slot
-        if (tid == 0) {
-            int64_t nt = tl + (int64_t)stages * gridDim.x;
-            if (nt < full_tiles) {
-                mbar_expect_tx(&bars[st], tile_load);
-                tma_load_1d(tile, owner + nt * tile_cand * n, tile_load, &bars[st]);
+    // the boundary-mask width is fixed per launch: one dispatch per CTA, the
+    // tile loop (TMA ring) instantiated per width
+    auto loop = [&](auto nw_tag) {
+        constexpr int W = decltype(nw_tag)::value;
+        int st = 0;
+        uint32_t parity = 0;
+        for (int64_t tl = blockIdx.x; tl < n_tiles; tl += gridDim.x) {
+            const int64_t c0 = tl * tile_cand;
+            const int cnt = (int)((n_cand - c0) < tile_cand ? (n_cand - c0) : tile_cand);
+            unsigned char* tile = tiles + st * L.tile_bytes;
+            if (tl < full_tiles) {
+                mbar_wait(&bars[st], parity);
+            } else {  // ragged last tile: plain loads
+                for (int b = tid; b < cnt * n; b += blockDim.x) tile[b] = owner[c0 * n + b];
+                __syncthreads();
             }
+            const uint32_t tile_s = sm_s + (uint32_t)(tile - sm);
+            stream_tile<PAIR, SQUARE, NT, W>(t, X, tile_s, tile, cnt, c0, out_mk, out_code, rank_base,
+                                             partial != nullptr, win, n_seen);
+            __syncthreads();  // every thread is done with this slot
+            if (tid == 0) {
+                int64_t nt = tl + (int64_t)stages * gridDim.x;
+                if (nt < full_tiles) {
+                    mbar_expect_tx(&bars[st], tile_load);
+                    tma_load_1d(tile, owner + nt * tile_cand * n, tile_load, &bars[st]);
+                }
+            }
+            if (++st == stages) { st = 0; parity ^= 1u; }
         }
-        if (++st == stages) { st = 0; parity ^= 1u; }
+    };
+    switch (nw) {
+#define DM_STREAM_LOOP(W) case W: loop(std::integral_constant<int, W>{}); break;
+        DM_STREAM_LOOP(1) DM_STREAM_LOOP(2) DM_STREAM_LOOP(3) DM_STREAM_LOOP(4) DM_STREAM_LOOP(5)
+        DM_STREAM_LOOP(6) DM_STREAM_LOOP(7) DM_STREAM_LOOP(8) DM_STREAM_LOOP(9) DM_STREAM_LOOP(10)
+        DM_STREAM_LOOP(11) DM_STREAM_LOOP(12) DM_STREAM_LOOP(13) DM_STREAM_LOOP(14) DM_STREAM_LOOP(15)
+        default: loop(std::integral_constant<int, 16>{}); break;
+#undef DM_STREAM_LOOP
     }
     if (partial) {
         Win w;
