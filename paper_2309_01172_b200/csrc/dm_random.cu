@@ -61,7 +61,12 @@ struct Feistel {
         return (L << h) | R;
     }
     __device__ __forceinline__ uint32_t operator()(uint32_t q) const {
+        // cycle walking: a second step is needed for ~1 - n/2^2h of the lanes,
+        // i.e. by some lane of almost every warp — take it branch-free for all
+        // lanes and keep the loop for the rare third step
         uint32_t x = once(q);
+        const uint32_t y = once(x);
+        x = x < n ? x : y;
         while (x >= n) x = once(x);
         return x;
     }
@@ -148,6 +153,7 @@ __global__ void __launch_bounds__(kRandThreads, 4) random_warp_kernel(dm_tables 
             r = 1 + (int)mulhi32(g.next(), rmax);
             uint32_t need = (uint32_t)(r - 1);
             unsigned char* dst = myrow;
+#pragma unroll 4
             for (int pos = 1; pos < n && need; ++pos) {
                 const uint32_t cut = mulhi32(g.next(), (uint32_t)(n - pos)) < need ? 1u : 0u;
                 *dst = (unsigned char)pos;          // kept only when this position is a cut
