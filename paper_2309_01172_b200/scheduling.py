@@ -41,13 +41,14 @@ def _check_inputs(stages, workers):
         raise T.SchedulingError("empty fleet: no schedulable peers")
 
 
-def _encode_runs(host, runs):
+def _encode_runs(host, runs, str_keys: bool = True):
     """Runs -> [(peer index, sorted indices)]; unknown peers get indices >= P
     (distinct per distinct id, so 'holds two runs' and link_between's
-    same-peer test keep working).  A key that is not a fleet id but whose
-    str() is (e.g. int 1 for '1') is costed as that peer, as fleet.peer()
-    str-converts (hardware.py:122-126); its 'unknown peer' verdict is restored
-    by _verify_host."""
+    same-peer test keep working).  str_keys: a key that is not a fleet id
+    but whose str() is (e.g. int 1 for '1') maps to that peer, as
+    fleet.peer() str-converts for costing (hardware.py:122-126); with
+    str_keys=False it stays unknown, as verify_assignment's `peer not in
+    fleet.peers` sees it (:187-188)."""
     unknown: dict = {}
     out = []
     n = host.n
@@ -55,7 +56,7 @@ def _encode_runs(host, runs):
         key = peer
         if key in host.index_of:
             pi = host.index_of[key]
-        elif str(key) in host.index_of:
+        elif str_keys and str(key) in host.index_of:
             pi = host.index_of[str(key)]
         else:
             pi = unknown.setdefault(key, host.P + len(unknown))
@@ -65,6 +66,10 @@ def _encode_runs(host, runs):
                 raise IndexError("list index out of range")
         out.append((pi, sidx))
     return out
+
+
+def _mixed_keys(host, runs) -> bool:
+    return any(peer not in host.index_of and str(peer) in host.index_of for peer, _ in runs)
 
 
 def _raise_cost_error(stages, fleet, runs, include_comm):
@@ -174,42 +179,16 @@ def _report(stages, fleet, runs, include_comm, trace, res, c=0, host=None):
                             include_comm=include_comm, trace=trace)
 
 
-def _verify_host(stages, fleet, runs):
-    """verify_assignment's (code, run) (scheduling.py:179-207) for Runs whose
-    peer keys are not all fleet ids (the device verdict keys peers by index)."""
-    seen, used = set(), set()
-    for r, (peer, indices) in enumerate(runs):
-        if not indices:
-            continue
-        if peer in used:
-            return _lib.DM_V_TWO_RUNS, r
-        used.add(peer)
-        if peer not in fleet.peers:
-            return _lib.DM_V_UNKNOWN_PEER, r
-        ordered = sorted(indices)
-        if ordered != list(range(ordered[0], ordered[-1] + 1)):
-            return _lib.DM_V_NOT_CONTIGUOUS, r
-        for i in ordered:
-            if i in seen:
-                return _lib.DM_V_ASSIGNED_TWICE, r
-            seen.add(i)
-        p = fleet.peer(peer)
-        for code, dim in ((_lib.DM_V_GPU, "gpu"), (_lib.DM_V_CPU, "cpu"), (_lib.DM_V_DISK, "disk")):
-            if sum(getattr(stages[i], f"{dim}_bytes") for i in ordered) > getattr(p, f"{dim}_bytes"):
-                return code, r
-    if len(seen) != len(stages):
-        return _lib.DM_V_UNASSIGNED, -1
-    return _lib.DM_V_OK, -1
-
-
 def _evaluate_many(stages, fleet, runs_list, include_comm, traces, host=None):
     """Score several candidate Runs of one instance in one dm_eval_runs launch."""
     host = host or build_host(stages, fleet, include_comm)
     enc = [_encode_runs(host, runs) for runs in runs_list]
     res = engine.eval_runs(host, enc)
-    for c, runs in enumerate(runs_list):
-        if any(peer not in host.index_of and str(peer) in host.index_of for peer, _ in runs):
-            res["code"][c], res["code_run"][c] = _verify_host(stages, fleet, tuple(runs))
+    mixed = [c for c, runs in enumerate(runs_list) if _mixed_keys(host, runs)]
+    if mixed:                     # verdicts with the raw keys (a second launch, rare)
+        raw = engine.eval_runs(host, [_encode_runs(host, runs_list[c], str_keys=False) for c in mixed])
+        for i, c in enumerate(mixed):
+            res["code"][c], res["code_run"][c] = raw["code"][i], raw["code_run"][i]
     out = []
     for c, runs in enumerate(runs_list):
         if int(res["status"][c]) != _lib.DM_OK:
@@ -244,9 +223,7 @@ def verify_assignment(stages, fleet, runs) -> str:
     stages = list(stages)
     runs = tuple(runs)
     host = build_host(stages, fleet, include_comm=False)
-    res = engine.eval_runs(host, [_encode_runs(host, runs)])
-    if any(peer not in host.index_of and str(peer) in host.index_of for peer, _ in runs):
-        res["code"][0], res["code_run"][0] = _verify_host(stages, fleet, runs)
+    res = engine.eval_runs(host, [_encode_runs(host, runs, str_keys=False)])
     return _reason(stages, fleet, runs, int(res["code"][0]), int(res["code_run"][0]))
 
 
