@@ -346,7 +346,8 @@ __device__ __forceinline__ double lds_f64s(uint32_t a) {
 }
 
 // Run-boundary mask of one owner row (NW 32-bit words, row starting `sh`
-// bits into the first aligned word): bit i-1 <=> owner[i] != owner[i-1].
+// bits into the first aligned word): bit i <=> owner[i] != owner[i-1] (bit 0
+// is always clear).
 // Fully unrolled per word count so every shift is a compile-time constant.
 template <int NW>
 __device__ __forceinline__ unsigned long long boundary_mask(uint32_t waddr, int sh) {
@@ -358,11 +359,15 @@ __device__ __forceinline__ unsigned long long boundary_mask(uint32_t waddr, int 
         cur = nxt;
         uint32_t x = wd ^ __byte_perm(prevw, wd, 0x6543);    // byte k vs byte k-1
         uint32_t nz = (x | ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu)) & 0x80808080u;
-        uint32_t nib = (nz * 0x00204081u) >> 28;             // bit k <=> byte k differs
-        if (j < 8) m0 |= nib << (4 * j); else m1 |= nib << (4 * j - 32);
+        // bit k <=> byte k differs: the four flags gathered by one multiply
+        // (high word; the product's terms are disjoint, so no carries), and
+        // accumulated with multiply-adds — both on the FMA pipe, the ALU pipe
+        // being the kernel's busiest
+        const uint32_t nib = __umulhi(nz, 0x02040810u) & 0xFu;
+        if (j < 8) m0 = nib * (1u << (4 * j)) + m0; else m1 = nib * (1u << (4 * j - 32)) + m1;
         prevw = wd;
     }
-    return (((unsigned long long)m1 << 32) | m0) >> 1;
+    return ((unsigned long long)m1 << 32) | m0;           // bit i <=> owner[i] != owner[i-1]
 }
 
 // Per-launch constants of the stream kernel's candidate loop.
@@ -440,13 +445,13 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
             for (uint32_t y = (uint32_t)(bm >> 32) & X.mask_hi; y; ) {
                 const uint32_t k = 31u - __clz(y);
                 y ^= 1u << k;
-                run(33u + k);
+                run(32u + k);
             }
         if (PAIR) {
             for (uint32_t y = (uint32_t)bm & X.mask_lo; y; ) {
                 const uint32_t k = 31u - __clz(y);
                 y ^= 1u << k;
-                run(1u + k);
+                run(k);
             }
         } else {
             // two runs per step: both owner-byte and table loads in flight
@@ -468,13 +473,13 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
             for (uint32_t y = (uint32_t)bm & X.mask_lo; y; ) {
                 const uint32_t k1 = 31u - __clz(y);
                 y ^= 1u << k1;
-                const uint32_t b1 = 1u + k1;
+                const uint32_t b1 = k1;
                 uint32_t w1, a1;
                 double v1;
                 if (y) {
                     const uint32_t k2 = 31u - __clz(y);
                     y ^= 1u << k2;
-                    const uint32_t b2 = 1u + k2;
+                    const uint32_t b2 = k2;
                     uint32_t w2, a2;
                     double v2;
                     fetch(b1, end, w1, a1, v1);
@@ -576,8 +581,10 @@ __global__ void __launch_bounds__(NT, MINB) eval_owner_stream_kernel(dm_tables t
     X.n = n; X.uP = (uint32_t)P; X.rowstride = (uint32_t)(n + 1) * X.uP;
     X.T_s = T_s; X.C_s = C_s; X.tri_k = 2u * (uint32_t)n + 1u;
     X.pmask = P >= 32 ? 0u : ~((1u << P) - 1u);
-    X.mask_lo = n - 1 >= 32 ? 0xffffffffu : ((1u << (n - 1)) - 1u);
-    X.mask_hi = n - 1 >= 64 ? 0xffffffffu : (n - 1 > 32 ? ((1u << (n - 33)) - 1u) : 0u);
+    // boundary positions 1..n-1: bits 1..min(n-1, 31) of the low word, bits
+    // 0..n-33 of the high word
+    X.mask_lo = n >= 32 ? 0xfffffffeu : (((1u << n) - 1u) & ~1u);
+    X.mask_hi = n - 32 >= 32 ? 0xffffffffu : (n > 32 ? ((1u << (n - 32)) - 1u) : 0u);
     StreamWin win;
     win.mk = __longlong_as_double(0x7ff0000000000000LL); win.rank = -1; win.n_feas = 0; win.csum = 0;
     uint32_t n_seen = 0;
