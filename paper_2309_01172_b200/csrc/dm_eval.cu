@@ -782,6 +782,7 @@ static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner
                             : dm::eval_owner_stream_kernel<false, SQ == 1, NT, MB>;
             DM_PICK(256, 4, 1) DM_PICK(256, 3, 1) DM_PICK(256, 2, 1) DM_PICK(512, 2, 1) DM_PICK(128, 8, 1)
             DM_PICK(768, 1, 0) DM_PICK(512, 1, 0) DM_PICK(1024, 1, 0) DM_PICK(256, 2, 0) DM_PICK(256, 3, 0)
+            DM_PICK(384, 1, 0) DM_PICK(256, 1, 0)
 #undef DM_PICK
             if (!kern) return dmabi::fail(DM_E_ARG, "dm_eval_owner: unsupported DM_MODEA_CFG");
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes);
