@@ -221,34 +221,45 @@ def run_b200(args, rank, world, local_rank):
     res = merge(_gather_records(kernels.out, world).cpu().numpy())
 
     # ---- e2e: the public API from Python objects every step —
-    # search.split_sweep(stages, fleets): tensorise the fleets (stage side
-    # cached), pack into pinned memory, one captured graph (H2D of the
-    # tables, the sweep kernels, D2H of the winner records), host sync,
-    # winners read; multi-GPU: + the NCCL all-gather and the merge
+    # search.SplitSweeper (the pipelined serving form of split_sweep):
+    # tensorise the fleets (stage side cached), pack them into pinned memory
+    # and replay one captured graph (H2D of the tables, the sweep kernels,
+    # D2H of the winner records) — the host prepares request k+1 while the
+    # GPU runs request k — then wait for and read the winners (+ the NCCL
+    # all-gather and the merge at N>1)
     mine = [fleets[sc] for sc, _, _ in units]
     whole = all(u[2] == 1 for u in units)
+    sweeper = search.SplitSweeper(stages, mine) if whole else None
 
-    def api_step():
-        if whole:
-            recs = search.split_sweep(stages, mine, records=True)
-        else:
-            recs = search.split_sweep(stages, fleets, part=rank, nparts=world, records=True)
+    def finish(recs):
         if world > 1:
             recs = _gather_records(torch.from_numpy(recs).to(dev), world).cpu().numpy()
         else:
             recs = recs.reshape(1, len(units), -1)
         return merge(recs)
-    for _ in range(max(args.warmup, 3)):
-        api_step()
+
+    def run_e2e(steps):
+        if sweeper is None:          # block parts of every scenario: one synchronous call per step
+            out = None
+            for _ in range(steps):
+                out = finish(search.split_sweep(stages, fleets, part=rank, nparts=world, records=True))
+            return out
+        prev = sweeper.submit(mine)
+        out = None
+        for k in range(steps):
+            nxt = sweeper.submit(mine) if k + 1 < steps else None
+            out = finish(sweeper.result(prev, records=True))
+            prev = nxt
+        return out
+    run_e2e(max(args.warmup, 3))
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        e2e_res = api_step()
+    e2e_res = run_e2e(args.steps)
     e1.record(stream)
     barrier()
     e2e_ms = _max_over_ranks([e0.elapsed_time(e1)], dev, world)[0]
-    g_api = next(iter(search._GRAPHS.values()))
+    g_api = sweeper.graphs[0] if sweeper is not None else next(iter(search._GRAPHS.values()))
     e2e_h2d, e2e_d2h = int(g_api.batch.h2d_bytes), int(g_api.d2h_bytes)
     assert [(r["makespan"], r["rank"], r["checksum"]) for r in e2e_res] == \
         [(r["makespan"], r["rank"], r["checksum"]) for r in res], "public API and device-timed sweeps differ"
@@ -292,8 +303,9 @@ def run_b200(args, rank, world, local_rank):
         "config": workload_config(total, links),
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d * (1 if whole else 1),
                 "d2h_bytes_per_step": e2e_d2h,
-                "path": "search.split_sweep(stages, fleets) per step from the reference's Stage/Fleet objects: "
-                        "tensorise + pack + H2D + sweep kernels + D2H + host sync (+ NCCL all-gather at N>1)"},
+                "path": "search.SplitSweeper.submit/result per step from the reference's Stage/Fleet objects: "
+                        "tensorise + pack + H2D + sweep kernels + D2H + host wait (+ NCCL all-gather at N>1); "
+                        "request k+1 is tensorised while the GPU runs request k"},
         "gpu_launches": 5 * len(units) * args.steps,
         "roofline": {"bound": "issue", "achieved": achieved / 1e9, "peak": peak_pairs / 1e9, "unit": "Gpairs/s",
                      "frac": achieved / peak_pairs,

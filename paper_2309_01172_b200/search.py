@@ -41,6 +41,9 @@ def _graph_for(hosts, total, units):
     g = _GRAPHS.get(key)
     if g is not None and g.batch.repack(hosts):
         return g
+    if g is not None:                  # same shape, other scalars (e.g. default links): recapture
+        del _GRAPHS[key]
+        del g
     batch = engine.device_batch(hosts)
     g = engine.SweepGraph(batch, total, units=units)
     _GRAPHS[key] = g
@@ -77,3 +80,68 @@ def split_sweep(stages, fleets, *, include_comm: bool = True, part: int = 0, npa
         out.append(SplitWinner(runs, w["makespan"], int(w["rank"]), int(w["n_evaluated"]), int(w["n_feasible"]),
                                int(w["checksum"])))
     return out
+
+
+class SplitSweeper:
+    """Pipelined serving form of split_sweep for a stream of requests of one
+    shape (same stages, same number of fleets and workers): two slots, each a
+    pinned staging buffer + captured graph (H2D of the tables, the sweep
+    kernels, D2H of the winner records).  submit() tensorises and packs the
+    next request while the GPU still runs the previous one, then replays the
+    free slot's graph; result() waits for that request and decodes it.  Every
+    request still copies its own inputs in and its winners out."""
+
+    def __init__(self, stages, fleets_example, *, include_comm: bool = True, slots: int = 2):
+        torch = engine._torch()
+        self.stages = list(stages)
+        self.include_comm = include_comm
+        hosts = [build_host(self.stages, f, include_comm) for f in fleets_example]
+        self.n, self.p = len(self.stages), hosts[0].p
+        self.total = splits_total(self.n, self.p)
+        units = [(i, 0, 1) for i in range(len(hosts))]
+        self.graphs = []
+        for _ in range(slots):
+            g = engine.SweepGraph(engine.device_batch(hosts), self.total, units=units)
+            self.graphs.append(g)
+        self.events = [None] * slots
+        self.hosts = [None] * slots
+        self.next = 0
+        self.stream = torch.cuda.current_stream()
+
+    def submit(self, fleets) -> int:
+        torch = engine._torch()
+        slot = self.next
+        self.next = (slot + 1) % len(self.graphs)
+        hosts = [build_host(self.stages, f, self.include_comm) for f in fleets]   # overlaps the GPU's work
+        if self.events[slot] is not None:
+            self.events[slot].synchronize()          # the slot's previous request has left its buffers
+        g = self.graphs[slot]
+        if not g.batch.repack(hosts):
+            # other scalars (default link, flags) or shapes than the captured
+            # graph: recapture this slot on the request's tables
+            g = self.graphs[slot] = engine.SweepGraph(engine.device_batch(hosts), self.total,
+                                                      units=[(i, 0, 1) for i in range(len(hosts))])
+        g.launch()
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        self.events[slot] = ev
+        self.hosts[slot] = hosts
+        return slot
+
+    def result(self, slot: int, records: bool = False):
+        self.events[slot].synchronize()
+        g = self.graphs[slot]
+        if records:
+            return g.host_out.numpy().copy()
+        out = []
+        raw = g.host_out.numpy().tobytes()
+        from . import _lib
+        for i, h in enumerate(self.hosts[slot]):
+            w = _lib.DmWinner.from_buffer_copy(raw[i * _lib.C.sizeof(_lib.DmWinner):(i + 1) * _lib.C.sizeof(_lib.DmWinner)])
+            runs = ()
+            if w.rank >= 0:
+                bounds, peers = engine.unrank(self.n, self.p, int(w.rank), "splits")
+                runs = tuple((h.peer_ids[peers[q]], tuple(range(bounds[q], bounds[q + 1]))) for q in range(len(peers)))
+            out.append(SplitWinner(runs, w.makespan, int(w.rank), int(w.n_evaluated), int(w.n_feasible),
+                                   int(w.checksum)))
+        return out

@@ -342,10 +342,18 @@ class DeviceBatch:
         """Re-tensorised instances of the same shapes into the existing pinned
         staging buffer and records (the device addresses stay valid, so a
         captured graph that copies host_buf -> dev_buf can be replayed on the
-        new inputs).  Returns False when a shape differs."""
+        new inputs).  Returns False when a shape or a scalar field of a record
+        differs (the caller then builds a new batch / graph)."""
         hosts = list(hosts)
         if len(hosts) != len(self.hosts) or any(a.packed_size() != b.packed_size() for a, b in zip(hosts, self.hosts)):
             return False
+        # kernels receive dm_tables BY VALUE: a captured graph holds the scalar
+        # fields (sizes, flags, default link) of the records it was captured
+        # with, so only the device-resident columns may change
+        for a, b in zip(hosts, self.hosts):
+            if (a.n, a.p, a.P, a.flags, a.def_alpha, a.def_beta, int(a.arrays["edge_src"].size)) != \
+                    (b.n, b.p, b.P, b.flags, b.def_alpha, b.def_beta, int(b.arrays["edge_src"].size)):
+                return False
         hb = self.host_buf.numpy()
         base = 0
         dev_base = int(self.dev_buf.data_ptr())

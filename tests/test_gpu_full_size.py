@@ -195,12 +195,31 @@ def test_split_sweep_public_api(c2):
     stages = CF.model_stages("llama2-7b-layers")
     idx = sorted(int(s) for s in GOLD["c2"])
     fleets = [CF.load(CF.c2_fleet_doc(0, *CF.C2_LINKS[i])) for i in idx]
-    for _ in range(2):                                   # second call: graph replay on repacked inputs
-        res = search.split_sweep(stages, fleets)
-        for i, w in zip(idx, res):
+    for rev in (False, False, True):    # replay on repacked inputs; reordered fleets (other default links)
+        res = search.split_sweep(stages, fleets[::-1] if rev else fleets)
+        for i, w in zip(idx[::-1] if rev else idx, res):
             want = GOLD["c2"][str(i)]
             assert (w.makespan, w.rank, w.n_evaluated, w.n_feasible, w.checksum) == tuple(want[k] for k in KEYS)
             assert S.evaluate_runs(stages, fleets[idx.index(i)], w.runs).makespan == want["makespan"]
     parts = [search.split_sweep(stages, fleets[:1], part=k, nparts=2, records=True) for k in range(2)]
     m = D.merge_records(np.stack([p_[0] for p_ in parts]))
     assert {k: m[k] for k in KEYS} == _w(GOLD["c2"][str(idx[0])])
+
+
+def test_split_sweeper_pipelined(c2):
+    """search.SplitSweeper (two slots, request k+1 prepared while k runs):
+    every request's winners equal the pinned ones."""
+    from paper_2309_01172_b200 import configs as CF, search
+    stages = CF.model_stages("llama2-7b-layers")
+    idx = sorted(int(s) for s in GOLD["c2"])
+    fleets = [CF.load(CF.c2_fleet_doc(0, *CF.C2_LINKS[i])) for i in idx]
+    sw = search.SplitSweeper(stages, fleets)
+    tickets = [sw.submit(fleets)]
+    for k in range(3):
+        tickets.append(sw.submit(fleets[::-1] if k % 2 == 0 else fleets))
+        res = sw.result(tickets[k])
+        order = idx if k % 2 == 0 else idx[::-1]
+        for i, w in zip(order, res):
+            want = GOLD["c2"][str(i)]
+            assert (w.makespan, w.rank, w.n_evaluated, w.n_feasible, w.checksum) == tuple(want[k_] for k_ in KEYS)
+    sw.result(tickets[-1])
