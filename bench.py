@@ -720,6 +720,23 @@ def api_latency_measure(dev):
                      "calls": len(times), "reference_ms_per_call": statistics.median(ref_times),
                      "same_report": rep.runs == ref.runs and rep.makespan == ref.makespan and rep.trace == ref.trace,
                      "makespan": rep.makespan, "trace": list(rep.trace)}
+    # evaluate_runs on C1's chosen runs (the reference's scoring entry point)
+    stages = CF.model_stages("gpt2-small")
+    fleet = CF.load(CF.c1_fleet_doc(10.0, 1e-3))
+    runs = S.schedule(stages, fleet).runs
+    for _ in range(3):
+        S.evaluate_runs(stages, fleet, runs)
+    times = []
+    for _ in range(50):
+        t0 = _t.perf_counter()
+        rep = S.evaluate_runs(stages, fleet, runs)
+        times.append((_t.perf_counter() - t0) * 1e3)
+    t0 = _t.perf_counter()
+    for _ in range(5):
+        ref = RS.evaluate_runs(stages, fleet, runs)
+    out["evaluate_runs_c1"] = {"ms_per_call": statistics.median(times), "ms_min": min(times),
+                               "reference_ms_per_call": (_t.perf_counter() - t0) * 1e3 / 5,
+                               "same_report": rep.makespan == ref.makespan and rep.runs == ref.runs}
     out["config"] = ("schedule() through the public API: C1 gpt2-small x 4 mixed GPUs (10 Gbit/s, 1 ms; exact subset "
                      "DP) and C3 llama2-70b x 256 workers with 32,640 pairwise links (proportional + hill climb); "
                      "reference = dagmesh.scheduling.schedule on the same objects")

@@ -165,6 +165,16 @@ DM_API int dm_eval_runs(const dm_tables* t, int32_t n_cand,
                  double* out_makespan, int32_t* out_code,
                  int32_t* out_code_run, int32_t* out_status, void* stream);
 
+/* dm_eval_runs_ws — dm_eval_runs with the total run count known to the
+ * caller and a caller workspace of dm_eval_runs_ws_bytes(n, n_cand,
+ * n_runs_total) bytes: stream-ordered with no host synchronisation and no
+ * allocation (the one-call API path). */
+DM_API int64_t dm_eval_runs_ws_bytes(int32_t n, int32_t n_cand, int32_t n_runs_total);
+DM_API int dm_eval_runs_ws(const dm_tables* t, int32_t n_cand, const int32_t* cand_ptr, const int32_t* run_peer,
+                           const int32_t* run_ptr, const int32_t* run_idx, int32_t n_runs_total,
+                           double* out_compute, double* out_read, double* out_makespan, int32_t* out_code,
+                           int32_t* out_code_run, int32_t* out_status, void* workspace, void* stream);
+
 /*
  * dm_eval_owner — Mode A scoring stream (the scoring-service form of
  * evaluate_runs).  Candidate c is the owner vector owner[c*n .. c*n+n-1]

@@ -91,6 +91,8 @@ _SIGS = {
     "dm_microbench_cross": (C.c_int, [C.c_int64, _P, _P, _P]),
     "dm_microbench_alu": (C.c_int, [C.c_int64, _P, _P, _P]),
     "dm_sched_out_bytes": (C.c_int64, [C.c_int32]),
+    "dm_eval_runs_ws_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "dm_eval_runs_ws": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "dm_schedule_report": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P]),
     "dm_sweep_timing": (C.c_int, [C.c_int32, _P, _P]),
     "dm_op_costs": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, _P, _P]),

@@ -713,6 +713,34 @@ int dm_eval_runs(const dm_tables* t, int32_t n_cand, const int32_t* cand_ptr, co
     return DM_OK;
 }
 
+int64_t dm_eval_runs_ws_bytes(int32_t n, int32_t n_cand, int32_t n_runs_total) {
+    if (n <= 0 || n_cand < 0 || n_runs_total < 0) return -1;
+    const size_t b_owner = (size_t)n_cand * n * sizeof(int32_t);
+    const size_t b_seen = ((size_t)n_cand * n + 15) & ~(size_t)15;
+    return (int64_t)(b_owner + b_seen + (size_t)(n_runs_total + 1) * sizeof(int32_t));
+}
+
+int dm_eval_runs_ws(const dm_tables* t, int32_t n_cand, const int32_t* cand_ptr, const int32_t* run_peer,
+                    const int32_t* run_ptr, const int32_t* run_idx, int32_t n_runs_total, double* out_compute,
+                    double* out_read, double* out_makespan, int32_t* out_code, int32_t* out_code_run,
+                    int32_t* out_status, void* workspace, void* stream) {
+    if (!t || n_cand < 0 || !cand_ptr || !run_peer || !run_ptr || t->n <= 0 || n_runs_total < 0 || !workspace)
+        return dmabi::fail(DM_E_ARG, "dm_eval_runs_ws: bad arguments");
+    if (n_cand == 0) return DM_OK;
+    const size_t b_owner = (size_t)n_cand * t->n * sizeof(int32_t);
+    const size_t b_seen = ((size_t)n_cand * t->n + 15) & ~(size_t)15;
+    int32_t* ws_owner = (int32_t*)workspace;
+    uint8_t* ws_seen = (uint8_t*)workspace + b_owner;
+    int32_t* ws_order = (int32_t*)((uint8_t*)workspace + b_owner + b_seen);
+    const int threads = 128, blocks = (n_cand + threads - 1) / threads;
+    dm::eval_runs_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(*t, n_cand, cand_ptr, run_peer, run_ptr,
+                                                                       run_idx, out_compute, out_read, out_makespan,
+                                                                       out_code, out_code_run, out_status, ws_owner,
+                                                                       ws_seen, ws_order);
+    DM_CHECK_LAUNCH();
+    return DM_OK;
+}
+
 static int eval_owner_impl(const dm_tables* t, int64_t n_cand, const void* owner, int32_t owner_bytes,
                            double* out_makespan, uint8_t* out_code, int64_t rank_base, dm_winner* out,
                            void* scratch, void* stream);

@@ -43,10 +43,14 @@ def eval_runs(hosts_or_batch, runs_per_cand, *, index: int = 0):
     """Score candidate Runs of ONE instance with dm_eval_runs.
 
     runs_per_cand: list (one per candidate) of lists of (peer_index, sorted
-    tuple of stage indices).  Returns dict of numpy arrays."""
+    tuple of stage indices).  Returns dict of numpy arrays.  A HostTables
+    instance goes through the per-thread ScheduleSlot (one H2D of tables and
+    runs, one launch, one D2H)."""
+    if isinstance(hosts_or_batch, HostTables):
+        return schedule_slot().eval_runs(hosts_or_batch, runs_per_cand)
     lib = _lib.load()
     torch = _torch()
-    batch = hosts_or_batch if isinstance(hosts_or_batch, DeviceBatch) else device_batch([hosts_or_batch], pin=False)
+    batch = hosts_or_batch
     n_cand = len(runs_per_cand)
     cand_ptr = [0]
     run_peer, run_ptr, run_idx = [], [0], []
@@ -209,26 +213,79 @@ class ScheduleSlot:
             sb = int(lib.dm_subset_dp_scratch_bytes(self.n_cap, min(self.p_cap, 20), 1))
             self.scratch = torch.empty(max(sb, 256), dtype=torch.uint8, device=self.device)
 
-    def upload(self, host: HostTables) -> int:
-        """Pack `host` and its dm_tables record into the pinned buffer, start
-        one H2D copy; returns the device address of the record."""
+    def upload(self, host: HostTables, extra: np.ndarray | None = None, dev_extra: int = 0):
+        """Pack `host`, its dm_tables record and `extra` (int32 payload) into
+        the pinned buffer, start one H2D copy; returns (device address of the
+        record, struct, device address of the payload, device address of
+        `dev_extra` scratch bytes after it)."""
         size = host.packed_size()
         rec_off = (size + 255) // 256 * 256
-        self._grow(rec_off + C.sizeof(_lib.DmTables), host.n, host.p)
+        ext_off = rec_off + 256
+        ext_bytes = 0 if extra is None else extra.nbytes
+        scr_off = (ext_off + ext_bytes + 255) // 256 * 256
+        self._grow(max(ext_off + ext_bytes, scr_off + dev_extra), host.n, host.p)
+        if scr_off + dev_extra > self.dev.numel():
+            self.dev = _torch().empty(scr_off + dev_extra, dtype=_torch().uint8, device=self.device)
         hb = self.host.numpy()
         offs = host.pack_into(hb, 0)
         rec = host.struct_record(offs, int(self.dev.data_ptr()))
         hb[rec_off: rec_off + C.sizeof(_lib.DmTables)] = np.frombuffer(rec.tobytes(), np.uint8)
-        total = rec_off + C.sizeof(_lib.DmTables)
+        if extra is not None:
+            hb[ext_off: ext_off + ext_bytes] = extra.view(np.uint8).reshape(-1)
+        total = ext_off + ext_bytes
         self.dev[:total].copy_(self.host[:total], non_blocking=True)
-        return int(self.dev.data_ptr()) + rec_off
+        base = int(self.dev.data_ptr())
+        self.last_struct = _lib.DmTables.from_buffer_copy(rec.tobytes())
+        return base + rec_off, base + ext_off, base + scr_off
+
+    def eval_runs(self, host: HostTables, runs_per_cand) -> dict:
+        """dm_eval_runs_ws on one instance: tables, record and the runs' CSR in
+        one H2D, outputs in one D2H."""
+        lib = _lib.load()
+        torch = _torch()
+        n_cand = len(runs_per_cand)
+        cand_ptr = [0]
+        run_peer, run_ptr, run_idx = [], [0], []
+        for runs in runs_per_cand:
+            for pe, idxs in runs:
+                run_peer.append(pe)
+                run_idx.extend(idxs)
+                run_ptr.append(len(run_idx))
+            cand_ptr.append(len(run_peer))
+        R = len(run_peer)
+        ints = np.concatenate([np.array(cand_ptr, np.int32), np.array(run_peer or [0], np.int32),
+                               np.array(run_ptr, np.int32), np.array(run_idx or [0], np.int32)])
+        o1 = len(cand_ptr)
+        o2 = o1 + max(R, 1)
+        o3 = o2 + len(run_ptr)
+        ws = int(lib.dm_eval_runs_ws_bytes(host.n, n_cand, R))
+        ws = (ws + 255) // 256 * 256
+        nf = 2 * max(R, 1) + n_cand
+        out_bytes = 8 * nf + 4 * 3 * n_cand
+        rec, ext, scr = self.upload(host, ints, ws + out_bytes)
+        out = scr + ws
+        s = _lib.stream_ptr()
+        _lib.check(lib.dm_eval_runs_ws(C.byref(self.last_struct), n_cand, ext, ext + 4 * o1, ext + 4 * o2,
+                                       ext + 4 * o3, R, out, out + 8 * max(R, 1), out + 16 * max(R, 1),
+                                       out + 8 * nf, out + 8 * nf + 4 * n_cand, out + 8 * nf + 8 * n_cand, scr, s))
+        if getattr(self, "ev_host", None) is None or self.ev_host.numel() < out_bytes:
+            self.ev_host = torch.empty(max(out_bytes, 4096), dtype=torch.uint8, pin_memory=True)
+        off = out - int(self.dev.data_ptr())
+        self.ev_host[:out_bytes].copy_(self.dev[off: off + out_bytes], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        raw = self.ev_host.numpy()[:out_bytes]
+        f = raw[: 8 * nf].view(np.float64)
+        i = raw[8 * nf:].view(np.int32)
+        return dict(compute=f[:R].copy(), read=f[max(R, 1): max(R, 1) + R].copy(),
+                    makespan=f[2 * max(R, 1):].copy(), code=i[:n_cand].copy(), code_run=i[n_cand: 2 * n_cand].copy(),
+                    status=i[2 * n_cand:].copy(), cand_ptr=np.array(cand_ptr))
 
     def schedule(self, host: HostTables, use_dp: bool, hill_after_dp: bool) -> dict:
         """schedule()'s search (scheduling.py:404-419) and the _evaluate of its
         result (:210-232) on the device; returns the decoded report record."""
         lib = _lib.load()
         s = _lib.stream_ptr()
-        rec = self.upload(host)
+        rec, _, _ = self.upload(host)
         n, p = host.n, host.p
         found = None
         owner = self.owner
