@@ -737,6 +737,26 @@ def api_latency_measure(dev):
     out["evaluate_runs_c1"] = {"ms_per_call": statistics.median(times), "ms_min": min(times),
                                "reference_ms_per_call": (_t.perf_counter() - t0) * 1e3 / 5,
                                "same_report": rep.makespan == ref.makespan and rep.runs == ref.runs}
+    # pipeline.sweep: bert-large (50 cells) on two fleets
+    # over a 12 x 10 link grid, n_b = 512 — the reference's own sweep beside it
+    from paper_2309_01172_b200 import pipeline as P
+    model = dagmesh.pipeline.build_bert_large()
+    fleets = [CF.load(CF.c1_fleet_doc(1.0, 5e-3)),
+              CF.load(CF.fleet_doc(CF.hetero_peers(8, 3), 5e-3, 1.0, name="hetero8"))]
+    bws = [float(x) for x in (0.1, 0.2, 0.5, 1, 2, 5, 10, 20, 50, 100, 200, 400)]
+    alphas = [i * 1e-3 for i in range(10)]
+    P.sweep(model, fleets, bws, alphas, 512)
+    t0 = _t.perf_counter()
+    got = P.sweep(model, fleets, bws, alphas, 512)
+    t_eng = (_t.perf_counter() - t0) * 1e3
+    t0 = _t.perf_counter()
+    want = dagmesh.pipeline.sweep(model, fleets, bws, alphas, 512)
+    t_ref = (_t.perf_counter() - t0) * 1e3
+    from dataclasses import astuple
+    out["sweep_bert_large"] = {"grid_points": len(fleets) * len(bws) * len(alphas), "ms_per_call": t_eng,
+                               "reference_ms_per_call": t_ref,
+                               "same_rows": [astuple(r) for r in got.rows] == [astuple(r) for r in want.rows]
+                               and got.infeasible == want.infeasible}
     out["config"] = ("schedule() through the public API: C1 gpt2-small x 4 mixed GPUs (10 Gbit/s, 1 ms; exact subset "
                      "DP) and C3 llama2-70b x 256 workers with 32,640 pairwise links (proportional + hill climb); "
                      "reference = dagmesh.scheduling.schedule on the same objects")
