@@ -164,6 +164,33 @@ struct SweepParams {
     int16_t order[kMitmMaxBlocks];    // the part's blocks, largest tiles first
 };
 
+// Where a sweep's side tables live.  One workspace (world = 1), or a pooled
+// sweep over `world` GPUs: entries [lo[q], lo[q+1]) of the concatenated
+// tables are built by rank q into ITS workspace, at the same offsets in every
+// workspace, and the sweep kernel of every rank loads each element from the
+// owner's workspace (peer memory over NVLink).
+constexpr int kPoolMax = 8;
+struct TabView {
+    int world;
+    int64_t lo[kPoolMax + 1];
+    const double* val[kPoolMax];
+    const uint8_t* bnd[kPoolMax];
+};
+
+template <bool POOL>
+__device__ __forceinline__ int tab_owner(const TabView& v, int64_t g) {
+    int q = 0;
+    if (POOL) {
+#pragma unroll
+        for (int k = 1; k < kPoolMax; ++k) q += (k < v.world && g >= v.lo[k]) ? 1 : 0;
+    }
+    return q;
+}
+template <bool POOL>
+__device__ __forceinline__ double tab_val(const TabView& v, int64_t g) { return __ldcg(v.val[tab_owner<POOL>(v, g)] + g); }
+template <bool POOL>
+__device__ __forceinline__ uint32_t tab_bnd(const TabView& v, int64_t g) { return __ldcg(v.bnd[tab_owner<POOL>(v, g)] + g); }
+
 // Feasibility histogram of the side tables: finite entries per (table,
 // boundary position); the sweep orders its tiles by the feasible pairs this
 // predicts (an upper bound) instead of the raw tile size.
@@ -264,19 +291,19 @@ struct Blk {
     int32_t rrow;      // image index of T[j][c][0] (right sides)
 };
 
-__device__ __forceinline__ double left_val(const MitmCtx& x, const Blk& B, const double* val, const uint8_t* bnd,
-                                           int64_t e) {
+template <bool POOL>
+__device__ __forceinline__ double left_val(const MitmCtx& x, const Blk& B, const TabView& tv_, int64_t e) {
     if (B.m == 0) return -__longlong_as_double(0x7ff0000000000000LL);
-    const double pv = val[B.offl + e];
-    const double tv = tval(x, B.j - 1, bnd[B.offl + e], B.c);
+    const double pv = tab_val<POOL>(tv_, B.offl + e);
+    const double tv = tval(x, B.j - 1, (int)tab_bnd<POOL>(tv_, B.offl + e), B.c);
     return tv > pv ? tv : pv;
 }
 
-__device__ __forceinline__ double right_val(const MitmCtx& x, const Blk& B, const double* val, const uint8_t* bnd,
-                                            int64_t e) {
+template <bool POOL>
+__device__ __forceinline__ double right_val(const MitmCtx& x, const Blk& B, const TabView& tv_, int64_t e) {
     if (B.m == 0) return __ldg(x.timg + B.rrow + x.n);
-    const double sv = val[B.offr + e];
-    const double tv = __ldg(x.timg + B.rrow + bnd[B.offr + e]);
+    const double sv = tab_val<POOL>(tv_, B.offr + e);
+    const double tv = __ldg(x.timg + B.rrow + tab_bnd<POOL>(tv_, B.offr + e));
     return tv > sv ? tv : sv;
 }
 
@@ -295,9 +322,10 @@ __device__ __forceinline__ int64_t right_rank(const MitmCtx& x, const Blk& B, co
     return side_rank(x, B.m, d, mk);
 }
 
-__device__ __forceinline__ double side_value(const MitmCtx& x, const Blk& B, bool left, const double* val,
-                                             const uint8_t* bnd, int64_t e) {
-    return left ? left_val(x, B, val, bnd, e) : right_val(x, B, val, bnd, e);
+template <bool POOL>
+__device__ __forceinline__ double side_value(const MitmCtx& x, const Blk& B, bool left, const TabView& tv,
+                                             int64_t e) {
+    return left ? left_val<POOL>(x, B, tv, e) : right_val<POOL>(x, B, tv, e);
 }
 
 // A side element finished from its loaded table value and boundary cut, the
@@ -546,12 +574,14 @@ __global__ void __launch_bounds__(256) memo_image_kernel(const dm_tables tp, dou
 // One thread per kTabPass consecutive entries of the concatenated tables:
 // colex unrank of the first, Gosper successor for the rest, then the runs
 // the entry covers (T from the global image through L1).  Binomials in
-// shared memory (Pascal's triangle).  CTA 0 also resets the tile counter.
+// shared memory (Pascal's triangle).  CTA 0 also resets the tile counter
+// and the incumbent.
 template <typename Mask>   // uint32_t when every cut position fits 32 bits (n <= 34), else uint64_t
 __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, const double* __restrict__ timg,
                                                           const __grid_constant__ SideTables st,
                                                           double* __restrict__ val, uint8_t* __restrict__ bnd,
-                                                          int* __restrict__ counter, int* __restrict__ hist) {
+                                                          int* __restrict__ counter, int* __restrict__ hist,
+                                                          int64_t e_lo, int64_t e_hi) {
     extern __shared__ __align__(16) int64_t binom_s[];
     const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, R1 = rmax + 1;
     int32_t* rowrel = reinterpret_cast<int32_t*>(binom_s + n * R1);       // memo_row(q, a) for a < n
@@ -584,8 +614,8 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
     const MitmCtx x{n, W, R1, binom_s, nullptr};
     auto T = [&](int q, int a, int b) { return __ldg(timg + rowrel[q * n + a] + b); };
     const double ninf = -__longlong_as_double(0x7ff0000000000000LL);
-    const int64_t E = st.start[st.n_tab];
-    for (int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTabPass; e0 < E;
+    const int64_t E = e_hi;                      // entries [e_lo, e_hi) (a pooled sweep's rank builds its slice)
+    for (int64_t e0 = e_lo + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTabPass; e0 < E;
          e0 += (int64_t)gridDim.x * blockDim.x * kTabPass) {
         int ti;
         {
@@ -663,8 +693,14 @@ __host__ __device__ inline size_t plan_smem(int np2, int hrows, int n, int rmax)
     return (size_t)np2 * 8 + (size_t)np2 * 4 + (size_t)hrows * kHistRow * 4 + (size_t)n * (rmax + 1) * 8 +
            (((size_t)np2 * 2 + 15) & ~(size_t)15);
 }
+// The histogram rows come from every workspace of a pooled sweep (each rank
+// counted the entries it built; the rows add up).
+struct HistSrc {
+    int n;
+    const int* h[kPoolMax];
+};
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, const __grid_constant__ SweepParams P,
-                                                            const int* __restrict__ hist, int hrows,
+                                                            const HistSrc hist, int hrows,
                                                             int16_t* __restrict__ pos, int32_t* __restrict__ tstart) {
     extern __shared__ __align__(16) unsigned char psm[];   // plan_smem bytes
     const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, nbp = P.nbp, R1 = rmax + 1;
@@ -676,7 +712,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
     int32_t* hp = ntl + np2;                         // [hrows][kHistRow]: per-row inclusive prefix
     int16_t* sidx = reinterpret_cast<int16_t*>(hp + hrows * kHistRow);                    // [np2]
     __shared__ int32_t wsum[kPlanThreads / 32];
-    for (int i = threadIdx.x; i < hrows * kHistRow; i += blockDim.x) hp[i] = hist[i];
+    for (int i = threadIdx.x; i < hrows * kHistRow; i += blockDim.x) {
+        int v = 0;
+        for (int q = 0; q < hist.n; ++q) v += __ldcg(hist.h[q] + i);
+        hp[i] = v;
+    }
     if (threadIdx.x < 32) {                      // Pascal's triangle, exact for n <= 64
         const int lane = threadIdx.x;
         int64_t v0 = lane == 0, v1 = 0, v2 = 0;
@@ -822,9 +862,12 @@ __device__ inline void sweep_prologue(const MitmLayout& L, unsigned char* sm) {
     __syncthreads();
 }
 
+// POOL: the tile queue `ctl` is rank 0's (every GPU of the pool takes tiles
+// from it with system-scope atomics) and tv spans the pool's workspaces.
+template <bool POOL>
 __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_kernel(
-        const dm_tables tp, const __grid_constant__ SweepParams P, int* __restrict__ ctl,
-        const double* __restrict__ timg, const double* __restrict__ val, const uint8_t* __restrict__ bnd,
+        const dm_tables tp, const __grid_constant__ SweepParams P, int* ctl, unsigned long long* gbest,
+        const double* __restrict__ timg, const __grid_constant__ TabView tv,
         dm_winner* partial, const int16_t* __restrict__ plan_pos, const int32_t* __restrict__ plan_tstart) {
     const dm_tables t = tp;   // register copy (no param-space references)
     extern __shared__ __align__(16) unsigned char sm[];
@@ -890,11 +933,11 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     const int nbp = P.nbp;
     for (int i = threadIdx.x; i < nbp; i += blockDim.x) pos_blk[i] = plan_pos[i];
     for (int i = threadIdx.x; i <= nbp; i += blockDim.x) tstart[i] = plan_tstart[i];
-    if (threadIdx.x == 0) s_g[0] = atomicAdd(ctl, 1);   // dynamic tile queue over the part's blocks
+    auto next_tile = [&]() { return POOL ? atomicAdd_system(ctl, 1) : atomicAdd(ctl, 1); };
+    if (threadIdx.x == 0) s_g[0] = next_tile();   // dynamic tile queue over the part's blocks
     // the best makespan any CTA of the sweep has found so far (bits of a
     // non-negative double): tiles whose minimum exceeds it skip the rank
     // derivation.  Stale reads only make the test more permissive.
-    unsigned long long* gbest = reinterpret_cast<unsigned long long*>(ctl) + 1;
     unsigned long long gb = 0x7ff0000000000000ull;
     __syncthreads();
     const int n_tiles = tstart[nbp];
@@ -933,7 +976,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         if (g >= n_tiles) break;           // uniform
         MITM_CLK(c_t0);
         if (threadIdx.x == 0) {
-            s_g[par ^ 1] = atomicAdd(ctl, 1);   // read after the end barrier
+            s_g[par ^ 1] = next_tile();   // read after the end barrier
             gb = *reinterpret_cast<volatile unsigned long long*>(gbest);
         }
         const int lo = s_lo[par];          // staged with the tile's finishing runs
@@ -961,7 +1004,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 const int e = threadIdx.x;
                 double v = inf;
                 if (e < nYr) {
-                    v = side_finish_s(B, !xl, B.m ? __ldcg(val + yoff + y0 + e) : 0.0, B.m ? __ldcg(bnd + yoff + y0 + e) : 0, s_col[par], s_row[par], n);
+                    v = side_finish_s(B, !xl, B.m ? tab_val<POOL>(tv, yoff + y0 + e) : 0.0, B.m ? (int)tab_bnd<POOL>(tv, yoff + y0 + e) : 0, s_col[par], s_row[par], n);
                     ymin = v < ymin ? v : ymin;
                 }
                 append_if(v != inf, v, by, &s_cnt[par][1]);
@@ -989,7 +1032,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
                 for (int u = 0; u < kMitmNR; ++u) {
                     const int e = u * kMitmThreads + threadIdx.x;
-                    if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
+                    if (e < nXr && B.m) { xr[u] = tab_val<POOL>(tv, xoff + x0 + e); xb[u] = tab_bnd<POOL>(tv, xoff + x0 + e); }
                 }
                 for (int r0 = 0; r0 < nXr; r0 += kMitmTX) {
                     int f = 0;
@@ -1006,7 +1049,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
                     for (int u = 0; u < kMitmNR; ++u) {
                         const int e = r0 + kMitmTX + u * kMitmThreads + threadIdx.x;
-                        if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
+                        if (e < nXr && B.m) { xr[u] = tab_val<POOL>(tv, xoff + x0 + e); xb[u] = tab_bnd<POOL>(tv, xoff + x0 + e); }
                     }
                     __syncwarp();
                     const int nsl = (f + 31) >> 5;
@@ -1049,12 +1092,12 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
+                if (e < nXr && B.m) { xr[u] = tab_val<POOL>(tv, xoff + x0 + e); xb[u] = tab_bnd<POOL>(tv, xoff + x0 + e); }
             }
     #pragma unroll
             for (int u = 0; u < kYc; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                if (e < nYr && B.m) { yr[u] = __ldcg(val + yoff + y0 + e); yb[u] = __ldcg(bnd + yoff + y0 + e); }
+                if (e < nYr && B.m) { yr[u] = tab_val<POOL>(tv, yoff + y0 + e); yb[u] = tab_bnd<POOL>(tv, yoff + y0 + e); }
             }
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
@@ -1069,7 +1112,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     #pragma unroll
                     for (int u = 0; u < kYc; ++u) {
                         const int e = (h + u) * kMitmThreads + threadIdx.x;
-                        if (e < nYr && B.m) { yr[u] = __ldcg(val + yoff + y0 + e); yb[u] = __ldcg(bnd + yoff + y0 + e); }
+                        if (e < nYr && B.m) { yr[u] = tab_val<POOL>(tv, yoff + y0 + e); yb[u] = tab_bnd<POOL>(tv, yoff + y0 + e); }
                     }
                 }
     #pragma unroll
@@ -1151,13 +1194,13 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             if (tm <= best && tm < inf) {
                 int64_t rx = INT64_MAX, ry = INT64_MAX;
                 for (int e = threadIdx.x; e < nXr; e += kMitmThreads) {
-                    if (side_value(x, B, xl, val, bnd, x0 + e) <= tm) {
+                    if (side_value<POOL>(x, B, xl, tv, x0 + e) <= tm) {
                         const int64_t r = xl ? left_rank(x, B, x0 + e) : right_rank(x, B, cum, x0 + e);
                         rx = r < rx ? r : rx;
                     }
                 }
                 for (int e = threadIdx.x; e < nYr; e += kMitmThreads) {
-                    if (side_value(x, B, !xl, val, bnd, y0 + e) <= tm) {
+                    if (side_value<POOL>(x, B, !xl, tv, y0 + e) <= tm) {
                         const int64_t r = xl ? right_rank(x, B, cum, y0 + e) : left_rank(x, B, y0 + e);
                         ry = r < ry ? r : ry;
                     }
@@ -1284,13 +1327,13 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         int64_t blocks = (W.entries + per - 1) / per;
         if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
         if (blocks < 1) blocks = 1;
-        if (t.n <= 34) side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist);
-        else side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist);
+        if (t.n <= 34) side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, 0, W.entries);
+        else side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, 0, W.entries);
         DM_CHECK_LAUNCH();
     }
     const int grid = mitm_grid(sms);
     if (phase & 2) {
-        DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+        DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
         if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
         // the tile order from the tables' histogram (on the sweep's stream: a
         // one-CTA kernel queued behind a running sweep would wait for its tail)
@@ -1298,10 +1341,14 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         while (np2 < sp.nbp) np2 <<= 1;
         const size_t psmem = plan_smem(np2, st.n_tab, t.n, rmax);
         DM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-        plan_kernel<<<1, kPlanThreads, psmem, s>>>(t, sp, hist, st.n_tab, plan_pos, plan_tstart);
+        HistSrc hs{};
+        hs.n = 1; hs.h[0] = hist;
+        plan_kernel<<<1, kPlanThreads, psmem, s>>>(t, sp, hs, st.n_tab, plan_pos, plan_tstart);
         DM_CHECK_LAUNCH();
-        splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial, plan_pos,
-                                                                plan_tstart);
+        TabView tv{};
+        tv.world = 1; tv.lo[0] = 0; tv.lo[1] = W.entries; tv.val[0] = val; tv.bnd[0] = bnd;
+        splits_sweep_kernel<false><<<grid, kMitmThreads, L.bytes, s>>>(
+            t, sp, ctl, reinterpret_cast<unsigned long long*>(ctl) + 1, timg, tv, partial, plan_pos, plan_tstart);
         DM_CHECK_LAUNCH();
         if (tm.on) {
             DM_CUDA(cudaEventRecord(tm.ev[2], s));
@@ -1309,6 +1356,126 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         }
     }
     if (own) DM_CUDA(cudaFreeAsync(buf, s));
+    *n_partials = grid;
+    return DM_OK;
+}
+
+// ------------------------------------------------------- pooled sweep
+// Control words of a pooled workspace, after the tile counter (int @0) and
+// the incumbent (u64 @8): this rank's barrier epoch, a timeout status, and
+// one arrival flag per rank of the pool (written by the peers).
+constexpr size_t kPoolEpochOff = 64, kPoolStatusOff = 68, kPoolFlagsOff = 128;
+
+struct PoolFlags {
+    int world, rank;
+    unsigned* flags[kPoolMax];   // rank q's flag array (peer memory for q != rank)
+};
+
+// Grid barrier across the pool's GPUs, stream-ordered (one thread): bump
+// this rank's epoch, publish it in every rank's flag slot `rank`
+// (system-scope release: the tables this rank's earlier kernels wrote are
+// visible to the peers that see the flag), then wait until every rank has
+// published the same epoch.  A peer that never arrives (30 s) sets the status
+// word instead of hanging the GPU.
+__global__ void pool_barrier_kernel(const PoolFlags pf, unsigned* epoch, int* status) {
+    if (threadIdx.x != 0) return;
+    const unsigned e = *epoch + 1u;
+    *epoch = e;
+    __threadfence_system();
+    for (int q = 0; q < pf.world; ++q)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(pf.flags[q] + pf.rank), "r"(e) : "memory");
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const unsigned* mine = pf.flags[pf.rank];
+    for (int q = 0; q < pf.world; ++q)
+        for (;;) {
+            unsigned v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + q) : "memory");
+            if ((int)(v - e) >= 0) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 30ull * 1000000000ull) { atomicExch(status, 1); return; }
+            __nanosleep(256);
+        }
+}
+
+int launch_splits_pooled(const dm_tables& t, int rank, int world, void* const* wss, int64_t ws_bytes,
+                         dm_winner* partial, int sms, int* n_partials, cudaStream_t s) {
+    if (!memo_valid(t)) return DM_E_TOO_LARGE;
+    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1);
+    if (!pe.ok) return DM_E_TOO_LARGE;
+    const SideTables& st = pe.st;
+    const MitmWorkspace& W = pe.ws;
+    const SweepParams& sp = pe.sp;
+    if (world < 1 || world > kPoolMax || rank < 0 || rank >= world || ws_bytes < (int64_t)W.bytes) return DM_E_ARG;
+    for (int q = 0; q < world; ++q) if (!wss[q]) return DM_E_ARG;
+    const MitmLayout L = mitm_layout(t.n, t.p);
+    const int rmax = t.n < t.p ? t.n : t.p;
+    auto at = [&](int q, size_t off) { return static_cast<unsigned char*>(wss[q]) + off; };
+    int* ctl = reinterpret_cast<int*>(at(rank, 0));
+    int* hist = reinterpret_cast<int*>(at(rank, W.off_hist));
+    int16_t* plan_pos = reinterpret_cast<int16_t*>(at(rank, W.off_plan));
+    int32_t* plan_tstart = reinterpret_cast<int32_t*>(at(rank, W.off_plan + (size_t)kMitmMaxBlocks * 2));
+    double* timg = reinterpret_cast<double*>(at(rank, W.off_timg));
+    TabView tv{};
+    HistSrc hs{};
+    PoolFlags pf{};
+    tv.world = world; hs.n = world; pf.world = world; pf.rank = rank;
+    for (int q = 0; q <= world; ++q) tv.lo[q] = (int64_t)((__int128)W.entries * q / world);
+    for (int q = 0; q < world; ++q) {
+        tv.val[q] = reinterpret_cast<const double*>(at(q, W.off_val));
+        tv.bnd[q] = at(q, W.off_bnd);
+        hs.h[q] = reinterpret_cast<const int*>(at(q, W.off_hist));
+        pf.flags[q] = reinterpret_cast<unsigned*>(at(q, kPoolFlagsOff));
+    }
+    unsigned* epoch = reinterpret_cast<unsigned*>(at(rank, kPoolEpochOff));
+    int* status = reinterpret_cast<int*>(at(rank, kPoolStatusOff));
+    // 1-2. T image (every rank: the sweep reads it locally) and this rank's
+    //      slice of the side tables; the counter reset of rank 0 is the
+    //      pool's tile queue (no rank still draws from it: the previous
+    //      pooled sweep ended with a barrier)
+    {
+        const int64_t work = (int64_t)rmax * t.n * t.n;
+        memo_image_kernel<<<(int)((work + 255) / 256), 256, 0, s>>>(t, timg, hist);
+        DM_CHECK_LAUNCH();
+        const size_t smem = (size_t)t.n * (rmax + 1) * 8 + (size_t)rmax * t.n * 4;
+        const int64_t per = (int64_t)256 * kTabPass, mine = tv.lo[rank + 1] - tv.lo[rank];
+        int64_t blocks = (mine + per - 1) / per;
+        if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+        if (blocks < 1) blocks = 1;
+        double* val = reinterpret_cast<double*>(at(rank, W.off_val));
+        uint8_t* bnd = at(rank, W.off_bnd);
+        if (t.n <= 34)
+            side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, tv.lo[rank],
+                                                                       tv.lo[rank + 1]);
+        else
+            side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, tv.lo[rank],
+                                                                       tv.lo[rank + 1]);
+        DM_CHECK_LAUNCH();
+    }
+    // 3. every slice built
+    if (world > 1) {
+        pool_barrier_kernel<<<1, 32, 0, s>>>(pf, epoch, status);
+        DM_CHECK_LAUNCH();
+    }
+    // 4-5. the same tile order on every rank (the pool's summed histogram),
+    //      tiles drawn from rank 0's queue
+    int np2 = 2;
+    while (np2 < sp.nbp) np2 <<= 1;
+    const size_t psmem = plan_smem(np2, st.n_tab, t.n, rmax);
+    DM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    plan_kernel<<<1, kPlanThreads, psmem, s>>>(t, sp, hs, st.n_tab, plan_pos, plan_tstart);
+    DM_CHECK_LAUNCH();
+    const int grid = mitm_grid(sms);
+    DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+    splits_sweep_kernel<true><<<grid, kMitmThreads, L.bytes, s>>>(
+        t, sp, reinterpret_cast<int*>(wss[0]), reinterpret_cast<unsigned long long*>(ctl) + 1, timg, tv, partial,
+        plan_pos, plan_tstart);
+    DM_CHECK_LAUNCH();
+    // 6. no rank rebuilds its slice (or resets the queue) while a peer still reads it
+    if (world > 1) {
+        pool_barrier_kernel<<<1, 32, 0, s>>>(pf, epoch, status);
+        DM_CHECK_LAUNCH();
+    }
     *n_partials = grid;
     return DM_OK;
 }
