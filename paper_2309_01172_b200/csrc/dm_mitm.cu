@@ -48,6 +48,8 @@
 #include "dm_mitm.cuh"
 #include "dm_abi_util.cuh"
 
+#include <cstdlib>
+
 namespace dm {
 
 #ifdef DM_MITM_TIMING
@@ -119,6 +121,8 @@ struct MitmLayout {
     size_t off_binom, off_cum, off_mbase, off_bm, off_bc, off_pos, off_tstart, off_bx, off_by, off_red, bytes;
 };
 
+constexpr size_t kMitmSmemCap = 108 * 1024;   // per CTA at kMitmCtasPerSm CTAs per SM
+
 __host__ __device__ inline MitmLayout mitm_layout(int n, int p) {
     MitmLayout L;
     L.M = memo_layout(n, p);
@@ -161,6 +165,7 @@ struct SweepParams {
     int64_t offL[kMitmMaxM], offR[kMitmMaxM];
     int8_t tabL[kMitmMaxM], tabR[kMitmMaxM];   // histogram row of L_k / R(m) (-1: not built by this part)
     int nbp;                          // blocks of this part
+    int ty;                           // Y elements per tile (kMitmTY, or a power-of-two fraction for finer tiles)
     int16_t order[kMitmMaxBlocks];    // the part's blocks, largest tiles first
 };
 
@@ -195,10 +200,11 @@ __device__ __forceinline__ uint32_t tab_bnd(const TabView& v, int64_t g) { retur
 // boundary position); the sweep orders its tiles by the feasible pairs this
 // predicts (an upper bound) instead of the raw tile size.
 constexpr int kHistRow = 72;          // boundary positions 0..64
+constexpr size_t kHistBytes = ((size_t)2 * kMitmMaxM * kHistRow * 4 + 255) & ~(size_t)255;
 
 // Global workspace: tile counter, T image, side-table values, boundary bytes.
 struct MitmWorkspace {
-    size_t off_hist, off_plan, off_timg, off_val, off_bnd, bytes;
+    size_t off_hist, off_plan, off_timg, off_val, off_bnd, off_hist_in, bytes;
     int64_t entries;
 };
 
@@ -428,11 +434,12 @@ inline int left_positions(int W, int rmax, int k) {
 // part, blocks are ordered by the estimated duration of one of their tiles
 // (its pairs plus ~256 pair-equivalents per element it builds), largest
 // first, for the dynamic tile queue.
-inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWorkspace& ws, SweepParams* sp) {
+inline bool mitm_plan(int n, int p, int part, int nparts, int tyw, SideTables& st, MitmWorkspace& ws,
+                      SweepParams* sp) {
     const int W = n - 1, rmax = n < p ? n : p;
     if (n < 1 || n > 64 || p < 1 || rmax > kMitmMaxM || nparts < 1 || part < 0 || part >= nparts) return false;
     const MitmLayout L = mitm_layout(n, p);
-    if (L.n_blocks > kMitmMaxBlocks || L.bytes > 108 * 1024) return false;
+    if (L.n_blocks > kMitmMaxBlocks || L.bytes > kMitmSmemCap) return false;
     const int nb = L.n_blocks;
     struct BlockCost { double tile, total; int m, b; };
     std::vector<BlockCost> blk(nb);
@@ -448,8 +455,8 @@ inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWo
                 R = R < 1 ? 1 : (R > (unsigned __int128)kThinRounds ? kThinRounds : R);
             }
             const unsigned __int128 txs = (unsigned __int128)kMitmTX * R;
-            const unsigned __int128 tx = nX < txs ? nX : txs, ty = nY < kMitmTY ? nY : kMitmTY;
-            const unsigned __int128 nt = ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
+            const unsigned __int128 tx = nX < txs ? nX : txs, ty = nY < (unsigned)tyw ? nY : (unsigned)tyw;
+            const unsigned __int128 nt = ((nX + txs - 1) / txs) * ((nY + tyw - 1) / tyw);
             tiles += nt;
             const double tc = (double)(tx * ty + 256 * (tx + ty));
             blk[b] = {tc, tc * (double)nt, m, b};
@@ -530,14 +537,17 @@ inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWo
     st.start[st.n_tab] = (int64_t)e;
     ws.entries = (int64_t)e;
     ws.off_hist = 256;
-    ws.off_plan = ws.off_hist + (((size_t)2 * kMitmMaxM * kHistRow * 4 + 255) & ~(size_t)255);
+    ws.off_plan = ws.off_hist + kHistBytes;
     ws.off_timg = ws.off_plan + (((size_t)kMitmMaxBlocks * 2 + (size_t)(kMitmMaxBlocks + 1) * 4 + 255) & ~(size_t)255);
     ws.off_val = ws.off_timg + ((((size_t)L.M.t_elems * 8) + 255) & ~(size_t)255);
     ws.off_bnd = ws.off_val + (((size_t)ws.entries * 8 + 255) & ~(size_t)255);
-    ws.bytes = ws.off_bnd + (((size_t)ws.entries + 255) & ~(size_t)255);
+    // a pool's histograms: every rank's copy, pushed by its barrier
+    ws.off_hist_in = ws.off_bnd + (((size_t)ws.entries + 255) & ~(size_t)255);
+    ws.bytes = ws.off_hist_in + (size_t)kPoolMax * kHistBytes;
     if (sp) {
         std::stable_sort(mine.begin(), mine.end(), [&](int a, int b) { return blk[a].tile > blk[b].tile; });
         sp->nbp = (int)mine.size();
+        sp->ty = tyw;
         for (int i = 0; i < sp->nbp; ++i) sp->order[i] = (int16_t)mine[i];
         for (int m = 0; m < kMitmMaxM; ++m) {
             sp->offL[m] = st.offL[m]; sp->offR[m] = st.offR[m];
@@ -751,7 +761,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
         int64_t R = nY >= kThinY ? 1 : kThinPairs / (kMitmTX * nY);
         R = R < 1 ? 1 : (R > kThinRounds ? kThinRounds : R);
         const int64_t txs = (int64_t)kMitmTX * R;
-        const int64_t nt = ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
+        const int64_t nt = ((nX + txs - 1) / txs) * ((nY + P.ty - 1) / P.ty);
         double fl = 1.0, fr = 1.0;
         if (m > 0 && P.tabL[j - 1] >= 0 && P.tabR[m] >= 0) {
             const int* hl = hp + P.tabL[j - 1] * kHistRow;
@@ -759,7 +769,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
             fl = (double)hl[c - 1];                              // boundary positions < c
             fr = (double)(hr[kHistRow - 1] - hr[c]);             // boundary positions > c
         }
-        const double ex = (double)(nX < txs ? nX : txs), ey = (double)(nY < kMitmTY ? nY : kMitmTY);
+        const double ex = (double)(nX < txs ? nX : txs), ey = (double)(nY < P.ty ? nY : P.ty);
         key[i] = fl * fr / (double)nt + 50.0 * (ex + ey);
         sidx[i] = (int16_t)i;
         ntl[i] = (int32_t)nt;
@@ -862,11 +872,12 @@ __device__ inline void sweep_prologue(const MitmLayout& L, unsigned char* sm) {
     __syncthreads();
 }
 
-// POOL: the tile queue `ctl` is rank 0's (every GPU of the pool takes tiles
-// from it with system-scope atomics) and tv spans the pool's workspaces.
+// POOL: tv spans the workspaces of a pool (elements loaded from the rank
+// holding them); this rank sweeps tiles deal_rank, deal_rank + deal_world, ...
 template <bool POOL>
 __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_kernel(
-        const dm_tables tp, const __grid_constant__ SweepParams P, int* ctl, unsigned long long* gbest,
+        const dm_tables tp, const __grid_constant__ SweepParams P, int* ctl, int deal_rank, int deal_world,
+        unsigned long long* gbest,
         const double* __restrict__ timg, const __grid_constant__ TabView tv,
         dm_winner* partial, const int16_t* __restrict__ plan_pos, const int32_t* __restrict__ plan_tstart) {
     const dm_tables t = tp;   // register copy (no param-space references)
@@ -933,7 +944,10 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     const int nbp = P.nbp;
     for (int i = threadIdx.x; i < nbp; i += blockDim.x) pos_blk[i] = plan_pos[i];
     for (int i = threadIdx.x; i <= nbp; i += blockDim.x) tstart[i] = plan_tstart[i];
-    auto next_tile = [&]() { return POOL ? atomicAdd_system(ctl, 1) : atomicAdd(ctl, 1); };
+    // tiles dealt round-robin over the pool's ranks in the plan's order
+    // (longest first, so the ranks' shares match), each rank's CTAs drawing
+    // from its own queue (world = 1: the whole order)
+    auto next_tile = [&]() { return atomicAdd(ctl, 1) * deal_world + deal_rank; };
     if (threadIdx.x == 0) s_g[0] = next_tile();   // dynamic tile queue over the part's blocks
     // the best makespan any CTA of the sweep has found so far (bits of a
     // non-negative double): tiles whose minimum exceeds it skip the rank
@@ -975,8 +989,12 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         const int g = s_g[par];
         if (g >= n_tiles) break;           // uniform
         MITM_CLK(c_t0);
+        // the next tile's index: the atomic is issued now, its result stored
+        // only before the element barrier (a pool's queue is peer memory; the
+        // round trip overlaps this tile's element loads)
+        int nxt = 0;
         if (threadIdx.x == 0) {
-            s_g[par ^ 1] = next_tile();   // read after the end barrier
+            nxt = next_tile();
             gb = *reinterpret_cast<volatile unsigned long long*>(gbest);
         }
         const int lo = s_lo[par];          // staged with the tile's finishing runs
@@ -984,14 +1002,21 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         const Blk B = block_of(blk, bm[blk], bc[blk]);
         const bool xl = B.nl >= B.nr;
         const int64_t nX = xl ? B.nl : B.nr, nY = xl ? B.nr : B.nl;
-        const int64_t nty = (nY + kMitmTY - 1) / kMitmTY;
+        const int64_t nty = (nY + P.ty - 1) / P.ty;
         const int64_t local = g - tstart[lo];
         const int64_t txs = (int64_t)kMitmTX * B.R;
-        const int64_t x0 = (local / nty) * txs, y0 = (local % nty) * kMitmTY;
+        const int64_t x0 = (local / nty) * txs, y0 = (local % nty) * P.ty;
         const int nXr = (int)(nX - x0 < txs ? nX - x0 : txs);
-        const int nYr = (int)(nY - y0 < kMitmTY ? nY - y0 : kMitmTY);
+        const int nYr = (int)(nY - y0 < P.ty ? nY - y0 : P.ty);
         const double best = s_best;
         const int64_t xoff = xl ? B.offl : B.offr, yoff = xl ? B.offr : B.offl;
+        // the workspace holding each side's elements (a pool's slice
+        // boundaries never split a tile side: one owner per side)
+        const int xo = tab_owner<POOL>(tv, xoff + x0), yo = tab_owner<POOL>(tv, yoff + y0);
+        const double* xvp = tv.val[xo] + xoff + x0;
+        const uint8_t* xbp = tv.bnd[xo] + xoff + x0;
+        const double* yvp = tv.val[yo] + yoff + y0;
+        const uint8_t* ybp = tv.bnd[yo] + yoff + y0;
         bool maybe_best = false;
         double xmin = inf, ymin = inf;
         int nyf = 0;
@@ -1004,12 +1029,13 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 const int e = threadIdx.x;
                 double v = inf;
                 if (e < nYr) {
-                    v = side_finish_s(B, !xl, B.m ? tab_val<POOL>(tv, yoff + y0 + e) : 0.0, B.m ? (int)tab_bnd<POOL>(tv, yoff + y0 + e) : 0, s_col[par], s_row[par], n);
+                    v = side_finish_s(B, !xl, B.m ? __ldcg(yvp + e) : 0.0, B.m ? (int)__ldcg(ybp + e) : 0, s_col[par], s_row[par], n);
                     ymin = v < ymin ? v : ymin;
                 }
                 append_if(v != inf, v, by, &s_cnt[par][1]);
             }
             if (ymin <= best) atomicOr(&s_flag[par], 2);
+            if (threadIdx.x == 0) s_g[par ^ 1] = nxt;
             __syncthreads();
             if ((threadIdx.x >> 5) == 1) stage(par ^ 1, s_g[par ^ 1]);
             MITM_CLK(c_t1);
@@ -1032,7 +1058,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
                 for (int u = 0; u < kMitmNR; ++u) {
                     const int e = u * kMitmThreads + threadIdx.x;
-                    if (e < nXr && B.m) { xr[u] = tab_val<POOL>(tv, xoff + x0 + e); xb[u] = tab_bnd<POOL>(tv, xoff + x0 + e); }
+                    if (e < nXr && B.m) { xr[u] = __ldcg(xvp + e); xb[u] = __ldcg(xbp + e); }
                 }
                 for (int r0 = 0; r0 < nXr; r0 += kMitmTX) {
                     int f = 0;
@@ -1049,7 +1075,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
                     for (int u = 0; u < kMitmNR; ++u) {
                         const int e = r0 + kMitmTX + u * kMitmThreads + threadIdx.x;
-                        if (e < nXr && B.m) { xr[u] = tab_val<POOL>(tv, xoff + x0 + e); xb[u] = tab_bnd<POOL>(tv, xoff + x0 + e); }
+                        if (e < nXr && B.m) { xr[u] = __ldcg(xvp + e); xb[u] = __ldcg(xbp + e); }
                     }
                     __syncwarp();
                     const int nsl = (f + 31) >> 5;
@@ -1092,12 +1118,12 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                if (e < nXr && B.m) { xr[u] = tab_val<POOL>(tv, xoff + x0 + e); xb[u] = tab_bnd<POOL>(tv, xoff + x0 + e); }
+                if (e < nXr && B.m) { xr[u] = __ldcg(xvp + e); xb[u] = __ldcg(xbp + e); }
             }
     #pragma unroll
             for (int u = 0; u < kYc; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                if (e < nYr && B.m) { yr[u] = tab_val<POOL>(tv, yoff + y0 + e); yb[u] = tab_bnd<POOL>(tv, yoff + y0 + e); }
+                if (e < nYr && B.m) { yr[u] = __ldcg(yvp + e); yb[u] = __ldcg(ybp + e); }
             }
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
@@ -1112,7 +1138,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     #pragma unroll
                     for (int u = 0; u < kYc; ++u) {
                         const int e = (h + u) * kMitmThreads + threadIdx.x;
-                        if (e < nYr && B.m) { yr[u] = tab_val<POOL>(tv, yoff + y0 + e); yb[u] = tab_bnd<POOL>(tv, yoff + y0 + e); }
+                        if (e < nYr && B.m) { yr[u] = __ldcg(yvp + e); yb[u] = __ldcg(ybp + e); }
                     }
                 }
     #pragma unroll
@@ -1125,6 +1151,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             }
             const int fl = (xmin <= best ? 1 : 0) | (ymin <= best ? 2 : 0);
             if (fl) atomicOr(&s_flag[par], fl);
+            if (threadIdx.x == 0) s_g[par ^ 1] = nxt;
             __syncthreads();
             if ((threadIdx.x >> 5) == 1) stage(par ^ 1, s_g[par ^ 1]);
             MITM_CLK(c_t1);
@@ -1261,13 +1288,26 @@ struct PlanEntry {
     SweepParams sp;
 };
 
-inline const PlanEntry& cached_plan(int n, int p, int part, int nparts) {
-    static thread_local std::vector<std::pair<std::array<int, 4>, std::unique_ptr<PlanEntry>>> cache;
-    const std::array<int, 4> key{n, p, part, nparts};
+// Y elements per tile: kMitmTY (measured: finer tiles cost more element
+// builds than they save in tail at 1, 2 and 4 GPUs; DM_MITM_TY overrides,
+// 128..1024, a power of two).
+inline int tile_height(int shares) {
+    const char* e = std::getenv("DM_MITM_TY");
+    if (e && e[0]) {
+        const int v = std::atoi(e);
+        if (v >= 128 && v <= kMitmTY && (v & (v - 1)) == 0) return v;
+    }
+    (void)shares;
+    return kMitmTY;
+}
+
+inline const PlanEntry& cached_plan(int n, int p, int part, int nparts, int ty) {
+    static thread_local std::vector<std::pair<std::array<int, 5>, std::unique_ptr<PlanEntry>>> cache;
+    const std::array<int, 5> key{n, p, part, nparts, ty};
     for (auto& kv : cache)
         if (kv.first == key) return *kv.second;
     auto e = std::make_unique<PlanEntry>();
-    e->ok = mitm_plan(n, p, part, nparts, e->st, e->ws, &e->sp);
+    e->ok = mitm_plan(n, p, part, nparts, ty, e->st, e->ws, &e->sp);
     if (cache.size() > 64) cache.erase(cache.begin());
     cache.emplace_back(key, std::move(e));
     return *cache.back().second;
@@ -1275,7 +1315,7 @@ inline const PlanEntry& cached_plan(int n, int p, int part, int nparts) {
 
 int64_t mitm_workspace_bytes(const dm_tables& t) {
     if (!memo_valid(t)) return -1;
-    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1);
+    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1, kMitmTY);
     return pe.ok ? (int64_t)pe.ws.bytes : -1;
 }
 
@@ -1293,7 +1333,7 @@ inline SweepTiming& sweep_timing() {
 int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* partial, int sms, void* ws,
                        int64_t ws_bytes, int* n_partials, cudaStream_t s, int phase) {
     if (!memo_valid(t)) return DM_E_TOO_LARGE;
-    const PlanEntry& pe = cached_plan(t.n, t.p, part, nparts);
+    const PlanEntry& pe = cached_plan(t.n, t.p, part, nparts, tile_height(nparts));
     if (!pe.ok) return DM_E_TOO_LARGE;
     const SideTables& st = pe.st;
     const MitmWorkspace& W = pe.ws;
@@ -1348,7 +1388,7 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         TabView tv{};
         tv.world = 1; tv.lo[0] = 0; tv.lo[1] = W.entries; tv.val[0] = val; tv.bnd[0] = bnd;
         splits_sweep_kernel<false><<<grid, kMitmThreads, L.bytes, s>>>(
-            t, sp, ctl, reinterpret_cast<unsigned long long*>(ctl) + 1, timg, tv, partial, plan_pos, plan_tstart);
+            t, sp, ctl, 0, 1, reinterpret_cast<unsigned long long*>(ctl) + 1, timg, tv, partial, plan_pos, plan_tstart);
         DM_CHECK_LAUNCH();
         if (tm.on) {
             DM_CUDA(cudaEventRecord(tm.ev[2], s));
@@ -1377,7 +1417,24 @@ struct PoolFlags {
 // visible to the peers that see the flag), then wait until every rank has
 // published the same epoch.  A peer that never arrives (30 s) sets the status
 // word instead of hanging the GPU.
-__global__ void pool_barrier_kernel(const PoolFlags pf, unsigned* epoch, int* status) {
+//
+// hist_src (the barrier after the table slices): this rank's histogram is
+// first pushed into slot `rank` of every workspace's histogram array (posted
+// peer stores, ordered before the flag), so each rank's plan kernel sums the
+// pool's histograms from its own memory.
+struct HistPush {
+    const int4* src;
+    int4* dst[kPoolMax];     // slot `rank` of rank q's histogram array
+    int n16;                 // 16-byte chunks (0: no push)
+};
+__global__ void __launch_bounds__(256) pool_barrier_kernel(const PoolFlags pf, const HistPush hp, unsigned* epoch,
+                                                           int* status) {
+    if (hp.n16 > 0) {
+        for (int q = 0; q < pf.world; ++q)
+            for (int i = threadIdx.x; i < hp.n16; i += blockDim.x) hp.dst[q][i] = __ldcg(hp.src + i);
+        __threadfence_system();
+        __syncthreads();
+    }
     if (threadIdx.x != 0) return;
     const unsigned e = *epoch + 1u;
     *epoch = e;
@@ -1401,7 +1458,7 @@ __global__ void pool_barrier_kernel(const PoolFlags pf, unsigned* epoch, int* st
 int launch_splits_pooled(const dm_tables& t, int rank, int world, void* const* wss, int64_t ws_bytes,
                          dm_winner* partial, int sms, int* n_partials, cudaStream_t s) {
     if (!memo_valid(t)) return DM_E_TOO_LARGE;
-    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1);
+    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1, tile_height(world));
     if (!pe.ok) return DM_E_TOO_LARGE;
     const SideTables& st = pe.st;
     const MitmWorkspace& W = pe.ws;
@@ -1420,45 +1477,79 @@ int launch_splits_pooled(const dm_tables& t, int rank, int world, void* const* w
     HistSrc hs{};
     PoolFlags pf{};
     tv.world = world; hs.n = world; pf.world = world; pf.rank = rank;
-    for (int q = 0; q <= world; ++q) tv.lo[q] = (int64_t)((__int128)W.entries * q / world);
+    // slice boundaries: table starts plus multiples of kSliceAlign entries,
+    // so every tile side — aligned to its own size (kMitmTY or kMitmTX * R,
+    // R <= kThinRounds) within its table — lies in one slice; each boundary
+    // the allowed point nearest to an equal share
+    {
+        constexpr int64_t kSliceAlign = (int64_t)kMitmTX * 840;   // 840 = lcm(1..8) rounds
+        static_assert(kThinRounds <= 8 && kMitmTX % kMitmTY == 0, "slice alignment covers every tile side");
+        std::vector<int64_t> pts;
+        for (int i = 0; i < st.n_tab; ++i)
+            for (int64_t e = st.start[i]; e < st.start[i + 1]; e += kSliceAlign) pts.push_back(e);
+        pts.push_back(W.entries);
+        tv.lo[0] = 0;
+        for (int q = 1; q < world; ++q) {
+            const int64_t want = (int64_t)((__int128)W.entries * q / world);
+            int64_t best = pts[0];
+            for (int64_t e : pts)
+                if ((e > want ? e - want : want - e) < (best > want ? best - want : want - best)) best = e;
+            tv.lo[q] = best < tv.lo[q - 1] ? tv.lo[q - 1] : best;
+        }
+        tv.lo[world] = W.entries;
+    }
     for (int q = 0; q < world; ++q) {
         tv.val[q] = reinterpret_cast<const double*>(at(q, W.off_val));
         tv.bnd[q] = at(q, W.off_bnd);
-        hs.h[q] = reinterpret_cast<const int*>(at(q, W.off_hist));
+        hs.h[q] = reinterpret_cast<const int*>(at(rank, W.off_hist_in + (size_t)q * kHistBytes));
         pf.flags[q] = reinterpret_cast<unsigned*>(at(q, kPoolFlagsOff));
+    }
+    {   // measurement: every rank builds and reads the whole tables locally (shared queue only)
+        const char* e = std::getenv("DM_POOL_REPLICATE");
+        if (e && e[0] == '1') {
+            tv.world = 1; tv.lo[1] = W.entries; tv.val[0] = tv.val[rank]; tv.bnd[0] = tv.bnd[rank];
+            hs.n = 1; hs.h[0] = hist;
+        }
     }
     unsigned* epoch = reinterpret_cast<unsigned*>(at(rank, kPoolEpochOff));
     int* status = reinterpret_cast<int*>(at(rank, kPoolStatusOff));
+    SweepTiming& tm = sweep_timing();
+    if (tm.on) {
+        for (auto& e : tm.ev) if (!e) DM_CUDA(cudaEventCreate(&e));
+        DM_CUDA(cudaEventRecord(tm.ev[0], s));
+    }
     // 1-2. T image (every rank: the sweep reads it locally) and this rank's
-    //      slice of the side tables; the counter reset of rank 0 is the
-    //      pool's tile queue (no rank still draws from it: the previous
-    //      pooled sweep ended with a barrier)
+    //      slice of the side tables (no peer still reads the previous
+    //      slice: the previous pooled sweep ended with a barrier)
     {
         const int64_t work = (int64_t)rmax * t.n * t.n;
         memo_image_kernel<<<(int)((work + 255) / 256), 256, 0, s>>>(t, timg, hist);
         DM_CHECK_LAUNCH();
         const size_t smem = (size_t)t.n * (rmax + 1) * 8 + (size_t)rmax * t.n * 4;
-        const int64_t per = (int64_t)256 * kTabPass, mine = tv.lo[rank + 1] - tv.lo[rank];
+        const int64_t e_lo = tv.world == 1 ? 0 : tv.lo[rank], e_hi = tv.world == 1 ? W.entries : tv.lo[rank + 1];
+        const int64_t per = (int64_t)256 * kTabPass, mine = e_hi - e_lo;
         int64_t blocks = (mine + per - 1) / per;
         if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
         if (blocks < 1) blocks = 1;
         double* val = reinterpret_cast<double*>(at(rank, W.off_val));
         uint8_t* bnd = at(rank, W.off_bnd);
         if (t.n <= 34)
-            side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, tv.lo[rank],
-                                                                       tv.lo[rank + 1]);
+            side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, e_lo, e_hi);
         else
-            side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, tv.lo[rank],
-                                                                       tv.lo[rank + 1]);
+            side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, e_lo, e_hi);
         DM_CHECK_LAUNCH();
     }
     // 3. every slice built
-    if (world > 1) {
-        pool_barrier_kernel<<<1, 32, 0, s>>>(pf, epoch, status);
-        DM_CHECK_LAUNCH();
-    }
+    HistPush push{};
+    push.src = reinterpret_cast<const int4*>(hist);
+    push.n16 = (int)(kHistBytes / 16);
+    for (int q = 0; q < world; ++q)
+        push.dst[q] = reinterpret_cast<int4*>(at(q, W.off_hist_in + (size_t)rank * kHistBytes));
+    pool_barrier_kernel<<<1, 256, 0, s>>>(pf, push, epoch, status);
+    DM_CHECK_LAUNCH();
+    if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
     // 4-5. the same tile order on every rank (the pool's summed histogram),
-    //      tiles drawn from rank 0's queue
+    //      every world-th tile of it swept here
     int np2 = 2;
     while (np2 < sp.nbp) np2 <<= 1;
     const size_t psmem = plan_smem(np2, st.n_tab, t.n, rmax);
@@ -1468,12 +1559,16 @@ int launch_splits_pooled(const dm_tables& t, int rank, int world, void* const* w
     const int grid = mitm_grid(sms);
     DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
     splits_sweep_kernel<true><<<grid, kMitmThreads, L.bytes, s>>>(
-        t, sp, reinterpret_cast<int*>(wss[0]), reinterpret_cast<unsigned long long*>(ctl) + 1, timg, tv, partial,
-        plan_pos, plan_tstart);
+        t, sp, ctl, rank, world, reinterpret_cast<unsigned long long*>(ctl) + 1, timg, tv, partial, plan_pos,
+        plan_tstart);
     DM_CHECK_LAUNCH();
+    if (tm.on) {
+        DM_CUDA(cudaEventRecord(tm.ev[2], s));
+        tm.pending = true;
+    }
     // 6. no rank rebuilds its slice (or resets the queue) while a peer still reads it
     if (world > 1) {
-        pool_barrier_kernel<<<1, 32, 0, s>>>(pf, epoch, status);
+        pool_barrier_kernel<<<1, 32, 0, s>>>(pf, HistPush{}, epoch, status);
         DM_CHECK_LAUNCH();
     }
     *n_partials = grid;

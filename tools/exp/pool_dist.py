@@ -67,6 +67,44 @@ def main():
     t_pool = timed(lambda: engine.splits_pooled(batch, rank, world, pool.ptrs, pool.bytes, pool.bufs), reps, stream)
     t_part = timed(lambda: engine.enum(batch, "splits", 0, total, bufs=bufs, part=rank, nparts=world), reps, stream)
     t_one = timed(lambda: engine.enum(batch, "splits", 0, total, bufs=bufs), reps, stream)
+    def burst(fn, k=10):
+        return timed(lambda: [fn() for _ in range(k)], 5, stream) / k
+    pool_fn = lambda: engine.splits_pooled(batch, rank, world, pool.ptrs, pool.bytes, pool.bufs)  # noqa: E731
+    b_pool = burst(pool_fn)
+    os.environ["DM_POOL_REPLICATE"] = "1"
+    b_repl = burst(pool_fn)
+    os.environ["DM_POOL_REPLICATE"] = "0"
+    b_part = burst(lambda: engine.enum(batch, "splits", 0, total, bufs=bufs, part=rank, nparts=world))
+    b_one = burst(lambda: engine.enum(batch, "splits", 0, total, bufs=bufs))
+    import ctypes as C
+    from paper_2309_01172_b200 import _lib
+    lib = _lib.load()
+    phases = {}
+    part_fn = lambda: engine.enum(batch, "splits", 0, total, bufs=bufs, part=rank, nparts=world)  # noqa: E731
+    one_fn = lambda: engine.enum(batch, "splits", 0, total, bufs=bufs)  # noqa: E731
+    for name, env, fn in (("pooled", "0", pool_fn), ("pooled_replicated_tables", "1", pool_fn),
+                          ("block_parts", "0", part_fn), ("single", "0", one_fn)):
+        os.environ["DM_POOL_REPLICATE"] = env
+        lib.dm_sweep_timing(1, None, None)
+        acc = []
+        for _ in range(5):
+            dist.barrier()
+            torch.cuda.synchronize()
+            fn()
+            a, b = C.c_float(0), C.c_float(0)
+            _lib.check(lib.dm_sweep_timing(-1, C.byref(a), C.byref(b)))
+            acc.append((a.value, b.value))
+        lib.dm_sweep_timing(0, None, None)
+        t = torch.tensor(np.median(np.array(acc), axis=0), dtype=torch.float64, device="cuda")
+        g = torch.empty(2 * world, dtype=torch.float64, device="cuda")
+        dist.all_gather_into_tensor(g, t)
+        phases[name] = g.view(world, 2).tolist()
+    os.environ["DM_POOL_REPLICATE"] = "0"
+    if rank == 0:
+        print(json.dumps({"phase_ms_per_rank [tables+barrier, plan+sweep]": phases}), flush=True)
+    if rank == 0:
+        print(json.dumps({"burst10_ms_per_sweep": {"pooled": b_pool, "pooled_replicated_tables": b_repl,
+                                                   "block_parts": b_part, "single": b_one}}), flush=True)
     # the parts' records merge to the single sweep too
     engine.enum(batch, "splits", 0, total, bufs=bufs, part=rank, nparts=world)
     merged = D.merge_records(D.all_gather_winner(bufs.out).cpu().numpy())
