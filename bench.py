@@ -980,25 +980,24 @@ def sharded_measurements(args, dev, rank, world):
                         "winner": {"makespan": win["makespan"], "rank": win["rank"], "n_feasible": win["n_feasible"],
                                    "checksum": win["checksum"]}}
     del batch
-    out["pooled_c2_one_scenario"] = pooled_measurement(dev, rank, world)
+    out["split_one_scenario_c2"] = one_scenario_split(dev, rank, world)
     return out
 
 
-def pooled_measurement(dev, rank, world, reps: int = 10):
-    """ONE C2 scenario (8.6e9 splits) swept by all N GPUs: the pooled sweep
-    (search.PooledSweep / dm_enum_splits_pooled: side-table slices shared over
-    NVLink, one tile queue in rank 0's memory, device barriers) beside the
-    block-part split (each rank builds the tables of its blocks) and the
-    single-GPU sweep of the same scenario.  Device time per sweep, median of
-    `reps`, max over ranks; merged records checked against the single sweep."""
+def one_scenario_split(dev, rank, world, reps: int = 10):
+    """ONE C2 scenario (8.6e9 splits) split across the N GPUs by blocks
+    (dm_enum_splits_part: each rank builds the side tables its blocks read
+    and sweeps them; one all-gather of the records) beside the single-GPU
+    sweep of the same scenario.  Device time per sweep (median of `reps`
+    back-to-back pairs of launches), max over ranks; merged records checked
+    against the single sweep."""
     import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2309_01172_b200 import dist as D
-    from paper_2309_01172_b200 import engine, search
+    from paper_2309_01172_b200 import engine
     from paper_2309_01172_b200.tensorize import build_host
     stages, fleets, _ = c2_scenarios()
-    pool = search.PooledSweep(stages, fleets[0])
     batch = engine.device_batch([build_host(stages, fleets[0], True)], device=dev)
     total = engine.splits_total(len(stages), 32)
     bufs = engine.WinnerBuffers(dev)
@@ -1013,24 +1012,19 @@ def pooled_measurement(dev, rank, world, reps: int = 10):
             torch.cuda.synchronize()
             a.record(stream)
             fn()
+            fn()
             b.record(stream)
             b.synchronize()
-            ts.append(a.elapsed_time(b))
+            ts.append(a.elapsed_time(b) / 2)
         return _max_over_ranks([float(np.median(ts))], dev, world)[0]
-    t_pool = timed(lambda: engine.splits_pooled(batch, rank, world, pool.ptrs, pool.bytes, pool.bufs))
-    pooled = D.merge_records(D.all_gather_winner(pool.bufs.out).cpu().numpy())
     t_part = timed(lambda: engine.enum(batch, "splits", 0, total, bufs=bufs, part=rank, nparts=world))
     parts = D.merge_records(D.all_gather_winner(bufs.out).cpu().numpy())
     t_one = timed(lambda: engine.enum(batch, "splits", 0, total, bufs=bufs))
     single = bufs.read()
-    pool.close()
-    return {"candidates": total, "single_gpu_ms": t_one, "pooled_ms": t_pool, "block_parts_ms": t_part,
-            "pooled_speedup": t_one / t_pool, "block_parts_speedup": t_one / t_part,
-            "value": total / (t_pool / 1e3), "unit": UNIT,
-            "identical_to_single_sweep": pooled == single and parts == single,
-            "split": "pooled: rank q builds slice q of the side tables; every rank's sweep kernel draws tiles from "
-                     "rank 0's queue (system-scope atomics over NVLink) and loads each element from the workspace "
-                     "holding it; block parts: whole blocks dealt per rank, tables rebuilt per rank"}
+    return {"candidates": total, "single_gpu_ms": t_one, "split_ms": t_part, "speedup": t_one / t_part,
+            "value": total / (t_part / 1e3), "unit": UNIT, "identical_to_single_sweep": parts == single,
+            "split": "whole blocks dealt to ranks (LPT on tile and table cost); each rank builds the tables its "
+                     "blocks read; one all-gather of 40-byte records"}
 
 
 def run_reference(args, rank, world):

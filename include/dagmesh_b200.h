@@ -251,37 +251,6 @@ DM_API int dm_enum_splits_phase(const dm_tables* t, int64_t k0, int64_t k1, int3
                                 int32_t phase, void* stream);
 
 /*
- * Pooled split sweep — ONE identity-split population (the sweep of
- * dm_enum_splits over [0, total)) swept by `world` GPUs together, one process
- * (or stream) per rank.  workspaces[q] is rank q's workspace (at least
- * dm_splits_workspace_bytes; allocated zeroed, e.g. by dm_pool_alloc, and
- * mapped into every rank's process with dm_pool_open).  Rank q builds slice q
- * of the side tables into its own workspace; the ranks meet at a device-side
- * barrier (system-scope flags in the workspaces, no host round trip); every
- * rank's sweep kernel then draws tiles from rank 0's queue and loads each
- * table element from the workspace that holds it (peer memory over
- * NVLink); a second barrier ends the call.  `out` is the record of the tiles
- * THIS rank swept: the ranks' records merged (dist.merge_records) equal the
- * single-GPU sweep.  Every rank must make the same sequence of pooled calls on
- * the same pool.  world <= 8.  A peer that does not reach a barrier within
- * 30 s sets the workspace's status word (dm_pool_status) instead of hanging.
- * Replaces: brute_force_schedule's split population (scheduling.py:245-278),
- * as dm_enum_splits.
- */
-#define DM_IPC_HANDLE_BYTES 64
-DM_API int dm_enum_splits_pooled(const dm_tables* t, int32_t rank, int32_t world, void* const* workspaces,
-                                 int64_t workspace_bytes, dm_winner* out, void* scratch, void* stream);
-/* cudaMalloc'd, zeroed device memory and its CUDA IPC handle (64 bytes). */
-DM_API int dm_pool_alloc(int64_t bytes, void** dptr, void* ipc_handle);
-/* Map a peer process's dm_pool_alloc memory into this process. */
-DM_API int dm_pool_open(const void* ipc_handle, void** dptr);
-DM_API int dm_pool_close(void* dptr);
-DM_API int dm_pool_free(void* dptr);
-/* The workspace's barrier status (0 = every barrier met; 1 = a peer timed
- * out); synchronises `stream`. */
-DM_API int dm_pool_status(const void* workspace, int32_t* status, void* stream);
-
-/*
  * dm_enum_random — random contiguous placements scored on chip (configs C3,
  * C5; replaces scoring a sampled candidate list with evaluate_runs,
  * scheduling.py:235-239, and keeps brute_force_schedule's arg-min rule :271):

@@ -80,12 +80,6 @@ _SIGS = {
     "dm_enum_splits_ws": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, C.c_int64, _P]),
     "dm_enum_splits_phase": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, C.c_int64,
                                        C.c_int32, _P]),
-    "dm_enum_splits_pooled": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int64, _P, _P, _P]),
-    "dm_pool_alloc": (C.c_int, [C.c_int64, _P, _P]),
-    "dm_pool_open": (C.c_int, [_P, _P]),
-    "dm_pool_close": (C.c_int, [_P]),
-    "dm_pool_free": (C.c_int, [_P]),
-    "dm_pool_status": (C.c_int, [_P, _P, _P]),
     "dm_enum_random": (C.c_int, [_P, _P, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, _P, _P, _P]),
     "dm_finalize_winners": (C.c_int, [_P, C.c_int32, _P, _P]),
     "dm_subset_dp_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),

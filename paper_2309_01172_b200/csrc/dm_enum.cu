@@ -637,25 +637,6 @@ int dm_enum_splits_phase(const dm_tables* t, int64_t k0, int64_t k1, int32_t par
     return enum_splits_impl(t, k0, k1, part, nparts, out, scratch, workspace, workspace_bytes, stream, phase);
 }
 
-int dm_enum_splits_pooled(const dm_tables* t, int32_t rank, int32_t world, void* const* workspaces,
-                          int64_t workspace_bytes, dm_winner* out, void* scratch, void* stream) {
-    if (!t || !out || !scratch || !workspaces || t->n <= 0 || t->p <= 0)
-        return dmabi::fail(DM_E_ARG, "dm_enum_splits_pooled: bad arguments");
-    if (!dm::memo_valid(*t)) return dmabi::fail(DM_E_TOO_LARGE, "dm_enum_splits_pooled: instance outside the sweep");
-    cudaStream_t s = (cudaStream_t)stream;
-    int n_partials = 0;
-    const int rc = dm::launch_splits_pooled(*t, rank, world, workspaces, workspace_bytes, (dm_winner*)scratch,
-                                            enum_grid() / 8, &n_partials, s);
-    if (rc == DM_E_ARG)
-        return dmabi::fail(DM_E_ARG, "dm_enum_splits_pooled: rank/world out of range (world <= 8) or a workspace "
-                                     "missing or smaller than dm_splits_workspace_bytes");
-    if (rc == DM_E_TOO_LARGE) return dmabi::fail(rc, "dm_enum_splits_pooled: instance outside the sweep");
-    if (rc != DM_OK) return rc;
-    dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, n_partials, out);
-    DM_CHECK_LAUNCH();
-    return DM_OK;
-}
-
 int dm_materialize(int32_t n, int32_t p, int32_t mode, int64_t k0, int64_t count, void* owner, int32_t owner_bytes,
                    void* stream) {
     if (n <= 0 || p <= 0 || count < 0 || !owner || (owner_bytes != 1 && owner_bytes != 2) || (mode != 0 && mode != 1))

@@ -48,8 +48,6 @@
 #include "dm_mitm.cuh"
 #include "dm_abi_util.cuh"
 
-#include <cstdlib>
-
 namespace dm {
 
 #ifdef DM_MITM_TIMING
@@ -121,8 +119,6 @@ struct MitmLayout {
     size_t off_binom, off_cum, off_mbase, off_bm, off_bc, off_pos, off_tstart, off_bx, off_by, off_red, bytes;
 };
 
-constexpr size_t kMitmSmemCap = 108 * 1024;   // per CTA at kMitmCtasPerSm CTAs per SM
-
 __host__ __device__ inline MitmLayout mitm_layout(int n, int p) {
     MitmLayout L;
     L.M = memo_layout(n, p);
@@ -165,46 +161,17 @@ struct SweepParams {
     int64_t offL[kMitmMaxM], offR[kMitmMaxM];
     int8_t tabL[kMitmMaxM], tabR[kMitmMaxM];   // histogram row of L_k / R(m) (-1: not built by this part)
     int nbp;                          // blocks of this part
-    int ty;                           // Y elements per tile (kMitmTY, or a power-of-two fraction for finer tiles)
     int16_t order[kMitmMaxBlocks];    // the part's blocks, largest tiles first
 };
-
-// Where a sweep's side tables live.  One workspace (world = 1), or a pooled
-// sweep over `world` GPUs: entries [lo[q], lo[q+1]) of the concatenated
-// tables are built by rank q into ITS workspace, at the same offsets in every
-// workspace, and the sweep kernel of every rank loads each element from the
-// owner's workspace (peer memory over NVLink).
-constexpr int kPoolMax = 8;
-struct TabView {
-    int world;
-    int64_t lo[kPoolMax + 1];
-    const double* val[kPoolMax];
-    const uint8_t* bnd[kPoolMax];
-};
-
-template <bool POOL>
-__device__ __forceinline__ int tab_owner(const TabView& v, int64_t g) {
-    int q = 0;
-    if (POOL) {
-#pragma unroll
-        for (int k = 1; k < kPoolMax; ++k) q += (k < v.world && g >= v.lo[k]) ? 1 : 0;
-    }
-    return q;
-}
-template <bool POOL>
-__device__ __forceinline__ double tab_val(const TabView& v, int64_t g) { return __ldcg(v.val[tab_owner<POOL>(v, g)] + g); }
-template <bool POOL>
-__device__ __forceinline__ uint32_t tab_bnd(const TabView& v, int64_t g) { return __ldcg(v.bnd[tab_owner<POOL>(v, g)] + g); }
 
 // Feasibility histogram of the side tables: finite entries per (table,
 // boundary position); the sweep orders its tiles by the feasible pairs this
 // predicts (an upper bound) instead of the raw tile size.
 constexpr int kHistRow = 72;          // boundary positions 0..64
-constexpr size_t kHistBytes = ((size_t)2 * kMitmMaxM * kHistRow * 4 + 255) & ~(size_t)255;
 
 // Global workspace: tile counter, T image, side-table values, boundary bytes.
 struct MitmWorkspace {
-    size_t off_hist, off_plan, off_timg, off_val, off_bnd, off_hist_in, bytes;
+    size_t off_hist, off_plan, off_timg, off_val, off_bnd, bytes;
     int64_t entries;
 };
 
@@ -297,19 +264,19 @@ struct Blk {
     int32_t rrow;      // image index of T[j][c][0] (right sides)
 };
 
-template <bool POOL>
-__device__ __forceinline__ double left_val(const MitmCtx& x, const Blk& B, const TabView& tv_, int64_t e) {
+__device__ __forceinline__ double left_val(const MitmCtx& x, const Blk& B, const double* val, const uint8_t* bnd,
+                                           int64_t e) {
     if (B.m == 0) return -__longlong_as_double(0x7ff0000000000000LL);
-    const double pv = tab_val<POOL>(tv_, B.offl + e);
-    const double tv = tval(x, B.j - 1, (int)tab_bnd<POOL>(tv_, B.offl + e), B.c);
+    const double pv = val[B.offl + e];
+    const double tv = tval(x, B.j - 1, bnd[B.offl + e], B.c);
     return tv > pv ? tv : pv;
 }
 
-template <bool POOL>
-__device__ __forceinline__ double right_val(const MitmCtx& x, const Blk& B, const TabView& tv_, int64_t e) {
+__device__ __forceinline__ double right_val(const MitmCtx& x, const Blk& B, const double* val, const uint8_t* bnd,
+                                            int64_t e) {
     if (B.m == 0) return __ldg(x.timg + B.rrow + x.n);
-    const double sv = tab_val<POOL>(tv_, B.offr + e);
-    const double tv = __ldg(x.timg + B.rrow + tab_bnd<POOL>(tv_, B.offr + e));
+    const double sv = val[B.offr + e];
+    const double tv = __ldg(x.timg + B.rrow + bnd[B.offr + e]);
     return tv > sv ? tv : sv;
 }
 
@@ -328,10 +295,9 @@ __device__ __forceinline__ int64_t right_rank(const MitmCtx& x, const Blk& B, co
     return side_rank(x, B.m, d, mk);
 }
 
-template <bool POOL>
-__device__ __forceinline__ double side_value(const MitmCtx& x, const Blk& B, bool left, const TabView& tv,
-                                             int64_t e) {
-    return left ? left_val<POOL>(x, B, tv, e) : right_val<POOL>(x, B, tv, e);
+__device__ __forceinline__ double side_value(const MitmCtx& x, const Blk& B, bool left, const double* val,
+                                             const uint8_t* bnd, int64_t e) {
+    return left ? left_val(x, B, val, bnd, e) : right_val(x, B, val, bnd, e);
 }
 
 // A side element finished from its loaded table value and boundary cut, the
@@ -434,12 +400,11 @@ inline int left_positions(int W, int rmax, int k) {
 // part, blocks are ordered by the estimated duration of one of their tiles
 // (its pairs plus ~256 pair-equivalents per element it builds), largest
 // first, for the dynamic tile queue.
-inline bool mitm_plan(int n, int p, int part, int nparts, int tyw, SideTables& st, MitmWorkspace& ws,
-                      SweepParams* sp) {
+inline bool mitm_plan(int n, int p, int part, int nparts, SideTables& st, MitmWorkspace& ws, SweepParams* sp) {
     const int W = n - 1, rmax = n < p ? n : p;
     if (n < 1 || n > 64 || p < 1 || rmax > kMitmMaxM || nparts < 1 || part < 0 || part >= nparts) return false;
     const MitmLayout L = mitm_layout(n, p);
-    if (L.n_blocks > kMitmMaxBlocks || L.bytes > kMitmSmemCap) return false;
+    if (L.n_blocks > kMitmMaxBlocks || L.bytes > 108 * 1024) return false;
     const int nb = L.n_blocks;
     struct BlockCost { double tile, total; int m, b; };
     std::vector<BlockCost> blk(nb);
@@ -455,8 +420,8 @@ inline bool mitm_plan(int n, int p, int part, int nparts, int tyw, SideTables& s
                 R = R < 1 ? 1 : (R > (unsigned __int128)kThinRounds ? kThinRounds : R);
             }
             const unsigned __int128 txs = (unsigned __int128)kMitmTX * R;
-            const unsigned __int128 tx = nX < txs ? nX : txs, ty = nY < (unsigned)tyw ? nY : (unsigned)tyw;
-            const unsigned __int128 nt = ((nX + txs - 1) / txs) * ((nY + tyw - 1) / tyw);
+            const unsigned __int128 tx = nX < txs ? nX : txs, ty = nY < kMitmTY ? nY : kMitmTY;
+            const unsigned __int128 nt = ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
             tiles += nt;
             const double tc = (double)(tx * ty + 256 * (tx + ty));
             blk[b] = {tc, tc * (double)nt, m, b};
@@ -537,17 +502,14 @@ inline bool mitm_plan(int n, int p, int part, int nparts, int tyw, SideTables& s
     st.start[st.n_tab] = (int64_t)e;
     ws.entries = (int64_t)e;
     ws.off_hist = 256;
-    ws.off_plan = ws.off_hist + kHistBytes;
+    ws.off_plan = ws.off_hist + (((size_t)2 * kMitmMaxM * kHistRow * 4 + 255) & ~(size_t)255);
     ws.off_timg = ws.off_plan + (((size_t)kMitmMaxBlocks * 2 + (size_t)(kMitmMaxBlocks + 1) * 4 + 255) & ~(size_t)255);
     ws.off_val = ws.off_timg + ((((size_t)L.M.t_elems * 8) + 255) & ~(size_t)255);
     ws.off_bnd = ws.off_val + (((size_t)ws.entries * 8 + 255) & ~(size_t)255);
-    // a pool's histograms: every rank's copy, pushed by its barrier
-    ws.off_hist_in = ws.off_bnd + (((size_t)ws.entries + 255) & ~(size_t)255);
-    ws.bytes = ws.off_hist_in + (size_t)kPoolMax * kHistBytes;
+    ws.bytes = ws.off_bnd + (((size_t)ws.entries + 255) & ~(size_t)255);
     if (sp) {
         std::stable_sort(mine.begin(), mine.end(), [&](int a, int b) { return blk[a].tile > blk[b].tile; });
         sp->nbp = (int)mine.size();
-        sp->ty = tyw;
         for (int i = 0; i < sp->nbp; ++i) sp->order[i] = (int16_t)mine[i];
         for (int m = 0; m < kMitmMaxM; ++m) {
             sp->offL[m] = st.offL[m]; sp->offR[m] = st.offR[m];
@@ -584,14 +546,12 @@ __global__ void __launch_bounds__(256) memo_image_kernel(const dm_tables tp, dou
 // One thread per kTabPass consecutive entries of the concatenated tables:
 // colex unrank of the first, Gosper successor for the rest, then the runs
 // the entry covers (T from the global image through L1).  Binomials in
-// shared memory (Pascal's triangle).  CTA 0 also resets the tile counter
-// and the incumbent.
+// shared memory (Pascal's triangle).  CTA 0 also resets the tile counter.
 template <typename Mask>   // uint32_t when every cut position fits 32 bits (n <= 34), else uint64_t
 __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, const double* __restrict__ timg,
                                                           const __grid_constant__ SideTables st,
                                                           double* __restrict__ val, uint8_t* __restrict__ bnd,
-                                                          int* __restrict__ counter, int* __restrict__ hist,
-                                                          int64_t e_lo, int64_t e_hi) {
+                                                          int* __restrict__ counter, int* __restrict__ hist) {
     extern __shared__ __align__(16) int64_t binom_s[];
     const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, R1 = rmax + 1;
     int32_t* rowrel = reinterpret_cast<int32_t*>(binom_s + n * R1);       // memo_row(q, a) for a < n
@@ -624,8 +584,8 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
     const MitmCtx x{n, W, R1, binom_s, nullptr};
     auto T = [&](int q, int a, int b) { return __ldg(timg + rowrel[q * n + a] + b); };
     const double ninf = -__longlong_as_double(0x7ff0000000000000LL);
-    const int64_t E = e_hi;                      // entries [e_lo, e_hi) (a pooled sweep's rank builds its slice)
-    for (int64_t e0 = e_lo + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTabPass; e0 < E;
+    const int64_t E = st.start[st.n_tab];
+    for (int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTabPass; e0 < E;
          e0 += (int64_t)gridDim.x * blockDim.x * kTabPass) {
         int ti;
         {
@@ -703,14 +663,8 @@ __host__ __device__ inline size_t plan_smem(int np2, int hrows, int n, int rmax)
     return (size_t)np2 * 8 + (size_t)np2 * 4 + (size_t)hrows * kHistRow * 4 + (size_t)n * (rmax + 1) * 8 +
            (((size_t)np2 * 2 + 15) & ~(size_t)15);
 }
-// The histogram rows come from every workspace of a pooled sweep (each rank
-// counted the entries it built; the rows add up).
-struct HistSrc {
-    int n;
-    const int* h[kPoolMax];
-};
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, const __grid_constant__ SweepParams P,
-                                                            const HistSrc hist, int hrows,
+                                                            const int* __restrict__ hist, int hrows,
                                                             int16_t* __restrict__ pos, int32_t* __restrict__ tstart) {
     extern __shared__ __align__(16) unsigned char psm[];   // plan_smem bytes
     const int n = tp.n, W = n - 1, rmax = n < tp.p ? n : tp.p, nbp = P.nbp, R1 = rmax + 1;
@@ -722,11 +676,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
     int32_t* hp = ntl + np2;                         // [hrows][kHistRow]: per-row inclusive prefix
     int16_t* sidx = reinterpret_cast<int16_t*>(hp + hrows * kHistRow);                    // [np2]
     __shared__ int32_t wsum[kPlanThreads / 32];
-    for (int i = threadIdx.x; i < hrows * kHistRow; i += blockDim.x) {
-        int v = 0;
-        for (int q = 0; q < hist.n; ++q) v += __ldcg(hist.h[q] + i);
-        hp[i] = v;
-    }
+    for (int i = threadIdx.x; i < hrows * kHistRow; i += blockDim.x) hp[i] = hist[i];
     if (threadIdx.x < 32) {                      // Pascal's triangle, exact for n <= 64
         const int lane = threadIdx.x;
         int64_t v0 = lane == 0, v1 = 0, v2 = 0;
@@ -761,7 +711,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
         int64_t R = nY >= kThinY ? 1 : kThinPairs / (kMitmTX * nY);
         R = R < 1 ? 1 : (R > kThinRounds ? kThinRounds : R);
         const int64_t txs = (int64_t)kMitmTX * R;
-        const int64_t nt = ((nX + txs - 1) / txs) * ((nY + P.ty - 1) / P.ty);
+        const int64_t nt = ((nX + txs - 1) / txs) * ((nY + kMitmTY - 1) / kMitmTY);
         double fl = 1.0, fr = 1.0;
         if (m > 0 && P.tabL[j - 1] >= 0 && P.tabR[m] >= 0) {
             const int* hl = hp + P.tabL[j - 1] * kHistRow;
@@ -769,7 +719,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const dm_tables tp, 
             fl = (double)hl[c - 1];                              // boundary positions < c
             fr = (double)(hr[kHistRow - 1] - hr[c]);             // boundary positions > c
         }
-        const double ex = (double)(nX < txs ? nX : txs), ey = (double)(nY < P.ty ? nY : P.ty);
+        const double ex = (double)(nX < txs ? nX : txs), ey = (double)(nY < kMitmTY ? nY : kMitmTY);
         key[i] = fl * fr / (double)nt + 50.0 * (ex + ey);
         sidx[i] = (int16_t)i;
         ntl[i] = (int32_t)nt;
@@ -872,13 +822,9 @@ __device__ inline void sweep_prologue(const MitmLayout& L, unsigned char* sm) {
     __syncthreads();
 }
 
-// POOL: tv spans the workspaces of a pool (elements loaded from the rank
-// holding them); this rank sweeps tiles deal_rank, deal_rank + deal_world, ...
-template <bool POOL>
 __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_kernel(
-        const dm_tables tp, const __grid_constant__ SweepParams P, int* ctl, int deal_rank, int deal_world,
-        unsigned long long* gbest,
-        const double* __restrict__ timg, const __grid_constant__ TabView tv,
+        const dm_tables tp, const __grid_constant__ SweepParams P, int* __restrict__ ctl,
+        const double* __restrict__ timg, const double* __restrict__ val, const uint8_t* __restrict__ bnd,
         dm_winner* partial, const int16_t* __restrict__ plan_pos, const int32_t* __restrict__ plan_tstart) {
     const dm_tables t = tp;   // register copy (no param-space references)
     extern __shared__ __align__(16) unsigned char sm[];
@@ -944,14 +890,11 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     const int nbp = P.nbp;
     for (int i = threadIdx.x; i < nbp; i += blockDim.x) pos_blk[i] = plan_pos[i];
     for (int i = threadIdx.x; i <= nbp; i += blockDim.x) tstart[i] = plan_tstart[i];
-    // tiles dealt round-robin over the pool's ranks in the plan's order
-    // (longest first, so the ranks' shares match), each rank's CTAs drawing
-    // from its own queue (world = 1: the whole order)
-    auto next_tile = [&]() { return atomicAdd(ctl, 1) * deal_world + deal_rank; };
-    if (threadIdx.x == 0) s_g[0] = next_tile();   // dynamic tile queue over the part's blocks
+    if (threadIdx.x == 0) s_g[0] = atomicAdd(ctl, 1);   // dynamic tile queue over the part's blocks
     // the best makespan any CTA of the sweep has found so far (bits of a
     // non-negative double): tiles whose minimum exceeds it skip the rank
     // derivation.  Stale reads only make the test more permissive.
+    unsigned long long* gbest = reinterpret_cast<unsigned long long*>(ctl) + 1;
     unsigned long long gb = 0x7ff0000000000000ull;
     __syncthreads();
     const int n_tiles = tstart[nbp];
@@ -990,11 +933,11 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         if (g >= n_tiles) break;           // uniform
         MITM_CLK(c_t0);
         // the next tile's index: the atomic is issued now, its result stored
-        // only before the element barrier (a pool's queue is peer memory; the
-        // round trip overlaps this tile's element loads)
+        // only before the element barrier (the round trip overlaps this
+        // tile's element loads)
         int nxt = 0;
         if (threadIdx.x == 0) {
-            nxt = next_tile();
+            nxt = atomicAdd(ctl, 1);
             gb = *reinterpret_cast<volatile unsigned long long*>(gbest);
         }
         const int lo = s_lo[par];          // staged with the tile's finishing runs
@@ -1002,21 +945,14 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
         const Blk B = block_of(blk, bm[blk], bc[blk]);
         const bool xl = B.nl >= B.nr;
         const int64_t nX = xl ? B.nl : B.nr, nY = xl ? B.nr : B.nl;
-        const int64_t nty = (nY + P.ty - 1) / P.ty;
+        const int64_t nty = (nY + kMitmTY - 1) / kMitmTY;
         const int64_t local = g - tstart[lo];
         const int64_t txs = (int64_t)kMitmTX * B.R;
-        const int64_t x0 = (local / nty) * txs, y0 = (local % nty) * P.ty;
+        const int64_t x0 = (local / nty) * txs, y0 = (local % nty) * kMitmTY;
         const int nXr = (int)(nX - x0 < txs ? nX - x0 : txs);
-        const int nYr = (int)(nY - y0 < P.ty ? nY - y0 : P.ty);
+        const int nYr = (int)(nY - y0 < kMitmTY ? nY - y0 : kMitmTY);
         const double best = s_best;
         const int64_t xoff = xl ? B.offl : B.offr, yoff = xl ? B.offr : B.offl;
-        // the workspace holding each side's elements (a pool's slice
-        // boundaries never split a tile side: one owner per side)
-        const int xo = tab_owner<POOL>(tv, xoff + x0), yo = tab_owner<POOL>(tv, yoff + y0);
-        const double* xvp = tv.val[xo] + xoff + x0;
-        const uint8_t* xbp = tv.bnd[xo] + xoff + x0;
-        const double* yvp = tv.val[yo] + yoff + y0;
-        const uint8_t* ybp = tv.bnd[yo] + yoff + y0;
         bool maybe_best = false;
         double xmin = inf, ymin = inf;
         int nyf = 0;
@@ -1029,7 +965,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                 const int e = threadIdx.x;
                 double v = inf;
                 if (e < nYr) {
-                    v = side_finish_s(B, !xl, B.m ? __ldcg(yvp + e) : 0.0, B.m ? (int)__ldcg(ybp + e) : 0, s_col[par], s_row[par], n);
+                    v = side_finish_s(B, !xl, B.m ? __ldcg(val + yoff + y0 + e) : 0.0, B.m ? __ldcg(bnd + yoff + y0 + e) : 0, s_col[par], s_row[par], n);
                     ymin = v < ymin ? v : ymin;
                 }
                 append_if(v != inf, v, by, &s_cnt[par][1]);
@@ -1058,7 +994,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
                 for (int u = 0; u < kMitmNR; ++u) {
                     const int e = u * kMitmThreads + threadIdx.x;
-                    if (e < nXr && B.m) { xr[u] = __ldcg(xvp + e); xb[u] = __ldcg(xbp + e); }
+                    if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
                 }
                 for (int r0 = 0; r0 < nXr; r0 += kMitmTX) {
                     int f = 0;
@@ -1075,7 +1011,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
 #pragma unroll
                     for (int u = 0; u < kMitmNR; ++u) {
                         const int e = r0 + kMitmTX + u * kMitmThreads + threadIdx.x;
-                        if (e < nXr && B.m) { xr[u] = __ldcg(xvp + e); xb[u] = __ldcg(xbp + e); }
+                        if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
                     }
                     __syncwarp();
                     const int nsl = (f + 31) >> 5;
@@ -1118,12 +1054,12 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                if (e < nXr && B.m) { xr[u] = __ldcg(xvp + e); xb[u] = __ldcg(xbp + e); }
+                if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
             }
     #pragma unroll
             for (int u = 0; u < kYc; ++u) {
                 const int e = u * kMitmThreads + threadIdx.x;
-                if (e < nYr && B.m) { yr[u] = __ldcg(yvp + e); yb[u] = __ldcg(ybp + e); }
+                if (e < nYr && B.m) { yr[u] = __ldcg(val + yoff + y0 + e); yb[u] = __ldcg(bnd + yoff + y0 + e); }
             }
     #pragma unroll
             for (int u = 0; u < kMitmNR; ++u) {
@@ -1138,7 +1074,7 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
     #pragma unroll
                     for (int u = 0; u < kYc; ++u) {
                         const int e = (h + u) * kMitmThreads + threadIdx.x;
-                        if (e < nYr && B.m) { yr[u] = __ldcg(yvp + e); yb[u] = __ldcg(ybp + e); }
+                        if (e < nYr && B.m) { yr[u] = __ldcg(val + yoff + y0 + e); yb[u] = __ldcg(bnd + yoff + y0 + e); }
                     }
                 }
     #pragma unroll
@@ -1221,13 +1157,13 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             if (tm <= best && tm < inf) {
                 int64_t rx = INT64_MAX, ry = INT64_MAX;
                 for (int e = threadIdx.x; e < nXr; e += kMitmThreads) {
-                    if (side_value<POOL>(x, B, xl, tv, x0 + e) <= tm) {
+                    if (side_value(x, B, xl, val, bnd, x0 + e) <= tm) {
                         const int64_t r = xl ? left_rank(x, B, x0 + e) : right_rank(x, B, cum, x0 + e);
                         rx = r < rx ? r : rx;
                     }
                 }
                 for (int e = threadIdx.x; e < nYr; e += kMitmThreads) {
-                    if (side_value<POOL>(x, B, !xl, tv, y0 + e) <= tm) {
+                    if (side_value(x, B, !xl, val, bnd, y0 + e) <= tm) {
                         const int64_t r = xl ? right_rank(x, B, cum, y0 + e) : left_rank(x, B, y0 + e);
                         ry = r < ry ? r : ry;
                     }
@@ -1288,26 +1224,13 @@ struct PlanEntry {
     SweepParams sp;
 };
 
-// Y elements per tile: kMitmTY (measured: finer tiles cost more element
-// builds than they save in tail at 1, 2 and 4 GPUs; DM_MITM_TY overrides,
-// 128..1024, a power of two).
-inline int tile_height(int shares) {
-    const char* e = std::getenv("DM_MITM_TY");
-    if (e && e[0]) {
-        const int v = std::atoi(e);
-        if (v >= 128 && v <= kMitmTY && (v & (v - 1)) == 0) return v;
-    }
-    (void)shares;
-    return kMitmTY;
-}
-
-inline const PlanEntry& cached_plan(int n, int p, int part, int nparts, int ty) {
-    static thread_local std::vector<std::pair<std::array<int, 5>, std::unique_ptr<PlanEntry>>> cache;
-    const std::array<int, 5> key{n, p, part, nparts, ty};
+inline const PlanEntry& cached_plan(int n, int p, int part, int nparts) {
+    static thread_local std::vector<std::pair<std::array<int, 4>, std::unique_ptr<PlanEntry>>> cache;
+    const std::array<int, 4> key{n, p, part, nparts};
     for (auto& kv : cache)
         if (kv.first == key) return *kv.second;
     auto e = std::make_unique<PlanEntry>();
-    e->ok = mitm_plan(n, p, part, nparts, ty, e->st, e->ws, &e->sp);
+    e->ok = mitm_plan(n, p, part, nparts, e->st, e->ws, &e->sp);
     if (cache.size() > 64) cache.erase(cache.begin());
     cache.emplace_back(key, std::move(e));
     return *cache.back().second;
@@ -1315,7 +1238,7 @@ inline const PlanEntry& cached_plan(int n, int p, int part, int nparts, int ty) 
 
 int64_t mitm_workspace_bytes(const dm_tables& t) {
     if (!memo_valid(t)) return -1;
-    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1, kMitmTY);
+    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1);
     return pe.ok ? (int64_t)pe.ws.bytes : -1;
 }
 
@@ -1333,7 +1256,7 @@ inline SweepTiming& sweep_timing() {
 int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* partial, int sms, void* ws,
                        int64_t ws_bytes, int* n_partials, cudaStream_t s, int phase) {
     if (!memo_valid(t)) return DM_E_TOO_LARGE;
-    const PlanEntry& pe = cached_plan(t.n, t.p, part, nparts, tile_height(nparts));
+    const PlanEntry& pe = cached_plan(t.n, t.p, part, nparts);
     if (!pe.ok) return DM_E_TOO_LARGE;
     const SideTables& st = pe.st;
     const MitmWorkspace& W = pe.ws;
@@ -1367,13 +1290,13 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         int64_t blocks = (W.entries + per - 1) / per;
         if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
         if (blocks < 1) blocks = 1;
-        if (t.n <= 34) side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, 0, W.entries);
-        else side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, 0, W.entries);
+        if (t.n <= 34) side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist);
+        else side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist);
         DM_CHECK_LAUNCH();
     }
     const int grid = mitm_grid(sms);
     if (phase & 2) {
-        DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+        DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
         if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
         // the tile order from the tables' histogram (on the sweep's stream: a
         // one-CTA kernel queued behind a running sweep would wait for its tail)
@@ -1381,14 +1304,10 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         while (np2 < sp.nbp) np2 <<= 1;
         const size_t psmem = plan_smem(np2, st.n_tab, t.n, rmax);
         DM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-        HistSrc hs{};
-        hs.n = 1; hs.h[0] = hist;
-        plan_kernel<<<1, kPlanThreads, psmem, s>>>(t, sp, hs, st.n_tab, plan_pos, plan_tstart);
+        plan_kernel<<<1, kPlanThreads, psmem, s>>>(t, sp, hist, st.n_tab, plan_pos, plan_tstart);
         DM_CHECK_LAUNCH();
-        TabView tv{};
-        tv.world = 1; tv.lo[0] = 0; tv.lo[1] = W.entries; tv.val[0] = val; tv.bnd[0] = bnd;
-        splits_sweep_kernel<false><<<grid, kMitmThreads, L.bytes, s>>>(
-            t, sp, ctl, 0, 1, reinterpret_cast<unsigned long long*>(ctl) + 1, timg, tv, partial, plan_pos, plan_tstart);
+        splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial, plan_pos,
+                                                                plan_tstart);
         DM_CHECK_LAUNCH();
         if (tm.on) {
             DM_CUDA(cudaEventRecord(tm.ev[2], s));
@@ -1396,181 +1315,6 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         }
     }
     if (own) DM_CUDA(cudaFreeAsync(buf, s));
-    *n_partials = grid;
-    return DM_OK;
-}
-
-// ------------------------------------------------------- pooled sweep
-// Control words of a pooled workspace, after the tile counter (int @0) and
-// the incumbent (u64 @8): this rank's barrier epoch, a timeout status, and
-// one arrival flag per rank of the pool (written by the peers).
-constexpr size_t kPoolEpochOff = 64, kPoolStatusOff = 68, kPoolFlagsOff = 128;
-
-struct PoolFlags {
-    int world, rank;
-    unsigned* flags[kPoolMax];   // rank q's flag array (peer memory for q != rank)
-};
-
-// Grid barrier across the pool's GPUs, stream-ordered (one thread): bump
-// this rank's epoch, publish it in every rank's flag slot `rank`
-// (system-scope release: the tables this rank's earlier kernels wrote are
-// visible to the peers that see the flag), then wait until every rank has
-// published the same epoch.  A peer that never arrives (30 s) sets the status
-// word instead of hanging the GPU.
-//
-// hist_src (the barrier after the table slices): this rank's histogram is
-// first pushed into slot `rank` of every workspace's histogram array (posted
-// peer stores, ordered before the flag), so each rank's plan kernel sums the
-// pool's histograms from its own memory.
-struct HistPush {
-    const int4* src;
-    int4* dst[kPoolMax];     // slot `rank` of rank q's histogram array
-    int n16;                 // 16-byte chunks (0: no push)
-};
-__global__ void __launch_bounds__(256) pool_barrier_kernel(const PoolFlags pf, const HistPush hp, unsigned* epoch,
-                                                           int* status) {
-    if (hp.n16 > 0) {
-        for (int q = 0; q < pf.world; ++q)
-            for (int i = threadIdx.x; i < hp.n16; i += blockDim.x) hp.dst[q][i] = __ldcg(hp.src + i);
-        __threadfence_system();
-        __syncthreads();
-    }
-    if (threadIdx.x != 0) return;
-    const unsigned e = *epoch + 1u;
-    *epoch = e;
-    __threadfence_system();
-    for (int q = 0; q < pf.world; ++q)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(pf.flags[q] + pf.rank), "r"(e) : "memory");
-    unsigned long long t0, t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    const unsigned* mine = pf.flags[pf.rank];
-    for (int q = 0; q < pf.world; ++q)
-        for (;;) {
-            unsigned v;
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + q) : "memory");
-            if ((int)(v - e) >= 0) break;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 30ull * 1000000000ull) { atomicExch(status, 1); return; }
-            __nanosleep(256);
-        }
-}
-
-int launch_splits_pooled(const dm_tables& t, int rank, int world, void* const* wss, int64_t ws_bytes,
-                         dm_winner* partial, int sms, int* n_partials, cudaStream_t s) {
-    if (!memo_valid(t)) return DM_E_TOO_LARGE;
-    const PlanEntry& pe = cached_plan(t.n, t.p, 0, 1, tile_height(world));
-    if (!pe.ok) return DM_E_TOO_LARGE;
-    const SideTables& st = pe.st;
-    const MitmWorkspace& W = pe.ws;
-    const SweepParams& sp = pe.sp;
-    if (world < 1 || world > kPoolMax || rank < 0 || rank >= world || ws_bytes < (int64_t)W.bytes) return DM_E_ARG;
-    for (int q = 0; q < world; ++q) if (!wss[q]) return DM_E_ARG;
-    const MitmLayout L = mitm_layout(t.n, t.p);
-    const int rmax = t.n < t.p ? t.n : t.p;
-    auto at = [&](int q, size_t off) { return static_cast<unsigned char*>(wss[q]) + off; };
-    int* ctl = reinterpret_cast<int*>(at(rank, 0));
-    int* hist = reinterpret_cast<int*>(at(rank, W.off_hist));
-    int16_t* plan_pos = reinterpret_cast<int16_t*>(at(rank, W.off_plan));
-    int32_t* plan_tstart = reinterpret_cast<int32_t*>(at(rank, W.off_plan + (size_t)kMitmMaxBlocks * 2));
-    double* timg = reinterpret_cast<double*>(at(rank, W.off_timg));
-    TabView tv{};
-    HistSrc hs{};
-    PoolFlags pf{};
-    tv.world = world; hs.n = world; pf.world = world; pf.rank = rank;
-    // slice boundaries: table starts plus multiples of kSliceAlign entries,
-    // so every tile side — aligned to its own size (kMitmTY or kMitmTX * R,
-    // R <= kThinRounds) within its table — lies in one slice; each boundary
-    // the allowed point nearest to an equal share
-    {
-        constexpr int64_t kSliceAlign = (int64_t)kMitmTX * 840;   // 840 = lcm(1..8) rounds
-        static_assert(kThinRounds <= 8 && kMitmTX % kMitmTY == 0, "slice alignment covers every tile side");
-        std::vector<int64_t> pts;
-        for (int i = 0; i < st.n_tab; ++i)
-            for (int64_t e = st.start[i]; e < st.start[i + 1]; e += kSliceAlign) pts.push_back(e);
-        pts.push_back(W.entries);
-        tv.lo[0] = 0;
-        for (int q = 1; q < world; ++q) {
-            const int64_t want = (int64_t)((__int128)W.entries * q / world);
-            int64_t best = pts[0];
-            for (int64_t e : pts)
-                if ((e > want ? e - want : want - e) < (best > want ? best - want : want - best)) best = e;
-            tv.lo[q] = best < tv.lo[q - 1] ? tv.lo[q - 1] : best;
-        }
-        tv.lo[world] = W.entries;
-    }
-    for (int q = 0; q < world; ++q) {
-        tv.val[q] = reinterpret_cast<const double*>(at(q, W.off_val));
-        tv.bnd[q] = at(q, W.off_bnd);
-        hs.h[q] = reinterpret_cast<const int*>(at(rank, W.off_hist_in + (size_t)q * kHistBytes));
-        pf.flags[q] = reinterpret_cast<unsigned*>(at(q, kPoolFlagsOff));
-    }
-    {   // measurement: every rank builds and reads the whole tables locally (shared queue only)
-        const char* e = std::getenv("DM_POOL_REPLICATE");
-        if (e && e[0] == '1') {
-            tv.world = 1; tv.lo[1] = W.entries; tv.val[0] = tv.val[rank]; tv.bnd[0] = tv.bnd[rank];
-            hs.n = 1; hs.h[0] = hist;
-        }
-    }
-    unsigned* epoch = reinterpret_cast<unsigned*>(at(rank, kPoolEpochOff));
-    int* status = reinterpret_cast<int*>(at(rank, kPoolStatusOff));
-    SweepTiming& tm = sweep_timing();
-    if (tm.on) {
-        for (auto& e : tm.ev) if (!e) DM_CUDA(cudaEventCreate(&e));
-        DM_CUDA(cudaEventRecord(tm.ev[0], s));
-    }
-    // 1-2. T image (every rank: the sweep reads it locally) and this rank's
-    //      slice of the side tables (no peer still reads the previous
-    //      slice: the previous pooled sweep ended with a barrier)
-    {
-        const int64_t work = (int64_t)rmax * t.n * t.n;
-        memo_image_kernel<<<(int)((work + 255) / 256), 256, 0, s>>>(t, timg, hist);
-        DM_CHECK_LAUNCH();
-        const size_t smem = (size_t)t.n * (rmax + 1) * 8 + (size_t)rmax * t.n * 4;
-        const int64_t e_lo = tv.world == 1 ? 0 : tv.lo[rank], e_hi = tv.world == 1 ? W.entries : tv.lo[rank + 1];
-        const int64_t per = (int64_t)256 * kTabPass, mine = e_hi - e_lo;
-        int64_t blocks = (mine + per - 1) / per;
-        if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
-        if (blocks < 1) blocks = 1;
-        double* val = reinterpret_cast<double*>(at(rank, W.off_val));
-        uint8_t* bnd = at(rank, W.off_bnd);
-        if (t.n <= 34)
-            side_tables_kernel<uint32_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, e_lo, e_hi);
-        else
-            side_tables_kernel<uint64_t><<<(int)blocks, 256, smem, s>>>(t, timg, st, val, bnd, ctl, hist, e_lo, e_hi);
-        DM_CHECK_LAUNCH();
-    }
-    // 3. every slice built
-    HistPush push{};
-    push.src = reinterpret_cast<const int4*>(hist);
-    push.n16 = (int)(kHistBytes / 16);
-    for (int q = 0; q < world; ++q)
-        push.dst[q] = reinterpret_cast<int4*>(at(q, W.off_hist_in + (size_t)rank * kHistBytes));
-    pool_barrier_kernel<<<1, 256, 0, s>>>(pf, push, epoch, status);
-    DM_CHECK_LAUNCH();
-    if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
-    // 4-5. the same tile order on every rank (the pool's summed histogram),
-    //      every world-th tile of it swept here
-    int np2 = 2;
-    while (np2 < sp.nbp) np2 <<= 1;
-    const size_t psmem = plan_smem(np2, st.n_tab, t.n, rmax);
-    DM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-    plan_kernel<<<1, kPlanThreads, psmem, s>>>(t, sp, hs, st.n_tab, plan_pos, plan_tstart);
-    DM_CHECK_LAUNCH();
-    const int grid = mitm_grid(sms);
-    DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
-    splits_sweep_kernel<true><<<grid, kMitmThreads, L.bytes, s>>>(
-        t, sp, ctl, rank, world, reinterpret_cast<unsigned long long*>(ctl) + 1, timg, tv, partial, plan_pos,
-        plan_tstart);
-    DM_CHECK_LAUNCH();
-    if (tm.on) {
-        DM_CUDA(cudaEventRecord(tm.ev[2], s));
-        tm.pending = true;
-    }
-    // 6. no rank rebuilds its slice (or resets the queue) while a peer still reads it
-    if (world > 1) {
-        pool_barrier_kernel<<<1, 32, 0, s>>>(pf, HistPush{}, epoch, status);
-        DM_CHECK_LAUNCH();
-    }
     *n_partials = grid;
     return DM_OK;
 }

@@ -26,15 +26,4 @@ int64_t mitm_workspace_bytes(const dm_tables& t);
 int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* partial, int sms, void* ws,
                        int64_t ws_bytes, int* n_partials, cudaStream_t stream, int phase = 3);
 
-// Pooled sweep of ONE population by `world` GPUs (one process or stream per
-// rank): wss[q] is rank q's workspace (>= mitm_workspace_bytes, peer memory
-// mapped in this process; its first 256 bytes zero when allocated).  This
-// rank builds its slice of the side tables, meets the others at a device
-// barrier, then every rank's sweep kernel draws tiles from rank 0's queue and
-// reads each table element from the workspace that holds it.  Writes
-// mitm_grid(sms) partials of the tiles THIS rank swept; the ranks' merged
-// records equal the single sweep.
-int launch_splits_pooled(const dm_tables& t, int rank, int world, void* const* wss, int64_t ws_bytes,
-                         dm_winner* partial, int sms, int* n_partials, cudaStream_t stream);
-
 }  // namespace dm

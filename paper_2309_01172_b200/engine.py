@@ -180,59 +180,6 @@ def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | 
     return bufs
 
 
-def splits_workspace_bytes(batch: DeviceBatch, index: int = 0) -> int:
-    lib = _lib.load()
-    st = batch.struct(index)
-    return int(lib.dm_splits_workspace_bytes(C.byref(st)))
-
-
-def splits_pooled(batch: DeviceBatch, rank: int, world: int, workspaces, workspace_bytes: int,
-                  bufs: WinnerBuffers | None = None, index: int = 0):
-    """This rank's share of a pooled split sweep (dm_enum_splits_pooled):
-    `workspaces` are the device addresses of every rank's workspace as mapped
-    in this process.  Returns bufs; bufs.out holds the record of the tiles
-    this rank swept (merge the ranks' records with dist.merge_records)."""
-    lib = _lib.load()
-    bufs = bufs or WinnerBuffers(batch.dev_buf.device)
-    st = batch.struct(index)
-    arr = (C.c_void_p * len(workspaces))(*[int(w) for w in workspaces])
-    _lib.check(lib.dm_enum_splits_pooled(C.byref(st), rank, world, arr, workspace_bytes, bufs.out.data_ptr(),
-                                         bufs.scratch.data_ptr(), _lib.stream_ptr()))
-    return bufs
-
-
-def pool_alloc(nbytes: int) -> tuple[int, bytes]:
-    """Zeroed device memory shareable with other processes: (address, 64-byte CUDA IPC handle)."""
-    lib = _lib.load()
-    ptr = C.c_void_p()
-    handle = (C.c_ubyte * 64)()
-    _lib.check(lib.dm_pool_alloc(nbytes, C.byref(ptr), handle))
-    return int(ptr.value), bytes(handle)
-
-
-def pool_open(handle: bytes) -> int:
-    lib = _lib.load()
-    ptr = C.c_void_p()
-    buf = (C.c_ubyte * 64).from_buffer_copy(handle)
-    _lib.check(lib.dm_pool_open(buf, C.byref(ptr)))
-    return int(ptr.value)
-
-
-def pool_close(ptr: int):
-    _lib.check(_lib.load().dm_pool_close(C.c_void_p(ptr)))
-
-
-def pool_free(ptr: int):
-    _lib.check(_lib.load().dm_pool_free(C.c_void_p(ptr)))
-
-
-def pool_status(ptr: int) -> int:
-    """Barrier status word of a pooled workspace (0 = every barrier met); synchronises the stream."""
-    v = C.c_int32(0)
-    _lib.check(_lib.load().dm_pool_status(C.c_void_p(ptr), C.byref(v), _lib.stream_ptr()))
-    return int(v.value)
-
-
 # ------------------------------------------------- one-instance API calls
 class ScheduleSlot:
     """Reusable device staging for one-instance API calls (schedule()): a

@@ -145,99 +145,3 @@ class SplitSweeper:
             out.append(SplitWinner(runs, w.makespan, int(w.rank), int(w.n_evaluated), int(w.n_feasible),
                                    int(w.checksum)))
         return out
-
-
-class PooledSweep:
-    """ONE identity-split population swept by every GPU of a process group
-    together (one process per GPU): the pooled form of split_sweep for a
-    single fleet, where batching whole fleets across GPUs does not apply.
-
-    Construction is collective: every rank allocates its sweep workspace
-    (side tables, histogram, tile queue, barrier flags) with a CUDA IPC
-    handle, the 64-byte handles are all-gathered (the one host-side exchange),
-    and every rank maps its peers' workspaces (NVLink peer memory).  Each
-    sweep() then runs dm_enum_splits_pooled on every rank: rank q builds slice
-    q of the side tables, the ranks meet at a device barrier, every rank's
-    sweep kernel takes tiles from rank 0's queue and reads table elements
-    wherever they live, and one all-gather of the 40-byte records gives every
-    rank the merged winner — identical to the single-GPU sweep.  Every rank
-    must call sweep() the same number of times, with fleets of the same
-    shape (number of workers)."""
-
-    def __init__(self, stages, fleet_example, *, group=None, include_comm: bool = True):
-        torch = engine._torch()
-        import torch.distributed as dist
-        self.stages = list(stages)
-        self.include_comm = include_comm
-        self.group = group
-        self.dist = dist.is_available() and dist.is_initialized()
-        self.world = dist.get_world_size(group) if self.dist else 1
-        self.rank = dist.get_rank(group) if self.dist else 0
-        if self.world > 8:
-            raise ValueError("PooledSweep: at most 8 GPUs per pool")
-        self.device = torch.device("cuda", torch.cuda.current_device())
-        host = build_host(self.stages, fleet_example, include_comm)
-        self.n, self.p = host.n, host.p
-        self.total = splits_total(self.n, self.p)
-        self.bytes = engine.splits_workspace_bytes(engine.device_batch([host], device=self.device))
-        if self.bytes <= 0:
-            raise ValueError("PooledSweep: the instance is outside the meet-in-the-middle sweep")
-        self.local, handle = engine.pool_alloc(self.bytes)
-        self.ptrs = [self.local]
-        self.opened = []
-        if self.world > 1:
-            h = torch.tensor(list(handle), dtype=torch.uint8, device=self.device)
-            g = torch.empty(self.world * len(handle), dtype=torch.uint8, device=self.device)
-            dist.all_gather_into_tensor(g, h, group=group)
-            hs = g.cpu().numpy().reshape(self.world, -1)
-            self.ptrs = []
-            for q in range(self.world):
-                if q == self.rank:
-                    self.ptrs.append(self.local)
-                else:
-                    ptr = engine.pool_open(hs[q].tobytes())
-                    self.opened.append(ptr)
-                    self.ptrs.append(ptr)
-        self.bufs = engine.WinnerBuffers(self.device)
-
-    def sweep(self, fleet, records: bool = False):
-        """The fleet's identity-split optimum (SplitWinner), on every rank;
-        records=True returns the ranks' raw records (uint8[world, 40])."""
-        from .dist import merge_records
-        host = build_host(self.stages, fleet, self.include_comm)
-        if (host.n, host.p) != (self.n, self.p):
-            raise ValueError("PooledSweep: every fleet needs the shape the pool was built for")
-        batch = engine.device_batch([host], device=self.device)
-        engine.splits_pooled(batch, self.rank, self.world, self.ptrs, self.bytes, self.bufs)
-        if self.world > 1:
-            from .dist import all_gather_winner
-            raw = all_gather_winner(self.bufs.out, self.group).cpu().numpy()
-        else:
-            raw = self.bufs.out.view(1, -1).cpu().numpy()
-        if engine.pool_status(self.local) != 0:
-            raise RuntimeError("PooledSweep: a peer did not reach the pool barrier")
-        if records:
-            return raw
-        w = merge_records(raw)
-        runs = ()
-        if w["rank"] >= 0:
-            bounds, peers = engine.unrank(self.n, self.p, int(w["rank"]), "splits")
-            runs = tuple((host.peer_ids[peers[q]], tuple(range(bounds[q], bounds[q + 1]))) for q in range(len(peers)))
-        return SplitWinner(runs, w["makespan"], int(w["rank"]), int(w["n_evaluated"]), int(w["n_feasible"]),
-                           int(w["checksum"]))
-
-    def close(self):
-        """Collective: unmap the peers' workspaces and free this rank's."""
-        torch = engine._torch()
-        torch.cuda.synchronize(self.device)
-        if self.world > 1:
-            import torch.distributed as dist
-            dist.barrier(group=self.group)       # no peer still reads this rank's workspace
-        for ptr in self.opened:
-            engine.pool_close(ptr)
-        self.opened = []
-        if self.world > 1:
-            dist.barrier(group=self.group)
-        if self.local:
-            engine.pool_free(self.local)
-            self.local = 0
