@@ -8,16 +8,43 @@ constexpr int TY = 1024;
 template <int V, int CPS, int NR>
 __global__ void __launch_bounds__(256, CPS) k(int iters, uint64_t* sink) {
     __shared__ __align__(16) double ys[TY];
-    for (int i = threadIdx.x; i < TY; i += blockDim.x) ys[i] = 1.0 + 1e-3 * ((i * 37) % 101);
+    __shared__ __align__(16) double yq[2 * TY];      // V5: (y, lo word + 2^42) per element
+    __shared__ __align__(16) uint32_t yh[TY];         // V5: hi word
+    for (int i = threadIdx.x; i < TY; i += blockDim.x) {
+        ys[i] = 1.0 + 1e-3 * ((i * 37) % 101);
+        yq[2 * i] = ys[i];
+        yq[2 * i + 1] = (double)(uint32_t)__double2loint(ys[i]) + 4398046511104.0;
+        yh[i] = (uint32_t)__double2hiint(ys[i]);
+    }
     __syncthreads();
-    double xv[NR]; uint64_t cs[NR]; uint32_t c32[NR];
+    double xv[NR]; uint64_t cs[NR]; uint32_t c32[NR]; double L[NR];
 #pragma unroll
-    for (int u = 0; u < NR; ++u) { xv[u] = 1.0 + 1e-3 * ((threadIdx.x + 13 * u) % 101); cs[u] = 0; c32[u] = 0; }
+    for (int u = 0; u < NR; ++u) { xv[u] = 1.0 + 1e-3 * ((threadIdx.x + 13 * u) % 101); cs[u] = 0; c32[u] = 0; L[u] = 0; }
+    const double4* y4 = reinterpret_cast<const double4*>(yq);
+    const uint2* h2 = reinterpret_cast<const uint2*>(yh);
     const double2* y2 = reinterpret_cast<const double2*>(ys);
     for (int it = 0; it < iters; ++it) {
 #pragma unroll 2
         for (int y = 0; y < TY / 2; ++y) {
             const double2 yy = y2[y];
+            if (V == 5) {
+                // count-encoded lo sum on the FP64 pipe: L += (x > y) * (lo + 2^42) via SEL + DFMA,
+                // hi words mod 2^32 with a predicated IADD (FMA pipe)
+                const double4 q = y4[y];
+                const uint2 h = h2[y];
+#pragma unroll
+                for (int u = 0; u < NR; ++u) {
+                    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t.reg .f64 d;\n\t"
+                        "setp.gt.f64 p, %2, %3;\n\tselp.b32 t, 1072693248, 0, p;\n\tmov.b64 d, {0, t};\n\t"
+                        "fma.rn.f64 %0, d, %4, %0;\n\t@p add.u32 %1, %1, %5;\n\t}"
+                        : "+d"(L[u]), "+r"(c32[u]) : "d"(xv[u]), "d"(q.x), "d"(q.y), "r"(h.x));
+                    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t.reg .f64 d;\n\t"
+                        "setp.gt.f64 p, %2, %3;\n\tselp.b32 t, 1072693248, 0, p;\n\tmov.b64 d, {0, t};\n\t"
+                        "fma.rn.f64 %0, d, %4, %0;\n\t@p add.u32 %1, %1, %5;\n\t}"
+                        : "+d"(L[u]), "+r"(c32[u]) : "d"(xv[u]), "d"(q.z), "d"(q.w), "r"(h.y));
+                }
+                continue;
+            }
 #pragma unroll
             for (int u = 0; u < NR; ++u) {
                 if (V == 0) {
@@ -48,7 +75,7 @@ __global__ void __launch_bounds__(256, CPS) k(int iters, uint64_t* sink) {
     }
     uint64_t c = 0;
 #pragma unroll
-    for (int u = 0; u < NR; ++u) c += cs[u] + c32[u];
+    for (int u = 0; u < NR; ++u) c += cs[u] + c32[u] + (uint64_t)L[u];
     if (c == 42) sink[0] = c;
 }
 
@@ -75,6 +102,9 @@ int main(int argc, char**) {
         return 0;
     }
     run<0, 2>("dsetp+fsel+sel+iadd3");
+    run<5, 2>("dsetp+sel+dfma+iadd (V5)");
+    run<5, 2, 4>("dsetp+sel+dfma+iadd (V5)");
+    run<5, 2, 6>("dsetp+sel+dfma+iadd (V5)");
     run<4, 2>("lo imad.wide + hi iadd3");
     run<4, 2, 16>("lo imad.wide + hi iadd3");
     run<0, 4>("dsetp+fsel+sel+iadd3");
