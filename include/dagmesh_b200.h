@@ -245,6 +245,8 @@ DM_API int dm_enum_splits_ws(const dm_tables* t, int64_t k0, int64_t k1, int32_t
  * sweep: phase 1 builds the side tables into `workspace` (required, at least
  * dm_splits_workspace_bytes), phase 2 sweeps them and writes `out`; phase 3
  * does both.  Phase 1 then phase 2 on the same workspace equals phase 3.
+ * Phase 2 itself splits into 4 (the tile plan, a one-CTA kernel a batch can
+ * run on a stream of its own) then 8 (the sweep kernel and `out`).
  * Instances that take the rank-range kernels do all their work in phase 2. */
 DM_API int dm_enum_splits_phase(const dm_tables* t, int64_t k0, int64_t k1, int32_t part, int32_t nparts,
                                 dm_winner* out, void* scratch, void* workspace, int64_t workspace_bytes,

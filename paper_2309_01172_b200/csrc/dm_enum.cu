@@ -560,7 +560,7 @@ bool nparts_full_range(const dm_tables* t, int64_t k0, int64_t k1) {
 int enum_splits_impl(const dm_tables* t, int64_t k0, int64_t k1, int part, int nparts, dm_winner* out,
                      void* scratch, void* ws, int64_t ws_bytes, void* stream, int phase = 3) {
     if (!t || !out || !scratch || t->n <= 0 || t->p <= 0 || nparts < 1 || part < 0 || part >= nparts ||
-        phase < 1 || phase > 3)
+        phase < 1 || phase > 15)
         return dmabi::fail(DM_E_ARG, "bad arguments");
     cudaStream_t s = (cudaStream_t)stream;
     const bool memo_ok = dm::memo_valid(*t) && !getenv_flag("DM_DISABLE_MEMO");
@@ -571,14 +571,14 @@ int enum_splits_impl(const dm_tables* t, int64_t k0, int64_t k1, int part, int n
         if (rc == DM_E_ARG) return dmabi::fail(DM_E_ARG, "split phases need a workspace of dm_splits_workspace_bytes");
         if (rc != DM_E_TOO_LARGE) {
             if (rc != DM_OK) return rc;
-            if (phase & 2) {
+            if (phase & (2 | 8)) {
                 dm::finalize_kernel<<<1, 1024, 0, s>>>((dm_winner*)scratch, n_partials, out);
                 DM_CHECK_LAUNCH();
             }
             return DM_OK;
         }
     }
-    if (!(phase & 2)) return DM_OK;     // the rank-range kernels have no table phase
+    if (!(phase & (2 | 8))) return DM_OK;     // the rank-range kernels have no table or plan phase
     dm::MemoLayout L = dm::memo_layout(t->n, t->p);
     const size_t memo_bytes = L.off_tail + dm::memo_cut_bytes(L);
     if (memo_ok && t->n <= 64 && memo_bytes <= 110 * 1024) {

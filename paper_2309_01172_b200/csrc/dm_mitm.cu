@@ -13,7 +13,8 @@
 // runs; the winner key (makespan, rank) is the reference's first strict
 // minimum in itertools order.
 //
-// Launches per sweep (phase 1: 1-2, phase 2: 3-5; dm_enum_splits_phase):
+// Launches per sweep (phase 1: 1-2, phase 2: 3-5 — or 4: 3 and 8: 4-5;
+// dm_enum_splits_phase):
 //  1. memo_image_kernel: T once into a global image (one entry per thread);
 //  2. side_tables_kernel: the side tables, every entry evaluated directly from
 //     its cut mask at full occupancy (T read through L1).  Left sides: the
@@ -1295,17 +1296,23 @@ int launch_splits_mitm(const dm_tables& t, int part, int nparts, dm_winner* part
         DM_CHECK_LAUNCH();
     }
     const int grid = mitm_grid(sms);
-    if (phase & 2) {
-        DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
-        if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
-        // the tile order from the tables' histogram (on the sweep's stream: a
-        // one-CTA kernel queued behind a running sweep would wait for its tail)
+    // phase 2 = plan + sweep; 4 = the plan alone, 8 = the sweep alone (a
+    // batch runs each plan on its own stream, off the sweeps' critical path)
+    const bool do_plan = phase & (2 | 4), do_sweep = phase & (2 | 8);
+    if (do_plan) {
+        // the tile order from the tables' histogram: a one-CTA kernel (on
+        // the sweep's stream, or its own — queued behind the next tables on
+        // theirs it would hold them until a running sweep's tail)
         int np2 = 2;
         while (np2 < sp.nbp) np2 <<= 1;
         const size_t psmem = plan_smem(np2, st.n_tab, t.n, rmax);
         DM_CUDA(cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
         plan_kernel<<<1, kPlanThreads, psmem, s>>>(t, sp, hist, st.n_tab, plan_pos, plan_tstart);
         DM_CHECK_LAUNCH();
+    }
+    if (do_sweep) {
+        DM_CUDA(cudaFuncSetAttribute(splits_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+        if (tm.on) DM_CUDA(cudaEventRecord(tm.ev[1], s));
         splits_sweep_kernel<<<grid, kMitmThreads, L.bytes, s>>>(t, sp, ctl, timg, val, bnd, partial, plan_pos,
                                                                 plan_tstart);
         DM_CHECK_LAUNCH();

@@ -155,7 +155,7 @@ def enum(batch: DeviceBatch, mode: str, k0: int, k1: int, bufs: WinnerBuffers | 
     """Mode B enumeration: 'bruteforce' | 'splits' | 'random'. Returns bufs
     (call bufs.read() to synchronise and fetch the winner).  'splits' takes
     `phase` (dm_enum_splits_phase): 1 = side tables only, 2 = sweep only,
-    3 = both."""
+    3 = both; 2 splits into 4 (tile plan) then 8 (sweep kernel)."""
     lib = _lib.load()
     bufs = bufs or WinnerBuffers(batch.dev_buf.device)
     st = batch.struct(index)
@@ -482,6 +482,10 @@ class SweepGraph:
         # ALU bound); every unit has its own workspace
         self.overlap = overlap and len(self.units) > 1
         self.side = torch.cuda.Stream(device=dev) if self.overlap else None
+        # each unit's one-CTA tile plan on a third stream: it waits for the
+        # unit's tables and runs in the previous sweep's tail, neither
+        # delaying the sweeps (main) nor holding back the next tables (side)
+        self.plan = torch.cuda.Stream(device=dev) if self.overlap else None
         self.unit_bufs = [bufs if (i == 0 and bufs is not None) else WinnerBuffers(dev)
                           for i in range(len(self.units))]
         for (idx, _, _), ub in zip(self.units, self.unit_bufs):
@@ -513,17 +517,24 @@ class SweepGraph:
         if self.overlap:
             main = torch.cuda.current_stream()
             self.side.wait_stream(main)
+            self.plan.wait_stream(main)
             ready = []
-            with torch.cuda.stream(self.side):
-                for (idx, part, nparts), ub in zip(self.units, self.unit_bufs):
+            for (idx, part, nparts), ub in zip(self.units, self.unit_bufs):
+                with torch.cuda.stream(self.side):
                     enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts, phase=1)
+                    tables = torch.cuda.Event()
+                    tables.record(self.side)
+                with torch.cuda.stream(self.plan):
+                    self.plan.wait_event(tables)
+                    enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts, phase=4)
                     ev = torch.cuda.Event()
-                    ev.record(self.side)
+                    ev.record(self.plan)
                     ready.append(ev)
             for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
                 main.wait_event(ready[i])
-                enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts, phase=2)
+                enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts, phase=8)
             main.wait_stream(self.side)
+            main.wait_stream(self.plan)
         else:
             for i, ((idx, part, nparts), ub) in enumerate(zip(self.units, self.unit_bufs)):
                 enum(b, "splits", 0, self.total, ub, index=idx, part=part, nparts=nparts)
