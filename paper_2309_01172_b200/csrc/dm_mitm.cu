@@ -583,7 +583,11 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
     }
     __syncthreads();
     const MitmCtx x{n, W, R1, binom_s, nullptr};
-    auto T = [&](int q, int a, int b) { return __ldg(timg + rowrel[q * n + a] + b); };
+    const double* __restrict__ tim = timg;
+    auto T = [=](int q, int a, int b) { return __ldg(tim + (uint32_t)(rowrel[q * n + a] + b)); };
+    auto hi_bit = [](Mask m) {           // index of the highest set bit, -1 for 0
+        if constexpr (sizeof(Mask) == 4) return 31 - __clz((int)m); else return 63 - __clzll((long long)m);
+    };
     const double ninf = -__longlong_as_double(0x7ff0000000000000LL);
     const int64_t E = st.start[st.n_tab];
     for (int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kTabPass; e0 < E;
@@ -610,28 +614,29 @@ __global__ void __launch_bounds__(256) side_tables_kernel(const dm_tables tp, co
             const int P = st.pos[ti];                                  // positions
             if (fresh) mk = (Mask)colex_unrank(x, k, P, e - st.start[ti]);
             else mk = (Mask)side_next((uint64_t)mk);
+            // runs visited from the highest cut bit down (FLO per cut, no
+            // bit reversal): cut bit b sits at position b + 1 in L_k and
+            // W - b in R(m); the run below bit hb ends at the next lower cut
+            // (position 0 / n past the last one — b = -1 in both formulas)
             double v = ninf;
-            int prev;
-            auto low_bit = [](Mask r) {
-                if constexpr (sizeof(Mask) == 4) return __ffs((int)r); else return __ffsll((long long)r);
-            };
-            if (!right) {                // L_k: runs q = 0..k-1 ending at the cuts (position 1 + b)
-                prev = 0;
-                int q = 0;
-                for (Mask r = mk; r; r &= r - 1, ++q) {
-                    const int c = low_bit(r);
-                    const double tv = T(q, prev, c);
+            int hb = hi_bit(mk);
+            const int prev = right ? W - hb : hb + 1;          // the entry's boundary cut
+            Mask r = mk;
+            if (!right) {                // L_k: run i = [c_{i-1}, c_i), row i
+                for (int i = k - 1; hb >= 0; --i) {
+                    r ^= (Mask)1 << hb;
+                    const int lb = hi_bit(r);
+                    const double tv = T(i, lb + 1, hb + 1);
                     v = tv > v ? tv : v;
-                    prev = c;
+                    hb = lb;
                 }
-            } else {                     // R(m): runs q = m, m-1, .. starting at the cuts (position W - b)
-                prev = n;
-                int q = km;
-                for (Mask r = mk; r; r &= r - 1, --q) {
-                    const int c = W + 1 - low_bit(r);
-                    const double tv = T(q, c, prev);
+            } else {                     // R(m): run i = [c_i, c_{i-1}) (mirrored), row km - i
+                for (int i = k - 1; hb >= 0; --i) {
+                    r ^= (Mask)1 << hb;
+                    const int lb = hi_bit(r);
+                    const double tv = T(km - i, W - hb, W - lb);
                     v = tv > v ? tv : v;
-                    prev = c;
+                    hb = lb;
                 }
             }
             val[e] = v;
