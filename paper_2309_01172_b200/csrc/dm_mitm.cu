@@ -96,6 +96,7 @@ constexpr int kTabPass = 16;                         // side-table entries per t
 constexpr int kThinY = 256;                          // blocks with a smaller side below this are "thin":
 constexpr int kThinPairs = 1 << 21;                  // their tiles span ~kThinPairs pairs in rounds of kMitmTX
 constexpr int kThinRounds = 8;                       // X elements, at most this many rounds per tile
+constexpr int kThinRing = 512;                       // per-warp ring of a thin tile's feasible X (>= 2 x 256)
 constexpr uint64_t kInfBits = 0x7ff0000000000000ULL;
 
 __host__ __device__ inline int mitm_j(int m) { return (m + 1) >> 1; }
@@ -138,7 +139,7 @@ __host__ __device__ inline MitmLayout mitm_layout(int n, int p) {
     off = (off + 1) & ~(size_t)1;
     L.off_pos = off; off += (size_t)nb * 2;
     off = (off + 15) & ~(size_t)15;
-    L.off_bx = off; off += (size_t)kMitmTX * 8;
+    L.off_bx = off; off += (size_t)(kMitmTX > kThinRing * (kMitmThreads / 32) ? kMitmTX : kThinRing * (kMitmThreads / 32)) * 8;
     L.off_by = off; off += (size_t)kMitmTY * 8;
     L.off_red = off; off += 64 * 8;
     L.bytes = off;
@@ -992,8 +993,12 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
             }
             int64_t nxf_all = 0;
             if (nyf > 0) {
-                // warp-private compaction of each round's feasible X
-                double* wbuf = bx + (threadIdx.x >> 5) * (kMitmNR * 32);
+                // warp-private compaction of each round's feasible X into a
+                // ring of kThinRing values; a cross pass takes full batches
+                // of 256 (8 slots per lane) as they fill and the remainder
+                // after the last round, so sparse rounds are not padded to
+                // whole slots one round at a time
+                double* wbuf = bx + (threadIdx.x >> 5) * kThinRing;
                 const int lane = threadIdx.x & 31;
                 double xr[kMitmNR];
                 int xb[kMitmNR];
@@ -1002,16 +1007,16 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                     const int e = u * kMitmThreads + threadIdx.x;
                     if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
                 }
+                int head = 0, fill = 0;       // warp-uniform ring state
                 for (int r0 = 0; r0 < nXr; r0 += kMitmTX) {
-                    int f = 0;
 #pragma unroll
                     for (int u = 0; u < kMitmNR; ++u) {
                         const int e = r0 + u * kMitmThreads + threadIdx.x;
                         const double v = e < nXr ? side_finish_s(B, xl, xr[u], xb[u], s_col[par], s_row[par], n) : inf;
                         xmin = v < xmin ? v : xmin;
                         const unsigned bal = __ballot_sync(0xffffffffu, v != inf);
-                        if (v != inf) wbuf[f + __popc(bal & ((1u << lane) - 1u))] = v;
-                        f += __popc(bal);
+                        if (v != inf) wbuf[(head + fill + __popc(bal & ((1u << lane) - 1u))) & (kThinRing - 1)] = v;
+                        fill += __popc(bal);
                     }
                     // the next round's elements are in flight during this round's cross product
 #pragma unroll
@@ -1019,15 +1024,18 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                         const int e = r0 + kMitmTX + u * kMitmThreads + threadIdx.x;
                         if (e < nXr && B.m) { xr[u] = __ldcg(val + xoff + x0 + e); xb[u] = __ldcg(bnd + xoff + x0 + e); }
                     }
+                    const bool last = r0 + kMitmTX >= nXr;
+                    if (fill < kMitmNR * 32 && !(last && fill > 0)) continue;
                     __syncwarp();
-                    const int nsl = (f + 31) >> 5;
+                    const int take = fill < kMitmNR * 32 ? fill : kMitmNR * 32;
+                    const int nsl = (take + 31) >> 5;
                     double xv[kMitmNR];
                     int nxf = 0;
 #pragma unroll
                     for (int u = 0; u < kMitmNR; ++u) {
                         const int e = u * 32 + lane;
-                        xv[u] = e < f ? wbuf[e] : inf;
-                        nxf += e < f;
+                        xv[u] = e < take ? wbuf[(head + e) & (kThinRing - 1)] : inf;
+                        nxf += e < take;
                     }
                     switch (nsl) {
                         case 0: break;
@@ -1043,7 +1051,35 @@ __global__ void __launch_bounds__(kMitmThreads, kMitmCtasPerSm) splits_sweep_ker
                     corr += (uint64_t)(nsl - nxf) * (uint64_t)nyf;
                     nxf_all += nxf;
                     MITM_COUNT(5, nsl * nyf);
+                    head = (head + take) & (kThinRing - 1);
+                    fill -= take;
                     __syncwarp();
+                    // a full batch on the last round can leave a remainder
+                    if (last && fill > 0) {
+                        const int nsl2 = (fill + 31) >> 5;
+                        int nxf2 = 0;
+#pragma unroll
+                        for (int u = 0; u < kMitmNR; ++u) {
+                            const int e = u * 32 + lane;
+                            xv[u] = e < fill ? wbuf[(head + e) & (kThinRing - 1)] : inf;
+                            nxf2 += e < fill;
+                        }
+                        switch (nsl2) {
+                            case 1: mitm_cross<1>(xv, by, nyf, cs); break;
+                            case 2: mitm_cross<2>(xv, by, nyf, cs); break;
+                            case 3: mitm_cross<3>(xv, by, nyf, cs); break;
+                            case 4: mitm_cross<4>(xv, by, nyf, cs); break;
+                            case 5: mitm_cross<5>(xv, by, nyf, cs); break;
+                            case 6: mitm_cross<6>(xv, by, nyf, cs); break;
+                            case 7: mitm_cross<7>(xv, by, nyf, cs); break;
+                            default: mitm_cross<8>(xv, by, nyf, cs); break;
+                        }
+                        corr += (uint64_t)(nsl2 - nxf2) * (uint64_t)nyf;
+                        nxf_all += nxf2;
+                        MITM_COUNT(5, nsl2 * nyf);
+                        fill = 0;
+                        __syncwarp();
+                    }
                 }
             }
             w.n_feas += nxf_all * nyf;
