@@ -402,6 +402,11 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
                                             double* __restrict__ out_mk, uint8_t* __restrict__ out_code,
                                             int64_t rank_base, bool fuse, StreamWin& win, uint32_t& n_seen) {
     const int n = X.n;
+    // the table's shared address as an opaque register value: otherwise the
+    // compiler rematerialises it (CTA id + window offset, four uniform
+    // instructions) at every run
+    uint32_t T_s;
+    asm volatile("mov.b32 %0, %1;" : "=r"(T_s) : "r"(X.T_s));
     // per-thread bases, advanced per candidate (no per-candidate address rebuild)
     double* omk = out_mk + c0 + threadIdx.x;
     uint8_t* ocode = out_code + c0 + threadIdx.x;
@@ -421,7 +426,7 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
             uint32_t idx;
             if (SQUARE) idx = b * X.rowstride + end * X.uP + w;
             else idx = ((b * (X.tri_k - b)) >> 1) * X.uP + (end - b - 1) * X.uP + w;
-            const uint32_t addr = X.T_s + 8u * idx;
+            const uint32_t addr = T_s + 8u * idx;
             double v = lds_f64s(addr);
             if (PAIR) {
                 // chain stages: the crossing read of run [b, end) is priced with
@@ -462,7 +467,7 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
                 uint32_t idx;
                 if (SQUARE) idx = b * X.rowstride + e * X.uP + w;
                 else idx = ((b * (X.tri_k - b)) >> 1) * X.uP + (e - b - 1) * X.uP + w;
-                addr = X.T_s + 8u * idx;
+                addr = T_s + 8u * idx;
                 v = lds_f64s(addr);
             };
             auto fold = [&](uint32_t w, uint32_t addr, double v) {
@@ -498,7 +503,7 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
         (void)prev_w;
         mk = __hiloint2double(__double2hiint(mk) & 0x7fffffff, __double2loint(mk));   // |mk| without the fp64 pipe
         const int nruns = __popcll(bm & (((unsigned long long)X.mask_hi << 32) | X.mask_lo)) + 1;
-        int code = bad != 0xffffffffu ? (int)lds_u8(X.C_s + ((bad - X.T_s) >> 3)) : DM_V_OK;
+        int code = bad != 0xffffffffu ? (int)lds_u8(X.C_s + ((bad - T_s) >> 3)) : DM_V_OK;
         bool unknown = false;
         if (__popc(seen) != nruns || (seen & X.pmask)) {        // repeated peer or owner >= P
             const unsigned char* row = tile + (size_t)ci * n;
