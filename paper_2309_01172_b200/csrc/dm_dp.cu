@@ -194,7 +194,7 @@ __host__ __device__ inline size_t dpw_bytes(int n, int p, int e_max) {
 
 // Copy the DP's columns of t into smem at b (warp-cooperative) and return a
 // dm_tables whose pointers refer to the copies.
-__device__ inline dm_tables dpw_stage(const dm_tables& t, unsigned char* b, int lane, int e_max) {
+__device__ inline dm_tables dpw_stage(const dm_tables& t, unsigned char* b, int lane, int e_max, int stride = 32) {
     const int n = t.n, p = t.p, n1 = n + 1, E = t.n_edges;
     dm_tables c = t;
     int64_t* pre = reinterpret_cast<int64_t*>(b); b += align_up(4 * (size_t)n1 * 8);
@@ -203,17 +203,17 @@ __device__ inline dm_tables dpw_stage(const dm_tables& t, unsigned char* b, int 
     int32_t* esrc = reinterpret_cast<int32_t*>(b); b += align_up((size_t)e_max * 4);
     double* em = reinterpret_cast<double*>(b); b += align_up((size_t)e_max * 8);
     double* peer = reinterpret_cast<double*>(b);
-    for (int i = lane; i < n1; i += 32) {
+    for (int i = lane; i < n1; i += stride) {
         pre[i] = t.pre_flops[i]; pre[n1 + i] = t.pre_gpu[i]; pre[2 * n1 + i] = t.pre_cpu[i];
         pre[3 * n1 + i] = t.pre_disk[i]; eptr[i] = t.edge_ptr[i];
     }
-    for (int i = lane; i < n; i += 32) {
+    for (int i = lane; i < n; i += stride) {
         col[i] = t.flops[i]; col[n + i] = t.gpu[i]; col[2 * n + i] = t.cpu[i]; col[3 * n + i] = t.disk[i];
     }
     const bool stage_edges = E <= e_max;
     if (stage_edges)
-        for (int e = lane; e < E; e += 32) { esrc[e] = t.edge_src[e]; em[e] = t.edge_m[e]; }
-    for (int w = lane; w < p; w += 32) {
+        for (int e = lane; e < E; e += stride) { esrc[e] = t.edge_src[e]; em[e] = t.edge_m[e]; }
+    for (int w = lane; w < p; w += stride) {
         peer[w] = t.speed[w]; peer[p + w] = t.cap_gpu[w]; peer[2 * p + w] = t.cap_cpu[w]; peer[3 * p + w] = t.cap_disk[w];
     }
     c.pre_flops = pre; c.pre_gpu = pre + n1; c.pre_cpu = pre + 2 * n1; c.pre_disk = pre + 3 * n1;
@@ -225,6 +225,149 @@ __device__ inline dm_tables dpw_stage(const dm_tables& t, unsigned char* b, int 
 }
 
 __device__ __forceinline__ int dpw_pair(int i, int j, int n) { return i * n - i * (i - 1) / 2 + (j - i - 1); }
+
+// ---- mid-size fleets (32 < 2^p <= 256): one CTA per scenario, one THREAD
+//      per target mask (masks ordered by popcount, so a warp's masks have the
+//      same source count), each thread folding every (i, wi) source of its
+//      mask with the same pull-form key — no cross-lane reductions; states
+//      (makespan, back pointer) of every level in shared memory, chunk costs
+//      in the per-CTA scratch (L1).
+constexpr int kDpLaneMaxP = 8;
+__host__ __device__ inline size_t dpl_smem(int n_max, int e_max) {
+    const size_t n1 = (size_t)n_max + 1, S = (size_t)1 << kDpLaneMaxP;
+    return align_up(n1 * S * sizeof(double)) + align_up(n1 * S * sizeof(int16_t)) +
+           align_up(n1 * kDpLaneMaxP * sizeof(int16_t)) + align_up(S) + align_up((size_t)n_max * kDpLaneMaxP * 8) +
+           dpw_cols_bytes(n_max, kDpLaneMaxP, e_max);
+}
+
+__global__ void __launch_bounds__(256, 2) subset_dp_lane_kernel(const dm_tables* __restrict__ tables, int32_t n_scen,
+                                                                int32_t n_max, int32_t e_max, int16_t* out_owner,
+                                                                double* out_mk,
+                                                                int32_t* out_found, unsigned char* scratch,
+                                                                size_t scratch_per_cta) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int sc = blockIdx.x; sc < n_scen; sc += gridDim.x) {
+        __syncthreads();
+        const dm_tables tg = tables[sc];
+        const int n = tg.n, p = tg.p, S = 1 << p, n1 = n + 1;
+        DpScratch d = dp_carve(scratch + (size_t)blockIdx.x * scratch_per_cta, n, p);
+        unsigned char* b = dsm;
+        double* mk = reinterpret_cast<double*>(b); b += align_up((size_t)n1 * S * sizeof(double));
+        int16_t* back = reinterpret_cast<int16_t*>(b); b += align_up((size_t)n1 * S * sizeof(int16_t));
+        int16_t* jlim = reinterpret_cast<int16_t*>(b); b += align_up((size_t)n1 * p * sizeof(int16_t));
+        uint8_t* order = b; b += align_up((size_t)S);
+        double* ccj = reinterpret_cast<double*>(b); b += align_up((size_t)n * p * sizeof(double));   // level j's chunk costs
+        // the instance columns the table builds read, staged in shared memory
+        // (their loops are dependent chains of loads)
+        const dm_tables t = dpw_stage(tg, b, threadIdx.x, e_max, blockDim.x);
+        __syncthreads();
+        // ---- _fits break points (:313-315) and chunk_cost (:294-302), as subset_dp_kernel
+        for (int it = threadIdx.x; it < n * p; it += blockDim.x) {
+            const int i = it / p, wi = it % p;
+            int j = i + 1;
+            while (j <= n && fits_range(t, wi, i, j)) ++j;
+            jlim[i * p + wi] = (int16_t)j;
+        }
+        for (int it = threadIdx.x; it < n * p; it += blockDim.x) {
+            const int i = it / p, wi = it % p;
+            double rd = 0.0;
+            for (int j = i + 1; j <= n; ++j) {
+                if (include_comm(t))
+                    for (int e = t.edge_ptr[j - 1]; e < t.edge_ptr[j]; ++e)
+                        if (t.edge_src[e] < i) rd = __dadd_rn(rd, comm_time(t.def_alpha, t.def_beta, t.edge_m[e]));
+                const double fl = col_range(t.flops, t.pre_flops, flops_exact(t), i, j, np_flops(t));
+                d.cc[((size_t)i * n1 + j) * p + wi] = fl / t.speed[wi] + rd;
+            }
+        }
+        // masks by popcount, then value
+        if (threadIdx.x < S) {
+            const int M = threadIdx.x, pc = __popc(M);
+            int pos = 0;
+            for (int q = 0; q < S; ++q) {
+                const int pq = __popc(q);
+                pos += (pq < pc || (pq == pc && q < M)) ? 1 : 0;
+            }
+            order[pos] = (uint8_t)M;
+        }
+        for (int it = threadIdx.x; it < n1 * S; it += blockDim.x) back[it] = -1;
+        __syncthreads();
+        if (threadIdx.x == 0) { mk[0] = 0.0; back[0] = 0; }  // state (0, 0)
+        __syncthreads();
+        const int M = threadIdx.x < S ? (int)order[threadIdx.x] : 0;
+        const int pc = __popc(M);
+        for (int j = 1; j <= n; ++j) {
+            // this level's chunk costs cc[i][j][wi] into shared memory (one
+            // parallel round of loads instead of one per source evaluation)
+            for (int it = threadIdx.x; it < j * p; it += blockDim.x)
+                ccj[it] = d.cc[((size_t)(it / p) * n1 + j) * p + (it % p)];
+            __syncthreads();
+            if (threadIdx.x < S && pc > 0 && pc <= j) {
+                double bv = 0.0;
+                int bsec = 0x7fffffff, bsrc = -1;
+                for (uint32_t mm = (uint32_t)M; mm; mm &= mm - 1) {
+                    const int wi = __ffs(mm) - 1;
+                    const int srcm = M ^ (1 << wi);
+                    // a source with pc-1 workers covers >= pc-1 stages; sources
+                    // evaluated branch-free, unrolled (independent loads in flight)
+#pragma unroll 4
+                    for (int i = pc - 1; i < j; ++i) {
+                        const int src = i * S + srcm;
+                        const bool ok = back[src] >= 0 && j < jlim[i * p + wi];
+                        const double m0 = mk[src];
+                        const double cc = ccj[i * p + wi];
+                        const double v = cc > m0 ? cc : m0;        // max(mk, chunk_cost) :316
+                        const int sec = i * 64 + (63 - wi);
+                        if (ok && (bsrc < 0 || key_less(v, sec, bv, bsec))) { bv = v; bsec = sec; bsrc = (i << 8) | wi; }
+                    }
+                }
+                if (bsrc >= 0) {
+                    mk[j * S + M] = bv;
+                    back[j * S + M] = (int16_t)bsrc;
+                }
+            }
+            __syncthreads();
+        }
+        // ---- finals: smallest (makespan, mask) among states with j == n (:321-325)
+        __shared__ double fv[32];
+        __shared__ int fm[32];
+        double bv = 0.0;
+        int bm = -1;
+        for (int q = threadIdx.x; q < S; q += blockDim.x) {
+            if (back[n * S + q] < 0) continue;
+            const double v = mk[n * S + q];
+            if (bm < 0 || v < bv || (v == bv && q < bm)) { bv = v; bm = q; }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ov = __shfl_down_sync(0xffffffffu, bv, off);
+            const int om = __shfl_down_sync(0xffffffffu, bm, off);
+            if (om >= 0 && (bm < 0 || ov < bv || (ov == bv && om < bm))) { bv = ov; bm = om; }
+        }
+        if (lane == 0) { fv[wid] = bv; fm[wid] = bm; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < nwarps; ++w)
+                if (fm[w] >= 0 && (bm < 0 || fv[w] < bv || (fv[w] == bv && fm[w] < bm))) { bv = fv[w]; bm = fm[w]; }
+            int16_t* own = out_owner + (size_t)sc * n_max;
+            for (int i = 0; i < n_max; ++i) own[i] = -1;
+            if (bm >= 0) {
+                int j = n, q = bm;
+                while (j > 0) {
+                    const int bb = back[j * S + q];
+                    const int i = bb >> 8, wi = bb & 0xff;
+                    for (int s2 = i; s2 < j; ++s2) own[s2] = (int16_t)wi;
+                    q &= ~(1 << wi);
+                    j = i;
+                }
+                out_mk[sc] = bv;
+                out_found[sc] = 1;
+            } else {
+                out_mk[sc] = __longlong_as_double(0x7ff0000000000000LL);
+                out_found[sc] = 0;
+            }
+        }
+    }
+}
 
 __global__ void __launch_bounds__(32 * kDpWarps) subset_dp_warp_kernel(const dm_tables* __restrict__ tables,
                                                                        int32_t n_scen, int32_t n_max,
@@ -536,6 +679,21 @@ int dm_subset_dp(const dm_tables* tables, int32_t n_scen, int32_t n_max, int32_t
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    {   // mid-size fleets: one thread per target mask
+        const char* dis = std::getenv("DM_DISABLE_DP_LANE");
+        const int e_max_l = 4 * n_max;
+        const size_t smem_l = dm::dpl_smem(n_max, e_max_l);
+        if (p_max <= dm::kDpLaneMaxP && n_max < 128 && smem_l <= 110 * 1024 && !(dis && dis[0] && dis[0] != '0')) {
+            int64_t grid = (int64_t)sms * 2;
+            if (grid > n_scen) grid = n_scen;
+            cudaFuncSetAttribute(dm::subset_dp_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_l);
+            dm::subset_dp_lane_kernel<<<(int)grid, 256, smem_l, (cudaStream_t)stream>>>(
+                tables, n_scen, n_max, e_max_l, out_owner, out_makespan, out_found, (unsigned char*)scratch,
+                dm::dp_scratch_bytes(n_max, p_max));
+            DM_CHECK_LAUNCH();
+            return DM_OK;
+        }
+    }
     const size_t n1 = (size_t)n_max + 1;
     const size_t st = dm::align_up((n1 << p_max) * 8) + dm::align_up((n1 << p_max) * 4) + dm::align_up(n1 * p_max * 2);
     const size_t cc = n1 * n1 * p_max * 8;

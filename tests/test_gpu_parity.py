@@ -265,6 +265,37 @@ def test_subset_dp_batch(oracle_mod, engine_ready):
         assert owner[s, :len(st)].tolist() == own.tolist()
 
 
+def test_subset_dp_mid_fleets(oracle_mod, engine_ready):
+    """Fleets of 6-8 workers (the thread-per-mask DP kernel): chosen runs and
+    makespans equal the oracle's _subset_dp restatement, including forced
+    ties (identical peers, uniform stages) and infeasible instances."""
+    rng = np.random.default_rng(66)
+    insts = []
+    for k in range(48):
+        n, p = int(rng.integers(8, 39)), int(rng.integers(6, 9))
+        st, fl = big_instance(rng, n, p, dag=k % 4 == 1, pressure=(0.02, 0.5) if k % 6 else (0.001, 0.01))
+        insts.append((st, fl))
+    for p in (6, 7, 8):                                          # ties: equal speeds, equal stages
+        st = [M.Stage(i, f"s{i}", 1e12, 2.0**20, 1024.0, 512.0, ((i - 1, 1 << 20),) if i else ())
+              for i in range(int(rng.integers(p, 30)))]
+        insts.append((st, uniform_fleet([50e12] * p, link=M.Link(1e-3, 8 / 1e10))))
+    hosts = [build_host(s, f) for s, f in insts]
+    batch = engine.device_batch(hosts)
+    n_max = max(h.n for h in hosts)
+    owner, mk, found, _ = engine.subset_dp(batch, n_max, 8)
+    owner, mk, found = owner.cpu().numpy(), mk.cpu().numpy(), found.cpu().numpy()
+    n_found = 0
+    for s, (st, fl) in enumerate(insts):
+        own, m = oracle_mod.Instance(st, fl).subset_dp()
+        if own is None:
+            assert found[s] == 0, s
+            continue
+        n_found += 1
+        assert found[s] == 1 and mk[s] == m, s
+        assert owner[s, :len(st)].tolist() == own.tolist(), s
+    assert n_found >= 20
+
+
 def test_prop_hill_batch_and_epilogue(oracle_mod, engine_ready):
     rng = np.random.default_rng(31)
     insts = [big_instance(rng, int(rng.integers(20, 80)), int(rng.integers(12, 40)), dag=k % 2 == 1, links=k % 5 == 0)
