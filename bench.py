@@ -248,7 +248,10 @@ def run_b200(args, rank, world, local_rank):
         out = None
         for k in range(steps):
             nxt = sweeper.submit(mine) if k + 1 < steps else None
-            out = finish(sweeper.result(prev, records=True))
+            if world > 1:            # all-gather on a side stream: not queued behind request k+1
+                out = merge(sweeper.gathered(prev))
+            else:
+                out = finish(sweeper.result(prev, records=True))
             prev = nxt
         return out
     run_e2e(max(args.warmup, 3))

@@ -128,6 +128,25 @@ class SplitSweeper:
         self.hosts[slot] = hosts
         return slot
 
+    def gathered(self, slot: int, group=None):
+        """Multi-GPU form of result(slot, records=True): the slot's DEVICE
+        records all-gathered over the process group (one NCCL all-gather) on
+        a stream of their own — it waits for this request's graph only, not
+        for the request queued behind it on the main stream — then copied to
+        the host: uint8[world, units, 40] (merge with dist.merge_records)."""
+        torch = engine._torch()
+        import torch.distributed as dist
+        if not hasattr(self, "_gstream"):
+            self._gstream = torch.cuda.Stream()
+        g = self.graphs[slot]
+        world = dist.get_world_size(group)
+        with torch.cuda.stream(self._gstream):
+            self._gstream.wait_event(self.events[slot])
+            out = torch.empty(world * g.out.numel(), dtype=torch.uint8, device=g.out.device)
+            dist.all_gather_into_tensor(out, g.out.reshape(-1), group=group)
+            host = out.view(world, g.out.shape[0], -1).cpu()
+        return host.numpy()
+
     def result(self, slot: int, records: bool = False):
         self.events[slot].synchronize()
         g = self.graphs[slot]
