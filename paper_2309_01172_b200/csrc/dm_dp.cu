@@ -560,24 +560,27 @@ __global__ void __launch_bounds__(32 * kDpCtaWarps) subset_dp_cta_kernel(const d
         const bool mvalid = M < S;
         const int pc = mvalid ? __popc(M) : 0;
         for (int j = 1; j <= n; ++j) {
-            double bv = 0.0;
+            double bv = __longlong_as_double(0x7ff0000000000000LL);
             int bsec = 0x7fffffff, bsrc = -1;
             if (mvalid && pc >= 1 && pc <= j) {
+                // a lane visits its sources in key order (i ascending, then
+                // worker descending), so within the lane the first strict
+                // minimum of the value alone is the key minimum; source values
+                // are finite, so the +inf start admits the first valid one
                 for (int i = g; i < j; i += G) {
                     const double* crow = cc + (size_t)dpw_pair(i, j, n) * p;
-                    for (uint32_t mm = (uint32_t)M; mm; mm &= mm - 1) {
-                        const int wi = __ffs(mm) - 1;
+                    for (uint32_t mm = (uint32_t)M; mm; ) {
+                        const int wi = 31 - __clz(mm);
+                        mm ^= 1u << wi;
                         const int src = i * S + (M ^ (1 << wi));
                         const int32_t bk = back[src];
                         const int jl = jlim[i * p + wi];
                         const double m0 = mk[src], c = crow[wi];
                         const double v = c > m0 ? c : m0;      // max(mk, chunk_cost) :316
-                        const int sec = i * 64 + (63 - wi);
-                        if (bk >= 0 && j < jl && (bsrc < 0 || key_less(v, sec, bv, bsec))) {
-                            bv = v; bsec = sec; bsrc = (i << 8) | wi;
-                        }
+                        if (bk >= 0 && j < jl && v < bv) { bv = v; bsrc = (i << 8) | wi; }
                     }
                 }
+                if (bsrc >= 0) bsec = (bsrc >> 8) * 64 + (63 - (bsrc & 0xff));
             }
             for (int off = 1; off < G; off <<= 1) {             // combine the G lanes of this mask
                 const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
