@@ -25,7 +25,6 @@ from __future__ import annotations
 
 import functools
 import json
-import math
 
 import numpy as np
 

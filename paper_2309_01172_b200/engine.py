@@ -10,7 +10,7 @@ import math
 import numpy as np
 
 from . import _lib
-from .tensorize import DeviceBatch, HostTables, build_host
+from .tensorize import DeviceBatch, HostTables
 
 _WINNER_BYTES = C.sizeof(_lib.DmWinner)
 

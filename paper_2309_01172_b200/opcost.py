@@ -22,7 +22,6 @@ from typing import NamedTuple
 import numpy as np
 
 from . import _lib
-from .refapi import FleetError
 from .tensorize import build_host
 
 ELEMENT_BYTES = 4
