@@ -390,10 +390,10 @@ struct StreamWin {
 // words).  Runs are visited from the last boundary down (FLO gives the
 // highest set bit in one instruction); per run: the owner byte, its bit in
 // `seen`, the table address, one 8-byte table load, the running maximum of
-// |T| and the running minimum of the addresses of failing runs (T's sign
-// bit) — table addresses grow with the run's first stage, so the minimum is
-// the first failing run in verify order (scheduling.py:184-203), whose
-// violation code is read once after the loop.  A peer seen twice
+// |T| and the address of the last failing run visited (T's sign bit) —
+// runs are visited by decreasing first stage and table addresses grow with
+// it, so that is the first failing run in verify order
+// (scheduling.py:184-203), whose violation code is read once after the loop.  A peer seen twice
 // (non-contiguous owner vector) or an owner index >= P (bit outside the
 // fleet) sends the candidate to the grouped general path.
 template <bool PAIR, bool SQUARE, int NT, int NW>
@@ -442,8 +442,7 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
                 }
             }
             mk = fabs(v) > fabs(mk) ? v : mk;                    // sign cleared after the loop
-            const uint32_t s = (uint32_t)(__double2hiint(v) >> 31);
-            bad = min(bad, addr | ~s);
+            bad = __double2hiint(v) < 0 ? addr : bad;           // runs visited by decreasing address
             end = b;
         };
         if (NW > 8)
@@ -473,7 +472,7 @@ __device__ __forceinline__ void stream_tile(const dm_tables& t, const StreamCtx&
             auto fold = [&](uint32_t w, uint32_t addr, double v) {
                 seen |= 1u << w;
                 mk = fabs(v) > fabs(mk) ? v : mk;
-                bad = min(bad, addr | ~(uint32_t)(__double2hiint(v) >> 31));
+                bad = __double2hiint(v) < 0 ? addr : bad;
             };
             for (uint32_t y = (uint32_t)bm & X.mask_lo; y; ) {
                 const uint32_t k1 = 31u - __clz(y);
