@@ -33,6 +33,22 @@ _DIM = {_lib.DM_V_GPU: "gpu", _lib.DM_V_CPU: "cpu", _lib.DM_V_DISK: "disk"}
 _INF = math.inf
 
 
+def _peer_load(*vals):
+    """T.PeerLoad(*vals).  The reference's PeerLoad is a frozen dataclass
+    with a plain __dict__ and no __post_init__: its generated __init__ sets
+    each field with object.__setattr__, so the same object is built by one
+    __dict__ update (a report carries one row per worker: 256 on C3).  Any
+    other class goes through its constructor."""
+    cls = T.PeerLoad
+    fields = getattr(cls, "__dataclass_fields__", None)
+    if (fields is None or hasattr(cls, "__slots__") or hasattr(cls, "__post_init__")
+            or len(fields) != len(vals)):
+        return cls(*vals)
+    obj = object.__new__(cls)
+    obj.__dict__.update(zip(fields, vals))
+    return obj
+
+
 def _check_inputs(stages, workers):
     """scheduling.py:281-285."""
     if not stages:
@@ -152,6 +168,7 @@ def _report(stages, fleet, runs, include_comm, trace, res, c=0, host=None):
     typed = host is not None and (bool(host.flags & (_lib.DM_F_NP_FLOPS | _lib.DM_F_NP_COMM))
                                   or bool(host.arrays["peer_np"].any()))
     makespan = 0.0
+    side = stage_side(stages) if stages else None
     for r in order:
         peer, idxs = runs[r]
         indices = tuple(sorted(idxs))
@@ -163,14 +180,20 @@ def _report(stages, fleet, runs, include_comm, trace, res, c=0, host=None):
         ordered_runs.append((peer, indices))
         load = compute + read
         makespan = max(makespan, load)          # :222, keeps the first maximal value's type
-        rows.append(T.PeerLoad(peer, indices, compute, read, load,
-                               sum(stages[i].gpu_bytes for i in indices),
-                               sum(stages[i].cpu_bytes for i in indices),
-                               sum(stages[i].disk_bytes for i in indices)))
+        rb = None
+        if side is not None and indices[-1] - indices[0] + 1 == len(indices) and 0 <= indices[0] \
+                and indices[-1] < len(stages):
+            rb = side.range_bytes(indices[0], indices[-1] + 1)       # contiguous run: exact prefixes
+        if rb is None:
+            rb = (sum(stages[i].gpu_bytes for i in indices), sum(stages[i].cpu_bytes for i in indices),
+                  sum(stages[i].disk_bytes for i in indices))
+        rows.append(_peer_load(peer, indices, compute, read, load, *rb))
     assigned = {peer for peer, idxs in runs if idxs}
-    for peer in fleet.worker_ids():
+    # the idle rows in worker order (the tensoriser's peer order starts with
+    # fleet.worker_ids(), so the sort is not repeated)
+    for peer in (host.peer_ids[:host.p] if host is not None else fleet.worker_ids()):
         if peer not in assigned:
-            rows.append(T.PeerLoad(peer, (), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0))
+            rows.append(_peer_load(peer, (), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0))
     mk = float(res["makespan"][c])
     if typed and mk == makespan:
         mk = makespan
@@ -282,7 +305,7 @@ def schedule(stages, fleet, *, include_comm: bool = True):
         # proportional split + hill climb keep run q on worker q and chain
         # stages read only from the previous run: links (q-1, q) suffice
         pairs = [(q - 1, q) for q in range(1, min(n, p))]
-    host = build_host(stages, fleet, include_comm, link_pairs=pairs)
+    host = build_host(stages, fleet, include_comm, link_pairs=pairs, workers=workers)
     out = engine.schedule_slot().schedule(host, use_dp, use_dp and bool(fleet.links))
     b, pe = out["bounds"], out["peers"]
     runs = tuple((workers[int(pe[q])], tuple(range(int(b[q]), int(b[q + 1])))) for q in range(out["n_runs"]))

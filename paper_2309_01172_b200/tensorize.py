@@ -131,7 +131,7 @@ class _StageSide:
 
     __slots__ = ("stages", "n", "flops", "pre_flops", "gpu", "pre_gpu", "cpu", "pre_cpu", "disk", "pre_disk",
                  "bytes_exact", "edge_ptr", "edge_src", "nbytes", "nbytes_f64", "is_chain", "backward",
-                 "np_flops", "np_bytes", "np_edges", "src_range_ok")
+                 "np_flops", "np_bytes", "np_edges", "src_range_ok", "byte_pre")
 
     def __init__(self, stages):
         self.stages = stages                      # keeps the (immutable) Stage objects alive: ids stay unique
@@ -162,9 +162,34 @@ class _StageSide:
 
         def _np(v):
             return type(v) not in (int, float, bool)
+        # per byte column: int when every value is a Python int, float when
+        # every value is a Python float, else None (range_bytes falls back)
+        def _kind(vals):
+            if all(type(v) is int for v in vals):
+                return int
+            if all(type(v) is float for v in vals):
+                return float
+            return None
+        kinds = tuple(_kind([getattr(s_, a) for s_ in stages]) for a in ("gpu_bytes", "cpu_bytes", "disk_bytes"))
+        pres = (self.pre_gpu, self.pre_cpu, self.pre_disk)
+        # Python-int prefixes (fast scalar access) and result types, or None
+        self.byte_pre = (tuple(pr.tolist() for pr in pres) + kinds
+                         if all(pr is not None for pr in pres) and all(k is not None for k in kinds) else None)
         self.np_flops = any(_np(s.flops) for s in stages)
         self.np_bytes = any(_np(s.gpu_bytes) or _np(s.cpu_bytes) or _np(s.disk_bytes) for s in stages)
         self.np_edges = any(_np(nb) for nb in nbs)
+
+
+    def range_bytes(self, a: int, b: int):
+        """(Σ gpu_bytes, Σ cpu_bytes, Σ disk_bytes) over stages [a, b) with
+        the value and type of the reference's sum() of the attributes
+        (scheduling.py:228-230), from the exact prefixes; None when a column
+        has no exact prefix or mixes types."""
+        bp = self.byte_pre
+        if bp is None:
+            return None
+        g, c, d, kg, kc, kd = bp
+        return kg(g[b] - g[a]), kc(c[b] - c[a]), kd(d[b] - d[a])
 
 
 _STAGE_CACHE: dict = {}
@@ -193,16 +218,17 @@ def stage_side(stages) -> _StageSide:
     return _stage_side(stages) if params is not None and params.frozen else _StageSide(stages)
 
 
-def build_host(stages, fleet, include_comm: bool = True, link_pairs=None) -> HostTables:
+def build_host(stages, fleet, include_comm: bool = True, link_pairs=None, workers=None) -> HostTables:
     """Tensorise one instance on the host (O(n + E + P + |links|); the stage
     side is cached per stage list).  ``link_pairs`` (peer-index pairs) limits
     the pairwise link matrix to the entries a caller's kernels will read
     (resolved with the fleet's own link_between, hardware.py:136-140; the
-    rest holds the default link) instead of every override."""
+    rest holds the default link) instead of every override.  ``workers``:
+    the caller's fleet.worker_ids() (the sort is not repeated)."""
     stages = list(stages)
     st = stage_side(stages)
     n = st.n
-    workers = tuple(fleet.worker_ids())
+    workers = tuple(fleet.worker_ids() if workers is None else workers)
     if len(workers) == len(fleet.peers):
         order = workers
     else:
