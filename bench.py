@@ -558,7 +558,7 @@ def dp_measure(dev, fp64_peak):
     trans = sum(range(1, n + 1)) * p * 2 ** (p - 1)
     ops = 2 * trans + 4 * (n * (n + 1) // 2) * p
     rate = len(fleets) / (ms / 1e3)
-    prof = ncu_metrics("subset_dp_warp_kernel")   # the round-2 capture of the warp form (the CTA form runs here)
+    prof = ncu_metrics("subset_dp_cta_kernel")    # the form this batch runs (one 4-warp CTA per DP)
     return {"config": "C1 gpt2-small (26 stages) x 4 workers, 1024 link-grid fleets (bw logspace(-1,2,32) x "
                       "alpha linspace(0,10ms,32)), one _subset_dp each", "dps": len(fleets), "ms": ms,
             "value": rate, "unit": "DPs/s", "timing": "device time of the launch (CUDA-graph replay, 20 steps)",
@@ -568,8 +568,9 @@ def dp_measure(dev, fp64_peak):
                          "work": f"{ops} fp64 ops per DP ({trans} pull-form transitions x (max + compare) + "
                                  "chunk costs)",
                          "ncu": prof,
-                         "note": "one warp per DP walks the j-recurrence sequentially: latency-bound, not "
-                                 "throughput-bound (see ncu warps/issue active)"}}
+                         "note": "one 4-warp CTA per DP walks the j-recurrence level by level (one barrier per "
+                                 "level): latency-bound, not throughput-bound (see ncu issue active and the "
+                                 "short-scoreboard / barrier stalls)"}}
 
 
 def c4_measure(dev, fp64_peak, n_scen=10 ** 6):
@@ -703,7 +704,10 @@ def dp_c4b_measure(dev, n_scen=4096):
     cpu = 8 / (_t.perf_counter() - t0)
     return {"config": f"C4b: {n_scen} scenarios, layer-cell chains n = L+2 in [26, 38], p in [5, 8] "
                       "(n^2 p 2^p <= 3e6: the exact subset-DP path)", "dps": n_scen, "ms": ms,
-            "value": n_scen / (ms / 1e3), "unit": "DPs/s", "oracle_spot_check": bool(ok), "cpu_baseline_1core": cpu}
+            "value": n_scen / (ms / 1e3), "unit": "DPs/s", "oracle_spot_check": bool(ok), "cpu_baseline_1core": cpu,
+            "roofline": {"bound": "latency", "ncu": ncu_metrics("subset_dp_lane_kernel"),
+                         "note": "one thread per target mask; the per-level barrier waits for the masks with the "
+                                 "most workers (barrier stalls dominate the ncu capture)"}}
 
 
 def api_latency_measure(dev):
