@@ -705,9 +705,9 @@ def dp_c4b_measure(dev, n_scen=4096):
     return {"config": f"C4b: {n_scen} scenarios, layer-cell chains n = L+2 in [26, 38], p in [5, 8] "
                       "(n^2 p 2^p <= 3e6: the exact subset-DP path)", "dps": n_scen, "ms": ms,
             "value": n_scen / (ms / 1e3), "unit": "DPs/s", "oracle_spot_check": bool(ok), "cpu_baseline_1core": cpu,
-            "roofline": {"bound": "latency", "ncu": ncu_metrics("subset_dp_lane_kernel"),
-                         "note": "one thread per target mask; the per-level barrier waits for the masks with the "
-                                 "most workers (barrier stalls dominate the ncu capture)"}}
+            "roofline": {"bound": "latency", "ncu": ncu_metrics("subset_dp_pair_kernel"),
+                         "note": "one thread per (target mask, worker) source family, one 1024-thread CTA per DP; "
+                                 "two barriers per level (the per-mask reduction) dominate the stalls"}}
 
 
 def api_latency_measure(dev):

@@ -226,50 +226,63 @@ __device__ inline dm_tables dpw_stage(const dm_tables& t, unsigned char* b, int 
 
 __device__ __forceinline__ int dpw_pair(int i, int j, int n) { return i * n - i * (i - 1) / 2 + (j - i - 1); }
 
-// ---- mid-size fleets (32 < 2^p <= 256): one CTA per scenario, one THREAD
-//      per target mask (masks ordered by popcount, so a warp's masks have the
-//      same source count), each thread folding every (i, wi) source of its
-//      mask with the same pull-form key — no cross-lane reductions; states
-//      (makespan, back pointer) of every level in shared memory, chunk costs
-//      in the per-CTA scratch (L1).
-constexpr int kDpLaneMaxP = 8;
-__host__ __device__ inline size_t dpl_smem(int n_max, int e_max) {
-    const size_t n1 = (size_t)n_max + 1, S = (size_t)1 << kDpLaneMaxP;
+constexpr int kDpLaneMaxP = 8;   // fleets of up to 8 workers: 2^p <= 256 target masks
+
+// ---- mid-size fleets (32 < 2^p <= 256): one CTA per scenario, one thread
+//      per (target mask, worker) SOURCE FAMILY: thread (M, wi) folds sources
+//      (i, M - wi) over i in key order (a value-only compare keeps the first
+//      strict minimum), writes its best to shared memory, and one thread per
+//      mask then reduces its workers with the full key — every thread of a
+//      level carries ~j source evaluations (a thread per mask would carry
+//      popcount(M) x j, and the masks with most workers would set each
+//      level's length).  Pairs are ordered by popcount so a warp's pairs have
+//      the same source count; states of every level in shared memory (int16
+//      back pointers), each level's chunk-cost column staged in shared memory
+//      while the previous level reduces, instance columns staged once.
+constexpr int kDpPairThreads = 1024;
+__host__ __device__ inline size_t dpp_smem(int n_max, int e_max) {
+    const size_t n1 = (size_t)n_max + 1, S = (size_t)1 << kDpLaneMaxP, P = (size_t)kDpLaneMaxP;
     return align_up(n1 * S * sizeof(double)) + align_up(n1 * S * sizeof(int16_t)) +
-           align_up(n1 * kDpLaneMaxP * sizeof(int16_t)) + align_up(S) + align_up((size_t)n_max * kDpLaneMaxP * 8) +
-           dpw_cols_bytes(n_max, kDpLaneMaxP, e_max);
+           align_up(n1 * P * sizeof(int16_t)) + align_up(S * P * 2) +             // jlim, pair (mask, worker)
+           align_up(S * P * sizeof(double)) + align_up(S * P) +                      // per-pair best value, stage
+           2 * align_up((size_t)n_max * P * 8) + dpw_cols_bytes(n_max, kDpLaneMaxP, e_max);
 }
 
-__global__ void __launch_bounds__(256, 2) subset_dp_lane_kernel(const dm_tables* __restrict__ tables, int32_t n_scen,
-                                                                int32_t n_max, int32_t e_max, int16_t* out_owner,
-                                                                double* out_mk,
-                                                                int32_t* out_found, unsigned char* scratch,
-                                                                size_t scratch_per_cta) {
+__global__ void __launch_bounds__(kDpPairThreads, 1) subset_dp_pair_kernel(const dm_tables* __restrict__ tables,
+                                                                           int32_t n_scen, int32_t n_max,
+                                                                           int32_t e_max, int16_t* out_owner,
+                                                                           double* out_mk, int32_t* out_found,
+                                                                           unsigned char* scratch,
+                                                                           size_t scratch_per_cta) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
     for (int sc = blockIdx.x; sc < n_scen; sc += gridDim.x) {
         __syncthreads();
         const dm_tables tg = tables[sc];
         const int n = tg.n, p = tg.p, S = 1 << p, n1 = n + 1;
+        const int npairs = p << (p - 1);                      // sum of popcounts over the 2^p masks
         DpScratch d = dp_carve(scratch + (size_t)blockIdx.x * scratch_per_cta, n, p);
         unsigned char* b = dsm;
         double* mk = reinterpret_cast<double*>(b); b += align_up((size_t)n1 * S * sizeof(double));
         int16_t* back = reinterpret_cast<int16_t*>(b); b += align_up((size_t)n1 * S * sizeof(int16_t));
         int16_t* jlim = reinterpret_cast<int16_t*>(b); b += align_up((size_t)n1 * p * sizeof(int16_t));
-        uint8_t* order = b; b += align_up((size_t)S);
-        double* ccj = reinterpret_cast<double*>(b); b += align_up((size_t)n * p * sizeof(double));   // level j's chunk costs
-        // the instance columns the table builds read, staged in shared memory
-        // (their loops are dependent chains of loads)
-        const dm_tables t = dpw_stage(tg, b, threadIdx.x, e_max, blockDim.x);
+        uint8_t* pm = b;                                      // pair -> mask
+        uint8_t* pw = b + (size_t)S * kDpLaneMaxP; b += align_up((size_t)S * kDpLaneMaxP * 2);   // pair -> worker
+        double* cv = reinterpret_cast<double*>(b); b += align_up((size_t)S * kDpLaneMaxP * sizeof(double));
+        int8_t* ci = reinterpret_cast<int8_t*>(b); b += align_up((size_t)S * kDpLaneMaxP);
+        double* ccb[2];
+        ccb[0] = reinterpret_cast<double*>(b); b += align_up((size_t)n_max * kDpLaneMaxP * 8);
+        ccb[1] = reinterpret_cast<double*>(b); b += align_up((size_t)n_max * kDpLaneMaxP * 8);
+        const dm_tables t = dpw_stage(tg, b, tid, e_max, blockDim.x);
         __syncthreads();
         // ---- _fits break points (:313-315) and chunk_cost (:294-302), as subset_dp_kernel
-        for (int it = threadIdx.x; it < n * p; it += blockDim.x) {
+        for (int it = tid; it < n * p; it += blockDim.x) {
             const int i = it / p, wi = it % p;
             int j = i + 1;
             while (j <= n && fits_range(t, wi, i, j)) ++j;
             jlim[i * p + wi] = (int16_t)j;
         }
-        for (int it = threadIdx.x; it < n * p; it += blockDim.x) {
+        for (int it = tid; it < n * p; it += blockDim.x) {
             const int i = it / p, wi = it % p;
             double rd = 0.0;
             for (int j = i + 1; j <= n; ++j) {
@@ -280,36 +293,34 @@ __global__ void __launch_bounds__(256, 2) subset_dp_lane_kernel(const dm_tables*
                 d.cc[((size_t)i * n1 + j) * p + wi] = fl / t.speed[wi] + rd;
             }
         }
-        // masks by popcount, then value
-        if (threadIdx.x < S) {
-            const int M = threadIdx.x, pc = __popc(M);
-            int pos = 0;
-            for (int q = 0; q < S; ++q) {
-                const int pq = __popc(q);
-                pos += (pq < pc || (pq == pc && q < M)) ? 1 : 0;
+        // pairs in (popcount, mask, worker) order: mask M's first pair sits
+        // after every pair of the masks with fewer workers and of the masks
+        // with as many workers and a smaller value
+        if (tid < S) {
+            const int M = tid, pc = __popc(M);
+            int base = 0;
+            for (int q = 0; q < M; ++q) base += __popc(q) == pc ? pc : 0;
+            for (int q = 0; q < S; ++q) base += __popc(q) < pc ? __popc(q) : 0;
+            int r = 0;
+            for (uint32_t mm = (uint32_t)M; mm; mm &= mm - 1, ++r) {
+                pm[base + r] = (uint8_t)M;
+                pw[base + r] = (uint8_t)(__ffs(mm) - 1);
             }
-            order[pos] = (uint8_t)M;
         }
-        for (int it = threadIdx.x; it < n1 * S; it += blockDim.x) back[it] = -1;
+        for (int it = tid; it < n1 * S; it += blockDim.x) back[it] = -1;
+        for (int it = tid; it < p; it += blockDim.x) ccb[1][it] = d.cc[((size_t)0 * n1 + 1) * p + it];   // level 1
         __syncthreads();
-        if (threadIdx.x == 0) { mk[0] = 0.0; back[0] = 0; }  // state (0, 0)
+        if (tid == 0) { mk[0] = 0.0; back[0] = 0; }  // state (0, 0)
         __syncthreads();
-        const int M = threadIdx.x < S ? (int)order[threadIdx.x] : 0;
-        const int pc = __popc(M);
         for (int j = 1; j <= n; ++j) {
-            // this level's chunk costs cc[i][j][wi] into shared memory (one
-            // parallel round of loads instead of one per source evaluation)
-            for (int it = threadIdx.x; it < j * p; it += blockDim.x)
-                ccj[it] = d.cc[((size_t)(it / p) * n1 + j) * p + (it % p)];
-            __syncthreads();
-            if (threadIdx.x < S && pc > 0 && pc <= j) {
-                double bv = 0.0;
-                int bsec = 0x7fffffff, bsrc = -1;
-                for (uint32_t mm = (uint32_t)M; mm; mm &= mm - 1) {
-                    const int wi = __ffs(mm) - 1;
+            const double* ccj = ccb[j & 1];
+            // ---- every (mask, worker) source family of level j
+            for (int q = tid; q < npairs; q += blockDim.x) {
+                const int M = pm[q], wi = pw[q], pc = __popc(M);
+                double bv = __longlong_as_double(0x7ff0000000000000LL);
+                int bi = -1;
+                if (pc <= j) {
                     const int srcm = M ^ (1 << wi);
-                    // a source with pc-1 workers covers >= pc-1 stages; sources
-                    // evaluated branch-free, unrolled (independent loads in flight)
 #pragma unroll 4
                     for (int i = pc - 1; i < j; ++i) {
                         const int src = i * S + srcm;
@@ -317,14 +328,37 @@ __global__ void __launch_bounds__(256, 2) subset_dp_lane_kernel(const dm_tables*
                         const double m0 = mk[src];
                         const double cc = ccj[i * p + wi];
                         const double v = cc > m0 ? cc : m0;        // max(mk, chunk_cost) :316
-                        const int sec = i * 64 + (63 - wi);
-                        if (ok && (bsrc < 0 || key_less(v, sec, bv, bsec))) { bv = v; bsec = sec; bsrc = (i << 8) | wi; }
+                        if (ok && v < bv) { bv = v; bi = i; }
                     }
                 }
-                if (bsrc >= 0) {
-                    mk[j * S + M] = bv;
-                    back[j * S + M] = (int16_t)bsrc;
+                cv[M * p + wi] = bv;
+                ci[M * p + wi] = (int8_t)bi;
+            }
+            __syncthreads();
+            // ---- each target mask reduces its workers with the full key;
+            //      the other threads stage level j+1's chunk costs
+            if (tid < S) {
+                const int M = tid, pc = __popc(M);
+                if (pc > 0 && pc <= j) {
+                    double bv = 0.0;
+                    int bsec = 0x7fffffff, bsrc = -1;
+                    for (uint32_t mm = (uint32_t)M; mm; mm &= mm - 1) {
+                        const int wi = __ffs(mm) - 1;
+                        const int i = ci[M * p + wi];
+                        if (i < 0) continue;
+                        const double v = cv[M * p + wi];
+                        const int sec = i * 64 + (63 - wi);
+                        if (bsrc < 0 || key_less(v, sec, bv, bsec)) { bv = v; bsec = sec; bsrc = (i << 8) | wi; }
+                    }
+                    if (bsrc >= 0) {
+                        mk[j * S + M] = bv;
+                        back[j * S + M] = (int16_t)bsrc;
+                    }
                 }
+            } else if (j < n) {
+                double* nxt = ccb[(j + 1) & 1];
+                for (int it = tid - S; it < (j + 1) * p; it += blockDim.x - S)
+                    nxt[it] = d.cc[((size_t)(it / p) * n1 + j + 1) * p + (it % p)];
             }
             __syncthreads();
         }
@@ -333,7 +367,7 @@ __global__ void __launch_bounds__(256, 2) subset_dp_lane_kernel(const dm_tables*
         __shared__ int fm[32];
         double bv = 0.0;
         int bm = -1;
-        for (int q = threadIdx.x; q < S; q += blockDim.x) {
+        for (int q = tid; q < S; q += blockDim.x) {
             if (back[n * S + q] < 0) continue;
             const double v = mk[n * S + q];
             if (bm < 0 || v < bv || (v == bv && q < bm)) { bv = v; bm = q; }
@@ -345,7 +379,7 @@ __global__ void __launch_bounds__(256, 2) subset_dp_lane_kernel(const dm_tables*
         }
         if (lane == 0) { fv[wid] = bv; fm[wid] = bm; }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             for (int w = 1; w < nwarps; ++w)
                 if (fm[w] >= 0 && (bm < 0 || fv[w] < bv || (fv[w] == bv && fm[w] < bm))) { bv = fv[w]; bm = fm[w]; }
             int16_t* own = out_owner + (size_t)sc * n_max;
@@ -682,15 +716,16 @@ int dm_subset_dp(const dm_tables* tables, int32_t n_scen, int32_t n_max, int32_t
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    {   // mid-size fleets: one thread per target mask
+    {   // mid-size fleets: one thread per (target mask, worker)
         const char* dis = std::getenv("DM_DISABLE_DP_LANE");
         const int e_max_l = 4 * n_max;
-        const size_t smem_l = dm::dpl_smem(n_max, e_max_l);
-        if (p_max <= dm::kDpLaneMaxP && n_max < 128 && smem_l <= 110 * 1024 && !(dis && dis[0] && dis[0] != '0')) {
-            int64_t grid = (int64_t)sms * 2;
+        const size_t smem_p = dm::dpp_smem(n_max, e_max_l);
+        if (p_max <= dm::kDpLaneMaxP && p_max >= 2 && n_max < 128 && smem_p <= 220 * 1024 &&
+            !(dis && dis[0] && dis[0] != '0')) {
+            int64_t grid = (int64_t)sms;
             if (grid > n_scen) grid = n_scen;
-            cudaFuncSetAttribute(dm::subset_dp_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_l);
-            dm::subset_dp_lane_kernel<<<(int)grid, 256, smem_l, (cudaStream_t)stream>>>(
+            cudaFuncSetAttribute(dm::subset_dp_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+            dm::subset_dp_pair_kernel<<<(int)grid, dm::kDpPairThreads, smem_p, (cudaStream_t)stream>>>(
                 tables, n_scen, n_max, e_max_l, out_owner, out_makespan, out_found, (unsigned char*)scratch,
                 dm::dp_scratch_bytes(n_max, p_max));
             DM_CHECK_LAUNCH();
