@@ -256,3 +256,40 @@ def test_tensoriser_link_matrix_and_stage_cache():
     assert h2.arrays["pre_flops"] is h.arrays["pre_flops"]              # cached stage side
     assert h2.def_alpha == 0.001 and "link_alpha" not in dict(h2.segments())
     assert TZ.stage_side(st) is TZ.stage_side(list(st))
+
+
+def test_report_fast_paths_match_reference_semantics():
+    """The report assembly's shortcuts build the same values and objects as
+    the reference's own code: per-run byte sums from the exact prefixes have
+    the value AND type of sum() over the stage attributes (ints stay ints,
+    floats stay floats, mixed columns fall back), and PeerLoad rows built
+    without the frozen dataclass's __init__ are equal, hash-equal and still
+    frozen."""
+    import dataclasses
+
+    from paper_2309_01172_b200 import scheduling as SCH
+    from paper_2309_01172_b200.tensorize import stage_side
+
+    def stages_of(vals):
+        return [M.Stage(i, f"s{i}", 1e9, g, c, d, ((i - 1, 8),) if i else ()) for i, (g, c, d) in enumerate(vals)]
+
+    rng = np.random.default_rng(3)
+    ints = [(int(rng.integers(1, 2**40)), int(rng.integers(1, 2**30)), int(rng.integers(0, 2**20))) for _ in range(40)]
+    floats = [(float(g), float(c), float(d)) for g, c, d in ints]
+    mixed = [(g if i % 2 else float(g), c, d) for i, (g, c, d) in enumerate(ints)]
+    for vals, exact in ((ints, True), (floats, True), (mixed, False)):
+        st = stages_of(vals)
+        side = stage_side(st)
+        for a, b in ((0, 1), (3, 17), (0, 40), (39, 40)):
+            got = side.range_bytes(a, b)
+            want = tuple(sum(getattr(st[i], f) for i in range(a, b)) for f in ("gpu_bytes", "cpu_bytes", "disk_bytes"))
+            if not exact:
+                assert got is None
+                continue
+            assert got == want and [type(x) for x in got] == [type(x) for x in want]
+    vals = ("7", (1, 2), 0.5, 0.25, 0.75, 10, 20.0, 30)
+    fast, ref = SCH._peer_load(*vals), M.PeerLoad(*vals)
+    assert type(fast) is type(ref) and fast == ref and hash(fast) == hash(ref) and repr(fast) == repr(ref)
+    assert dataclasses.astuple(fast) == dataclasses.astuple(ref)
+    with pytest.raises(dataclasses.FrozenInstanceError):
+        fast.peer = "8"
