@@ -499,6 +499,18 @@ def test_splits_phase_needs_workspace(engine_ready):
                                   None, 0, 3, _lib.stream_ptr())
     assert rc == 0
     assert bufs.read() == engine.enum(batch, "splits", 0, total).read()
+    # the phase sequences 1+2 and 1+4+8 (plan and sweep apart) equal phase 3,
+    # for the whole population and for block parts
+    for nparts in (1, 3):
+        want = [engine.enum(batch, "splits", 0, total, part=q, nparts=nparts).read() for q in range(nparts)]
+        for seq in ((1, 2), (1, 4, 8)):
+            got = []
+            for q in range(nparts):
+                b2 = engine.WinnerBuffers(batch.dev_buf.device)
+                for ph in seq:
+                    engine.enum(batch, "splits", 0, total, b2, part=q, nparts=nparts, phase=ph)
+                got.append(b2.read())
+            assert got == want, (nparts, seq)
     torch.cuda.synchronize()
 
 
