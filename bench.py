@@ -1073,6 +1073,9 @@ def main():
         line = run_reference(args, rank, world)
     else:
         if world > 1:
+            # stdout carries the one JSON line: NCCL's own banner stays off
+            # unless the caller asked for NCCL logging
+            os.environ.setdefault("NCCL_DEBUG", "WARN")
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
