@@ -1073,13 +1073,21 @@ def main():
         line = run_reference(args, rank, world)
     else:
         if world > 1:
-            # stdout carries the one JSON line: NCCL's own banner stays off
-            # unless the caller asked for NCCL logging
-            os.environ.setdefault("NCCL_DEBUG", "WARN")
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            # stdout carries the one JSON line: NCCL's version banner (printed
+            # at communicator creation, which device_id makes eager) goes to
+            # stderr
+            sys.stdout.flush()
+            saved = os.dup(1)
+            os.dup2(2, 1)
+            try:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+                dist.barrier()
+            finally:
+                os.dup2(saved, 1)
+                os.close(saved)
         line = run_b200(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
