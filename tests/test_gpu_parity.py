@@ -248,7 +248,18 @@ def test_argmin_scores(engine_ready):
 
 
 # ------------------------------------------------------------ batched solvers
-def test_subset_dp_batch(oracle_mod, engine_ready):
+@pytest.mark.parametrize("form", ["default", "cta", "warp", "generic"])
+def test_subset_dp_batch(oracle_mod, engine_ready, monkeypatch, form):
+    """Every DP kernel form on the criterion-6 instances vs the oracle:
+    the launcher's choice, the 4-warp CTA form, the warp form and the generic
+    one-CTA-per-scenario kernel."""
+    if form == "cta":
+        monkeypatch.setenv("DM_DP_CTA", "1")
+    elif form == "warp":
+        monkeypatch.setenv("DM_DP_CTA", "0")
+    elif form == "generic":
+        monkeypatch.setenv("DM_DISABLE_DP_WARP", "1")
+        monkeypatch.setenv("DM_DISABLE_DP_LANE", "1")
     insts = [i for i in criterion6_instances(count=80)]
     hosts = [build_host(s, f) for s, f in insts]
     batch = engine.device_batch(hosts)
@@ -265,10 +276,14 @@ def test_subset_dp_batch(oracle_mod, engine_ready):
         assert owner[s, :len(st)].tolist() == own.tolist()
 
 
-def test_subset_dp_mid_fleets(oracle_mod, engine_ready):
-    """Fleets of 6-8 workers (the thread-per-mask DP kernel): chosen runs and
-    makespans equal the oracle's _subset_dp restatement, including forced
-    ties (identical peers, uniform stages) and infeasible instances."""
+@pytest.mark.parametrize("knob", [None, "DM_DISABLE_DP_LANE"])
+def test_subset_dp_mid_fleets(oracle_mod, engine_ready, monkeypatch, knob):
+    """Fleets of 6-8 workers (the thread-per-(mask, worker) DP kernel, and
+    with DM_DISABLE_DP_LANE the generic one-CTA-per-scenario kernel): chosen
+    runs and makespans equal the oracle's _subset_dp restatement, including
+    forced ties (identical peers, uniform stages) and infeasible instances."""
+    if knob:
+        monkeypatch.setenv(knob, "1")
     rng = np.random.default_rng(66)
     insts = []
     for k in range(48):
