@@ -759,6 +759,22 @@ def api_latency_measure(dev):
     out["evaluate_runs_c1"] = {"ms_per_call": statistics.median(times), "ms_min": min(times),
                                "reference_ms_per_call": (_t.perf_counter() - t0) * 1e3 / 5,
                                "same_report": rep.makespan == ref.makespan and rep.runs == ref.runs}
+    # brute_force_schedule on C1 (62,704 candidates in itertools order, the
+    # reference's exhaustive search entry point), beside the reference's own
+    for _ in range(3):
+        S.brute_force_schedule(stages, fleet)
+    times = []
+    for _ in range(20):
+        t0 = _t.perf_counter()
+        rep = S.brute_force_schedule(stages, fleet)
+        times.append((_t.perf_counter() - t0) * 1e3)
+    t0 = _t.perf_counter()
+    ref = RS.brute_force_schedule(stages, fleet)
+    t_ref = (_t.perf_counter() - t0) * 1e3
+    out["brute_force_c1"] = {"candidates": 62704, "ms_per_call": statistics.median(times), "ms_min": min(times),
+                             "reference_ms_per_call": t_ref,
+                             "same_report": rep.makespan == ref.makespan and rep.runs == ref.runs
+                             and rep.trace == ref.trace}
     # pipeline.sweep: bert-large (50 cells) on two fleets
     # over a 12 x 10 link grid, n_b = 512 — the reference's own sweep beside it
     from paper_2309_01172_b200 import pipeline as P
